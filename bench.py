@@ -1,0 +1,338 @@
+"""Benchmark: CVT-iteration voxels/s of the geodesic LSRCVT hot path.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl b200|reference]
+
+A step is one Lloyd iteration (voronoi_classify + centroidal_update: LOS
+classification, phi-propagated vote, clamped site move) over the whole volume;
+value = voxels x steps / device time. Default workload is
+BASELINE.json configs[1] (C2: 128^3 gaussian-mix, 1 band, 512 'g'-weighted
+sites). Under torchrun each rank runs its own volume instance (independent
+objects, no data-path collective): "scaling": "weak".
+
+--impl reference times the reference algorithm's CPU implementation (the C
+oracle port in oracle/, all host threads) on the same config; rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+CONFIGS = {
+    "c1": dict(kind="spiral", dims=(256, 256, 1), iso=[0.3, 0.55, 0.8],
+               seeding=dict(alpha=64, gamma=1.0, weight_field="g", block_size=16, seed=0),
+               label="C1 2D 256^2 spiral, 2 nested bands, 69 g-weighted sites"),
+    "c2": dict(kind="gaussian-mix", dims=(128, 128, 128), iso=[0.3, 0.7],
+               seeding=dict(alpha=512, weight_field="g", seed=0),
+               label="C2 3D 128^3 gaussian-mix, 1 band, 512 g-weighted sites"),
+    "c3": dict(kind="horseshoe", dims=(256, 256, 256), iso=[0.0, 0.12, 0.3],
+               seeding=dict(alpha=4096, seed=0),
+               label="C3 3D 256^3 horseshoe shells, 2 bands, 4097 unweighted sites"),
+    "c4": dict(kind="random-smooth", dims=(512, 512, 512), iso=[0.35, 0.5, 0.65, 0.8],
+               seeding=dict(alpha=32768, weight_field="g", seed=0),
+               label="C4 3D 512^3 random-smooth, 3 bands, 32k g-weighted sites"),
+}
+L2_BYTES = 126 * 2**20
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def build_workload(cfg, rank, use_gpu_masks=True):
+    from paper_2208_06970_b200 import (IsobandSpec, SeedingParams, classify_isobands, label_components,
+                                       seed_sites, synth_field, voxel_weights)
+
+    grid = synth_field(cfg["kind"], cfg["dims"], rank)
+    spec = IsobandSpec("f", cfg["iso"])
+    if use_gpu_masks:
+        labels = label_components(classify_isobands(grid, spec))
+    else:
+        from oracle import oracle
+        from paper_2208_06970_b200.grid import ComponentInfo, LabelMap
+
+        layer = oracle.isobands(grid.fields["f"], spec.iso_values)
+        comp, table = oracle.label_components(layer, grid.dims, spec.n_bands)
+        labels = LabelMap(grid.dims, layer, comp,
+                          [ComponentInfo(t["id"], t["layer"], t["voxel_count"], tuple(t["bbox"]), (0, 0))
+                           for t in table], spec.iso_values, "f")
+    params = SeedingParams(**cfg["seeding"])
+    sites, _ = seed_sites(grid, labels, params)
+    return grid, labels, params, sites, voxel_weights(grid, params)
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def run_reference(args, cfg, world, rank):
+    """CPU arm: the oracle port of the reference algorithm, all host threads."""
+    if rank != 0:
+        return
+    from oracle import oracle
+
+    oracle.build()
+    grid, labels, params, sites, weights = build_workload(cfg, 0, use_gpu_masks=False)
+    n = grid.size
+    pos = np.array([s.position for s in sites])
+    sc = np.array([s.component_id for s in sites], np.int32)
+    w = None if params.weight_field is None else weights
+    comp = labels.component
+
+    def step(p):
+        c = oracle.classify(grid.dims, grid.spacing, comp, p, sc, labels.n_components)
+        return oracle.centroidal(grid.dims, grid.spacing, comp, c["site_of"], c["src"], w, p, sc)["new_pos"]
+
+    for _ in range(args.warmup):
+        pos = step(pos)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        pos = step(pos)
+    dt = time.perf_counter() - t0
+    value = n * args.steps / dt
+    threads = oracle.num_threads()
+    line = {
+        "impl": "reference", "metric": "CVT-iteration voxels/s", "value": value, "unit": "voxels/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": cfg["label"], "dims": list(cfg["dims"]), "sites": len(sites)},
+        "cpu_baseline": {"value": value, "unit": "voxels/s", "cores": threads, "kind": "port",
+                         "sample": f"{args.steps} full Lloyd iterations after {args.warmup} warm-up, C oracle "
+                                   f"(restated numba kernels, OpenMP eval + serial commit)"},
+        "e2e": {"value": value, "unit": "voxels/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(grid, labels, params, weights, pos, sc, budget_s=20.0, max_iters=3):
+    from oracle import oracle
+
+    oracle.build()
+    w = None if params.weight_field is None else weights
+    comp = labels.component
+    t0 = time.perf_counter()
+    it = 0
+    p = pos
+    while it < max_iters and (it == 0 or time.perf_counter() - t0 < budget_s):
+        c = oracle.classify(grid.dims, grid.spacing, comp, p, sc, labels.n_components)
+        p = oracle.centroidal(grid.dims, grid.spacing, comp, c["site_of"], c["src"], w, p, sc)["new_pos"]
+        it += 1
+    dt = time.perf_counter() - t0
+    return {"value": grid.size * it / dt, "unit": "voxels/s", "cores": oracle.num_threads(), "kind": "port",
+            "sample": f"{it} Lloyd iteration(s) of the same workload from the timed region's starting sites"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    cfg = CONFIGS[args.config]
+    world, rank, local = dist_setup(args)
+    if args.impl == "reference":
+        run_reference(args, cfg, world, rank)
+        return
+
+    import torch
+
+    from paper_2208_06970_b200 import _lib, centroidal_update, voronoi_classify
+    from paper_2208_06970_b200.tessellation import engine_for, lloyd_weight_mode, voxel_length
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    grid, labels, params, sites, weights = build_workload(cfg, rank)
+    n = grid.size
+    S = len(sites)
+    L = _lib.lib()
+    eng = engine_for(labels, grid.spacing, S)
+    pos0 = np.array([s.position for s in sites])
+    sc_np = np.array([s.component_id for s in sites], np.int32)
+    pos_d = torch.from_numpy(pos0).cuda()
+    sc_d = torch.from_numpy(sc_np).cuda()
+    mode, w_d = lloyd_weight_mode(torch, grid, params, weights)
+    backoff = 0.5 * voxel_length(grid.dims, grid.spacing)
+    state_bytes = n * (8 + 8 + 4 + 1)
+    flush = state_bytes < 2 * L2_BYTES
+    scratch = torch.empty(2 * L2_BYTES // 4, dtype=torch.float32, device="cuda") if flush else None
+
+    def step(p):
+        eng.classify(p, sc_d, want_state=True)
+        p2, disp, _, _ = eng.centroidal(p, sc_d, mode, w_d, backoff)
+        return p2, disp
+
+    for _ in range(args.warmup):
+        pos_d, _ = step(pos_d)
+    torch.cuda.synchronize()
+    pos_start = pos_d.cpu().numpy()
+
+    # timed region
+    _lib.check(L.lrcvt_plan_set_timing(eng.plan, 1), "set_timing")
+    E = C = 0
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    launches0 = L.lrcvt_launch_count()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for k in range(args.steps):
+            if flush:
+                scratch.zero_()
+            ev[k][0].record()
+            pos_d, _ = step(pos_d)
+            ev[k][1].record()
+            st = eng.stats
+            E += st.evaluations
+            C += st.commits
+        torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    launches = int(L.lrcvt_launch_count() - launches0)
+    ms = sum(a.elapsed_time(b) for a, b in ev)
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    el, eitems, ems = _lib.ctypes.c_int64(), _lib.ctypes.c_int64(), _lib.ctypes.c_double()
+    L.lrcvt_plan_timing(eng.plan, _lib.ctypes.byref(el), _lib.ctypes.byref(eitems), _lib.ctypes.byref(ems))
+    _lib.check(L.lrcvt_plan_set_timing(eng.plan, 0), "set_timing")
+    value = n * args.steps * world / (ms / 1e3)
+    hbm, peak_kind = peaks()
+    # dominant kernel: k_eval; algorithmic bytes = 20 B per evaluated voxel
+    eval_bytes = 20.0 * eitems.value
+    achieved = eval_bytes / (ems.value / 1e3) / 1e9 if ems.value > 0 else 0.0
+    b_iter = 29.0 * n + 20.0 * E / args.steps + 16.0 * C / args.steps
+    traffic = None
+    prof = ROOT / "profiles" / f"ncu_{args.config}_k_eval.json"
+    if prof.exists():
+        traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
+
+    # end-to-end through the public API with host numpy in/out
+    e2e = None
+    if not args.no_e2e:
+        from paper_2208_06970_b200.seeding import Site
+
+        cur = [Site(tuple(p), int(c)) for p, c in zip(pos_start, sc_np)]
+        ke = max(1, min(args.steps, 10))
+        cur_sites = cur
+        for _ in range(1):
+            t_ = voronoi_classify(grid, labels, cur_sites, weights if params.weight_field else None)
+            cur_sites, _ = centroidal_update(t_)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(ke):
+            t_ = voronoi_classify(grid, labels, cur_sites, weights if params.weight_field else None)
+            cur_sites, _ = centroidal_update(t_)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        h2d = 2 * S * (24 + 4)
+        d2h = n * (8 + 8 + 1) + S * (24 + 8) + 64
+        e2e = {"value": n * ke * world / dt, "unit": "voxels/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h,
+               "note": "voronoi_classify + centroidal_update per step, numpy in/out; weights array resident "
+                       "after first upload"}
+
+    line = {
+        "metric": "CVT-iteration voxels/s", "value": value, "unit": "voxels/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg["label"], "dims": list(cfg["dims"]), "voxels": n, "sites": S,
+                   "inband": eng.inband, "l2": "flushed between steps (256 MiB write)" if flush
+                   else f"state {state_bytes / 2**20:.0f} MiB > L2", "E_per_step": E / args.steps,
+                   "C_per_step": C / args.steps},
+        "roofline": {"bound": "hbm", "kernel": "k_eval", "achieved": achieved, "peak": hbm,
+                     "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / hbm, "traffic": traffic,
+                     "launches": el.value, "avg_launch_us": 1e3 * ems.value / max(el.value, 1),
+                     "bytes_per_launch": eval_bytes / max(el.value, 1),
+                     "eval_share_of_step": ems.value / ms if ms else None,
+                     "iteration_B": b_iter, "iteration_frac": b_iter / (ms / args.steps / 1e3) / 1e9 / hbm},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+    }
+    if e2e:
+        line["e2e"] = e2e
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(grid, labels, params, weights, pos_start, sc_np)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,136 @@
+/*
+ * lrcvt_cuda.h -- C ABI of the B200 (sm_100a) LSRCVT hot path.
+ *
+ * Plain pointers and sizes only. Every pointer argument named d_* is a
+ * DEVICE pointer (cudaMalloc / torch CUDA tensor storage) on the current
+ * device; `stream` is a cudaStream_t (NULL = legacy default stream). Calls are
+ * stream-ordered; the entry points that return statistics synchronise the
+ * stream once at the end (the reference returns Python ints there).
+ *
+ * Each entry point replaces one call site of the reference's kernel seam,
+ * `lrcvt._kernels` imported as `K` in /root/reference/pkg/src/lrcvt/
+ * tessellation.py (cited per function below). INTEGRATION.md shows the
+ * ctypes binding a maintainer adds to the reference.
+ *
+ * Per-voxel state layout (HBM, flat x-fastest index v = x + nx*(y + ny*z),
+ * grid.py:3-5):
+ *   d_site_src : int32[N][2]  (site_of[v], src[v]) packed; -1 = none
+ *   d_dist     : float64[N]   geodesic distance, +inf = unassigned
+ *   d_state    : uint8[N]     LOS=1 | ACTIVE=2 | NODE=4 (tessellation.py:28-30)
+ * lrcvt_unpack_site_src() splits the pair into the reference's separate
+ * site_of / src arrays (tessellation.py:52-54).
+ *
+ * Return codes: 0 = success; > 0 = number of sites outside their recorded
+ * component (the caller raises ValueError, tessellation.py:139-140);
+ * < 0 = error (LRCVT_E_*), message via lrcvt_last_error().
+ */
+#ifndef LRCVT_CUDA_H
+#define LRCVT_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LRCVT_E_CUDA (-1)
+#define LRCVT_E_ARG (-2)
+#define LRCVT_E_NOMEM (-3)
+
+/* weight modes for lrcvt_centroidal_update (seeding.py:59-68 voxel_weights) */
+#define LRCVT_W_ONES 0    /* weight_field None: m_v = 1                      */
+#define LRCVT_W_F64 1     /* explicit float64[N] weights (m_v ** gamma)       */
+#define LRCVT_W_F32_G1 2  /* float32[N] weight field, gamma == 1 (exact)      */
+#define LRCVT_W_F32_G2 3  /* float32[N] weight field, gamma == 2 (exact m*m)  */
+
+typedef struct lrcvt_plan lrcvt_plan;
+
+typedef struct {
+  int64_t rounds;        /* report["rounds"], tessellation.py:199-200     */
+  int64_t sweeps;        /* report["sweeps"]                               */
+  int64_t assigned;      /* report["assigned"], tessellation.py:203        */
+  int64_t evaluations;   /* E: voxels evaluated over all rounds + sweeps   */
+  int64_t commits;       /* C: committed improvements                      */
+  int64_t bad_sites;     /* sites outside their component                  */
+  int64_t phase1_rounds; /* rounds of phase 1 (subset of `rounds`)         */
+  int64_t eligible;      /* in-band voxels of components that have sites   */
+} lrcvt_classify_stats;
+
+/* Plan: geometry + the static component volume (borrowed, must outlive the
+ * plan) + scratch sized for up to max_sites sites. Replaces the per-call
+ * scratch allocation of tessellation.py:142-149. */
+int lrcvt_plan_create(lrcvt_plan **plan, int64_t nx, int64_t ny, int64_t nz, double sx,
+                      double sy, double sz, const int32_t *d_comp, int32_t n_components,
+                      int64_t max_sites, void *stream);
+int lrcvt_plan_destroy(lrcvt_plan *plan);
+/* in-band voxel count of the plan's component volume */
+int64_t lrcvt_plan_inband(const lrcvt_plan *plan);
+
+/* voronoi_classify core: replaces K._place_seeds (tessellation.py:136),
+ * K._seed_worklist + K._run_phase (:151-156), the phase-2 loop with
+ * K._run_phase / K._eval_list / K._apply_and_enqueue (:161-189) and the state
+ * bits (:191-194). d_site_pos is float64[n_sites][3], d_site_comp int32.
+ * d_state may be NULL. */
+int lrcvt_classify(lrcvt_plan *plan, int64_t n_sites, const double *d_site_pos,
+                   const int32_t *d_site_comp, int32_t *d_site_src, double *d_dist,
+                   uint8_t *d_state, lrcvt_classify_stats *stats, void *stream);
+
+/* centroidal_update core: replaces K._phi_chains + K._centroid_targets +
+ * K._move_sites (tessellation.py:233-241). d_weights is NULL (LRCVT_W_ONES),
+ * float64[N] (LRCVT_W_F64) or float32[N] (LRCVT_W_F32_*). backoff = 0.5 *
+ * voxel_length (tessellation.py:237-240). Outputs: d_new_pos float64[S][3],
+ * d_disp float64[S], optional d_sums float64[4][S] (wsum, tx, ty, tz), and
+ * *empty_regions (report["empty_regions"]). */
+int lrcvt_centroidal_update(lrcvt_plan *plan, int64_t n_sites, const double *d_site_pos,
+                            const int32_t *d_site_comp, const int32_t *d_site_src,
+                            int32_t weight_mode, const void *d_weights, double backoff,
+                            double *d_new_pos, double *d_disp, double *d_sums,
+                            int64_t *empty_regions, void *stream);
+
+/* split packed (site_of, src) into two int32[N] arrays */
+int lrcvt_unpack_site_src(const int32_t *d_site_src, int64_t n, int32_t *d_site_of,
+                          int32_t *d_src, void *stream);
+
+/* batch of K._segment_hit_t (_kernels.py:45-125): d_segs float64[n][6]
+ * (ax, ay, az, bx, by, bz), d_want int32[n] -> d_t float64[n]. Backs
+ * raycast_same_component (tessellation.py:82-99). */
+int lrcvt_segment_hit_t(int64_t nx, int64_t ny, int64_t nz, double sx, double sy, double sz,
+                        const int32_t *d_comp, const double *d_segs, const int32_t *d_want,
+                        int64_t n, double *d_t, void *stream);
+
+/* classify_isobands (grid.py:140-163): d_field float32[n], d_iso float64
+ * [n_iso] strictly increasing -> d_layer int32[n] (band index or -1). */
+int lrcvt_isobands(int64_t n, const float *d_field, const double *d_iso, int32_t n_iso,
+                   int32_t *d_layer, void *stream);
+
+/* label_components (grid.py:166-220): face-connected components of each
+ * layer 0..n_layers-1 -> d_component int32[N] with dense ids ordered by
+ * (layer, first voxel in row-major order); *n_components receives the count
+ * (the call synchronises the stream). */
+int lrcvt_label_components(int64_t nx, int64_t ny, int64_t nz, const int32_t *d_layer,
+                           int32_t n_layers, int32_t *d_component, int32_t *n_components,
+                           void *stream);
+
+/* ComponentInfo table (grid.py:199-211) for ids 0..n_components-1:
+ * d_count uint64[nc] voxel counts, d_bbox int32[nc][6] inclusive
+ * (x0, y0, z0, x1, y1, z1), d_layer_of int32[nc]. */
+int lrcvt_component_table(int64_t nx, int64_t ny, int64_t nz, const int32_t *d_component,
+                          const int32_t *d_layer, int32_t n_components, uint64_t *d_count,
+                          int32_t *d_bbox, int32_t *d_layer_of, void *stream);
+
+/* Instrumentation for bench.py: enable CUDA-event timing of every k_eval
+ * launch (the dominant kernel) on the plan; read back launches, voxels
+ * evaluated and summed device milliseconds. lrcvt_launch_count() counts this
+ * library's own kernel launches (CUB-internal kernels excluded). */
+int lrcvt_plan_set_timing(lrcvt_plan *plan, int enable);
+int lrcvt_plan_timing(const lrcvt_plan *plan, int64_t *launches, int64_t *items, double *ms);
+unsigned long long lrcvt_launch_count(void);
+
+const char *lrcvt_last_error(void);
+int lrcvt_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LRCVT_CUDA_H */

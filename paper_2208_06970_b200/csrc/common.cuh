@@ -1,0 +1,162 @@
+// common.cuh -- shared device helpers for the LSRCVT hot path (sm_100a).
+//
+// Every floating-point helper here reproduces the reference numba kernels
+// bit for bit. The translation unit is compiled with --fmad=false, and the
+// few expressions whose rounding matters are written with explicit
+// __dmul_rn/__dadd_rn/__dsub_rn so no flag change can contract them.
+//
+// Reference: /root/reference/pkg/src/lrcvt/_kernels.py
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define LRCVT_EPS 1e-9  // _kernels.py:15
+#define LRCVT_NONE (-1)
+
+namespace lrcvt {
+
+// Grid geometry, passed by value to every kernel.
+struct Geo {
+  int nx, ny, nz;
+  int nxy;
+  int64_t n;
+  double sx, sy, sz;
+  double inv_nx, inv_nxy;  // for exact division via fp64 reciprocal + fixup
+  int dyadic;              // spacing values are powers of two (exact centre diffs)
+  double off_len[26];      // |offset_k| in world units when dyadic
+  int off_d[26];           // flat index delta of offset k
+};
+
+// _kernels.py:17-25: dz, dy, dx lexicographic, dx fastest, (0,0,0) excluded.
+__host__ __device__ inline void offset_of(int k, int& dx, int& dy, int& dz) {
+  int j = k < 13 ? k : k + 1;  // skip the centre (index 13 of the 27-cube)
+  dz = j / 9 - 1;
+  dy = (j / 3) % 3 - 1;
+  dx = j % 3 - 1;
+}
+
+// v -> (x, y, z) without integer division: fp64 reciprocal, then one-step
+// fixup (exact for v < 2^31).
+__device__ __forceinline__ void coords(const Geo& g, int v, int& x, int& y, int& z) {
+  int q = __double2int_rz((double)v * g.inv_nxy);
+  int r = v - q * g.nxy;
+  if (r < 0) { q--; r += g.nxy; } else if (r >= g.nxy) { q++; r -= g.nxy; }
+  z = q;
+  int q2 = __double2int_rz((double)r * g.inv_nx);
+  int r2 = r - q2 * g.nx;
+  if (r2 < 0) { q2--; r2 += g.nx; } else if (r2 >= g.nx) { q2++; r2 -= g.nx; }
+  y = q2;
+  x = r2;
+}
+
+// _kernels.py:29-34: (x + 0.5) * s
+__device__ __forceinline__ double centre1(int x, double s) {
+  return __dmul_rn(__dadd_rn((double)x, 0.5), s);
+}
+
+// _kernels.py:37-42: sqrt(dx*dx + dy*dy + dz*dz), left-to-right, no FMA.
+__device__ __forceinline__ double dist3(double ax, double ay, double az, double bx,
+                                        double by, double bz) {
+  double dx = __dsub_rn(bx, ax), dy = __dsub_rn(by, ay), dz = __dsub_rn(bz, az);
+  return __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)),
+                              __dmul_rn(dz, dz)));
+}
+
+// _kernels.py:136-144
+__device__ __forceinline__ bool beats(double d, int s, double cur_d, int cur_s) {
+  if (d < __dsub_rn(cur_d, LRCVT_EPS)) return true;
+  if (fabs(__dsub_rn(d, cur_d)) <= LRCVT_EPS && s < cur_s) return true;
+  return false;
+}
+
+// Exact pre-screen: returns a threshold T such that any candidate distance
+// d >= T cannot satisfy beats(d, *, cur_d, *). Derivation:
+// T - cur_d >= 2e-9 + |cur_d|*1e-15 - ulp(T)/2 > EPS, so d - cur_d rounds
+// above EPS and d >= cur_d - EPS. cur_d == inf gives T == inf (no screen).
+__device__ __forceinline__ double beat_threshold(double cur_d) {
+  return __dadd_rn(cur_d, __dadd_rn(2e-9, __dmul_rn(fabs(cur_d), 1e-15)));
+}
+
+// read-only 32-byte load (two LDG.128 through the non-coherent path)
+__device__ __forceinline__ double4 ld_d4(const double4* p) {
+  const double2* q = reinterpret_cast<const double2*>(p);
+  const double2 a = __ldg(q), b = __ldg(q + 1);
+  return make_double4(a.x, a.y, b.x, b.y);
+}
+
+__device__ __forceinline__ int clampi(int a, int lo, int hi) {
+  return a < lo ? lo : (a > hi ? hi : a);
+}
+
+// floor(a / s) clamped into [0, n-1] as the reference does (int(np.floor()),
+// then min/max). Values far outside int range saturate before clamping,
+// which gives the same clamp result.
+__device__ __forceinline__ int cell_of(double a, double s, int n) {
+  double f = floor(__ddiv_rn(a, s));
+  f = fmin(fmax(f, -1.0), (double)n);
+  return clampi((int)f, 0, n - 1);
+}
+
+// _kernels.py:45-125: parametric t of the first entry into a voxel whose
+// component is not `want`; 1.0 if none.
+__device__ inline double segment_hit_t(const int* __restrict__ comp, const Geo& g,
+                                       double ax, double ay, double az, double bx,
+                                       double by, double bz, int want) {
+  int cx = cell_of(ax, g.sx, g.nx), cy = cell_of(ay, g.sy, g.ny), cz = cell_of(az, g.sz, g.nz);
+  int ex = cell_of(bx, g.sx, g.nx), ey = cell_of(by, g.sy, g.ny), ez = cell_of(bz, g.sz, g.nz);
+  if (__ldg(comp + cx + g.nx * (cy + g.ny * cz)) != want) return 0.0;
+  double dx = __dsub_rn(bx, ax), dy = __dsub_rn(by, ay), dz = __dsub_rn(bz, az);
+  int stepx = dx > 0 ? 1 : -1, stepy = dy > 0 ? 1 : -1, stepz = dz > 0 ? 1 : -1;
+  const double big = 1e30;
+  double tmaxx, tmaxy, tmaxz, tdx, tdy, tdz;
+  if (dx != 0.0) {
+    double nxt = dx > 0 ? __dmul_rn((double)(cx + 1), g.sx) : __dmul_rn((double)cx, g.sx);
+    tmaxx = __ddiv_rn(__dsub_rn(nxt, ax), dx);
+    tdx = __ddiv_rn(g.sx, fabs(dx));
+  } else { tmaxx = big; tdx = big; }
+  if (dy != 0.0) {
+    double nxt = dy > 0 ? __dmul_rn((double)(cy + 1), g.sy) : __dmul_rn((double)cy, g.sy);
+    tmaxy = __ddiv_rn(__dsub_rn(nxt, ay), dy);
+    tdy = __ddiv_rn(g.sy, fabs(dy));
+  } else { tmaxy = big; tdy = big; }
+  if (dz != 0.0) {
+    double nxt = dz > 0 ? __dmul_rn((double)(cz + 1), g.sz) : __dmul_rn((double)cz, g.sz);
+    tmaxz = __ddiv_rn(__dsub_rn(nxt, az), dz);
+    tdz = __ddiv_rn(g.sz, fabs(dz));
+  } else { tmaxz = big; tdz = big; }
+  int max_steps = abs(ex - cx) + abs(ey - cy) + abs(ez - cz) + 8;
+  for (int i = 0; i < max_steps; i++) {
+    if (cx == ex && cy == ey && cz == ez) return 1.0;
+    double t = fmin(tmaxx, fmin(tmaxy, tmaxz));
+    if (t > 1.0) {
+      if (__ldg(comp + ex + g.nx * (ey + g.ny * ez)) == want) return 1.0;
+      return 1.0 - 1e-12;
+    }
+    if (tmaxx == t) { cx += stepx; tmaxx = __dadd_rn(tmaxx, tdx); }
+    if (tmaxy == t) { cy += stepy; tmaxy = __dadd_rn(tmaxy, tdy); }
+    if (tmaxz == t) { cz += stepz; tmaxz = __dadd_rn(tmaxz, tdz); }
+    if (cx < 0 || cy < 0 || cz < 0 || cx >= g.nx || cy >= g.ny || cz >= g.nz) return t;
+    if (__ldg(comp + cx + g.nx * (cy + g.ny * cz)) != want) return t;
+  }
+  return 1.0;
+}
+
+__device__ __forceinline__ bool segment_clear(const int* __restrict__ comp, const Geo& g,
+                                              double ax, double ay, double az, double bx,
+                                              double by, double bz, int want) {
+  return segment_hit_t(comp, g, ax, ay, az, bx, by, bz, want) >= 1.0;
+}
+
+// Warp-aggregated append of `take` (0/1) items; returns this lane's slot
+// (valid only when take). All 32 lanes must call it.
+__device__ __forceinline__ int warp_append(int* counter, bool take) {
+  unsigned m = __ballot_sync(0xffffffffu, take);
+  int lane = threadIdx.x & 31;
+  int leader = __ffs(m) - 1;
+  int base = 0;
+  if (m && lane == leader) base = atomicAdd(counter, __popc(m));
+  base = __shfl_sync(0xffffffffu, base, leader < 0 ? 0 : leader);
+  return base + __popc(m & ((1u << lane) - 1u));
+}
+
+}  // namespace lrcvt

@@ -1,0 +1,662 @@
+// lrcvt_capi.cu -- plan object, host orchestration and the extern "C"
+// entry points declared in include/lrcvt_cuda.h.
+#include <cub/cub.cuh>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "../../include/lrcvt_cuda.h"
+#include "classify.cuh"
+#include "vote.cuh"
+#include "masks.cuh"
+
+using namespace lrcvt;
+
+namespace {
+
+thread_local std::string g_last_error;
+// number of this library's own kernel launches (CUB's internal kernels not
+// counted); read by bench.py for the "gpu_launches" claim
+unsigned long long g_launches = 0;
+#define LAUNCHED(k) (g_launches += (k))
+
+int set_error(int code, const char* what, cudaError_t e = cudaSuccess) {
+  char buf[512];
+  if (e != cudaSuccess)
+    snprintf(buf, sizeof buf, "%s: %s (%s)", what, cudaGetErrorString(e), cudaGetErrorName(e));
+  else
+    snprintf(buf, sizeof buf, "%s", what);
+  g_last_error = buf;
+  return code;
+}
+
+#define CK(call)                                                        \
+  do {                                                                  \
+    cudaError_t e_ = (call);                                            \
+    if (e_ != cudaSuccess) return set_error(LRCVT_E_CUDA, #call, e_);   \
+  } while (0)
+
+#define CKR(call)                                                       \
+  do {                                                                  \
+    int r_ = (call);                                                    \
+    if (r_ != 0) return r_;                                             \
+  } while (0)
+
+#define CKL(what)                                                       \
+  do {                                                                  \
+    cudaError_t e_ = cudaGetLastError();                                \
+    if (e_ != cudaSuccess) return set_error(LRCVT_E_CUDA, what, e_);    \
+  } while (0)
+
+bool is_pow2(double s) {
+  int e;
+  double m = frexp(s, &e);
+  return s > 0 && m == 0.5;
+}
+
+int grid_for(int64_t n, int block, int cap = 1 << 30) {
+  int64_t b = (n + block - 1) / block;
+  if (b < 1) b = 1;
+  if (b > cap) b = cap;
+  return (int)b;
+}
+
+struct EligiblePred {
+  const int* comp;
+  const uint8_t* has_site;
+  __device__ __forceinline__ bool operator()(const int v) const {
+    const int c = comp[v];
+    return c >= 0 && has_site[c];
+  }
+};
+
+struct IsRoot {
+  const int* L;
+  __device__ __forceinline__ bool operator()(const int v) const { return L[v] == v; }
+};
+
+struct CountInband {
+  const int* comp;
+  __device__ __forceinline__ int operator()(const int v) const { return comp[v] >= 0 ? 1 : 0; }
+};
+
+__global__ void k_pack_sites(const double* __restrict__ pos3, int n, double4* __restrict__ out) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s < n) out[s] = make_double4(pos3[3 * s], pos3[3 * s + 1], pos3[3 * s + 2], 0.0);
+}
+
+__global__ void k_unpack_sites(const double4* __restrict__ in, int n, double* __restrict__ pos3) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s < n) {
+    const double4 p = in[s];
+    pos3[3 * s] = p.x; pos3[3 * s + 1] = p.y; pos3[3 * s + 2] = p.z;
+  }
+}
+
+__global__ void k_unpack_ss(const int2* __restrict__ ss, int64_t n, int* __restrict__ site_of,
+                            int* __restrict__ src) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+    const int2 a = ss[i];
+    site_of[i] = a.x;
+    src[i] = a.y;
+  }
+}
+
+__global__ void k_segment_batch(Geo g, const int* __restrict__ comp, const double* __restrict__ segs,
+                                const int* __restrict__ want, int64_t n, double* __restrict__ t) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double* s = segs + 6 * i;
+  t[i] = segment_hit_t(comp, g, s[0], s[1], s[2], s[3], s[4], s[5], want[i]);
+}
+
+Geo make_geo(int64_t nx, int64_t ny, int64_t nz, double sx, double sy, double sz) {
+  Geo g;
+  memset(&g, 0, sizeof g);
+  g.nx = (int)nx; g.ny = (int)ny; g.nz = (int)nz;
+  g.nxy = (int)(nx * ny);
+  g.n = nx * ny * nz;
+  g.sx = sx; g.sy = sy; g.sz = sz;
+  g.inv_nx = 1.0 / (double)nx;
+  g.inv_nxy = 1.0 / (double)(nx * ny);
+  g.dyadic = is_pow2(sx) && is_pow2(sy) && is_pow2(sz);
+  for (int k = 0; k < 26; k++) {
+    int dx, dy, dz;
+    offset_of(k, dx, dy, dz);
+    g.off_d[k] = dx + (int)nx * (dy + (int)ny * dz);
+    // exact |c_w - c_v| when spacing is dyadic (centre differences are exact)
+    volatile double ex = dx * sx, ey = dy * sy, ez = dz * sz;
+    volatile double s2 = ex * ex;
+    s2 = s2 + ey * ey;
+    s2 = s2 + ez * ez;
+    g.off_len[k] = sqrt((double)s2);
+  }
+  return g;
+}
+
+bool geo_ok(int64_t nx, int64_t ny, int64_t nz, double sx, double sy, double sz) {
+  if (nx < 1 || ny < 1 || nz < 1) return false;
+  if (!(sx > 0 && sy > 0 && sz > 0)) return false;
+  const int64_t n = nx * ny * nz;
+  return n < (int64_t(1) << 31) - 1 && nx < (1 << 30) && ny < (1 << 30) && nz < (1 << 30);
+}
+
+}  // namespace
+
+struct lrcvt_plan {
+  Geo g;
+  const int* comp = nullptr;
+  int n_components = 0;
+  int64_t max_sites = 0;
+  int64_t n_inband = 0;
+  int64_t n_eligible = 0;
+  // frontier machinery
+  int* list_a = nullptr;
+  int* list_b = nullptr;
+  int* eligible = nullptr;
+  Prop* imp = nullptr;
+  uint32_t* bm = nullptr;
+  int64_t bm_words = 0;
+  int* counters = nullptr;
+  int* h_counters = nullptr;  // pinned
+  uint8_t* has_site = nullptr;
+  // sites
+  double4* site_pos = nullptr;
+  double4* new_pos = nullptr;
+  int* sk_key = nullptr;
+  int* sk_key2 = nullptr;
+  int* sk_val = nullptr;
+  int* sk_val2 = nullptr;
+  double* sk_d = nullptr;
+  // vote
+  unsigned long long* acc = nullptr;
+  double* sums = nullptr;
+  int* vt_key = nullptr;
+  int* vt_key2 = nullptr;
+  int* vt_idx = nullptr;
+  int* vt_idx2 = nullptr;
+  double4* vt_terms = nullptr;
+  int* seg_b = nullptr;
+  int* seg_e = nullptr;
+  // cub
+  void* cub_tmp = nullptr;
+  size_t cub_bytes = 0;
+  // optional per-launch timing of the dominant kernel (k_eval)
+  bool timing = false;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  int64_t eval_launches = 0;
+  int64_t eval_items = 0;
+  double eval_ms = 0.0;
+};
+
+namespace {
+
+template <typename T>
+int dalloc(T** p, int64_t count) {
+  if (count < 1) count = 1;
+  cudaError_t e = cudaMalloc((void**)p, sizeof(T) * (size_t)count);
+  if (e != cudaSuccess) return set_error(LRCVT_E_NOMEM, "cudaMalloc", e);
+  return 0;
+}
+
+int note_eval(lrcvt_plan* p, int64_t items) {
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, p->ev0, p->ev1));
+  p->eval_ms += ms;
+  p->eval_launches++;
+  p->eval_items += items;
+  return 0;
+}
+
+int sync_counters(lrcvt_plan* p, cudaStream_t st, int n = C_NCOUNTERS) {
+  CK(cudaMemcpyAsync(p->h_counters, p->counters, sizeof(int) * n, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return 0;
+}
+
+// eligible list for the current site set (tessellation.py:161-164)
+int prepare_eligible(lrcvt_plan* p, int n_sites, const int* site_comp, cudaStream_t st) {
+  CK(cudaMemsetAsync(p->has_site, 0, p->n_components > 0 ? p->n_components : 1, st));
+  if (n_sites > 0) {
+    k_mark_site_comps<<<grid_for(n_sites, 256), 256, 0, st>>>(site_comp, n_sites, p->has_site);
+    CKL("k_mark_site_comps"); LAUNCHED(1);
+  }
+  EligiblePred pred{p->comp, p->has_site};
+  cub::CountingInputIterator<int> it(0);
+  size_t bytes = p->cub_bytes;
+  CK(cub::DeviceSelect::If(p->cub_tmp, bytes, it, p->eligible, p->counters + C_ASSIGNED,
+                           (int)p->g.n, pred, st));
+  CKR(sync_counters(p, st));
+  p->n_eligible = p->h_counters[C_ASSIGNED];
+  return 0;
+}
+
+// one relaxation round loop (_kernels.py:337-385). list_in holds n items.
+int run_phase(lrcvt_plan* p, bool phase2, int** cur, int** nxt, int n, int2* ss, double* dist,
+              lrcvt_classify_stats* st_out, cudaStream_t st) {
+  const Geo& g = p->g;
+  while (n > 0) {
+    st_out->rounds++;
+    st_out->evaluations += n;
+    CK(cudaMemsetAsync(p->counters, 0, sizeof(int) * 2, st));
+    const int blocks = grid_for(n, 128);
+    if (p->timing) CK(cudaEventRecord(p->ev0, st));
+    if (phase2) {
+      if (g.dyadic)
+        k_eval<true, true><<<blocks, 128, 0, st>>>(*cur, n, g, p->comp, ss, dist, p->site_pos, p->bm, p->imp, p->counters);
+      else
+        k_eval<true, false><<<blocks, 128, 0, st>>>(*cur, n, g, p->comp, ss, dist, p->site_pos, p->bm, p->imp, p->counters);
+    } else {
+      k_eval<false, true><<<blocks, 128, 0, st>>>(*cur, n, g, p->comp, ss, dist, p->site_pos, p->bm, p->imp, p->counters);
+    }
+    CKL("k_eval");
+    if (p->timing) CK(cudaEventRecord(p->ev1, st));
+    k_commit<<<blocks, 128, 0, st>>>(p->imp, p->counters, g, p->comp, ss, dist, p->bm, *nxt);
+    CKL("k_commit");
+    LAUNCHED(2);
+    CKR(sync_counters(p, st, 2));
+    if (p->timing) CKR(note_eval(p, n));
+    st_out->commits += p->h_counters[C_NIMP];
+    n = p->h_counters[C_NNEXT];
+    int* t = *cur; *cur = *nxt; *nxt = t;
+  }
+  return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+int lrcvt_version(void) { return 1; }
+
+const char* lrcvt_last_error(void) { return g_last_error.c_str(); }
+
+int lrcvt_plan_create(lrcvt_plan** plan, int64_t nx, int64_t ny, int64_t nz, double sx, double sy,
+                      double sz, const int32_t* d_comp, int32_t n_components, int64_t max_sites,
+                      void* stream) {
+  if (!plan || !d_comp || !geo_ok(nx, ny, nz, sx, sy, sz) || n_components < 0 || max_sites < 0)
+    return set_error(LRCVT_E_ARG, "lrcvt_plan_create: bad arguments");
+  cudaStream_t st = (cudaStream_t)stream;
+  lrcvt_plan* p = new lrcvt_plan();
+  p->g = make_geo(nx, ny, nz, sx, sy, sz);
+  p->comp = d_comp;
+  p->n_components = n_components;
+  p->max_sites = max_sites;
+  const int64_t n = p->g.n;
+  int rc = 0;
+  rc |= dalloc(&p->counters, C_NCOUNTERS);
+  if (cudaMallocHost((void**)&p->h_counters, sizeof(int) * C_NCOUNTERS) != cudaSuccess) rc = LRCVT_E_NOMEM;
+  if (rc) { lrcvt_plan_destroy(p); return set_error(LRCVT_E_NOMEM, "plan counters"); }
+  // count in-band voxels
+  {
+    CountInband op{d_comp};
+    cub::CountingInputIterator<int> it(0);
+    cub::TransformInputIterator<int, CountInband, cub::CountingInputIterator<int>> tin(it, op);
+    size_t bytes = 0;
+    CK(cub::DeviceReduce::Sum(nullptr, bytes, tin, p->counters, (int)n, st));
+    void* tmp = nullptr;
+    CK(cudaMallocAsync(&tmp, bytes, st));
+    CK(cub::DeviceReduce::Sum(tmp, bytes, tin, p->counters, (int)n, st));
+    CK(cudaFreeAsync(tmp, st));
+    if (sync_counters(p, st, 1)) { lrcvt_plan_destroy(p); return LRCVT_E_CUDA; }
+    p->n_inband = p->h_counters[0];
+  }
+  const int64_t nin = p->n_inband > 0 ? p->n_inband : 1;
+  const int64_t S = max_sites > 0 ? max_sites : 1;
+  p->bm_words = (n + 31) / 32;
+  rc = 0;
+  rc |= dalloc(&p->list_a, nin);
+  rc |= dalloc(&p->list_b, nin);
+  rc |= dalloc(&p->eligible, nin);
+  rc |= dalloc(&p->imp, nin);
+  rc |= dalloc(&p->bm, p->bm_words);
+  rc |= dalloc(&p->has_site, n_components > 0 ? n_components : 1);
+  rc |= dalloc(&p->site_pos, S);
+  rc |= dalloc(&p->new_pos, S);
+  rc |= dalloc(&p->sk_key, S);
+  rc |= dalloc(&p->sk_key2, S);
+  rc |= dalloc(&p->sk_val, S);
+  rc |= dalloc(&p->sk_val2, S);
+  rc |= dalloc(&p->sk_d, S);
+  rc |= dalloc(&p->acc, 4 * S);
+  rc |= dalloc(&p->sums, 4 * S);
+  rc |= dalloc(&p->seg_b, S);
+  rc |= dalloc(&p->seg_e, S);
+  if (rc) { lrcvt_plan_destroy(p); return LRCVT_E_NOMEM; }
+  if (cudaMemsetAsync(p->bm, 0, sizeof(uint32_t) * p->bm_words, st) != cudaSuccess) {
+    lrcvt_plan_destroy(p);
+    return set_error(LRCVT_E_CUDA, "bitmap clear");
+  }
+  // cub temp storage: max over the uses
+  size_t need = 0, b = 0;
+  {
+    EligiblePred pred{p->comp, p->has_site};
+    cub::CountingInputIterator<int> it(0);
+    cub::DeviceSelect::If(nullptr, b, it, p->eligible, p->counters, (int)n, pred, st);
+    need = b > need ? b : need;
+    b = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, b, p->sk_key, p->sk_key2, p->sk_val, p->sk_val2, (int)S, 0, 32, st);
+    need = b > need ? b : need;
+    b = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, b, p->list_a, p->list_b, p->list_a, p->list_b, (int)nin, 0, 32, st);
+    need = b > need ? b : need;
+  }
+  p->cub_bytes = need;
+  if (dalloc((char**)&p->cub_tmp, (int64_t)need)) { lrcvt_plan_destroy(p); return LRCVT_E_NOMEM; }
+  *plan = p;
+  return 0;
+}
+
+int lrcvt_plan_destroy(lrcvt_plan* p) {
+  if (!p) return 0;
+  void* bufs[] = {p->counters, p->list_a, p->list_b, p->eligible, p->imp, p->bm, p->has_site,
+                  p->site_pos, p->new_pos, p->sk_key, p->sk_key2, p->sk_val, p->sk_val2, p->sk_d,
+                  p->acc, p->sums, p->vt_key, p->vt_key2, p->vt_idx, p->vt_idx2, p->vt_terms,
+                  p->seg_b, p->seg_e, p->cub_tmp};
+  for (void* b : bufs)
+    if (b) cudaFree(b);
+  if (p->h_counters) cudaFreeHost(p->h_counters);
+  if (p->ev0) cudaEventDestroy(p->ev0);
+  if (p->ev1) cudaEventDestroy(p->ev1);
+  delete p;
+  return 0;
+}
+
+int64_t lrcvt_plan_inband(const lrcvt_plan* p) { return p ? p->n_inband : -1; }
+
+int lrcvt_plan_set_timing(lrcvt_plan* p, int enable) {
+  if (!p) return set_error(LRCVT_E_ARG, "lrcvt_plan_set_timing");
+  if (enable && !p->ev0) {
+    CK(cudaEventCreate(&p->ev0));
+    CK(cudaEventCreate(&p->ev1));
+  }
+  p->timing = enable != 0;
+  p->eval_launches = 0;
+  p->eval_items = 0;
+  p->eval_ms = 0.0;
+  return 0;
+}
+
+int lrcvt_plan_timing(const lrcvt_plan* p, int64_t* launches, int64_t* items, double* ms) {
+  if (!p || !launches || !items || !ms) return set_error(LRCVT_E_ARG, "lrcvt_plan_timing");
+  *launches = p->eval_launches;
+  *items = p->eval_items;
+  *ms = p->eval_ms;
+  return 0;
+}
+
+unsigned long long lrcvt_launch_count(void) { return g_launches; }
+
+int lrcvt_classify(lrcvt_plan* p, int64_t n_sites, const double* d_site_pos,
+                   const int32_t* d_site_comp, int32_t* d_site_src, double* d_dist,
+                   uint8_t* d_state, lrcvt_classify_stats* stats, void* stream) {
+  if (!p || n_sites < 0 || n_sites > p->max_sites || !d_site_src || !d_dist || !stats)
+    return set_error(LRCVT_E_ARG, "lrcvt_classify: bad arguments");
+  if (n_sites > 0 && (!d_site_pos || !d_site_comp))
+    return set_error(LRCVT_E_ARG, "lrcvt_classify: null site arrays");
+  cudaStream_t st = (cudaStream_t)stream;
+  const Geo& g = p->g;
+  const int S = (int)n_sites;
+  int2* ss = reinterpret_cast<int2*>(d_site_src);
+  memset(stats, 0, sizeof *stats);
+  // tessellation.py:120-122
+  k_fill_state<<<grid_for(g.n, 256, 148 * 32), 256, 0, st>>>(ss, d_dist, g.n);
+  CKL("k_fill_state"); LAUNCHED(1);
+  CK(cudaMemsetAsync(p->counters, 0, sizeof(int) * C_NCOUNTERS, st));
+  if (S == 0) {  // tessellation.py:126-134
+    if (d_state) CK(cudaMemsetAsync(d_state, 0, (size_t)g.n, st));
+    CK(cudaStreamSynchronize(st));
+    return 0;
+  }
+  k_pack_sites<<<grid_for(S, 256), 256, 0, st>>>(d_site_pos, S, p->site_pos);
+  CKL("k_pack_sites"); LAUNCHED(1);
+  // _place_seeds (tessellation.py:136-140)
+  k_site_voxel<<<grid_for(S, 256), 256, 0, st>>>(g, p->comp, p->site_pos, d_site_comp, S, p->sk_key,
+                                                 p->sk_val, p->sk_d, p->counters);
+  CKL("k_site_voxel"); LAUNCHED(1);
+  CKR(sync_counters(p, st, C_BAD + 1));
+  if (p->h_counters[C_BAD]) {
+    stats->bad_sites = p->h_counters[C_BAD];
+    return p->h_counters[C_BAD];
+  }
+  {
+    size_t bytes = p->cub_bytes;
+    CK(cub::DeviceRadixSort::SortPairs(p->cub_tmp, bytes, p->sk_key, p->sk_key2, p->sk_val,
+                                       p->sk_val2, S, 0, 32, st));
+  }
+  // groups -> seeds, then the phase-1 worklist (tessellation.py:151)
+  CK(cudaMemsetAsync(p->counters, 0, sizeof(int) * 2, st));
+  k_seed_groups<<<grid_for(S, 128), 128, 0, st>>>(g, p->comp, p->sk_key2, p->sk_val2, p->sk_d, S, ss,
+                                                  d_dist, p->bm, p->list_a, p->counters);
+  CKL("k_seed_groups"); LAUNCHED(1);
+  CKR(sync_counters(p, st, 2));
+  int n_wl = p->h_counters[C_NNEXT];
+  int* cur = p->list_a;
+  int* nxt = p->list_b;
+  // phase 1 (tessellation.py:152-156)
+  if (run_phase(p, false, &cur, &nxt, n_wl, ss, d_dist, stats, st)) return LRCVT_E_CUDA;
+  stats->phase1_rounds = stats->rounds;
+  // phase 2 (tessellation.py:161-189)
+  if (prepare_eligible(p, S, d_site_comp, st)) return LRCVT_E_CUDA;
+  stats->eligible = p->n_eligible;
+  const int n_el = (int)p->n_eligible;
+  CK(cudaMemcpyAsync(cur, p->eligible, sizeof(int) * n_el, cudaMemcpyDeviceToDevice, st));
+  n_wl = n_el;
+  for (;;) {
+    if (run_phase(p, true, &cur, &nxt, n_wl, ss, d_dist, stats, st)) return LRCVT_E_CUDA;
+    stats->sweeps++;
+    stats->evaluations += n_el;
+    CK(cudaMemsetAsync(p->counters, 0, sizeof(int) * 2, st));
+    const int blocks = grid_for(n_el, 128);
+    if (p->timing) CK(cudaEventRecord(p->ev0, st));
+    if (g.dyadic)
+      k_eval<true, true><<<blocks, 128, 0, st>>>(p->eligible, n_el, g, p->comp, ss, d_dist, p->site_pos, p->bm, p->imp, p->counters);
+    else
+      k_eval<true, false><<<blocks, 128, 0, st>>>(p->eligible, n_el, g, p->comp, ss, d_dist, p->site_pos, p->bm, p->imp, p->counters);
+    CKL("k_eval sweep");
+    if (p->timing) CK(cudaEventRecord(p->ev1, st));
+    k_commit<<<blocks, 128, 0, st>>>(p->imp, p->counters, g, p->comp, ss, d_dist, p->bm, cur);
+    CKL("k_commit sweep");
+    LAUNCHED(2);
+    CKR(sync_counters(p, st, 2));
+    if (p->timing) CKR(note_eval(p, n_el));
+    if (p->h_counters[C_NIMP] == 0) break;
+    stats->commits += p->h_counters[C_NIMP];
+    n_wl = p->h_counters[C_NNEXT];
+  }
+  // state bits + assigned (tessellation.py:191-204)
+  CK(cudaMemsetAsync(p->counters + C_ASSIGNED, 0, sizeof(int), st));
+  k_state<<<grid_for(g.n, 256, 148 * 16), 256, 0, st>>>(ss, g.n, d_state, p->counters);
+  CKL("k_state"); LAUNCHED(1);
+  CKR(sync_counters(p, st, C_ASSIGNED + 1));
+  stats->assigned = p->h_counters[C_ASSIGNED];
+  return 0;
+}
+
+int lrcvt_centroidal_update(lrcvt_plan* p, int64_t n_sites, const double* d_site_pos,
+                            const int32_t* d_site_comp, const int32_t* d_site_src,
+                            int32_t weight_mode, const void* d_weights, double backoff,
+                            double* d_new_pos, double* d_disp, double* d_sums,
+                            int64_t* empty_regions, void* stream) {
+  if (!p || n_sites < 0 || n_sites > p->max_sites || !d_site_src || !d_new_pos || !d_disp ||
+      weight_mode < 0 || weight_mode > 3 || (weight_mode != LRCVT_W_ONES && !d_weights))
+    return set_error(LRCVT_E_ARG, "lrcvt_centroidal_update: bad arguments");
+  cudaStream_t st = (cudaStream_t)stream;
+  const Geo& g = p->g;
+  const int S = (int)n_sites;
+  const int2* ss = reinterpret_cast<const int2*>(d_site_src);
+  if (empty_regions) *empty_regions = 0;
+  if (S == 0) return 0;
+  k_pack_sites<<<grid_for(S, 256), 256, 0, st>>>(d_site_pos, S, p->site_pos);
+  CKL("k_pack_sites"); LAUNCHED(1);
+  if (prepare_eligible(p, S, d_site_comp, st)) return LRCVT_E_CUDA;
+  const int n_el = (int)p->n_eligible;
+  const bool exact = weight_mode == LRCVT_W_ONES && g.dyadic && g.nx <= (1 << 20) &&
+                     g.ny <= (1 << 20) && g.nz <= (1 << 20);
+  if (exact) {
+    CK(cudaMemsetAsync(p->acc, 0, sizeof(unsigned long long) * 4 * S, st));
+    if (n_el > 0) {
+      k_vote_exact<<<grid_for(n_el, 256, 148 * 8), 256, 0, st>>>(p->eligible, n_el, g, ss, p->acc, S);
+      CKL("k_vote_exact"); LAUNCHED(1);
+    }
+    k_vote_exact_finish<<<grid_for(S, 256), 256, 0, st>>>(p->acc, S, 0.5 * g.sx, 0.5 * g.sy, 0.5 * g.sz,
+                                                          p->sums);
+    CKL("k_vote_exact_finish"); LAUNCHED(1);
+  } else {
+    const int64_t nin = p->n_inband > 0 ? p->n_inband : 1;
+    int rc = 0;
+    if (!p->vt_key) {
+      rc |= dalloc(&p->vt_key, nin);
+      rc |= dalloc(&p->vt_key2, nin);
+      rc |= dalloc(&p->vt_idx, nin);
+      rc |= dalloc(&p->vt_idx2, nin);
+      rc |= dalloc(&p->vt_terms, nin);
+      if (rc) return LRCVT_E_NOMEM;
+    }
+    CK(cudaMemsetAsync(p->seg_b, 0, sizeof(int) * S, st));
+    CK(cudaMemsetAsync(p->seg_e, 0, sizeof(int) * S, st));
+    if (n_el > 0) {
+      k_vote_terms<<<grid_for(n_el, 256, 148 * 8), 256, 0, st>>>(
+          p->eligible, n_el, g, ss, (const double*)d_weights, (const float*)d_weights, weight_mode, S,
+          p->vt_key, p->vt_idx, p->vt_terms);
+      CKL("k_vote_terms"); LAUNCHED(1);
+      int bits = 1;
+      while ((1ll << bits) <= S) bits++;
+      size_t bytes = p->cub_bytes;
+      CK(cub::DeviceRadixSort::SortPairs(p->cub_tmp, bytes, p->vt_key, p->vt_key2, p->vt_idx, p->vt_idx2,
+                                         n_el, 0, bits, st));
+      k_segments<<<grid_for(n_el, 256, 148 * 8), 256, 0, st>>>(p->vt_key2, n_el, S, p->seg_b, p->seg_e);
+      CKL("k_segments"); LAUNCHED(1);
+    }
+    k_vote_serial<<<grid_for(S, 128), 128, 0, st>>>(p->vt_idx2, p->vt_terms, p->seg_b, p->seg_e, S, p->sums);
+    CKL("k_vote_serial"); LAUNCHED(1);
+  }
+  CK(cudaMemsetAsync(p->counters + C_BAD, 0, sizeof(int), st));
+  k_move_sites<<<grid_for(S, 128), 128, 0, st>>>(g, p->comp, p->site_pos, d_site_comp, p->sums, S, backoff,
+                                                 p->new_pos, d_disp, p->counters + C_BAD);
+  CKL("k_move_sites"); LAUNCHED(1);
+  k_unpack_sites<<<grid_for(S, 256), 256, 0, st>>>(p->new_pos, S, d_new_pos);
+  CKL("k_unpack_sites"); LAUNCHED(1);
+  if (d_sums) CK(cudaMemcpyAsync(d_sums, p->sums, sizeof(double) * 4 * S, cudaMemcpyDeviceToDevice, st));
+  CKR(sync_counters(p, st, C_BAD + 1));
+  if (empty_regions) *empty_regions = p->h_counters[C_BAD];
+  return 0;
+}
+
+int lrcvt_unpack_site_src(const int32_t* d_site_src, int64_t n, int32_t* d_site_of, int32_t* d_src,
+                          void* stream) {
+  if (!d_site_src || !d_site_of || !d_src || n < 0) return set_error(LRCVT_E_ARG, "lrcvt_unpack_site_src");
+  if (n == 0) return 0;
+  k_unpack_ss<<<grid_for(n, 256, 148 * 16), 256, 0, (cudaStream_t)stream>>>(
+      reinterpret_cast<const int2*>(d_site_src), n, d_site_of, d_src);
+  CKL("k_unpack_ss"); LAUNCHED(1);
+  return 0;
+}
+
+int lrcvt_segment_hit_t(int64_t nx, int64_t ny, int64_t nz, double sx, double sy, double sz,
+                        const int32_t* d_comp, const double* d_segs, const int32_t* d_want, int64_t n,
+                        double* d_t, void* stream) {
+  if (!geo_ok(nx, ny, nz, sx, sy, sz) || !d_comp || n < 0 || (n > 0 && (!d_segs || !d_want || !d_t)))
+    return set_error(LRCVT_E_ARG, "lrcvt_segment_hit_t: bad arguments");
+  if (n == 0) return 0;
+  Geo g = make_geo(nx, ny, nz, sx, sy, sz);
+  k_segment_batch<<<grid_for(n, 128), 128, 0, (cudaStream_t)stream>>>(g, d_comp, d_segs, d_want, n, d_t);
+  CKL("k_segment_batch"); LAUNCHED(1);
+  return 0;
+}
+
+
+int lrcvt_isobands(int64_t n, const float* d_field, const double* d_iso, int32_t n_iso, int32_t* d_layer,
+                   void* stream) {
+  if (n < 0 || !d_field || !d_iso || !d_layer || n_iso < 2 || n_iso > 64)
+    return set_error(LRCVT_E_ARG, "lrcvt_isobands: bad arguments");
+  if (n == 0) return 0;
+  if ((((uintptr_t)d_field) | ((uintptr_t)d_layer)) & 15)
+    return set_error(LRCVT_E_ARG, "lrcvt_isobands: arrays must be 16-byte aligned");
+  k_isobands<<<grid_for(n / 4 + 1, 256, 148 * 16), 256, 0, (cudaStream_t)stream>>>(d_field, n, d_iso, n_iso,
+                                                                                    d_layer);
+  CKL("k_isobands"); LAUNCHED(1);
+  return 0;
+}
+
+int lrcvt_label_components(int64_t nx, int64_t ny, int64_t nz, const int32_t* d_layer, int32_t n_layers,
+                           int32_t* d_component, int32_t* n_components, void* stream) {
+  if (!geo_ok(nx, ny, nz, 1, 1, 1) || !d_layer || !d_component || !n_components || n_layers < 0)
+    return set_error(LRCVT_E_ARG, "lrcvt_label_components: bad arguments");
+  cudaStream_t st = (cudaStream_t)stream;
+  Geo g = make_geo(nx, ny, nz, 1, 1, 1);
+  const int64_t n = g.n;
+  int *L = nullptr, *roots = nullptr, *roots2 = nullptr, *keys = nullptr, *keys2 = nullptr, *cnt = nullptr;
+  void* tmp = nullptr;
+  int h_cnt = 0;
+  int rc = 0;
+  size_t b1 = 0, b2 = 0;
+  IsRoot pred{nullptr};
+  cub::CountingInputIterator<int> it(0);
+  CK(cudaMallocAsync((void**)&L, sizeof(int) * n, st));
+  CK(cudaMallocAsync((void**)&cnt, sizeof(int), st));
+  k_ccl_init<<<grid_for(n, 256, 148 * 16), 256, 0, st>>>(d_layer, n, n_layers, L);
+  CKL("k_ccl_init"); LAUNCHED(1);
+  k_ccl_merge<<<grid_for(n, 256, 148 * 16), 256, 0, st>>>(g, d_layer, n_layers, L);
+  CKL("k_ccl_merge"); LAUNCHED(1);
+  k_ccl_compress<<<grid_for(n, 256, 148 * 16), 256, 0, st>>>(n, L);
+  CKL("k_ccl_compress"); LAUNCHED(1);
+  pred.L = L;
+  CK(cub::DeviceSelect::If(nullptr, b1, it, (int*)nullptr, cnt, (int)n, pred, st));
+  CK(cudaMallocAsync((void**)&roots, sizeof(int) * n, st));
+  CK(cudaMallocAsync(&tmp, b1, st));
+  CK(cub::DeviceSelect::If(tmp, b1, it, roots, cnt, (int)n, pred, st));
+  CK(cudaMemcpyAsync(&h_cnt, cnt, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (h_cnt > 0) {
+    CK(cudaMallocAsync((void**)&roots2, sizeof(int) * h_cnt, st));
+    CK(cudaMallocAsync((void**)&keys, sizeof(int) * h_cnt, st));
+    CK(cudaMallocAsync((void**)&keys2, sizeof(int) * h_cnt, st));
+    k_ccl_root_keys<<<grid_for(h_cnt, 256), 256, 0, st>>>(roots, h_cnt, d_layer, keys);
+    CKL("k_ccl_root_keys"); LAUNCHED(1);
+    int bits = 1;
+    while ((1ll << bits) <= n_layers) bits++;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, b2, keys, keys2, roots, roots2, h_cnt, 0, bits, st));
+    CK(cudaFreeAsync(tmp, st));
+    CK(cudaMallocAsync(&tmp, b2, st));
+    CK(cub::DeviceRadixSort::SortPairs(tmp, b2, keys, keys2, roots, roots2, h_cnt, 0, bits, st));
+    k_ccl_root_ids<<<grid_for(h_cnt, 256), 256, 0, st>>>(roots2, h_cnt, d_component);
+    CKL("k_ccl_root_ids"); LAUNCHED(1);
+  }
+  k_ccl_relabel<<<grid_for(n, 256, 148 * 16), 256, 0, st>>>(L, n, d_component);
+  CKL("k_ccl_relabel"); LAUNCHED(1);
+  CK(cudaFreeAsync(L, st));
+  CK(cudaFreeAsync(cnt, st));
+  CK(cudaFreeAsync(roots, st));
+  CK(cudaFreeAsync(tmp, st));
+  if (roots2) CK(cudaFreeAsync(roots2, st));
+  if (keys) CK(cudaFreeAsync(keys, st));
+  if (keys2) CK(cudaFreeAsync(keys2, st));
+  CK(cudaStreamSynchronize(st));
+  *n_components = h_cnt;
+  return rc;
+}
+
+int lrcvt_component_table(int64_t nx, int64_t ny, int64_t nz, const int32_t* d_component,
+                          const int32_t* d_layer, int32_t n_components, uint64_t* d_count, int32_t* d_bbox,
+                          int32_t* d_layer_of, void* stream) {
+  if (!geo_ok(nx, ny, nz, 1, 1, 1) || !d_component || !d_layer || n_components < 0 ||
+      (n_components > 0 && (!d_count || !d_bbox || !d_layer_of)))
+    return set_error(LRCVT_E_ARG, "lrcvt_component_table: bad arguments");
+  if (n_components == 0) return 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  Geo g = make_geo(nx, ny, nz, 1, 1, 1);
+  k_ccl_table_init<<<grid_for(n_components, 256), 256, 0, st>>>(n_components, (unsigned long long*)d_count,
+                                                                d_bbox);
+  CKL("k_ccl_table_init"); LAUNCHED(1);
+  k_ccl_table<<<grid_for(g.n, 256, 148 * 16), 256, 0, st>>>(g, d_component, d_layer,
+                                                            (unsigned long long*)d_count, d_bbox, d_layer_of);
+  CKL("k_ccl_table"); LAUNCHED(1);
+  return 0;
+}
+
+}  // extern "C"

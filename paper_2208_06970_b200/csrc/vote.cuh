@@ -1,0 +1,186 @@
+// vote.cuh -- phi-propagated weighted-centroid vote and clamped site move
+// (centroidal_update, tessellation.py:211-248).
+//
+// phi(v), the first line-of-sight ancestor (_kernels.py:457-486), is found
+// by chasing src inside the vote kernels (chains are short: depth <= ~13).
+//
+// Two ways to form the per-site sums of _kernels.py:513-532, both bit-exact
+// with the reference's increasing-voxel-order fp64 accumulation:
+//   * EXACT path (unit weights, power-of-two spacing): every term is a
+//     multiple of s/2 and every partial sum is exactly representable, so
+//     the sequential fp64 sum equals the exact integer sum. Kernels reduce
+//     (2x+1) integers with warp match/reduce + 64-bit integer atomics and
+//     scale once: order-independent AND identical to the reference.
+//   * ORDERED path (any f64 weights): terms RN(w*a) are formed in parallel,
+//     a stable radix sort groups them by site in voxel order, and one thread
+//     per site adds them in exactly the reference order.
+#pragma once
+#include "common.cuh"
+
+namespace lrcvt {
+
+// first LOS ancestor: follow src until src[u] == u (_kernels.py:473-481)
+__device__ __forceinline__ int phi_chase(const int2* __restrict__ ss, int v, int2 a) {
+  int u = v;
+  while (a.y != u && a.y >= 0) {
+    u = a.y;
+    a = ss[u];
+  }
+  return u;
+}
+
+// EXACT path. acc layout: [4][S] u64 = count, sum(2x+1), sum(2y+1), sum(2z+1).
+__global__ void __launch_bounds__(256) k_vote_exact(const int* __restrict__ list, int n, Geo g,
+                                                    const int2* __restrict__ ss,
+                                                    unsigned long long* __restrict__ acc,
+                                                    int n_sites) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x; i0 < n; i0 += stride) {
+    const int64_t i = i0 + threadIdx.x;
+    int s = -1;
+    unsigned cx = 0, cy = 0, cz = 0;
+    if (i < n) {
+      const int v = list[i];
+      const int2 a = ss[v];
+      s = a.x;
+      if (s >= 0) {
+        const int u = phi_chase(ss, v, a);
+        int x, y, z;
+        coords(g, u, x, y, z);
+        cx = 2u * x + 1u; cy = 2u * y + 1u; cz = 2u * z + 1u;
+      }
+    }
+    const unsigned grp = __match_any_sync(0xffffffffu, s);
+    const unsigned one = s >= 0 ? 1u : 0u;
+    const unsigned c0 = __reduce_add_sync(grp, one);
+    const unsigned c1 = __reduce_add_sync(grp, cx);
+    const unsigned c2 = __reduce_add_sync(grp, cy);
+    const unsigned c3 = __reduce_add_sync(grp, cz);
+    const int lane = threadIdx.x & 31;
+    if (s >= 0 && lane == __ffs(grp) - 1) {
+      atomicAdd(acc + s, (unsigned long long)c0);
+      atomicAdd(acc + n_sites + s, (unsigned long long)c1);
+      atomicAdd(acc + 2 * n_sites + s, (unsigned long long)c2);
+      atomicAdd(acc + 3 * n_sites + s, (unsigned long long)c3);
+    }
+  }
+}
+
+__global__ void k_vote_exact_finish(const unsigned long long* __restrict__ acc, int n_sites,
+                                    double hx, double hy, double hz,
+                                    double* __restrict__ sums) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n_sites) return;
+  sums[s] = (double)acc[s];
+  sums[n_sites + s] = __dmul_rn((double)acc[n_sites + s], hx);
+  sums[2 * n_sites + s] = __dmul_rn((double)acc[2 * n_sites + s], hy);
+  sums[3 * n_sites + s] = __dmul_rn((double)acc[3 * n_sites + s], hz);
+}
+
+// ORDERED path, step 1: per eligible voxel (list sorted by voxel), the key
+// (site, or n_sites for unassigned) and the four products w, RN(w*ax), ...
+__global__ void __launch_bounds__(256) k_vote_terms(const int* __restrict__ list, int n, Geo g,
+                                                    const int2* __restrict__ ss,
+                                                    const double* __restrict__ w64,
+                                                    const float* __restrict__ w32, int w_mode,
+                                                    int n_sites, int* __restrict__ key,
+                                                    int* __restrict__ idx,
+                                                    double4* __restrict__ terms) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+    const int v = list[i];
+    const int2 a = ss[v];
+    idx[i] = (int)i;
+    if (a.x < 0) { key[i] = n_sites; continue; }
+    key[i] = a.x;
+    const int u = phi_chase(ss, v, a);
+    int x, y, z;
+    coords(g, u, x, y, z);
+    double w;
+    if (w_mode == 0) w = 1.0;
+    else if (w_mode == 1) w = w64[v];
+    else if (w_mode == 2) w = (double)w32[v];                            // m**1.0
+    else { const double m = (double)w32[v]; w = __dmul_rn(m, m); }     // m**2.0
+    terms[i] = make_double4(w, __dmul_rn(w, centre1(x, g.sx)), __dmul_rn(w, centre1(y, g.sy)),
+                            __dmul_rn(w, centre1(z, g.sz)));
+  }
+}
+
+// step 2 (after the stable sort by key): segment starts/ends per site.
+__global__ void k_segments(const int* __restrict__ skey, int n, int n_sites,
+                           int* __restrict__ seg_begin, int* __restrict__ seg_end) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+    const int k = skey[i];
+    if (k >= n_sites) continue;
+    if (i == 0 || skey[i - 1] != k) seg_begin[k] = (int)i;
+    if (i == n - 1 || skey[i + 1] != k) seg_end[k] = (int)i + 1;
+  }
+}
+
+// step 3: one thread per site adds its terms in increasing voxel order.
+__global__ void __launch_bounds__(128) k_vote_serial(const int* __restrict__ sidx,
+                                                     const double4* __restrict__ terms,
+                                                     const int* __restrict__ seg_begin,
+                                                     const int* __restrict__ seg_end,
+                                                     int n_sites, double* __restrict__ sums) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n_sites) return;
+  double w = 0.0, tx = 0.0, ty = 0.0, tz = 0.0;
+  const int b = seg_begin[s], e = seg_end[s];
+  int j = b;
+  // 4-deep software prefetch keeps several gathers in flight per thread
+  for (; j + 4 <= e; j += 4) {
+    double4 t[4];
+#pragma unroll
+    for (int q = 0; q < 4; q++) t[q] = terms[sidx[j + q]];
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+      w = __dadd_rn(w, t[q].x); tx = __dadd_rn(tx, t[q].y);
+      ty = __dadd_rn(ty, t[q].z); tz = __dadd_rn(tz, t[q].w);
+    }
+  }
+  for (; j < e; j++) {
+    const double4 t = terms[sidx[j]];
+    w = __dadd_rn(w, t.x); tx = __dadd_rn(tx, t.y); ty = __dadd_rn(ty, t.z); tz = __dadd_rn(tz, t.w);
+  }
+  sums[s] = w; sums[n_sites + s] = tx; sums[2 * n_sites + s] = ty; sums[3 * n_sites + s] = tz;
+}
+
+// _kernels.py:535-582, one thread per site. counters[0] += empty regions.
+__global__ void k_move_sites(Geo g, const int* __restrict__ comp, const double4* __restrict__ site_pos,
+                             const int* __restrict__ site_comp, const double* __restrict__ sums,
+                             int n_sites, double backoff, double4* __restrict__ new_pos,
+                             double* __restrict__ disp, int* __restrict__ empty_count) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n_sites) return;
+  const double4 a = site_pos[s];
+  new_pos[s] = a;
+  disp[s] = 0.0;
+  const double wsum = sums[s];
+  if (wsum <= 0.0) { atomicAdd(empty_count, 1); return; }
+  const double bx = __ddiv_rn(sums[n_sites + s], wsum);
+  const double by = __ddiv_rn(sums[2 * n_sites + s], wsum);
+  const double bz = __ddiv_rn(sums[3 * n_sites + s], wsum);
+  const double seg = dist3(a.x, a.y, a.z, bx, by, bz);
+  if (seg == 0.0) return;
+  const int want = site_comp[s];
+  const double thit = segment_hit_t(comp, g, a.x, a.y, a.z, bx, by, bz, want);
+  double px, py, pz;
+  if (thit >= 1.0) {
+    px = bx; py = by; pz = bz;
+  } else {
+    const double travel = __dsub_rn(__dmul_rn(thit, seg), backoff);
+    if (travel <= 0.0) return;
+    const double f = __ddiv_rn(travel, seg);
+    px = __dadd_rn(a.x, __dmul_rn(__dsub_rn(bx, a.x), f));
+    py = __dadd_rn(a.y, __dmul_rn(__dsub_rn(by, a.y), f));
+    pz = __dadd_rn(a.z, __dmul_rn(__dsub_rn(bz, a.z), f));
+  }
+  const int cx = cell_of(px, g.sx, g.nx), cy = cell_of(py, g.sy, g.ny), cz = cell_of(pz, g.sz, g.nz);
+  if (__ldg(comp + cx + g.nx * (cy + g.ny * cz)) != want) return;
+  new_pos[s] = make_double4(px, py, pz, 0.0);
+  disp[s] = dist3(a.x, a.y, a.z, px, py, pz);
+}
+
+}  // namespace lrcvt
