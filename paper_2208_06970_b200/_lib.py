@@ -77,7 +77,8 @@ SIGNATURES = {
     ),
     "lrcvt_component_table": (
         c_int,
-        [c_int64, c_int64, c_int64, c_void_p, c_void_p, c_int32, c_void_p, c_void_p, c_void_p],
+        [c_int64, c_int64, c_int64, c_void_p, c_void_p, c_int32, c_void_p, c_void_p, c_void_p,
+         c_void_p],
     ),
     "lrcvt_aggregate": (
         c_int,

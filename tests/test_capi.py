@@ -41,6 +41,26 @@ def test_ctypes_signatures_cover_header():
     assert set(declared_symbols()) <= set(_lib.SIGNATURES)
 
 
+def declared_arities():
+    out = {}
+    for h in (ROOT / "include").glob("*.h"):
+        txt = re.sub(r"/\*.*?\*/", "", h.read_text(), flags=re.S)
+        for name, params in re.findall(r"\b(lrcvt_\w+)\s*\(([^)]*)\)\s*;", txt):
+            params = params.strip()
+            out[name] = 0 if params in ("", "void") else params.count(",") + 1
+    return out
+
+
+def test_ctypes_arity_matches_header():
+    """A ctypes argtypes list shorter than the C prototype silently passes the
+    trailing arguments as C int (a truncated stream pointer crashes)."""
+    from paper_2208_06970_b200 import _lib
+
+    for name, arity in declared_arities().items():
+        if name in _lib.SIGNATURES:
+            assert len(_lib.SIGNATURES[name][1]) == arity, name
+
+
 def test_bad_arguments_rejected_without_device():
     """Argument validation happens before any device work."""
     from paper_2208_06970_b200 import _lib
