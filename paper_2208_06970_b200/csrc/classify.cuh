@@ -95,149 +95,213 @@ __global__ void k_eligible(const int* __restrict__ comp, const uint8_t* __restri
 // frontier bitmap; newly set bits are appended to `next`. Reproduces the
 // stamp-deduplicated enqueue of _kernels.py:313-333 (self=false) and
 // _kernels.py:425-454 (self=true). All 32 lanes must call it.
+// Three unrolled stages keep every load/atomic of a stage independent (26
+// requests in flight per thread instead of 26 dependent round trips).
 __device__ __forceinline__ void mark_and_append(const Geo& g, const int* __restrict__ comp,
                                                 bool active, int v, bool self,
                                                 uint32_t* __restrict__ bm,
                                                 int* __restrict__ next, int* counter) {
   unsigned newmask = 0;
-  int x = 0, y = 0, z = 0, cv = 0;
   if (active) {
+    int x, y, z;
     coords(g, v, x, y, z);
-    cv = __ldg(comp + v);
-    if (self) {
-      uint32_t bit = 1u << (v & 31);
-      if (!(__ldcg(bm + (v >> 5)) & bit)) {
-        uint32_t old = atomicOr(bm + (v >> 5), bit);
-        if (!(old & bit)) newmask |= 1u << 26;
-      }
-    }
+    const int cv = __ldg(comp + v);
+    const unsigned inb = inbounds_mask(x, y, z, g.nx, g.ny, g.nz);
+    int cu[26];
 #pragma unroll
     for (int k = 0; k < 26; k++) {
-      int dx, dy, dz;
-      offset_of(k, dx, dy, dz);
-      int ux = x + dx, uy = y + dy, uz = z + dz;
-      if (ux < 0 || uy < 0 || uz < 0 || ux >= g.nx || uy >= g.ny || uz >= g.nz) continue;
-      int u = v + g.off_d[k];
-      if (__ldg(comp + u) != cv) continue;
-      uint32_t bit = 1u << (u & 31);
-      if (__ldcg(bm + (u >> 5)) & bit) continue;
-      uint32_t old = atomicOr(bm + (u >> 5), bit);
-      if (!(old & bit)) newmask |= 1u << k;
+      const int u = v + off_dx(k) + off_dy(k) * g.nx + off_dz(k) * g.nxy;
+      cu[k] = ((inb >> k) & 1u) ? __ldg(comp + u) : -2;
+    }
+    unsigned same = self ? (1u << 26) : 0u;
+#pragma unroll
+    for (int k = 0; k < 26; k++) same |= (cu[k] == cv ? 1u : 0u) << k;
+    uint32_t words[27];
+#pragma unroll
+    for (int k = 0; k < 27; k++) {
+      const int u = k < 26 ? v + off_dx(k) + off_dy(k) * g.nx + off_dz(k) * g.nxy : v;
+      words[k] = ((same >> k) & 1u) ? __ldcg(bm + (u >> 5)) : 0xffffffffu;
+    }
+#pragma unroll
+    for (int k = 0; k < 27; k++) {
+      const int u = k < 26 ? v + off_dx(k) + off_dy(k) * g.nx + off_dz(k) * g.nxy : v;
+      const uint32_t bit = 1u << (u & 31);
+      if (((same >> k) & 1u) && !(words[k] & bit)) {
+        const uint32_t old = atomicOr(bm + (u >> 5), bit);
+        if (!(old & bit)) newmask |= 1u << k;
+      }
     }
   }
-  int cnt = __popc(newmask);
-  int lane = threadIdx.x & 31;
+  const int cnt = __popc(newmask);
+  const int lane = threadIdx.x & 31;
   int incl = cnt;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
-    int t = __shfl_up_sync(0xffffffffu, incl, o);
+    const int t = __shfl_up_sync(0xffffffffu, incl, o);
     if (lane >= o) incl += t;
   }
-  int total = __shfl_sync(0xffffffffu, incl, 31);
+  const int total = __shfl_sync(0xffffffffu, incl, 31);
   int base = 0;
   if (lane == 31 && total) base = atomicAdd(counter, total);
   base = __shfl_sync(0xffffffffu, base, 31);
   int pos = base + incl - cnt;
   if (newmask & (1u << 26)) next[pos++] = v;
-  newmask &= (1u << 26) - 1;
+  newmask &= ALL26;
   while (newmask) {
-    int k = __ffs(newmask) - 1;
+    const int k = __ffs(newmask) - 1;
     newmask &= newmask - 1;
-    next[pos++] = v + g.off_d[k];
+    const char4 o = c_off[k];
+    next[pos++] = nbr_index(v, o, g.nx, g.nxy);
   }
 }
 
 // _kernels.py:147-246 for one voxel. Returns improved; fills the proposal.
+//
+// Written as a resumable per-lane state machine. Each iteration of the
+// outer loop first ADVANCES the lane through its neighbours (reference
+// OFFSETS order, rolled loop over the in-bounds mask, next neighbour's loads
+// software-pipelined) until it either finishes or reaches a candidate that
+// needs a line-of-sight ray; then every lane with a pending ray runs its DDA
+// together. A warp thus pays max(rays per lane) DDA passes instead of the
+// sum that divergent inline rays cost. The decision sequence per voxel is
+// unchanged: a ray is cast exactly when the reference casts it, and its
+// result is applied before the lane looks at the next neighbour.
 template <bool PHASE2, bool DYADIC>
-__device__ __forceinline__ bool eval_voxel(const Geo& g, int v, const int* __restrict__ comp,
+__device__ __forceinline__ bool eval_voxel(const Geo& g, const double* __restrict__ s_len, int v,
+                                           bool active,
+                                           const int* __restrict__ comp,
                                            const int2* __restrict__ ss,
                                            const double* __restrict__ dist,
                                            const double4* __restrict__ site_pos,
                                            Prop& out) {
-  int x, y, z;
-  coords(g, v, x, y, z);
-  const int cv = __ldg(comp + v);
+  int x = 0, y = 0, z = 0;
+  if (active) coords(g, v, x, y, z);
+  const int cv = active ? __ldg(comp + v) : -3;
   const double px = centre1(x, g.sx), py = centre1(y, g.sy), pz = centre1(z, g.sz);
-  const int2 sv = ss[v];
-  double best_d = dist[v];
+  const int2 sv = active ? ss[v] : make_int2(-1, -1);
+  double best_d = active ? dist[v] : 0.0;
   int best_s = sv.x, best_src = sv.y;
   const double orig_d = best_d;
   const int orig_s = best_s;
   int failed_site = -1;
-  int cache_s = -1;  // same-site distance memo (pure function of (v, site))
-  double cache_d = 0.0;
-  int cache_u = -1;  // same-node shortcut memo
-  double cache_ud = 0.0;
+  int cache_s = -1, cache_s2 = -1;  // site -> distance memo (pure in (v, site))
+  double cache_d = 0.0, cache_d2 = 0.0;
+  int cache_u = -1, cache_u2 = -1;  // node -> candidate memo (pure in (v, u) per round)
+  double cache_ud = 0.0, cache_ud2 = 0.0;
   double thr = beat_threshold(best_d);
 
-#pragma unroll
-  for (int k = 0; k < 26; k++) {
-    int dx, dy, dz;
-    offset_of(k, dx, dy, dz);
-    int wx = x + dx, wy = y + dy, wz = z + dz;
-    if (wx < 0 || wy < 0 || wz < 0 || wx >= g.nx || wy >= g.ny || wz >= g.nz) continue;
-    const int w = v + g.off_d[k];
-    if (__ldg(comp + w) != cv) continue;
-    const int2 nw = ss[w];
-    const int sw = nw.x;
-    if (sw < 0) continue;
-    if (PHASE2) {
-      const double len = DYADIC ? g.off_len[k]
-                                : dist3(px, py, pz, centre1(wx, g.sx), centre1(wy, g.sy),
-                                        centre1(wz, g.sz));
-      const double d = __dadd_rn(dist[w], len);
-      if (beats(d, sw, best_d, best_s)) {
-        best_d = d; best_s = sw; best_src = w; thr = beat_threshold(best_d);
-      }
-    }
-    const int u = nw.y;
-    if (u == w) {
-      // w sees its site: try the same direct connection
-      double d;
-      if (sw == cache_s) {
-        d = cache_d;
-      } else {
-        const double4 sp = ld_d4(site_pos + sw);
-        d = dist3(px, py, pz, sp.x, sp.y, sp.z);
-        cache_s = sw; cache_d = d;
-      }
-      if (d < thr && beats(d, sw, best_d, best_s) && sw != failed_site) {
-        const double4 sp = ld_d4(site_pos + sw);
-        if (segment_clear(comp, g, px, py, pz, sp.x, sp.y, sp.z, cv)) {
-          best_d = d; best_s = sw; best_src = v; thr = beat_threshold(best_d);
-        } else {
-          failed_site = sw;
-        }
-      }
-    } else if (PHASE2 && u >= 0) {
-      // shortcut to w's own path node u
-      const int2 nu = ss[u];
-      const int su = nu.x;
-      if (su >= 0 && __ldg(comp + u) == cv) {
-        const double du = dist[u];
-        // d = RN(du + |p - c_u|) >= du: exact skip when du already loses
-        if (du < thr) {
-          int ux, uy, uz;
-          coords(g, u, ux, uy, uz);
-          const double upx = centre1(ux, g.sx), upy = centre1(uy, g.sy), upz = centre1(uz, g.sz);
-          double d;
-          if (u == cache_u) {
-            d = cache_ud;
+  unsigned rem = active ? inbounds_mask(x, y, z, g.nx, g.ny, g.nz) : 0u;
+  bool done = rem == 0;
+  char4 o = c_off[done ? 0 : __ffs(rem) - 1];
+  int w = active ? nbr_index(v, o, g.nx, g.nxy) : 0;
+  int cw = done ? -4 : __ldg(comp + w);
+  int2 nw = done ? make_int2(-1, -1) : ss[w];
+  double dw = (PHASE2 && !done) ? dist[w] : 0.0;
+
+  // pending ray: segment p -> (qx, qy, qz); on success best := (rd, rs, rsrc)
+  bool pending = false;
+  bool ray_los = false;
+  double qx = 0, qy = 0, qz = 0, rd = 0;
+  int rs = 0, rsrc = 0;
+
+  while (!done) {
+    // ---- advance until a ray is needed or the neighbours run out
+    while (!done && !pending) {
+      rem &= rem - 1;
+      const char4 o2 = rem ? c_off[__ffs(rem) - 1] : o;
+      const int w2 = nbr_index(v, o2, g.nx, g.nxy);
+      const int cw2 = __ldg(comp + w2);
+      const int2 nw2 = ss[w2];
+      const double dw2 = PHASE2 ? dist[w2] : 0.0;
+
+      const int sw = nw.x;
+      if (cw == cv && sw >= 0) {
+        if (PHASE2) {
+          double len;
+          if (DYADIC) {
+            len = s_len[o.w];
           } else {
-            d = __dadd_rn(du, dist3(px, py, pz, upx, upy, upz));
-            cache_u = u; cache_ud = d;
+            len = dist3(px, py, pz, centre1(x + o.x, g.sx), centre1(y + o.y, g.sy),
+                        centre1(z + o.z, g.sz));
           }
-          if (beats(d, su, best_d, best_s)) {
-            if (segment_clear(comp, g, px, py, pz, upx, upy, upz, cv)) {
-              best_d = d; best_s = su; best_src = u; thr = beat_threshold(best_d);
+          const double d = __dadd_rn(dw, len);
+          if (beats(d, sw, best_d, best_s)) {
+            best_d = d; best_s = sw; best_src = w; thr = beat_threshold(best_d);
+          }
+        }
+        const int u = nw.y;
+        if (u == w) {
+          // w sees its site: try the same direct connection. d is a pure
+          // function of (v, site): two-entry memo, exact lower-bound skip.
+          double d = 0.0;
+          bool have = true;
+          if (sw == cache_s) {
+            d = cache_d;
+          } else if (sw == cache_s2) {
+            d = cache_d2;
+          } else {
+            const double4 sp = ld_d4(site_pos + sw);
+            if (dist_lower(px, py, pz, sp.x, sp.y, sp.z) >= thr) {
+              have = false;
+            } else {
+              d = dist3(px, py, pz, sp.x, sp.y, sp.z);
+              cache_s2 = cache_s; cache_d2 = cache_d;
+              cache_s = sw; cache_d = d;
+            }
+          }
+          if (have && d < thr && beats(d, sw, best_d, best_s) && sw != failed_site) {
+            const double4 sp = ld_d4(site_pos + sw);
+            pending = true; ray_los = true;
+            qx = sp.x; qy = sp.y; qz = sp.z; rd = d; rs = sw; rsrc = v;
+          }
+        } else if (PHASE2 && u >= 0) {
+          // shortcut to w's own path node u. d = RN(du + |p - c_u|) >= du, so
+          // dist[u] alone prescreens before site/comp of u are fetched.
+          const double du = dist[u];
+          if (du < thr) {
+            double d = 0.0;
+            bool have = false;
+            double upx = 0, upy = 0, upz = 0;
+            if (u == cache_u) {
+              d = cache_ud; have = true;
+            } else if (u == cache_u2) {
+              d = cache_ud2; have = true;
+            }
+            const int2 nu = ss[u];
+            const int su = nu.x;
+            if (su >= 0 && __ldg(comp + u) == cv) {
+              int ux, uy, uz;
+              coords(g, u, ux, uy, uz);
+              upx = centre1(ux, g.sx); upy = centre1(uy, g.sy); upz = centre1(uz, g.sz);
+              if (!have && __dadd_rn(du, dist_lower(px, py, pz, upx, upy, upz)) < thr) {
+                d = __dadd_rn(du, dist3(px, py, pz, upx, upy, upz));
+                cache_u2 = cache_u; cache_ud2 = cache_ud;
+                cache_u = u; cache_ud = d;
+                have = true;
+              }
+              if (have && beats(d, su, best_d, best_s)) {
+                pending = true; ray_los = false;
+                qx = upx; qy = upy; qz = upz; rd = d; rs = su; rsrc = u;
+              }
             }
           }
         }
       }
+      if (!rem) done = true;
+      o = o2; w = w2; cw = cw2; nw = nw2; dw = dw2;
+    }
+    // ---- lanes with a pending ray trace it together
+    if (pending) {
+      if (segment_clear(comp, g, px, py, pz, qx, qy, qz, cv)) {
+        best_d = rd; best_s = rs; best_src = rsrc; thr = beat_threshold(best_d);
+      } else if (ray_los) {
+        failed_site = rs;
+      }
+      pending = false;
     }
   }
   out.d = best_d; out.v = v; out.s = best_s; out.src = best_src; out.pad = 0;
-  return (best_s != orig_s) || (best_d < __dsub_rn(orig_d, LRCVT_EPS));
+  return active && ((best_s != orig_s) || (best_d < __dsub_rn(orig_d, LRCVT_EPS)));
 }
 
 // _kernels.py:249-282: evaluate a frontier list against the pre-round state.
@@ -252,14 +316,15 @@ __global__ void __launch_bounds__(128) k_eval(const int* __restrict__ list, int 
                                               uint32_t* __restrict__ bm,
                                               Prop* __restrict__ imp,
                                               int* __restrict__ counters) {
+  __shared__ double s_len[8];
+  if (threadIdx.x < 8) s_len[threadIdx.x] = len_of(g, threadIdx.x == 0 ? 1 : threadIdx.x);
+  __syncthreads();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  bool improved = false;
   Prop pr;
-  if (i < n) {
-    const int v = list[i];
-    bm[v >> 5] = 0u;
-    improved = eval_voxel<PHASE2, DYADIC>(g, v, comp, ss, dist, site_pos, pr);
-  }
+  const bool active = i < n;
+  const int v = active ? list[i] : 0;
+  if (active) bm[v >> 5] = 0u;
+  const bool improved = eval_voxel<PHASE2, DYADIC>(g, s_len, v, active, comp, ss, dist, site_pos, pr);
   const int slot = warp_append(counters + C_NIMP, improved);
   if (improved) imp[slot] = pr;
 }

@@ -23,16 +23,72 @@ struct Geo {
   double sx, sy, sz;
   double inv_nx, inv_nxy;  // for exact division via fp64 reciprocal + fixup
   int dyadic;              // spacing values are powers of two (exact centre diffs)
-  double off_len[26];      // |offset_k| in world units when dyadic
+  double len_cls[8];       // |offset| in world units by class (exact when dyadic)
   int off_d[26];           // flat index delta of offset k
 };
 
 // _kernels.py:17-25: dz, dy, dx lexicographic, dx fastest, (0,0,0) excluded.
+__host__ __device__ constexpr int off_dx(int k) { return (k < 13 ? k : k + 1) % 3 - 1; }
+__host__ __device__ constexpr int off_dy(int k) { return ((k < 13 ? k : k + 1) / 3) % 3 - 1; }
+__host__ __device__ constexpr int off_dz(int k) { return (k < 13 ? k : k + 1) / 9 - 1; }
 __host__ __device__ inline void offset_of(int k, int& dx, int& dy, int& dz) {
-  int j = k < 13 ? k : k + 1;  // skip the centre (index 13 of the 27-cube)
-  dz = j / 9 - 1;
-  dy = (j / 3) % 3 - 1;
-  dx = j % 3 - 1;
+  dx = off_dx(k); dy = off_dy(k); dz = off_dz(k);
+}
+// |offset| class: bit0 = dx != 0, bit1 = dy != 0, bit2 = dz != 0
+__host__ __device__ constexpr int off_cls(int k) {
+  return (off_dx(k) != 0) | ((off_dy(k) != 0) << 1) | ((off_dz(k) != 0) << 2);
+}
+// 26-bit masks of the offsets that step toward -x/+x/-y/+y/-z/+z
+__host__ __device__ constexpr unsigned off_mask(int axis, int sgn) {
+  unsigned m = 0;
+  for (int k = 0; k < 26; k++) {
+    const int d = axis == 0 ? off_dx(k) : axis == 1 ? off_dy(k) : off_dz(k);
+    if (d == sgn) m |= 1u << k;
+  }
+  return m;
+}
+constexpr unsigned ALL26 = (1u << 26) - 1u;
+
+// neighbours of (x, y, z) that lie inside the grid, as a 26-bit mask in the
+// reference's scan order (bit k = OFFSETS[k])
+__device__ __forceinline__ unsigned inbounds_mask(int x, int y, int z, int nx, int ny, int nz) {
+  unsigned m = ALL26;
+  if (x == 0) m &= ~off_mask(0, -1);
+  if (x == nx - 1) m &= ~off_mask(0, 1);
+  if (y == 0) m &= ~off_mask(1, -1);
+  if (y == ny - 1) m &= ~off_mask(1, 1);
+  if (z == 0) m &= ~off_mask(2, -1);
+  if (z == nz - 1) m &= ~off_mask(2, 1);
+  return m;
+}
+
+// packed per-offset table: dx, dy, dz, length class
+__constant__ char4 c_off[26] = {
+#define LRCVT_OFF(k) \
+  { (signed char)off_dx(k), (signed char)off_dy(k), (signed char)off_dz(k), (signed char)off_cls(k) }
+    LRCVT_OFF(0),  LRCVT_OFF(1),  LRCVT_OFF(2),  LRCVT_OFF(3),  LRCVT_OFF(4),  LRCVT_OFF(5),
+    LRCVT_OFF(6),  LRCVT_OFF(7),  LRCVT_OFF(8),  LRCVT_OFF(9),  LRCVT_OFF(10), LRCVT_OFF(11),
+    LRCVT_OFF(12), LRCVT_OFF(13), LRCVT_OFF(14), LRCVT_OFF(15), LRCVT_OFF(16), LRCVT_OFF(17),
+    LRCVT_OFF(18), LRCVT_OFF(19), LRCVT_OFF(20), LRCVT_OFF(21), LRCVT_OFF(22), LRCVT_OFF(23),
+    LRCVT_OFF(24), LRCVT_OFF(25)
+#undef LRCVT_OFF
+};
+
+// |offset| by class with static indices only (dynamic indexing of the
+// by-value Geo parameter would force a local-memory copy)
+__device__ __forceinline__ double len_of(const Geo& g, int cls) {
+  double r = g.len_cls[1];
+  r = cls == 2 ? g.len_cls[2] : r;
+  r = cls == 3 ? g.len_cls[3] : r;
+  r = cls == 4 ? g.len_cls[4] : r;
+  r = cls == 5 ? g.len_cls[5] : r;
+  r = cls == 6 ? g.len_cls[6] : r;
+  r = cls == 7 ? g.len_cls[7] : r;
+  return r;
+}
+
+__device__ __forceinline__ int nbr_index(const int v, const char4 o, const int nx, const int nxy) {
+  return v + o.x + o.y * nx + o.z * nxy;
 }
 
 // v -> (x, y, z) without integer division: fp64 reciprocal, then one-step
@@ -77,6 +133,16 @@ __device__ __forceinline__ double beat_threshold(double cur_d) {
   return __dadd_rn(cur_d, __dadd_rn(2e-9, __dmul_rn(fabs(cur_d), 1e-15)));
 }
 
+// Exact lower bound on the distance the reference computes, RN(sqrt(RN(
+// dx*dx + dy*dy + dz*dz))), for an exact prescreen: the rounded sum of
+// squares is >= RN(m*m) for m = max(|dx|,|dy|,|dz|) (monotone rounding of
+// nonnegative terms) and RN(sqrt(RN(m*m))) >= m*(1 - 2^-51).
+__device__ __forceinline__ double dist_lower(double ax, double ay, double az, double bx,
+                                             double by, double bz) {
+  const double m = fmax(fabs(__dsub_rn(bx, ax)), fmax(fabs(__dsub_rn(by, ay)), fabs(__dsub_rn(bz, az))));
+  return __dmul_rn(m, 1.0 - 0x1p-50);
+}
+
 // read-only 32-byte load (two LDG.128 through the non-coherent path)
 __device__ __forceinline__ double4 ld_d4(const double4* p) {
   const double2* q = reinterpret_cast<const double2*>(p);
@@ -99,9 +165,17 @@ __device__ __forceinline__ int cell_of(double a, double s, int n) {
 
 // _kernels.py:45-125: parametric t of the first entry into a voxel whose
 // component is not `want`; 1.0 if none.
-__device__ inline double segment_hit_t(const int* __restrict__ comp, const Geo& g,
-                                       double ax, double ay, double az, double bx,
-                                       double by, double bz, int want) {
+// Box: the six scalars the DDA needs, passed by value so the out-of-line
+// ray function does not force the whole Geo parameter into local memory.
+struct Box {
+  int nx, ny, nz;
+  double sx, sy, sz;
+};
+__device__ __forceinline__ Box box_of(const Geo& g) { return Box{g.nx, g.ny, g.nz, g.sx, g.sy, g.sz}; }
+
+__device__ __noinline__ double segment_hit_box(const int* __restrict__ comp, const Box g,
+                                               double ax, double ay, double az, double bx,
+                                               double by, double bz, int want) {
   int cx = cell_of(ax, g.sx, g.nx), cy = cell_of(ay, g.sy, g.ny), cz = cell_of(az, g.sz, g.nz);
   int ex = cell_of(bx, g.sx, g.nx), ey = cell_of(by, g.sy, g.ny), ez = cell_of(bz, g.sz, g.nz);
   if (__ldg(comp + cx + g.nx * (cy + g.ny * cz)) != want) return 0.0;
@@ -139,6 +213,12 @@ __device__ inline double segment_hit_t(const int* __restrict__ comp, const Geo& 
     if (__ldg(comp + cx + g.nx * (cy + g.ny * cz)) != want) return t;
   }
   return 1.0;
+}
+
+__device__ __forceinline__ double segment_hit_t(const int* __restrict__ comp, const Geo& g,
+                                               double ax, double ay, double az, double bx,
+                                               double by, double bz, int want) {
+  return segment_hit_box(comp, box_of(g), ax, ay, az, bx, by, bz, want);
 }
 
 __device__ __forceinline__ bool segment_clear(const int* __restrict__ comp, const Geo& g,

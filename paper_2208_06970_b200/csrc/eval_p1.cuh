@@ -1,0 +1,190 @@
+// eval_p1.cuh -- phase-1 evaluation (_eval_voxel with phase2 = False,
+// _kernels.py:147-246; tessellation.py:151-156).
+//
+// Phase 1 only admits line-of-sight candidates, so the per-neighbour work is
+// a site id, a distance that depends only on (voxel, site) and a `_beats`
+// test; rays are the only expensive step. The kernel gathers, tabulates and
+// folds instead of walking neighbours with dependent loads (see below).
+#pragma once
+#include "classify.cuh"
+
+namespace lrcvt {
+
+constexpr int P1_TAB = 4;  // distinct-site distance table
+
+// Phase-1 evaluation (LOS candidates only):
+//   A  gather the 26 neighbours' candidate sites (immediate offsets, all
+//      loads in flight together) into a per-thread shared-memory row;
+//   B  compute the distance to each distinct neighbour site once;
+//   C  SPECULATIVE fold in OFFSETS order over the row with table lookups
+//      only, assuming every ray it needs is clear (96% are); each assumed
+//      ray (voxel, site) goes into a block-wide shared-memory queue together
+//      with the fold state before it;
+//   D  the whole block traces the queued rays, one per thread;
+//   E  each lane replays its rays' outcomes in order: if all were clear the
+//      speculative fold IS the reference's fold; at the first blocked ray the
+//      lane rewinds to the state before it, records failed_site and finishes
+//      the fold non-speculatively (rays traced inline; rare).
+// Ray outcomes are pure functions of (voxel, site), so the decision sequence
+// is exactly the reference's in every case.
+constexpr int P1_SPEC = 3;  // speculated rays per lane
+
+template <int BLOCK>
+__global__ void __launch_bounds__(BLOCK) k_eval_p1(const int* __restrict__ list, int n, Geo g,
+                                                   const int* __restrict__ comp,
+                                                   const int2* __restrict__ ss,
+                                                   const double* __restrict__ dist,
+                                                   const double4* __restrict__ site_pos,
+                                                   uint32_t* __restrict__ bm,
+                                                   Prop* __restrict__ imp,
+                                                   int* __restrict__ counters) {
+  __shared__ int s_row[26][BLOCK];  // [k][thread]: conflict-free column per thread
+  __shared__ int q_v[BLOCK * P1_SPEC], q_s[BLOCK * P1_SPEC];
+  __shared__ unsigned char q_ok[BLOCK * P1_SPEC];
+  __shared__ int q_n;
+  if (threadIdx.x == 0) q_n = 0;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool active = i < n;
+  const int v = active ? __ldg(list + i) : 0;
+  int* row = &s_row[0][threadIdx.x];
+  int x = 0, y = 0, z = 0, cv = -3;
+  double px = 0, py = 0, pz = 0;
+  int ts[P1_TAB];
+  double td[P1_TAB];
+#pragma unroll
+  for (int j = 0; j < P1_TAB; j++) { ts[j] = -1; td[j] = 0.0; }
+  double best_d = 0.0, orig_d = 0.0;
+  int best_s = -1, best_src = -1, orig_s = -1;
+  if (active) {
+    bm[v >> 5] = 0u;
+    coords(g, v, x, y, z);
+    cv = __ldg(comp + v);
+    px = centre1(x, g.sx); py = centre1(y, g.sy); pz = centre1(z, g.sz);
+    const unsigned inb = inbounds_mask(x, y, z, g.nx, g.ny, g.nz);
+    // ---- A
+    int cw[26];
+    int2 nw[26];
+#pragma unroll
+    for (int k = 0; k < 26; k++) {
+      const int w = v + off_dx(k) + off_dy(k) * g.nx + off_dz(k) * g.nxy;
+      const bool ok = (inb >> k) & 1u;
+      cw[k] = ok ? __ldg(comp + w) : -4;
+      nw[k] = ok ? ss[w] : make_int2(-1, -1);
+    }
+    int nt = 0;
+#pragma unroll
+    for (int k = 0; k < 26; k++) {
+      const int w = v + off_dx(k) + off_dy(k) * g.nx + off_dz(k) * g.nxy;
+      const int s = (cw[k] == cv && nw[k].x >= 0 && nw[k].y == w) ? nw[k].x : -1;
+      row[k * BLOCK] = s;
+      // ---- B: distinct-site table
+      bool seen = s < 0;
+#pragma unroll
+      for (int j = 0; j < P1_TAB; j++) seen |= ts[j] == s;
+      if (!seen && nt < P1_TAB) {
+#pragma unroll
+        for (int j = 0; j < P1_TAB; j++)
+          if (j == nt) ts[j] = s;
+        nt++;
+      }
+    }
+    const int2 sv = ss[v];
+    best_d = dist[v];
+    best_s = sv.x; best_src = sv.y;
+    orig_d = best_d; orig_s = best_s;
+  }
+#pragma unroll
+  for (int j = 0; j < P1_TAB; j++) {
+    if (ts[j] >= 0) {
+      const double4 sp = ld_d4(site_pos + ts[j]);
+      td[j] = dist3(px, py, pz, sp.x, sp.y, sp.z);
+    }
+  }
+  __syncthreads();  // q_n initialised
+  // ---- C: speculative fold
+  int failed = -1;
+  int nspec = 0, kstop = 26;
+  int sp_slot[P1_SPEC], sp_k[P1_SPEC], sp_s[P1_SPEC], sp_src[P1_SPEC];
+  double sp_d[P1_SPEC];
+#pragma unroll
+  for (int q = 0; q < P1_SPEC; q++) { sp_slot[q] = 0; sp_k[q] = 0; sp_s[q] = 0; sp_src[q] = 0; sp_d[q] = 0; }
+  if (active) {
+    for (int k = 0; k < 26; k++) {
+      const int s = row[k * BLOCK];
+      if (s < 0) continue;
+      double d;
+      if (s == ts[0]) d = td[0];
+      else if (s == ts[1]) d = td[1];
+      else if (s == ts[2]) d = td[2];
+      else if (s == ts[3]) d = td[3];
+      else {  // more than P1_TAB distinct sites around v (rare)
+        const double4 sp = ld_d4(site_pos + s);
+        d = dist3(px, py, pz, sp.x, sp.y, sp.z);
+      }
+      if (beats(d, s, best_d, best_s) && s != failed) {
+        if (nspec == P1_SPEC) { kstop = k; break; }  // window full: finish after replay
+        const int slot = atomicAdd(&q_n, 1);
+        q_v[slot] = v; q_s[slot] = s;
+#pragma unroll
+        for (int q = 0; q < P1_SPEC; q++)
+          if (q == nspec) { sp_slot[q] = slot; sp_k[q] = k; sp_s[q] = best_s; sp_src[q] = best_src; sp_d[q] = best_d; }
+        nspec++;
+        best_d = d; best_s = s; best_src = v;  // assume clear
+      }
+    }
+  }
+  __syncthreads();
+  // ---- D: the block traces the queued rays
+  const int nq = q_n;
+  for (int j = threadIdx.x; j < nq; j += BLOCK) {
+    const int rv = q_v[j];
+    int rx, ry, rz;
+    coords(g, rv, rx, ry, rz);
+    const double4 sp = ld_d4(site_pos + q_s[j]);
+    q_ok[j] = segment_clear(comp, g, centre1(rx, g.sx), centre1(ry, g.sy), centre1(rz, g.sz), sp.x, sp.y,
+                            sp.z, __ldg(comp + rv))
+                  ? 1 : 0;
+  }
+  __syncthreads();
+  // ---- E: replay outcomes; rewind at the first blocked ray
+  int kres = 26;  // resume point of the non-speculative tail
+  if (active) {
+#pragma unroll
+    for (int q = 0; q < P1_SPEC; q++) {
+      if (q < nspec && kres == 26 && !q_ok[sp_slot[q]]) {
+        best_d = sp_d[q]; best_s = sp_s[q]; best_src = sp_src[q];
+        failed = row[sp_k[q] * BLOCK];
+        kres = sp_k[q] + 1;
+      }
+    }
+    if (kres == 26 && kstop < 26) kres = kstop;  // window overflow, all clear
+    for (int k = kres; k < 26; k++) {
+      const int s = row[k * BLOCK];
+      if (s < 0) continue;
+      double d;
+      if (s == ts[0]) d = td[0];
+      else if (s == ts[1]) d = td[1];
+      else if (s == ts[2]) d = td[2];
+      else if (s == ts[3]) d = td[3];
+      else {
+        const double4 sp = ld_d4(site_pos + s);
+        d = dist3(px, py, pz, sp.x, sp.y, sp.z);
+      }
+      if (beats(d, s, best_d, best_s) && s != failed) {
+        const double4 sp = ld_d4(site_pos + s);
+        if (segment_clear(comp, g, px, py, pz, sp.x, sp.y, sp.z, cv)) {
+          best_d = d; best_s = s; best_src = v;
+        } else {
+          failed = s;
+        }
+      }
+    }
+  }
+  const bool improved = active && ((best_s != orig_s) || (best_d < __dsub_rn(orig_d, LRCVT_EPS)));
+  Prop pr;
+  pr.d = best_d; pr.v = v; pr.s = best_s; pr.src = best_src; pr.pad = 0;
+  const int slot = warp_append(counters + C_NIMP, improved);
+  if (improved) imp[slot] = pr;
+}
+
+}  // namespace lrcvt

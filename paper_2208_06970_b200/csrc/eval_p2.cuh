@@ -1,0 +1,217 @@
+// eval_p2.cuh -- phase-2 evaluation (_eval_voxel with phase2 = True,
+// _kernels.py:147-246; tessellation.py:158-189).
+//
+// Same gather / tabulate / fold structure as eval_p1.cuh, with the three
+// phase-2 candidates per neighbour w in OFFSETS order:
+//   path      (dist[w] + |c_w - p|, site(w), w)          no ray
+//   LOS       (|p - site(w)|, site(w), v)  if src(w)==w  ray to the site
+//   shortcut  (dist[u] + |p - c_u|, site(u), u), u = src(w) != w, u in
+//             the same component and assigned            ray to c_u
+// A  the 26 neighbours' (site, node, dist) go into a per-thread shared-memory
+//    row with all loads in flight together;
+// B  the LOS distance of each distinct neighbour site and the shortcut
+//    candidate of each distinct node are computed once (both are pure
+//    functions of (v, site) / (v, node) within a round);
+// C  the fold reads the row and the tables only; a candidate that needs a
+//    ray parks the lane, the parked lanes trace together, apply the outcome
+//    and resume at the next neighbour -- the reference's decision sequence.
+#pragma once
+#include "classify.cuh"
+
+namespace lrcvt {
+
+constexpr int P2_STAB = 4;  // distinct LOS sites
+constexpr int P2_NTAB = 6;  // distinct shortcut nodes
+
+template <int BLOCK, bool DYADIC>
+__global__ void __launch_bounds__(BLOCK) k_eval_p2(const int* __restrict__ list, int n, Geo g,
+                                                   const int* __restrict__ comp,
+                                                   const int2* __restrict__ ss,
+                                                   const double* __restrict__ dist,
+                                                   const double4* __restrict__ site_pos,
+                                                   uint32_t* __restrict__ bm,
+                                                   Prop* __restrict__ imp,
+                                                   int* __restrict__ counters) {
+  __shared__ int s_site[26][BLOCK];    // site(w) or -1 (not a candidate source)
+  __shared__ int s_node[26][BLOCK];    // -2: w is LOS; -1: no shortcut; else src(w)
+  __shared__ double s_dw[26][BLOCK];   // dist[w] + |c_w - p| (path candidate)
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool active = i < n;
+  const int v = active ? __ldg(list + i) : 0;
+  const int t = threadIdx.x;
+  int x = 0, y = 0, z = 0, cv = -3;
+  double px = 0, py = 0, pz = 0;
+  int ts[P2_STAB];
+  double td[P2_STAB];
+  int tu[P2_NTAB], tus[P2_NTAB];
+  double tud[P2_NTAB];
+#pragma unroll
+  for (int j = 0; j < P2_STAB; j++) { ts[j] = -1; td[j] = 0.0; }
+#pragma unroll
+  for (int j = 0; j < P2_NTAB; j++) { tu[j] = -1; tus[j] = -1; tud[j] = 0.0; }
+  double best_d = 0.0, orig_d = 0.0;
+  int best_s = -1, best_src = -1, orig_s = -1;
+  bool done = !active;
+  if (active) {
+    bm[v >> 5] = 0u;
+    coords(g, v, x, y, z);
+    cv = __ldg(comp + v);
+    px = centre1(x, g.sx); py = centre1(y, g.sy); pz = centre1(z, g.sz);
+    const unsigned inb = inbounds_mask(x, y, z, g.nx, g.ny, g.nz);
+    // ---- A: gather (two batches of 13 to bound register pressure)
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+      int cw[13];
+      int2 nw[13];
+      double dw[13];
+#pragma unroll
+      for (int q = 0; q < 13; q++) {
+        const int k = 13 * h + q;
+        const int w = v + off_dx(k) + off_dy(k) * g.nx + off_dz(k) * g.nxy;
+        const bool ok = (inb >> k) & 1u;
+        cw[q] = ok ? __ldg(comp + w) : -4;
+        nw[q] = ok ? ss[w] : make_int2(-1, -1);
+        dw[q] = ok ? dist[w] : 0.0;
+      }
+#pragma unroll
+      for (int q = 0; q < 13; q++) {
+        const int k = 13 * h + q;
+        const int w = v + off_dx(k) + off_dy(k) * g.nx + off_dz(k) * g.nxy;
+        const bool cand = cw[q] == cv && nw[q].x >= 0;
+        s_site[k][t] = cand ? nw[q].x : -1;
+        s_node[k][t] = !cand ? -1 : (nw[q].y == w ? -2 : (nw[q].y >= 0 ? nw[q].y : -1));
+        double len;
+        if (DYADIC) {
+          len = len_of(g, off_cls(k));
+        } else {
+          len = dist3(px, py, pz, centre1(x + off_dx(k), g.sx), centre1(y + off_dy(k), g.sy),
+                      centre1(z + off_dz(k), g.sz));
+        }
+        s_dw[k][t] = __dadd_rn(dw[q], len);
+      }
+    }
+    // ---- B: distinct LOS sites and distinct shortcut nodes
+    int nts = 0, ntu = 0;
+#pragma unroll
+    for (int k = 0; k < 26; k++) {
+      const int s = s_site[k][t];
+      const int u = s_node[k][t];
+      if (u == -2) {
+        bool seen = false;
+#pragma unroll
+        for (int j = 0; j < P2_STAB; j++) seen |= ts[j] == s;
+        if (!seen && nts < P2_STAB) {
+#pragma unroll
+          for (int j = 0; j < P2_STAB; j++)
+            if (j == nts) ts[j] = s;
+          nts++;
+        }
+      } else if (u >= 0) {
+        bool seen = false;
+#pragma unroll
+        for (int j = 0; j < P2_NTAB; j++) seen |= tu[j] == u;
+        if (!seen && ntu < P2_NTAB) {
+#pragma unroll
+          for (int j = 0; j < P2_NTAB; j++)
+            if (j == ntu) tu[j] = u;
+          ntu++;
+        }
+      }
+    }
+    const int2 sv = ss[v];
+    best_d = dist[v];
+    best_s = sv.x; best_src = sv.y;
+    orig_d = best_d; orig_s = best_s;
+  }
+#pragma unroll
+  for (int j = 0; j < P2_STAB; j++) {
+    if (ts[j] >= 0) {
+      const double4 sp = ld_d4(site_pos + ts[j]);
+      td[j] = dist3(px, py, pz, sp.x, sp.y, sp.z);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < P2_NTAB; j++) {
+    const int u = tu[j];
+    if (u >= 0) {
+      const int2 nu = ss[u];
+      if (nu.x >= 0 && __ldg(comp + u) == cv) {
+        int ux, uy, uz;
+        coords(g, u, ux, uy, uz);
+        tus[j] = nu.x;
+        tud[j] = __dadd_rn(dist[u], dist3(px, py, pz, centre1(ux, g.sx), centre1(uy, g.sy),
+                                          centre1(uz, g.sz)));
+      }
+    }
+  }
+  // ---- C: fold
+  int failed = -1;
+  int k = 0;
+  while (!done) {
+    int rs = -1, rsrc = -1;
+    double rd = 0.0;
+    bool los = false;
+    for (; k < 26; k++) {
+      const int s = s_site[k][t];
+      if (s < 0) continue;
+      const int u = s_node[k][t];
+      const double dpath = s_dw[k][t];
+      if (beats(dpath, s, best_d, best_s)) {
+        best_d = dpath; best_s = s; best_src = nbr_index(v, c_off[k], g.nx, g.nxy);
+      }
+      if (u == -2) {
+        double d;
+        if (s == ts[0]) d = td[0];
+        else if (s == ts[1]) d = td[1];
+        else if (s == ts[2]) d = td[2];
+        else if (s == ts[3]) d = td[3];
+        else {
+          const double4 sp = ld_d4(site_pos + s);
+          d = dist3(px, py, pz, sp.x, sp.y, sp.z);
+        }
+        if (beats(d, s, best_d, best_s) && s != failed) { rs = s; rd = d; rsrc = v; los = true; break; }
+      } else if (u >= 0) {
+        int su = -1;
+        double d = 0.0;
+        bool hit = false;
+#pragma unroll
+        for (int j = 0; j < P2_NTAB; j++)
+          if (tu[j] == u) { su = tus[j]; d = tud[j]; hit = true; }
+        if (!hit) {  // more than P2_NTAB distinct nodes (rare)
+          const int2 nu = ss[u];
+          if (nu.x >= 0 && __ldg(comp + u) == cv) {
+            int ux, uy, uz;
+            coords(g, u, ux, uy, uz);
+            su = nu.x;
+            d = __dadd_rn(dist[u], dist3(px, py, pz, centre1(ux, g.sx), centre1(uy, g.sy),
+                                         centre1(uz, g.sz)));
+          }
+        }
+        if (su >= 0 && beats(d, su, best_d, best_s)) { rs = su; rd = d; rsrc = u; los = false; break; }
+      }
+    }
+    if (rs < 0) { done = true; break; }
+    double qx, qy, qz;
+    if (los) {
+      const double4 sp = ld_d4(site_pos + rs);
+      qx = sp.x; qy = sp.y; qz = sp.z;
+    } else {
+      int ux, uy, uz;
+      coords(g, rsrc, ux, uy, uz);
+      qx = centre1(ux, g.sx); qy = centre1(uy, g.sy); qz = centre1(uz, g.sz);
+    }
+    if (segment_clear(comp, g, px, py, pz, qx, qy, qz, cv)) {
+      best_d = rd; best_s = rs; best_src = rsrc;
+    } else if (los) {
+      failed = rs;
+    }
+    k++;
+  }
+  const bool improved = active && ((best_s != orig_s) || (best_d < __dsub_rn(orig_d, LRCVT_EPS)));
+  Prop pr;
+  pr.d = best_d; pr.v = v; pr.s = best_s; pr.src = best_src; pr.pad = 0;
+  const int slot = warp_append(counters + C_NIMP, improved);
+  if (improved) imp[slot] = pr;
+}
+
+}  // namespace lrcvt

@@ -12,6 +12,9 @@
 #include "classify.cuh"
 #include "vote.cuh"
 #include "masks.cuh"
+#include "eval_wf.cuh"
+#include "eval_p1.cuh"
+#include "eval_p2.cuh"
 
 using namespace lrcvt;
 
@@ -128,12 +131,15 @@ Geo make_geo(int64_t nx, int64_t ny, int64_t nz, double sx, double sy, double sz
     int dx, dy, dz;
     offset_of(k, dx, dy, dz);
     g.off_d[k] = dx + (int)nx * (dy + (int)ny * dz);
-    // exact |c_w - c_v| when spacing is dyadic (centre differences are exact)
-    volatile double ex = dx * sx, ey = dy * sy, ez = dz * sz;
+  }
+  // exact |c_w - c_v| by offset class when spacing is dyadic (centre
+  // differences are then exact): sqrt(dx*dx + dy*dy + dz*dz), same order
+  for (int c = 0; c < 8; c++) {
+    volatile double ex = (c & 1) ? sx : 0.0, ey = (c & 2) ? sy : 0.0, ez = (c & 4) ? sz : 0.0;
     volatile double s2 = ex * ex;
     s2 = s2 + ey * ey;
     s2 = s2 + ez * ez;
-    g.off_len[k] = sqrt((double)s2);
+    g.len_cls[c] = sqrt((double)s2);
   }
   return g;
 }
@@ -191,6 +197,8 @@ struct lrcvt_plan {
   int64_t eval_launches = 0;
   int64_t eval_items = 0;
   double eval_ms = 0.0;
+  // resident CTAs for the persistent wavefront eval kernels
+  int wf_blocks[3] = {0, 0, 0};
 };
 
 namespace {
@@ -235,6 +243,23 @@ int prepare_eligible(lrcvt_plan* p, int n_sites, const int* site_comp, cudaStrea
   return 0;
 }
 
+// wavefront eval launch over list[0..n): persistent grid, capped at the
+// resident CTA count
+int launch_eval(lrcvt_plan* p, bool phase2, const int* list, int n, int2* ss, double* dist,
+                cudaStream_t st) {
+  const Geo& g = p->g;
+  const int var = !phase2 ? 0 : (g.dyadic ? 1 : 2);
+  const int blocks = grid_for(n, 128, p->wf_blocks[var] > 0 ? p->wf_blocks[var] : 148);
+  if (!phase2)
+    k_eval_p1<128><<<grid_for(n, 128), 128, 0, st>>>(list, n, g, p->comp, ss, dist, p->site_pos, p->bm, p->imp, p->counters);
+  else if (g.dyadic)
+    k_eval_p2<64, true><<<grid_for(n, 64), 64, 0, st>>>(list, n, g, p->comp, ss, dist, p->site_pos, p->bm, p->imp, p->counters);
+  else
+    k_eval_p2<64, false><<<grid_for(n, 64), 64, 0, st>>>(list, n, g, p->comp, ss, dist, p->site_pos, p->bm, p->imp, p->counters);
+  CKL("k_eval_wf");
+  return 0;
+}
+
 // one relaxation round loop (_kernels.py:337-385). list_in holds n items.
 int run_phase(lrcvt_plan* p, bool phase2, int** cur, int** nxt, int n, int2* ss, double* dist,
               lrcvt_classify_stats* st_out, cudaStream_t st) {
@@ -242,18 +267,10 @@ int run_phase(lrcvt_plan* p, bool phase2, int** cur, int** nxt, int n, int2* ss,
   while (n > 0) {
     st_out->rounds++;
     st_out->evaluations += n;
-    CK(cudaMemsetAsync(p->counters, 0, sizeof(int) * 2, st));
+    CK(cudaMemsetAsync(p->counters, 0, sizeof(int) * (C_WORK + 1), st));
     const int blocks = grid_for(n, 128);
     if (p->timing) CK(cudaEventRecord(p->ev0, st));
-    if (phase2) {
-      if (g.dyadic)
-        k_eval<true, true><<<blocks, 128, 0, st>>>(*cur, n, g, p->comp, ss, dist, p->site_pos, p->bm, p->imp, p->counters);
-      else
-        k_eval<true, false><<<blocks, 128, 0, st>>>(*cur, n, g, p->comp, ss, dist, p->site_pos, p->bm, p->imp, p->counters);
-    } else {
-      k_eval<false, true><<<blocks, 128, 0, st>>>(*cur, n, g, p->comp, ss, dist, p->site_pos, p->bm, p->imp, p->counters);
-    }
-    CKL("k_eval");
+    CKR(launch_eval(p, phase2, *cur, n, ss, dist, st));
     if (p->timing) CK(cudaEventRecord(p->ev1, st));
     k_commit<<<blocks, 128, 0, st>>>(p->imp, p->counters, g, p->comp, ss, dist, p->bm, *nxt);
     CKL("k_commit");
@@ -346,6 +363,17 @@ int lrcvt_plan_create(lrcvt_plan** plan, int64_t nx, int64_t ny, int64_t nz, dou
     need = b > need ? b : need;
   }
   p->cub_bytes = need;
+  {
+    int dev = 0, sms = 148, nb = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_eval_wf<false, true>, 128, 0);
+    p->wf_blocks[0] = nb * sms;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_eval_wf<true, true>, 128, 0);
+    p->wf_blocks[1] = nb * sms;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_eval_wf<true, false>, 128, 0);
+    p->wf_blocks[2] = nb * sms;
+  }
   if (dalloc((char**)&p->cub_tmp, (int64_t)need)) { lrcvt_plan_destroy(p); return LRCVT_E_NOMEM; }
   *plan = p;
   return 0;
@@ -450,14 +478,10 @@ int lrcvt_classify(lrcvt_plan* p, int64_t n_sites, const double* d_site_pos,
     if (run_phase(p, true, &cur, &nxt, n_wl, ss, d_dist, stats, st)) return LRCVT_E_CUDA;
     stats->sweeps++;
     stats->evaluations += n_el;
-    CK(cudaMemsetAsync(p->counters, 0, sizeof(int) * 2, st));
+    CK(cudaMemsetAsync(p->counters, 0, sizeof(int) * (C_WORK + 1), st));
     const int blocks = grid_for(n_el, 128);
     if (p->timing) CK(cudaEventRecord(p->ev0, st));
-    if (g.dyadic)
-      k_eval<true, true><<<blocks, 128, 0, st>>>(p->eligible, n_el, g, p->comp, ss, d_dist, p->site_pos, p->bm, p->imp, p->counters);
-    else
-      k_eval<true, false><<<blocks, 128, 0, st>>>(p->eligible, n_el, g, p->comp, ss, d_dist, p->site_pos, p->bm, p->imp, p->counters);
-    CKL("k_eval sweep");
+    CKR(launch_eval(p, true, p->eligible, n_el, ss, d_dist, st));
     if (p->timing) CK(cudaEventRecord(p->ev1, st));
     k_commit<<<blocks, 128, 0, st>>>(p->imp, p->counters, g, p->comp, ss, d_dist, p->bm, cur);
     CKL("k_commit sweep");
@@ -532,8 +556,8 @@ int lrcvt_centroidal_update(lrcvt_plan* p, int64_t n_sites, const double* d_site
       k_segments<<<grid_for(n_el, 256, 148 * 8), 256, 0, st>>>(p->vt_key2, n_el, S, p->seg_b, p->seg_e);
       CKL("k_segments"); LAUNCHED(1);
     }
-    k_vote_serial<<<grid_for(S, 128), 128, 0, st>>>(p->vt_idx2, p->vt_terms, p->seg_b, p->seg_e, S, p->sums);
-    CKL("k_vote_serial"); LAUNCHED(1);
+    k_vote_warp<4><<<grid_for(S, 4), 128, 0, st>>>(p->vt_idx2, p->vt_terms, p->seg_b, p->seg_e, S, p->sums);
+    CKL("k_vote_warp"); LAUNCHED(1);
   }
   CK(cudaMemsetAsync(p->counters + C_BAD, 0, sizeof(int), st));
   k_move_sites<<<grid_for(S, 128), 128, 0, st>>>(g, p->comp, p->site_pos, d_site_comp, p->sums, S, backoff,

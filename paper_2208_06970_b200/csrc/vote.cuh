@@ -118,33 +118,41 @@ __global__ void k_segments(const int* __restrict__ skey, int n, int n_sites,
   }
 }
 
-// step 3: one thread per site adds its terms in increasing voxel order.
-__global__ void __launch_bounds__(128) k_vote_serial(const int* __restrict__ sidx,
-                                                     const double4* __restrict__ terms,
-                                                     const int* __restrict__ seg_begin,
-                                                     const int* __restrict__ seg_end,
-                                                     int n_sites, double* __restrict__ sums) {
-  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+// step 3: one warp per site. Lanes gather 32 consecutive terms of the
+// site's segment (coalesced: sorted indices are increasing) into shared
+// memory; lanes 0-3 then each run one of the four sequential fp64 chains
+// (w, tx, ty, tz) over them in increasing voxel order -- the reference's
+// exact accumulation order. The next chunk's gather is issued before the
+// adds so its latency overlaps the serial chain.
+template <int WARPS>
+__global__ void __launch_bounds__(WARPS * 32) k_vote_warp(const int* __restrict__ sidx,
+                                                         const double4* __restrict__ terms,
+                                                         const int* __restrict__ seg_begin,
+                                                         const int* __restrict__ seg_end,
+                                                         int n_sites, double* __restrict__ sums) {
+  __shared__ double buf[WARPS][32][4];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int s = blockIdx.x * WARPS + wid;
   if (s >= n_sites) return;
-  double w = 0.0, tx = 0.0, ty = 0.0, tz = 0.0;
   const int b = seg_begin[s], e = seg_end[s];
-  int j = b;
-  // 4-deep software prefetch keeps several gathers in flight per thread
-  for (; j + 4 <= e; j += 4) {
-    double4 t[4];
-#pragma unroll
-    for (int q = 0; q < 4; q++) t[q] = terms[sidx[j + q]];
-#pragma unroll
-    for (int q = 0; q < 4; q++) {
-      w = __dadd_rn(w, t[q].x); tx = __dadd_rn(tx, t[q].y);
-      ty = __dadd_rn(ty, t[q].z); tz = __dadd_rn(tz, t[q].w);
+  double acc = 0.0;
+  int j0 = b;
+  double4 t = make_double4(0, 0, 0, 0);
+  if (j0 + lane < e) t = terms[sidx[j0 + lane]];
+  while (j0 < e) {
+    buf[wid][lane][0] = t.x; buf[wid][lane][1] = t.y; buf[wid][lane][2] = t.z; buf[wid][lane][3] = t.w;
+    __syncwarp();
+    const int cnt = min(32, e - j0);
+    const int jn = j0 + 32;
+    t = make_double4(0, 0, 0, 0);
+    if (jn + lane < e) t = terms[sidx[jn + lane]];
+    if (lane < 4) {
+      for (int q = 0; q < cnt; q++) acc = __dadd_rn(acc, buf[wid][q][lane]);
     }
+    __syncwarp();
+    j0 = jn;
   }
-  for (; j < e; j++) {
-    const double4 t = terms[sidx[j]];
-    w = __dadd_rn(w, t.x); tx = __dadd_rn(tx, t.y); ty = __dadd_rn(ty, t.z); tz = __dadd_rn(tz, t.w);
-  }
-  sums[s] = w; sums[n_sites + s] = tx; sums[2 * n_sites + s] = ty; sums[3 * n_sites + s] = tz;
+  if (lane < 4) sums[lane * n_sites + s] = acc;
 }
 
 // _kernels.py:535-582, one thread per site. counters[0] += empty regions.
