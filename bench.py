@@ -270,6 +270,8 @@ def main():
         ms = float(t.item())
     el, eitems, ems = _lib.ctypes.c_int64(), _lib.ctypes.c_int64(), _lib.ctypes.c_double()
     L.lrcvt_plan_timing(eng.plan, _lib.ctypes.byref(el), _lib.ctypes.byref(eitems), _lib.ctypes.byref(ems))
+    prof = (_lib.ctypes.c_double * 6)()
+    L.lrcvt_plan_profile(eng.plan, prof)
     _lib.check(L.lrcvt_plan_set_timing(eng.plan, 0), "set_timing")
     value = n * args.steps * world / (ms / 1e3)
     hbm, peak_kind = peaks()
@@ -278,9 +280,9 @@ def main():
     achieved = eval_bytes / (ems.value / 1e3) / 1e9 if ems.value > 0 else 0.0
     b_iter = 29.0 * n + 20.0 * E / args.steps + 16.0 * C / args.steps
     traffic = None
-    prof = ROOT / "profiles" / f"ncu_{args.config}_k_eval.json"
-    if prof.exists():
-        traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
+    prof_path = ROOT / "profiles" / f"ncu_{args.config}_k_eval.json"
+    if prof_path.exists():
+        traffic = json.loads(prof_path.read_text()).get("dram_bytes_per_launch")
 
     # end-to-end through the public API with host numpy in/out
     e2e = None
@@ -320,6 +322,9 @@ def main():
                      "launches": el.value, "avg_launch_us": 1e3 * ems.value / max(el.value, 1),
                      "bytes_per_launch": eval_bytes / max(el.value, 1),
                      "eval_share_of_step": ems.value / ms if ms else None,
+                     "breakdown_ms_per_step": {"eval_phase1": prof[0] / args.steps,
+                                               "eval_phase2": prof[1] / args.steps,
+                                               "commit": prof[2] / args.steps},
                      "iteration_B": b_iter, "iteration_frac": b_iter / (ms / args.steps / 1e3) / 1e9 / hbm},
         "gpu_launches": launches,
         "clocks": clk.summary(),

@@ -126,6 +126,9 @@ int lrcvt_component_table(int64_t nx, int64_t ny, int64_t nz, const int32_t *d_c
 int lrcvt_plan_set_timing(lrcvt_plan *plan, int enable);
 int lrcvt_plan_timing(const lrcvt_plan *plan, int64_t *launches, int64_t *items, double *ms);
 unsigned long long lrcvt_launch_count(void);
+/* with timing enabled: out6 = {phase-1 eval ms, phase-2 eval ms, commit ms,
+ * phase-1 voxels evaluated, phase-2 voxels evaluated, proposals committed} */
+int lrcvt_plan_profile(const lrcvt_plan *plan, double *out6);
 
 const char *lrcvt_last_error(void);
 int lrcvt_version(void);

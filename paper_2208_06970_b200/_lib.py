@@ -67,6 +67,7 @@ SIGNATURES = {
     "lrcvt_plan_set_timing": (c_int, [c_void_p, c_int]),
     "lrcvt_plan_timing": (c_int, [c_void_p, POINTER(c_int64), POINTER(c_int64), POINTER(c_double)]),
     "lrcvt_launch_count": (ctypes.c_ulonglong, []),
+    "lrcvt_plan_profile": (c_int, [c_void_p, POINTER(c_double)]),
     "lrcvt_isobands": (
         c_int,
         [c_int64, c_void_p, c_void_p, c_int32, c_void_p, c_void_p],

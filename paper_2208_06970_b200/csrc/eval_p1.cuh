@@ -32,6 +32,7 @@ constexpr int P1_SPEC = 3;  // speculated rays per lane
 template <int BLOCK>
 __global__ void __launch_bounds__(BLOCK) k_eval_p1(const int* __restrict__ list, int n, Geo g,
                                                    const int* __restrict__ comp,
+                                                   const uint32_t* __restrict__ nbm,
                                                    const int2* __restrict__ ss,
                                                    const double* __restrict__ dist,
                                                    const double4* __restrict__ site_pos,
@@ -39,10 +40,15 @@ __global__ void __launch_bounds__(BLOCK) k_eval_p1(const int* __restrict__ list,
                                                    Prop* __restrict__ imp,
                                                    int* __restrict__ counters) {
   __shared__ int s_row[26][BLOCK];  // [k][thread]: conflict-free column per thread
+  // per-warp queue of speculated rays (no block-wide barrier needed)
   __shared__ int q_v[BLOCK * P1_SPEC], q_s[BLOCK * P1_SPEC];
   __shared__ unsigned char q_ok[BLOCK * P1_SPEC];
-  __shared__ int q_n;
-  if (threadIdx.x == 0) q_n = 0;
+  __shared__ int q_n[BLOCK / 32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int* qv = q_v + wid * 32 * P1_SPEC;
+  int* qs = q_s + wid * 32 * P1_SPEC;
+  unsigned char* qok = q_ok + wid * 32 * P1_SPEC;
+  if (lane == 0) q_n[wid] = 0;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const bool active = i < n;
   const int v = active ? __ldg(list + i) : 0;
@@ -56,26 +62,23 @@ __global__ void __launch_bounds__(BLOCK) k_eval_p1(const int* __restrict__ list,
   double best_d = 0.0, orig_d = 0.0;
   int best_s = -1, best_src = -1, orig_s = -1;
   if (active) {
-    bm[v >> 5] = 0u;
+    bm[v >> 5] = 0u;  // consume this round's frontier word
     coords(g, v, x, y, z);
     cv = __ldg(comp + v);
     px = centre1(x, g.sx); py = centre1(y, g.sy); pz = centre1(z, g.sz);
-    const unsigned inb = inbounds_mask(x, y, z, g.nx, g.ny, g.nz);
+    const unsigned same = __ldg(nbm + v);
     // ---- A
-    int cw[26];
     int2 nw[26];
 #pragma unroll
     for (int k = 0; k < 26; k++) {
       const int w = v + off_dx(k) + off_dy(k) * g.nx + off_dz(k) * g.nxy;
-      const bool ok = (inb >> k) & 1u;
-      cw[k] = ok ? __ldg(comp + w) : -4;
-      nw[k] = ok ? ss[w] : make_int2(-1, -1);
+      nw[k] = ((same >> k) & 1u) ? ss[w] : make_int2(-1, -1);
     }
     int nt = 0;
 #pragma unroll
     for (int k = 0; k < 26; k++) {
       const int w = v + off_dx(k) + off_dy(k) * g.nx + off_dz(k) * g.nxy;
-      const int s = (cw[k] == cv && nw[k].x >= 0 && nw[k].y == w) ? nw[k].x : -1;
+      const int s = (nw[k].x >= 0 && nw[k].y == w) ? nw[k].x : -1;
       row[k * BLOCK] = s;
       // ---- B: distinct-site table
       bool seen = s < 0;
@@ -100,7 +103,7 @@ __global__ void __launch_bounds__(BLOCK) k_eval_p1(const int* __restrict__ list,
       td[j] = dist3(px, py, pz, sp.x, sp.y, sp.z);
     }
   }
-  __syncthreads();  // q_n initialised
+  __syncwarp();  // q_n initialised
   // ---- C: speculative fold
   int failed = -1;
   int nspec = 0, kstop = 26;
@@ -123,8 +126,8 @@ __global__ void __launch_bounds__(BLOCK) k_eval_p1(const int* __restrict__ list,
       }
       if (beats(d, s, best_d, best_s) && s != failed) {
         if (nspec == P1_SPEC) { kstop = k; break; }  // window full: finish after replay
-        const int slot = atomicAdd(&q_n, 1);
-        q_v[slot] = v; q_s[slot] = s;
+        const int slot = atomicAdd(&q_n[wid], 1);
+        qv[slot] = v; qs[slot] = s;
 #pragma unroll
         for (int q = 0; q < P1_SPEC; q++)
           if (q == nspec) { sp_slot[q] = slot; sp_k[q] = k; sp_s[q] = best_s; sp_src[q] = best_src; sp_d[q] = best_d; }
@@ -133,25 +136,25 @@ __global__ void __launch_bounds__(BLOCK) k_eval_p1(const int* __restrict__ list,
       }
     }
   }
-  __syncthreads();
-  // ---- D: the block traces the queued rays
-  const int nq = q_n;
-  for (int j = threadIdx.x; j < nq; j += BLOCK) {
-    const int rv = q_v[j];
+  __syncwarp();
+  // ---- D: the warp traces its queued rays, one per lane
+  const int nq = q_n[wid];
+  for (int j = lane; j < nq; j += 32) {
+    const int rv = qv[j];
     int rx, ry, rz;
     coords(g, rv, rx, ry, rz);
-    const double4 sp = ld_d4(site_pos + q_s[j]);
-    q_ok[j] = segment_clear(comp, g, centre1(rx, g.sx), centre1(ry, g.sy), centre1(rz, g.sz), sp.x, sp.y,
-                            sp.z, __ldg(comp + rv))
-                  ? 1 : 0;
+    const double4 sp = ld_d4(site_pos + qs[j]);
+    qok[j] = segment_clear(comp, g, centre1(rx, g.sx), centre1(ry, g.sy), centre1(rz, g.sz), sp.x, sp.y,
+                           sp.z, __ldg(comp + rv))
+                 ? 1 : 0;
   }
-  __syncthreads();
+  __syncwarp();
   // ---- E: replay outcomes; rewind at the first blocked ray
   int kres = 26;  // resume point of the non-speculative tail
   if (active) {
 #pragma unroll
     for (int q = 0; q < P1_SPEC; q++) {
-      if (q < nspec && kres == 26 && !q_ok[sp_slot[q]]) {
+      if (q < nspec && kres == 26 && !qok[sp_slot[q]]) {
         best_d = sp_d[q]; best_s = sp_s[q]; best_src = sp_src[q];
         failed = row[sp_k[q] * BLOCK];
         kres = sp_k[q] + 1;

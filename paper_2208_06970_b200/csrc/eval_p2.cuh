@@ -24,8 +24,9 @@ constexpr int P2_STAB = 4;  // distinct LOS sites
 constexpr int P2_NTAB = 6;  // distinct shortcut nodes
 
 template <int BLOCK, bool DYADIC>
-__global__ void __launch_bounds__(BLOCK) k_eval_p2(const int* __restrict__ list, int n, Geo g,
+__global__ void __launch_bounds__(BLOCK, 512 / BLOCK) k_eval_p2(const int* __restrict__ list, int n, Geo g,
                                                    const int* __restrict__ comp,
+                                                   const uint32_t* __restrict__ nbm,
                                                    const int2* __restrict__ ss,
                                                    const double* __restrict__ dist,
                                                    const double4* __restrict__ site_pos,
@@ -53,23 +54,21 @@ __global__ void __launch_bounds__(BLOCK) k_eval_p2(const int* __restrict__ list,
   int best_s = -1, best_src = -1, orig_s = -1;
   bool done = !active;
   if (active) {
-    bm[v >> 5] = 0u;
+    bm[v >> 5] = 0u;  // consume this round's frontier word
     coords(g, v, x, y, z);
     cv = __ldg(comp + v);
     px = centre1(x, g.sx); py = centre1(y, g.sy); pz = centre1(z, g.sz);
-    const unsigned inb = inbounds_mask(x, y, z, g.nx, g.ny, g.nz);
+    const unsigned same = __ldg(nbm + v);
     // ---- A: gather (two batches of 13 to bound register pressure)
 #pragma unroll
     for (int h = 0; h < 2; h++) {
-      int cw[13];
       int2 nw[13];
       double dw[13];
 #pragma unroll
       for (int q = 0; q < 13; q++) {
         const int k = 13 * h + q;
         const int w = v + off_dx(k) + off_dy(k) * g.nx + off_dz(k) * g.nxy;
-        const bool ok = (inb >> k) & 1u;
-        cw[q] = ok ? __ldg(comp + w) : -4;
+        const bool ok = (same >> k) & 1u;
         nw[q] = ok ? ss[w] : make_int2(-1, -1);
         dw[q] = ok ? dist[w] : 0.0;
       }
@@ -77,7 +76,7 @@ __global__ void __launch_bounds__(BLOCK) k_eval_p2(const int* __restrict__ list,
       for (int q = 0; q < 13; q++) {
         const int k = 13 * h + q;
         const int w = v + off_dx(k) + off_dy(k) * g.nx + off_dz(k) * g.nxy;
-        const bool cand = cw[q] == cv && nw[q].x >= 0;
+        const bool cand = nw[q].x >= 0;
         s_site[k][t] = cand ? nw[q].x : -1;
         s_node[k][t] = !cand ? -1 : (nw[q].y == w ? -2 : (nw[q].y >= 0 ? nw[q].y : -1));
         double len;

@@ -12,7 +12,6 @@
 #include "classify.cuh"
 #include "vote.cuh"
 #include "masks.cuh"
-#include "eval_wf.cuh"
 #include "eval_p1.cuh"
 #include "eval_p2.cuh"
 
@@ -165,8 +164,9 @@ struct lrcvt_plan {
   int* list_b = nullptr;
   int* eligible = nullptr;
   Prop* imp = nullptr;
-  uint32_t* bm = nullptr;
+  uint32_t* bm = nullptr;  // frontier bitmap (1 bit per voxel)
   int64_t bm_words = 0;
+  uint32_t* nbm = nullptr;  // static same-component neighbour masks
   int* counters = nullptr;
   int* h_counters = nullptr;  // pinned
   uint8_t* has_site = nullptr;
@@ -193,12 +193,13 @@ struct lrcvt_plan {
   size_t cub_bytes = 0;
   // optional per-launch timing of the dominant kernel (k_eval)
   bool timing = false;
-  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr;
   int64_t eval_launches = 0;
   int64_t eval_items = 0;
   double eval_ms = 0.0;
-  // resident CTAs for the persistent wavefront eval kernels
-  int wf_blocks[3] = {0, 0, 0};
+  // breakdown: [0] phase-1 eval ms, [1] phase-2 eval ms, [2] commit ms,
+  // [3] phase-1 items, [4] phase-2 items, [5] committed proposals
+  double prof[6] = {0, 0, 0, 0, 0, 0};
 };
 
 namespace {
@@ -211,12 +212,17 @@ int dalloc(T** p, int64_t count) {
   return 0;
 }
 
-int note_eval(lrcvt_plan* p, int64_t items) {
-  float ms = 0.f;
+int note_eval(lrcvt_plan* p, int64_t items, bool phase2, int64_t n_imp) {
+  float ms = 0.f, ms2 = 0.f;
   CK(cudaEventElapsedTime(&ms, p->ev0, p->ev1));
+  CK(cudaEventElapsedTime(&ms2, p->ev1, p->ev2));
   p->eval_ms += ms;
   p->eval_launches++;
   p->eval_items += items;
+  p->prof[phase2 ? 1 : 0] += ms;
+  p->prof[2] += ms2;
+  p->prof[phase2 ? 4 : 3] += (double)items;
+  p->prof[5] += (double)n_imp;
   return 0;
 }
 
@@ -243,40 +249,45 @@ int prepare_eligible(lrcvt_plan* p, int n_sites, const int* site_comp, cudaStrea
   return 0;
 }
 
-// wavefront eval launch over list[0..n): persistent grid, capped at the
-// resident CTA count
+// eval launch over list[0..n): proposals -> p->imp
 int launch_eval(lrcvt_plan* p, bool phase2, const int* list, int n, int2* ss, double* dist,
                 cudaStream_t st) {
   const Geo& g = p->g;
-  const int var = !phase2 ? 0 : (g.dyadic ? 1 : 2);
-  const int blocks = grid_for(n, 128, p->wf_blocks[var] > 0 ? p->wf_blocks[var] : 148);
   if (!phase2)
-    k_eval_p1<128><<<grid_for(n, 128), 128, 0, st>>>(list, n, g, p->comp, ss, dist, p->site_pos, p->bm, p->imp, p->counters);
+    k_eval_p1<128><<<grid_for(n, 128), 128, 0, st>>>(list, n, g, p->comp, p->nbm, ss, dist, p->site_pos,
+                                                     p->bm, p->imp, p->counters);
   else if (g.dyadic)
-    k_eval_p2<64, true><<<grid_for(n, 64), 64, 0, st>>>(list, n, g, p->comp, ss, dist, p->site_pos, p->bm, p->imp, p->counters);
+    k_eval_p2<64, true><<<grid_for(n, 64), 64, 0, st>>>(list, n, g, p->comp, p->nbm, ss, dist, p->site_pos,
+                                                        p->bm, p->imp, p->counters);
   else
-    k_eval_p2<64, false><<<grid_for(n, 64), 64, 0, st>>>(list, n, g, p->comp, ss, dist, p->site_pos, p->bm, p->imp, p->counters);
-  CKL("k_eval_wf");
+    k_eval_p2<64, false><<<grid_for(n, 64), 64, 0, st>>>(list, n, g, p->comp, p->nbm, ss, dist, p->site_pos,
+                                                         p->bm, p->imp, p->counters);
+  CKL("k_eval");
+  return 0;
+}
+
+// commit + enqueue of up to n_upper proposals (count read on device)
+int launch_commit(lrcvt_plan* p, int n_upper, int2* ss, double* dist, int* next, cudaStream_t st) {
+  k_commit<<<grid_for(n_upper, 128), 128, 0, st>>>(p->imp, p->counters, p->g, p->nbm, ss, dist, p->bm, next);
+  CKL("k_commit");
   return 0;
 }
 
 // one relaxation round loop (_kernels.py:337-385). list_in holds n items.
 int run_phase(lrcvt_plan* p, bool phase2, int** cur, int** nxt, int n, int2* ss, double* dist,
               lrcvt_classify_stats* st_out, cudaStream_t st) {
-  const Geo& g = p->g;
   while (n > 0) {
     st_out->rounds++;
     st_out->evaluations += n;
-    CK(cudaMemsetAsync(p->counters, 0, sizeof(int) * (C_WORK + 1), st));
-    const int blocks = grid_for(n, 128);
+    CK(cudaMemsetAsync(p->counters, 0, sizeof(int) * 2, st));
     if (p->timing) CK(cudaEventRecord(p->ev0, st));
     CKR(launch_eval(p, phase2, *cur, n, ss, dist, st));
     if (p->timing) CK(cudaEventRecord(p->ev1, st));
-    k_commit<<<blocks, 128, 0, st>>>(p->imp, p->counters, g, p->comp, ss, dist, p->bm, *nxt);
-    CKL("k_commit");
+    CKR(launch_commit(p, n, ss, dist, *nxt, st));
     LAUNCHED(2);
+    if (p->timing) CK(cudaEventRecord(p->ev2, st));
     CKR(sync_counters(p, st, 2));
-    if (p->timing) CKR(note_eval(p, n));
+    if (p->timing) CKR(note_eval(p, n, phase2, p->h_counters[C_NIMP]));
     st_out->commits += p->h_counters[C_NIMP];
     n = p->h_counters[C_NNEXT];
     int* t = *cur; *cur = *nxt; *nxt = t;
@@ -331,6 +342,7 @@ int lrcvt_plan_create(lrcvt_plan** plan, int64_t nx, int64_t ny, int64_t nz, dou
   rc |= dalloc(&p->eligible, nin);
   rc |= dalloc(&p->imp, nin);
   rc |= dalloc(&p->bm, p->bm_words);
+  rc |= dalloc(&p->nbm, n);
   rc |= dalloc(&p->has_site, n_components > 0 ? n_components : 1);
   rc |= dalloc(&p->site_pos, S);
   rc |= dalloc(&p->new_pos, S);
@@ -344,6 +356,7 @@ int lrcvt_plan_create(lrcvt_plan** plan, int64_t nx, int64_t ny, int64_t nz, dou
   rc |= dalloc(&p->seg_b, S);
   rc |= dalloc(&p->seg_e, S);
   if (rc) { lrcvt_plan_destroy(p); return LRCVT_E_NOMEM; }
+  k_nbr_mask<<<grid_for(n, 256, 148 * 16), 256, 0, st>>>(p->g, d_comp, p->nbm);
   if (cudaMemsetAsync(p->bm, 0, sizeof(uint32_t) * p->bm_words, st) != cudaSuccess) {
     lrcvt_plan_destroy(p);
     return set_error(LRCVT_E_CUDA, "bitmap clear");
@@ -363,17 +376,6 @@ int lrcvt_plan_create(lrcvt_plan** plan, int64_t nx, int64_t ny, int64_t nz, dou
     need = b > need ? b : need;
   }
   p->cub_bytes = need;
-  {
-    int dev = 0, sms = 148, nb = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_eval_wf<false, true>, 128, 0);
-    p->wf_blocks[0] = nb * sms;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_eval_wf<true, true>, 128, 0);
-    p->wf_blocks[1] = nb * sms;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_eval_wf<true, false>, 128, 0);
-    p->wf_blocks[2] = nb * sms;
-  }
   if (dalloc((char**)&p->cub_tmp, (int64_t)need)) { lrcvt_plan_destroy(p); return LRCVT_E_NOMEM; }
   *plan = p;
   return 0;
@@ -381,7 +383,7 @@ int lrcvt_plan_create(lrcvt_plan** plan, int64_t nx, int64_t ny, int64_t nz, dou
 
 int lrcvt_plan_destroy(lrcvt_plan* p) {
   if (!p) return 0;
-  void* bufs[] = {p->counters, p->list_a, p->list_b, p->eligible, p->imp, p->bm, p->has_site,
+  void* bufs[] = {p->counters, p->list_a, p->list_b, p->eligible, p->imp, p->bm, p->nbm, p->has_site,
                   p->site_pos, p->new_pos, p->sk_key, p->sk_key2, p->sk_val, p->sk_val2, p->sk_d,
                   p->acc, p->sums, p->vt_key, p->vt_key2, p->vt_idx, p->vt_idx2, p->vt_terms,
                   p->seg_b, p->seg_e, p->cub_tmp};
@@ -390,6 +392,7 @@ int lrcvt_plan_destroy(lrcvt_plan* p) {
   if (p->h_counters) cudaFreeHost(p->h_counters);
   if (p->ev0) cudaEventDestroy(p->ev0);
   if (p->ev1) cudaEventDestroy(p->ev1);
+  if (p->ev2) cudaEventDestroy(p->ev2);
   delete p;
   return 0;
 }
@@ -401,7 +404,9 @@ int lrcvt_plan_set_timing(lrcvt_plan* p, int enable) {
   if (enable && !p->ev0) {
     CK(cudaEventCreate(&p->ev0));
     CK(cudaEventCreate(&p->ev1));
+    CK(cudaEventCreate(&p->ev2));
   }
+  for (double& d : p->prof) d = 0.0;
   p->timing = enable != 0;
   p->eval_launches = 0;
   p->eval_items = 0;
@@ -414,6 +419,12 @@ int lrcvt_plan_timing(const lrcvt_plan* p, int64_t* launches, int64_t* items, do
   *launches = p->eval_launches;
   *items = p->eval_items;
   *ms = p->eval_ms;
+  return 0;
+}
+
+int lrcvt_plan_profile(const lrcvt_plan* p, double* out6) {
+  if (!p || !out6) return set_error(LRCVT_E_ARG, "lrcvt_plan_profile");
+  for (int i = 0; i < 6; i++) out6[i] = p->prof[i];
   return 0;
 }
 
@@ -458,8 +469,8 @@ int lrcvt_classify(lrcvt_plan* p, int64_t n_sites, const double* d_site_pos,
   }
   // groups -> seeds, then the phase-1 worklist (tessellation.py:151)
   CK(cudaMemsetAsync(p->counters, 0, sizeof(int) * 2, st));
-  k_seed_groups<<<grid_for(S, 128), 128, 0, st>>>(g, p->comp, p->sk_key2, p->sk_val2, p->sk_d, S, ss,
-                                                  d_dist, p->bm, p->list_a, p->counters);
+  k_seed_groups<<<grid_for(S, 128), 128, 0, st>>>(g, p->nbm, p->sk_key2, p->sk_val2, p->sk_d, S, ss,
+                                                  d_dist, p->bm, p->list_a, p->counters);  // marks bm (round-1 frontier)
   CKL("k_seed_groups"); LAUNCHED(1);
   CKR(sync_counters(p, st, 2));
   int n_wl = p->h_counters[C_NNEXT];
@@ -478,16 +489,17 @@ int lrcvt_classify(lrcvt_plan* p, int64_t n_sites, const double* d_site_pos,
     if (run_phase(p, true, &cur, &nxt, n_wl, ss, d_dist, stats, st)) return LRCVT_E_CUDA;
     stats->sweeps++;
     stats->evaluations += n_el;
-    CK(cudaMemsetAsync(p->counters, 0, sizeof(int) * (C_WORK + 1), st));
-    const int blocks = grid_for(n_el, 128);
+    CK(cudaMemsetAsync(p->counters, 0, sizeof(int) * 2, st));
     if (p->timing) CK(cudaEventRecord(p->ev0, st));
+    // verification sweep: full eval over eligible; improved voxels' neighbours
+    // become the next worklist (tessellation.py:179-189)
     CKR(launch_eval(p, true, p->eligible, n_el, ss, d_dist, st));
     if (p->timing) CK(cudaEventRecord(p->ev1, st));
-    k_commit<<<blocks, 128, 0, st>>>(p->imp, p->counters, g, p->comp, ss, d_dist, p->bm, cur);
-    CKL("k_commit sweep");
+    CKR(launch_commit(p, n_el, ss, d_dist, cur, st));
     LAUNCHED(2);
+    if (p->timing) CK(cudaEventRecord(p->ev2, st));
     CKR(sync_counters(p, st, 2));
-    if (p->timing) CKR(note_eval(p, n_el));
+    if (p->timing) CKR(note_eval(p, n_el, true, p->h_counters[C_NIMP]));
     if (p->h_counters[C_NIMP] == 0) break;
     stats->commits += p->h_counters[C_NIMP];
     n_wl = p->h_counters[C_NNEXT];

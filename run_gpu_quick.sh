@@ -7,7 +7,7 @@ import json,sys
 for l in sys.stdin:
     if l.startswith('{'):
         d=json.loads(l); r=d['roofline']
-        print(d['config']['workload'][:12], 'ms/step %.3f'%d['ms_per_step'], 'Gvox/s %.3f'%(d['value']/1e9), 'eval avg us %.1f'%r['avg_launch_us'], 'eval share %.2f'%r['eval_share_of_step'], 'launches', d['gpu_launches'])
+        print(d['config']['workload'][:12], 'ms/step %.3f'%d['ms_per_step'], 'Gvox/s %.3f'%(d['value']/1e9), 'eval avg us %.1f'%r['avg_launch_us'], 'eval share %.2f'%r['eval_share_of_step'], 'launches', d['gpu_launches'], {k: round(v,3) for k,v in r['breakdown_ms_per_step'].items()})
     else: print(l.rstrip()[:300])
 "
 done
