@@ -119,6 +119,23 @@ int lrcvt_component_table(int64_t nx, int64_t ny, int64_t nz, const int32_t *d_c
                           const int32_t *d_layer, int32_t n_components, uint64_t *d_count,
                           int32_t *d_bbox, int32_t *d_layer_of, void *stream);
 
+/* aggregate_moments core (pipeline.py:187-238) + per-cell histograms
+ * (stats.py:194-203 rule on fixed global axes). Cells: regions 0..n_sites-1
+ * (site_of == r) and stray cells n_sites + c (unassigned in-band voxels of
+ * component c); n_cells = n_sites + n_components. field_ptrs is a HOST array
+ * of n_fields DEVICE float32[n] pointers; pairs a HOST int32[n_pairs][2] of
+ * field indices. Outputs (device): d_count int64[n_cells]; d_sums
+ * float64[n_cells][n_pairs][15] raw power sums in ORDERS order (stats.py:19);
+ * d_minmax float64[n_cells][n_pairs][4] = (min_x, max_x, min_y, max_y).
+ * n_bins > 0 also fills d_hist int64[n_cells][n_fields][n_bins + 2] (bins,
+ * underflow, overflow) on axes = HOST float64[n_fields][2] (lo, hi); NaN
+ * entries are replaced by the in-band min / max (hi <= lo -> lo + 1). */
+int lrcvt_aggregate(int64_t n, int32_t n_fields, const float *const *field_ptrs,
+                    const int32_t *d_component, const int32_t *d_site_of, int32_t n_sites,
+                    int32_t n_components, int32_t n_pairs, const int32_t *pairs, int32_t n_bins,
+                    double *axes, int64_t *d_count, double *d_sums, double *d_minmax,
+                    int64_t *d_hist, void *stream);
+
 /* Instrumentation for bench.py: enable CUDA-event timing of every k_eval
  * launch (the dominant kernel) on the plan; read back launches, voxels
  * evaluated and summed device milliseconds. lrcvt_launch_count() counts this

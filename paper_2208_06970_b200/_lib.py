@@ -33,10 +33,6 @@ class ClassifyStats(ctypes.Structure):
         return {name: int(getattr(self, name)) for name, _ in self._fields_}
 
 
-class AggregateStats(ctypes.Structure):
-    _fields_ = [("n_cells", c_int64), ("n_pairs", c_int64), ("n_fields", c_int64)]
-
-
 # name -> (restype, argtypes); mirrors include/lrcvt_cuda.h exactly
 SIGNATURES = {
     "lrcvt_version": (c_int, []),
@@ -83,8 +79,8 @@ SIGNATURES = {
     ),
     "lrcvt_aggregate": (
         c_int,
-        [c_int64, c_int32, c_void_p, c_void_p, c_void_p, c_int32, c_void_p, c_int32, c_void_p,
-         c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p],
+        [c_int64, c_int32, c_void_p, c_void_p, c_void_p, c_int32, c_int32, c_int32, c_void_p,
+         c_int32, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p],
     ),
 }
 

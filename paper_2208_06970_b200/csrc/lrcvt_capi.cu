@@ -7,6 +7,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "../../include/lrcvt_cuda.h"
 #include "classify.cuh"
@@ -14,6 +15,7 @@
 #include "masks.cuh"
 #include "eval_p1.cuh"
 #include "eval_p2.cuh"
+#include "aggregate.cuh"
 
 using namespace lrcvt;
 
@@ -78,6 +80,11 @@ struct EligiblePred {
 struct IsRoot {
   const int* L;
   __device__ __forceinline__ bool operator()(const int v) const { return L[v] == v; }
+};
+
+struct IsInband {
+  const int* comp;
+  __device__ __forceinline__ bool operator()(const int v) const { return comp[v] >= 0; }
 };
 
 struct CountInband {
@@ -692,6 +699,119 @@ int lrcvt_component_table(int64_t nx, int64_t ny, int64_t nz, const int32_t* d_c
   k_ccl_table<<<grid_for(g.n, 256, 148 * 16), 256, 0, st>>>(g, d_component, d_layer,
                                                             (unsigned long long*)d_count, d_bbox, d_layer_of);
   CKL("k_ccl_table"); LAUNCHED(1);
+  return 0;
+}
+
+
+int lrcvt_aggregate(int64_t n, int32_t n_fields, const float* const* field_ptrs, const int32_t* d_component,
+                    const int32_t* d_site_of, int32_t n_sites, int32_t n_components, int32_t n_pairs,
+                    const int32_t* pairs, int32_t n_bins, double* axes, int64_t* d_count, double* d_sums,
+                    double* d_minmax, int64_t* d_hist, void* stream) {
+  if (n < 0 || n >= (int64_t(1) << 31) || n_fields < 1 || n_fields > 16 || !field_ptrs || !d_component ||
+      !d_site_of || n_sites < 0 || n_components < 0 || n_pairs < 1 || n_pairs > 136 || !pairs || n_bins < 0 ||
+      n_bins > 1024 || !d_count || !d_sums || !d_minmax || (n_bins > 0 && (!d_hist || !axes)))
+    return set_error(LRCVT_E_ARG, "lrcvt_aggregate: bad arguments");
+  for (int i = 0; i < 2 * n_pairs; i++)
+    if (pairs[i] < 0 || pairs[i] >= n_fields) return set_error(LRCVT_E_ARG, "lrcvt_aggregate: bad pair");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int n_cells = n_sites + n_components;
+  if (n_cells == 0) return 0;
+  int *inband = nullptr, *cnt = nullptr, *key = nullptr, *key2 = nullptr, *val = nullptr, *val2 = nullptr;
+  int *segb = nullptr, *sege = nullptr, *d_pairs = nullptr;
+  const float** d_fields = nullptr;
+  double* d_axes = nullptr;
+  unsigned long long* d_lohi = nullptr;
+  void* tmp = nullptr;
+  size_t b1 = 0, b2 = 0;
+  int h_cnt = 0;
+  IsInband pred{d_component};
+  cub::CountingInputIterator<int> it(0);
+  CK(cudaMallocAsync((void**)&inband, sizeof(int) * (n > 0 ? n : 1), st));
+  CK(cudaMallocAsync((void**)&cnt, sizeof(int), st));
+  CK(cub::DeviceSelect::If(nullptr, b1, it, inband, cnt, (int)n, pred, st));
+  CK(cudaMallocAsync(&tmp, b1, st));
+  CK(cub::DeviceSelect::If(tmp, b1, it, inband, cnt, (int)n, pred, st));
+  CK(cudaMemcpyAsync(&h_cnt, cnt, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  CK(cudaFreeAsync(tmp, st));
+  tmp = nullptr;
+  const int m = h_cnt;
+  const int mm = m > 0 ? m : 1;
+  CK(cudaMallocAsync((void**)&key, sizeof(int) * mm, st));
+  CK(cudaMallocAsync((void**)&key2, sizeof(int) * mm, st));
+  CK(cudaMallocAsync((void**)&val, sizeof(int) * mm, st));
+  CK(cudaMallocAsync((void**)&val2, sizeof(int) * mm, st));
+  CK(cudaMallocAsync((void**)&segb, sizeof(int) * n_cells, st));
+  CK(cudaMallocAsync((void**)&sege, sizeof(int) * n_cells, st));
+  CK(cudaMallocAsync((void**)&d_pairs, sizeof(int) * 2 * n_pairs, st));
+  CK(cudaMallocAsync((void**)&d_fields, sizeof(float*) * n_fields, st));
+  CK(cudaMemcpyAsync(d_pairs, pairs, sizeof(int) * 2 * n_pairs, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d_fields, field_ptrs, sizeof(float*) * n_fields, cudaMemcpyHostToDevice, st));
+  CK(cudaMemsetAsync(segb, 0, sizeof(int) * n_cells, st));
+  CK(cudaMemsetAsync(sege, 0, sizeof(int) * n_cells, st));
+  if (m > 0) {
+    k_agg_keys<<<grid_for(m, 256, 148 * 16), 256, 0, st>>>(inband, m, d_site_of, d_component, n_sites, key, val);
+    CKL("k_agg_keys"); LAUNCHED(1);
+    int bits = 1;
+    while ((1ll << bits) <= n_cells) bits++;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, b2, key, key2, val, val2, m, 0, bits, st));
+    CK(cudaMallocAsync(&tmp, b2, st));
+    CK(cub::DeviceRadixSort::SortPairs(tmp, b2, key, key2, val, val2, m, 0, bits, st));
+    k_segments<<<grid_for(m, 256, 148 * 16), 256, 0, st>>>(key2, m, n_cells, segb, sege);
+    CKL("k_segments"); LAUNCHED(1);
+  }
+  {
+    const int64_t warps = (int64_t)n_cells * n_pairs;
+    k_agg_moments<<<grid_for(warps * 32, 128), 128, 0, st>>>(val2, segb, sege, n_cells, d_fields, d_pairs,
+                                                             n_pairs, (long long*)d_count, d_sums, d_minmax);
+    CKL("k_agg_moments"); LAUNCHED(1);
+  }
+  if (n_bins > 0) {
+    CK(cudaMallocAsync((void**)&d_axes, sizeof(double) * 2 * n_fields, st));
+    bool any_auto = false;
+    for (int f = 0; f < n_fields; f++) any_auto |= !(axes[2 * f] == axes[2 * f]) || !(axes[2 * f + 1] == axes[2 * f + 1]);
+    if (any_auto) {  // stats.py:186-191 auto range over in-band values
+      CK(cudaMallocAsync((void**)&d_lohi, sizeof(unsigned long long) * 2 * n_fields, st));
+      std::vector<unsigned long long> init(2 * n_fields);
+      for (int f = 0; f < n_fields; f++) { init[2 * f] = ~0ull; init[2 * f + 1] = 0ull; }
+      CK(cudaMemcpyAsync(d_lohi, init.data(), sizeof(unsigned long long) * 2 * n_fields, cudaMemcpyHostToDevice, st));
+      for (int f = 0; f < n_fields; f++) {
+        if (m > 0) {
+          k_field_range<<<grid_for(m, 256, 148 * 8), 256, 0, st>>>(inband, m, field_ptrs[f], d_lohi + 2 * f);
+          CKL("k_field_range"); LAUNCHED(1);
+        }
+      }
+      CK(cudaMemcpyAsync(init.data(), d_lohi, sizeof(unsigned long long) * 2 * n_fields, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      for (int f = 0; f < n_fields; f++) {
+        if (axes[2 * f] == axes[2 * f] && axes[2 * f + 1] == axes[2 * f + 1]) continue;
+        double lo = 0.0, hi = 1.0;
+        if (m > 0) {
+          auto k2f = [](unsigned long long k) {
+            const unsigned u = (unsigned)k;
+            const unsigned bits = (u & 0x80000000u) ? (u ^ 0x80000000u) : ~u;
+            float fv;
+            memcpy(&fv, &bits, 4);
+            return (double)fv;
+          };
+          lo = k2f(init[2 * f]);
+          hi = k2f(init[2 * f + 1]);
+        }
+        if (hi <= lo) hi = lo + 1.0;  // stats.py:189-190
+        axes[2 * f] = lo;
+        axes[2 * f + 1] = hi;
+      }
+    }
+    CK(cudaMemcpyAsync(d_axes, axes, sizeof(double) * 2 * n_fields, cudaMemcpyHostToDevice, st));
+    const int64_t warps = (int64_t)n_cells * n_fields;
+    k_agg_hist<1024><<<grid_for(warps * 32, 128), 128, 0, st>>>(val2, segb, sege, n_cells, d_fields, n_fields,
+                                                                d_axes, n_bins, (long long*)d_hist);
+    CKL("k_agg_hist"); LAUNCHED(1);
+  }
+  for (void* b : {(void*)inband, (void*)cnt, (void*)key, (void*)key2, (void*)val, (void*)val2, (void*)segb,
+                  (void*)sege, (void*)d_pairs, (void*)d_fields, (void*)d_axes, (void*)d_lohi, tmp})
+    if (b) CK(cudaFreeAsync(b, st));
+  CK(cudaStreamSynchronize(st));
   return 0;
 }
 

@@ -22,7 +22,7 @@ def declared_symbols():
 def test_header_declares_entry_points():
     syms = declared_symbols()
     for must in ("lrcvt_plan_create", "lrcvt_classify", "lrcvt_centroidal_update", "lrcvt_isobands",
-                 "lrcvt_label_components", "lrcvt_segment_hit_t"):
+                 "lrcvt_label_components", "lrcvt_aggregate", "lrcvt_segment_hit_t"):
         assert must in syms
 
 
