@@ -171,6 +171,59 @@ def run_reference(args, cfg, world, rank):
     print(json.dumps(line), flush=True)
 
 
+def one_off_passes(grid, labels, eng, config, S, reps=3):
+    """Device-resident timing of the passes reported beside the iteration
+    metric: isoband + component masks, and the per-cell
+    aggregation (3 field pairs' moments + 64-bin histograms of f and g)."""
+    import ctypes
+
+    import torch
+
+    from paper_2208_06970_b200 import _lib
+    from paper_2208_06970_b200.pipeline import cell_aggregates_device
+
+    L = _lib.lib()
+    st = _lib.stream_handle(torch)
+    n = grid.size
+    nx, ny, nz = grid.dims
+    f = torch.from_numpy(grid.fields["f"]).cuda()
+    g = torch.from_numpy(grid.fields["g"]).cuda()
+    iso = torch.tensor(CONFIGS[config]["iso"], dtype=torch.float64, device="cuda")
+    layer = torch.empty(n, dtype=torch.int32, device="cuda")
+    comp = torch.empty(n, dtype=torch.int32, device="cuda")
+    nc = ctypes.c_int32()
+
+    def masks():
+        _lib.check(L.lrcvt_isobands(n, f.data_ptr(), iso.data_ptr(), iso.numel(), layer.data_ptr(), st), "iso")
+        _lib.check(L.lrcvt_label_components(nx, ny, nz, layer.data_ptr(), iso.numel() - 1, comp.data_ptr(),
+                                            ctypes.byref(nc), st), "ccl")
+
+    ss_site = eng.ss[:, 0].contiguous()
+    pair_idx = np.array([[0, 0], [0, 1], [1, 1]], np.int32)
+
+    def agg():
+        cell_aggregates_device([f, g], eng.comp, ss_site, S, labels.n_components, pair_idx, bins=64)
+
+    out = {}
+    for name, fn, bytes_per_voxel in (("masks", masks, 8 + 12), ("aggregate", agg, 16)):
+        fn()
+        torch.cuda.synchronize()
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record()
+        for _ in range(reps):
+            fn()
+        t1.record()
+        torch.cuda.synchronize()
+        ms = t0.elapsed_time(t1) / reps
+        out[name] = {"ms": ms, "voxels_per_s": n / (ms / 1e3),
+                     "algorithmic_GBps": bytes_per_voxel * n / (ms / 1e3) / 1e9}
+    out["masks"]["note"] = "isobands (f32 read + i32 write) + 6-conn CCL with dense ids; bytes counted 20/voxel"
+    out["aggregate"]["note"] = ("per-cell n, 15 power sums x 3 pairs, min/max, 64-bin hist of f and g; "
+                                "16 B/voxel (f, g, site_of, component)")
+    return out
+
+
 def cpu_baseline(grid, labels, params, weights, pos, sc, budget_s=20.0, max_iters=3):
     from oracle import oracle
 
@@ -198,6 +251,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-passes", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     cfg = CONFIGS[args.config]
@@ -281,8 +335,12 @@ def main():
     b_iter = 29.0 * n + 20.0 * E / args.steps + 16.0 * C / args.steps
     traffic = None
     prof_path = ROOT / "profiles" / f"ncu_{args.config}_k_eval.json"
-    if prof_path.exists():
-        traffic = json.loads(prof_path.read_text()).get("dram_bytes_per_launch")
+    if prof_path.exists() and el.value:
+        per_item = json.loads(prof_path.read_text()).get("dram_bytes_per_item")
+        if per_item:
+            traffic = per_item * eitems.value / el.value
+
+    passes = one_off_passes(grid, labels, eng, args.config, S) if not args.no_passes else None
 
     # end-to-end through the public API with host numpy in/out
     e2e = None
@@ -303,11 +361,13 @@ def main():
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
         h2d = 2 * S * (24 + 4)
-        d2h = n * (8 + 8 + 1) + S * (24 + 8) + 64
+        d2h = S * (24 + 8) + 64
         e2e = {"value": n * ke * world / dt, "unit": "voxels/s", "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h,
-               "note": "voronoi_classify + centroidal_update per step, numpy in/out; weights array resident "
-                       "after first upload"}
+               "note": "public API per step: voronoi_classify(grid, labels, sites, weights) + "
+                       "centroidal_update(tess) with host Site lists in and out (sites + comps H2D, new "
+                       "positions + displacements D2H); per-voxel tessellation arrays stay in HBM until read; "
+                       "labels/weights uploaded once"}
 
     line = {
         "metric": "CVT-iteration voxels/s", "value": value, "unit": "voxels/s", "n_gpus": world,
@@ -331,6 +391,8 @@ def main():
     }
     if e2e:
         line["e2e"] = e2e
+    if passes:
+        line["passes"] = passes
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(grid, labels, params, weights, pos_start, sc_np)
     if rank == 0:

@@ -149,12 +149,36 @@ def default_pairs(field_names: list[str]) -> list[tuple[str, str]]:
     return [(a, b) for i, a in enumerate(field_names) for b in field_names[i:]]
 
 
-def cell_aggregates(grid: VoxelGrid, labels: LabelMap, site_of: np.ndarray, n_sites: int,
-                    pairs: list[tuple[str, str]], bins: int = 0, axes=None) -> dict:
-    """GPU per-cell pass (lrcvt_aggregate). Cells 0..S-1 are regions, S + c
-    is the unassigned remainder of component c. Returns numpy arrays."""
+def cell_aggregates_device(fields_d: list, comp_d, site_d, n_sites: int, n_comp: int,
+                           pair_idx: np.ndarray, bins: int = 0, axes: np.ndarray | None = None) -> dict:
+    """Device-resident per-cell pass (lrcvt_aggregate) on CUDA tensors:
+    fields_d float32[N] each, comp_d / site_d int32[N]. Returns CUDA tensors
+    count[C], sums[C, P, 15], minmax[C, P, 4] (+ hist[C, F, bins + 2]) and the
+    axes actually used (numpy [F, 2])."""
     torch = _lib.require_cuda()
     L = _lib.lib()
+    n_cells = n_sites + n_comp
+    P, F = len(pair_idx), len(fields_d)
+    C = max(n_cells, 1)
+    count = torch.zeros(C, dtype=torch.int64, device="cuda")
+    sums = torch.zeros((C, P, 15), dtype=torch.float64, device="cuda")
+    minmax = torch.zeros((C, P, 4), dtype=torch.float64, device="cuda")
+    hist = torch.zeros((C, F, bins + 2), dtype=torch.int64, device="cuda") if bins else None
+    ptrs = (ctypes.c_void_p * F)(*[f.data_ptr() for f in fields_d])
+    pr = np.ascontiguousarray(pair_idx, dtype=np.int32)
+    ax = np.full((F, 2), np.nan) if axes is None else np.array(axes, dtype=np.float64).reshape(F, 2).copy()
+    _lib.check(L.lrcvt_aggregate(int(comp_d.numel()), F, ptrs, comp_d.data_ptr(), site_d.data_ptr(), n_sites,
+                                 n_comp, P, pr.ctypes.data, bins, ax.ctypes.data, count.data_ptr(),
+                                 sums.data_ptr(), minmax.data_ptr(), hist.data_ptr() if hist is not None else None,
+                                 _lib.stream_handle(torch)), "lrcvt_aggregate")
+    return {"n_cells": n_cells, "count": count, "sums": sums, "minmax": minmax, "hist": hist, "axes": ax}
+
+
+def cell_aggregates(grid: VoxelGrid, labels: LabelMap, site_of: np.ndarray, n_sites: int,
+                    pairs: list[tuple[str, str]], bins: int = 0, axes=None) -> dict:
+    """GPU per-cell pass from host arrays. Cells 0..S-1 are regions, S + c is
+    the unassigned remainder of component c. Returns numpy arrays."""
+    torch = _lib.require_cuda()
     names: list[str] = []
     for a, b in pairs:
         for nm in (a, b):
@@ -169,27 +193,19 @@ def cell_aggregates(grid: VoxelGrid, labels: LabelMap, site_of: np.ndarray, n_si
     n_comp = labels.n_components
     if labels.component.size and labels.component.max() >= n_comp:
         n_comp = int(labels.component.max()) + 1
-    n_cells = n_sites + n_comp
-    P, F = len(pairs), len(names)
-    count = torch.zeros(max(n_cells, 1), dtype=torch.int64, device="cuda")
-    sums = torch.zeros((max(n_cells, 1), P, 15), dtype=torch.float64, device="cuda")
-    minmax = torch.zeros((max(n_cells, 1), P, 4), dtype=torch.float64, device="cuda")
-    hist = torch.zeros((max(n_cells, 1), F, bins + 2), dtype=torch.int64, device="cuda") if bins else None
-    ptrs = (ctypes.c_void_p * F)(*[f.data_ptr() for f in fields_d])
     pr = np.array([[names.index(a), names.index(b)] for a, b in pairs], dtype=np.int32)
-    ax = np.full((F, 2), np.nan)
+    ax = np.full((len(names), 2), np.nan)
     if axes is not None:
         for i, nm in enumerate(names):
             if nm in axes:
                 ax[i] = axes[nm]
-    _lib.check(L.lrcvt_aggregate(grid.size, F, ptrs, comp_d.data_ptr(), site_d.data_ptr(), n_sites, n_comp, P,
-                                 pr.ctypes.data, bins, ax.ctypes.data, count.data_ptr(), sums.data_ptr(),
-                                 minmax.data_ptr(), hist.data_ptr() if hist is not None else None,
-                                 _lib.stream_handle(torch)), "lrcvt_aggregate")
-    out = {"names": names, "n_cells": n_cells, "count": count.cpu().numpy()[:n_cells],
-           "sums": sums.cpu().numpy()[:n_cells], "minmax": minmax.cpu().numpy()[:n_cells], "axes": ax}
-    if hist is not None:
-        out["hist"] = hist.cpu().numpy()[:n_cells]
+    d = cell_aggregates_device(fields_d, comp_d, site_d, n_sites, n_comp, pr, bins, ax)
+    n_cells = d["n_cells"]
+    out = {"names": names, "n_cells": n_cells, "count": d["count"].cpu().numpy()[:n_cells],
+           "sums": d["sums"].cpu().numpy()[:n_cells], "minmax": d["minmax"].cpu().numpy()[:n_cells],
+           "axes": d["axes"]}
+    if d["hist"] is not None:
+        out["hist"] = d["hist"].cpu().numpy()[:n_cells]
     return out
 
 

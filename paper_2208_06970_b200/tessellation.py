@@ -63,6 +63,54 @@ class Tessellation:
         return np.array([s.component_id for s in self.sites], dtype=np.int32)
 
 
+class DeviceTessellation(Tessellation):
+    """A Tessellation whose per-voxel arrays (site_of, dist, src, state) stay
+    in HBM until first read: attribute access materialises them as numpy in
+    the reference dtypes, once. centroidal_update() consumes the device copy
+    directly, so a classify -> update step moves no per-voxel data over PCIe
+    unless the caller looks at the arrays. Assigning an array makes the host
+    copy authoritative from then on."""
+
+    def __init__(self, dims, spacing, component, sites, report, weights, engine, dev):
+        self._dev = dev  # (ss int32[N, 2], dist float64[N], state uint8[N]) on the GPU
+        self._host: dict = {}
+        self._dirty = False
+        self._engine = engine
+        self.dims = dims
+        self.spacing = spacing
+        self.component = component
+        self.sites = sites
+        self.report = report
+        self.weights = weights
+
+    def _get(self, name):
+        host = self._host
+        if name not in host:
+            ss, dist, state = self._dev
+            if name in ("site_of", "src"):
+                a = ss.cpu().numpy()
+                host.setdefault("site_of", np.ascontiguousarray(a[:, 0]))
+                host.setdefault("src", np.ascontiguousarray(a[:, 1]))
+            elif name == "dist":
+                host["dist"] = dist.cpu().numpy()
+            else:
+                host["state"] = state.cpu().numpy()
+        return host[name]
+
+    def _set(self, name, value):
+        self._host[name] = value
+        self._dirty = True
+
+    site_of = property(lambda self: self._get("site_of"), lambda self, v: self._set("site_of", v))
+    dist = property(lambda self: self._get("dist"), lambda self, v: self._set("dist", v))
+    src = property(lambda self: self._get("src"), lambda self, v: self._set("src", v))
+    state = property(lambda self: self._get("state"), lambda self, v: self._set("state", v))
+
+    def device_state(self):
+        """(ss, dist, state) device tensors while they are authoritative, else None."""
+        return None if self._dirty else self._dev
+
+
 def voxel_length(dims, spacing) -> float:
     """Mean spacing over the axes that extend (tessellation.py:74-79)."""
     active = [s for d, s in zip(dims, spacing) if d > 1]
@@ -125,22 +173,33 @@ class Engine:
     def inband(self) -> int:
         return int(self.L.lrcvt_plan_inband(self.plan))
 
-    def classify(self, site_pos, site_comp, want_state=True) -> dict:
-        """site_pos float64[S,3], site_comp int32[S] (device tensors)."""
+    def classify(self, site_pos, site_comp, want_state=True, out=None) -> dict:
+        """site_pos float64[S,3], site_comp int32[S] (device tensors). Writes
+        the engine's own state buffers, or `out` = (ss, dist, state) tensors."""
         S = int(site_pos.shape[0])
         self.reserve(S)
+        ss, dist, state = out if out is not None else (self.ss, self.dist, self.state)
         rc = _lib.check(self.L.lrcvt_classify(
-            self.plan, S, _lib.ptr(site_pos), _lib.ptr(site_comp), self.ss.data_ptr(),
-            self.dist.data_ptr(), self.state.data_ptr() if want_state else None,
+            self.plan, S, _lib.ptr(site_pos), _lib.ptr(site_comp), ss.data_ptr(),
+            dist.data_ptr(), state.data_ptr() if want_state else None,
             ctypes.byref(self.stats), _lib.stream_handle(self.torch)), "lrcvt_classify")
-        self.version += 1
+        if out is None:
+            self.version += 1
         if rc > 0:
             raise ValueError(f"{rc} sites sit outside their recorded component")
         return self.stats.as_dict()
 
+    def new_state(self):
+        """Fresh (ss, dist, state) device tensors from torch's caching allocator."""
+        t = self.torch
+        return (t.empty((self.n, 2), dtype=t.int32, device="cuda"),
+                t.empty(self.n, dtype=t.float64, device="cuda"),
+                t.empty(self.n, dtype=t.uint8, device="cuda"))
+
     def centroidal(self, site_pos, site_comp, weight_mode: int, weights, backoff: float,
-                   want_sums=False):
+                   want_sums=False, ss=None):
         torch = self.torch
+        ss = self.ss if ss is None else ss
         S = int(site_pos.shape[0])
         self.reserve(S)
         new_pos = torch.empty((S, 3), dtype=torch.float64, device="cuda")
@@ -148,7 +207,7 @@ class Engine:
         sums = torch.empty((4, S), dtype=torch.float64, device="cuda") if want_sums else None
         empty = ctypes.c_int64(0)
         _lib.check(self.L.lrcvt_centroidal_update(
-            self.plan, S, _lib.ptr(site_pos), _lib.ptr(site_comp), self.ss.data_ptr(),
+            self.plan, S, _lib.ptr(site_pos), _lib.ptr(site_comp), ss.data_ptr(),
             weight_mode, _lib.ptr(weights), float(backoff), new_pos.data_ptr(), disp.data_ptr(),
             _lib.ptr(sums), ctypes.byref(empty), _lib.stream_handle(torch)),
             "lrcvt_centroidal_update")
@@ -251,23 +310,29 @@ def voronoi_classify(grid: VoxelGrid, labels: LabelMap, sites: list[Site],
     torch = _lib.require_cuda()
     eng = engine_for(labels, grid.spacing, len(sites))
     _, site_comp, pos_d, comp_d = _site_arrays(torch, sites)
-    st = eng.classify(pos_d, comp_d)
-    site_of, dist, src, state = eng.host_arrays()
+    dev = eng.new_state()
+    st = eng.classify(pos_d, comp_d, out=dev)
     report = {"rounds": st["rounds"], "sweeps": st["sweeps"],
               "components_without_sites": _no_site_components(labels, site_comp),
               "assigned": st["assigned"]}
-    tess = Tessellation(grid.dims, grid.spacing, site_of, dist, src, state, comp, list(sites),
-                        report, weights)
-    tess._b200 = (eng, eng.version, site_of, src)
+    tess = DeviceTessellation(grid.dims, grid.spacing, comp, list(sites), report, weights, eng, dev)
     tess._b200_stats = st
     return tess
 
 
-def _weights_mode(torch, weights: np.ndarray | None):
+def _weights_mode(torch, weights: np.ndarray | None, eng: "Engine | None" = None):
+    """float64 weights on the device; the upload is cached on the engine for
+    as long as the caller keeps passing the same array object."""
     if weights is None:
         return _lib.W_ONES, None
+    cached = getattr(eng, "_wcache", None) if eng is not None else None
+    if cached is not None and cached[0] is weights:
+        return _lib.W_F64, cached[1]
     w = np.ascontiguousarray(weights, dtype=np.float64)
-    return _lib.W_F64, torch.from_numpy(w).to("cuda")
+    dev = torch.from_numpy(w).to("cuda")
+    if eng is not None:
+        eng._wcache = (weights, dev)
+    return _lib.W_F64, dev
 
 
 def centroidal_update(tess: Tessellation, weights: np.ndarray | None = None) -> tuple[list[Site], float]:
@@ -279,10 +344,11 @@ def centroidal_update(tess: Tessellation, weights: np.ndarray | None = None) -> 
     if len(tess.sites) == 0:
         tess.report["empty_regions"] = 0
         return [], 0.0
-    cached = getattr(tess, "_b200", None)
-    if (cached is not None and cached[0].version == cached[1] and cached[2] is tess.site_of
-            and cached[3] is tess.src):
-        eng = cached[0]
+    dev = tess.device_state() if isinstance(tess, DeviceTessellation) else None
+    ss = None
+    if dev is not None:
+        eng = tess._engine
+        ss = dev[0]
     else:
         labels = LabelMap(tess.dims, np.zeros(0, np.int32), tess.component,
                           iso_values=[], field_name="")
@@ -292,9 +358,9 @@ def centroidal_update(tess: Tessellation, weights: np.ndarray | None = None) -> 
         eng.upload(tess.site_of, tess.src)
         del labels
     pos, _, pos_d, comp_d = _site_arrays(torch, tess.sites)
-    mode, w_d = _weights_mode(torch, weights)
+    mode, w_d = _weights_mode(torch, weights, eng)
     vlen = voxel_length(tess.dims, tess.spacing)
-    new_pos, disp, empty, _ = eng.centroidal(pos_d, comp_d, mode, w_d, 0.5 * vlen)
+    new_pos, disp, empty, _ = eng.centroidal(pos_d, comp_d, mode, w_d, 0.5 * vlen, ss=ss)
     tess.report["empty_regions"] = int(empty)
     new_pos = new_pos.cpu().numpy()
     disp = disp.cpu().numpy()
