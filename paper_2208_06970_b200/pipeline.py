@@ -56,37 +56,33 @@ def _combine_traces(block_traces: list[list[float]]) -> list[float]:
 
 
 def tessellate_block(grid: VoxelGrid, iso: IsobandSpec, seeding: SeedingParams, lloyd: LloydParams,
-                     block, total_in_band: int, comp_off: int):
+                     block, total_in_band: int, comp_off: int, label_fn=None, lloyd_fn=None):
     """One block of pipeline.py:82-108: sub-grid, local labels, alpha share,
     GPU Lloyd loop. Returns (sub_labels, tess, trace) or None when the block
     has no component."""
-    (x0, x1), (y0, y1), (z0, z1) = block
-    nx, ny, nz = grid.dims
-    sub_dims = (x1 - x0, y1 - y0, z1 - z0)
-    sub_fields = {name: np.ascontiguousarray(arr.reshape(nz, ny, nx)[z0:z1, y0:y1, x0:x1]).ravel()
-                  for name, arr in grid.fields.items()}
-    sub = VoxelGrid(sub_dims, grid.spacing, sub_fields)
-    sub_labels = label_components(classify_isobands(sub, iso))
+    sub = sub_grid(grid, block)
+    sub_labels = (label_fn or gpu_label)(sub, iso)
     if sub_labels.n_components == 0:
         return None
-    sub_seed = SeedingParams(
-        alpha=max(seeding.alpha * sub_labels.in_band_count() / max(total_in_band, 1), 1e-9),
-        gamma=seeding.gamma, weight_field=seeding.weight_field, block_size=seeding.block_size,
-        seed=seeding.seed + comp_off)
-    tess, trace = lrcvt(sub, sub_labels, sub_seed, lloyd)
+    sub_seed = block_seeding(seeding, sub_labels.in_band_count(), total_in_band, comp_off)
+    tess, trace = (lloyd_fn or lrcvt)(sub, sub_labels, sub_seed, lloyd)
     return sub, sub_labels, tess, trace
 
 
 def run_pipeline(grid: VoxelGrid, iso: IsobandSpec, seeding: SeedingParams, lloyd: LloydParams,
-                 blocks: tuple[int, int, int] = (1, 1, 1)) -> PipelineResult:
+                 blocks: tuple[int, int, int] = (1, 1, 1), label_fn=None, lloyd_fn=None) -> PipelineResult:
     """pipeline.py:45-160. blocks == (1,1,1): one tessellation of the whole
     grid. Otherwise each block is an independent LSRCVT (block faces are
     restrictions) merged with component/site id offsets in block order."""
+    label_fn = label_fn or gpu_label
+    lloyd_fn = lloyd_fn or lrcvt
     if tuple(blocks) == (1, 1, 1):
-        labels = label_components(classify_isobands(grid, iso))
-        tess, trace = lrcvt(grid, labels, seeding, lloyd)
+        labels = label_fn(grid, iso)
+        tess, trace = lloyd_fn(grid, labels, seeding, lloyd)
         return PipelineResult(grid, labels, tess, trace, [trace])
-    total_in_band = int(np.count_nonzero(classify_isobands(grid, iso).layer != NONE_ID))
+    total_in_band = 0
+    for block in block_list(grid.dims, blocks):
+        total_in_band += label_fn(sub_grid(grid, block), iso).in_band_count()
     n = grid.size
     nx, ny, _ = grid.dims
     out = {
@@ -99,7 +95,7 @@ def run_pipeline(grid: VoxelGrid, iso: IsobandSpec, seeding: SeedingParams, lloy
     block_traces: list[list[float]] = []
     comp_off = site_off = 0
     for block in block_list(grid.dims, blocks):
-        res = tessellate_block(grid, iso, seeding, lloyd, block, total_in_band, comp_off)
+        res = tessellate_block(grid, iso, seeding, lloyd, block, total_in_band, comp_off, label_fn, lloyd_fn)
         if res is None:
             continue
         sub, sub_labels, tess, trace = res
@@ -111,6 +107,106 @@ def run_pipeline(grid: VoxelGrid, iso: IsobandSpec, seeding: SeedingParams, lloy
                           src=out["src"], state=out["state"], component=out["component"], sites=sites,
                           report={"blocks": tuple(blocks), "n_blocks": len(block_traces)})
     return PipelineResult(grid, labels, merged, _combine_traces(block_traces), block_traces)
+
+
+def sub_grid(grid: VoxelGrid, block) -> VoxelGrid:
+    (x0, x1), (y0, y1), (z0, z1) = block
+    nx, ny, nz = grid.dims
+    return VoxelGrid((x1 - x0, y1 - y0, z1 - z0), grid.spacing,
+                     {name: np.ascontiguousarray(arr.reshape(nz, ny, nx)[z0:z1, y0:y1, x0:x1]).ravel()
+                      for name, arr in grid.fields.items()})
+
+
+def gpu_label(sub: VoxelGrid, iso: IsobandSpec) -> LabelMap:
+    return label_components(classify_isobands(sub, iso))
+
+
+def block_seeding(seeding: SeedingParams, in_band: int, total_in_band: int, comp_off: int) -> SeedingParams:
+    """pipeline.py:91-105: alpha is a global budget shared by in-band voxel
+    count; per-block sampling streams offset by the running component count."""
+    return SeedingParams(alpha=max(seeding.alpha * in_band / max(total_in_band, 1), 1e-9), gamma=seeding.gamma,
+                         weight_field=seeding.weight_field, block_size=seeding.block_size,
+                         seed=seeding.seed + comp_off)
+
+
+def run_pipeline_distributed(grid: VoxelGrid, iso: IsobandSpec, seeding: SeedingParams, lloyd: LloydParams,
+                             blocks: tuple[int, int, int], label_fn=gpu_label, lloyd_fn=lrcvt,
+                             group=None, dst: int = 0) -> PipelineResult | None:
+    """Block mode over torch.distributed ranks (one GPU each), the reference's
+    own distributed semantics (pipeline.py:45-160): block b is
+    tessellated by rank b % world with no data-path communication. Control
+    exchanges only: one all_gather of per-block (component count, in-band
+    count) fixes total_in_band and the component-id offsets that seed each
+    block's RNG stream, and a final gather brings block results to `dst`,
+    which merges them in the reference's block order. Returns the merged
+    PipelineResult on `dst` (bit-identical to run_pipeline), None elsewhere.
+    label_fn / lloyd_fn default to the GPU kernels."""
+    import torch.distributed as dist
+
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    blist = block_list(grid.dims, blocks)
+    mine = [b for b in range(len(blist)) if b % world == rank]
+    local = {}
+    for b in mine:
+        sub = sub_grid(grid, blist[b])
+        lab = label_fn(sub, iso)
+        local[b] = (sub, lab)
+    counts = {b: (local[b][1].n_components, local[b][1].in_band_count()) for b in mine}
+    gathered: list = [None] * world
+    dist.all_gather_object(gathered, counts, group=group)
+    allc = {b: c for d in gathered for b, c in d.items()}
+    total_in_band = sum(c[1] for c in allc.values())
+    comp_off_of, off = {}, 0
+    for b in range(len(blist)):
+        comp_off_of[b] = off
+        off += allc[b][0]
+    results = {}
+    for b in mine:
+        sub, lab = local[b]
+        if lab.n_components == 0:
+            continue
+        tess, trace = lloyd_fn(sub, lab, block_seeding(seeding, lab.in_band_count(), total_in_band,
+                                                       comp_off_of[b]), lloyd)
+        results[b] = (_portable_labels(lab), _portable_tess(tess), trace)
+    out_list: list = [None] * world if rank == dst else None
+    dist.gather_object(results, out_list, dst=dst, group=group)
+    if rank != dst:
+        return None
+    allr = {b: r for d in out_list for b, r in d.items()}
+    n = grid.size
+    out = {
+        "layer": np.full(n, NONE_ID, dtype=np.int32), "component": np.full(n, NONE_ID, dtype=np.int32),
+        "site_of": np.full(n, NONE_ID, dtype=np.int32), "dist": np.full(n, np.inf),
+        "src": np.full(n, NONE_ID, dtype=np.int32), "state": np.zeros(n, dtype=np.uint8),
+    }
+    table: list[ComponentInfo] = []
+    sites: list[Site] = []
+    block_traces: list[list[float]] = []
+    comp_off = site_off = 0
+    for b in range(len(blist)):
+        if b not in allr:
+            continue
+        lab, tess, trace = allr[b]
+        block_traces.append(trace)
+        comp_off, site_off = merge_block(grid, blist[b], lab, tess, out, table, sites, comp_off, site_off)
+    labels = LabelMap(dims=grid.dims, layer=out["layer"], component=out["component"], component_table=table,
+                      iso_values=list(iso.iso_values), field_name=iso.field_name)
+    merged = Tessellation(dims=grid.dims, spacing=grid.spacing, site_of=out["site_of"], dist=out["dist"],
+                          src=out["src"], state=out["state"], component=out["component"], sites=sites,
+                          report={"blocks": tuple(blocks), "n_blocks": len(block_traces)})
+    return PipelineResult(grid, labels, merged, _combine_traces(block_traces), block_traces)
+
+
+def _portable_labels(lab: LabelMap) -> LabelMap:
+    """Plain LabelMap without cached device objects, for pickling."""
+    return LabelMap(lab.dims, np.asarray(lab.layer), np.asarray(lab.component), list(lab.component_table),
+                    list(lab.iso_values), lab.field_name)
+
+
+def _portable_tess(t: Tessellation) -> Tessellation:
+    """Plain-numpy copy (device-resident tessellations materialised) for pickling."""
+    return Tessellation(t.dims, t.spacing, np.asarray(t.site_of), np.asarray(t.dist), np.asarray(t.src),
+                        np.asarray(t.state), np.asarray(t.component), list(t.sites), dict(t.report), None)
 
 
 def merge_block(grid, block, sub_labels, tess, out, table, sites, comp_off, site_off):

@@ -362,13 +362,40 @@ def dump_lloyd(G, S, T, big: bool):
         print(f"{name}: {time.time() - t0:.1f}s", file=sys.stderr)
 
 
+def dump_blocks(G, S, T, P):
+    """Block-mode run_pipeline (pipeline.py:45-160) results for the
+    distributed block driver."""
+    arrays, meta = {}, {}
+    for name, kind, dims, iso, sp, lp, blocks in (
+        ("spiral48_b221", "spiral", (48, 48, 1), [0.3, 0.55, 0.8], dict(alpha=40, seed=7),
+         dict(max_updates=6, ds_tolerance=0.05), (2, 2, 1)),
+        ("smooth24_b112", "random-smooth", (24, 24, 24), [0.35, 0.75], dict(alpha=30, seed=3, weight_field="g"),
+         dict(max_updates=3, ds_tolerance=1e-9), (1, 1, 2)),
+        ("gmix20_b212", "gaussian-mix", (20, 18, 16), [0.3, 0.7], dict(alpha=25, seed=1),
+         dict(max_updates=2, ds_tolerance=1e-9), (2, 1, 2)),
+    ):
+        g = G.synth_field(kind, dims, 0)
+        res = P.run_pipeline(g, G.IsobandSpec("f", iso), S.SeedingParams(**sp), T.LloydParams(**lp), blocks)
+        for key in ("site_of", "dist", "src", "state"):
+            arrays[f"{name}/{key}"] = getattr(res.tess, key)
+        arrays[f"{name}/layer"] = res.labels.layer
+        arrays[f"{name}/component"] = res.labels.component
+        arrays[f"{name}/sites"] = np.array([[*s.position, s.component_id] for s in res.tess.sites])
+        meta[name] = {"kind": kind, "dims": list(dims), "iso": iso, "seeding": sp, "lloyd": lp,
+                      "blocks": list(blocks), "trace": res.trace, "block_traces": res.block_traces,
+                      "table": table_json(res.labels)}
+    np.savez_compressed(OUT / "blocks.npz", **arrays)
+    (OUT / "blocks.json").write_text(json.dumps(meta))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--big", action="store_true", help="also record C2 128^3 and C3 256^3 trajectories")
     ap.add_argument("--only", default="")
     a = ap.parse_args()
     G, S, T, P, ST, K = ref()
-    todo = a.only.split(",") if a.only else ["classify", "raycast", "masks", "aggregate", "seeding", "lloyd"]
+    todo = a.only.split(",") if a.only else ["classify", "raycast", "masks", "aggregate", "seeding", "lloyd",
+                                             "blocks"]
     if "classify" in todo:
         dump_classify(G, S, T, K)
     if "raycast" in todo:
@@ -381,6 +408,8 @@ def main():
         dump_seeding(G, S)
     if "lloyd" in todo:
         dump_lloyd(G, S, T, a.big)
+    if "blocks" in todo:
+        dump_blocks(G, S, T, P)
 
 
 if __name__ == "__main__":
