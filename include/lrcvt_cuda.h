@@ -88,6 +88,12 @@ int lrcvt_centroidal_update(lrcvt_plan *plan, int64_t n_sites, const double *d_s
                             double *d_new_pos, double *d_disp, double *d_sums,
                             int64_t *empty_regions, void *stream);
 
+/* Sticky plan flag: the caller guarantees that centroidal_update is called
+ * with the same site-component set as the preceding lrcvt_classify (true
+ * inside a Lloyd loop, where components never change), so the eligible-voxel
+ * list (tessellation.py:161-164) built by the classify is reused. */
+int lrcvt_plan_reuse_eligible(lrcvt_plan *plan, int enable);
+
 /* split packed (site_of, src) into two int32[N] arrays */
 int lrcvt_unpack_site_src(const int32_t *d_site_src, int64_t n, int32_t *d_site_of,
                           int32_t *d_src, void *stream);

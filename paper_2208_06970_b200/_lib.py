@@ -12,7 +12,10 @@ import ctypes
 from ctypes import POINTER, c_double, c_int, c_int32, c_int64, c_void_p
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().with_name("liblrcvt_cuda.so")
+import os
+
+# LRCVT_LIB overrides the in-tree library (A/B timing of two builds)
+LIB_PATH = Path(os.environ.get("LRCVT_LIB") or Path(__file__).resolve().with_name("liblrcvt_cuda.so"))
 
 W_ONES, W_F64, W_F32_G1, W_F32_G2 = 0, 1, 2, 3
 
@@ -54,6 +57,7 @@ SIGNATURES = {
         [c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_int32, c_void_p, c_double,
          c_void_p, c_void_p, c_void_p, POINTER(c_int64), c_void_p],
     ),
+    "lrcvt_plan_reuse_eligible": (c_int, [c_void_p, c_int]),
     "lrcvt_unpack_site_src": (c_int, [c_void_p, c_int64, c_void_p, c_void_p, c_void_p]),
     "lrcvt_segment_hit_t": (
         c_int,

@@ -28,6 +28,22 @@ struct Prop {
   int v, s, src, pad;
 };
 
+// Device-resident round control: the worklist pointers and size live in HBM
+// so relaxation rounds can run back to back without the host (CUDA-graph
+// conditional WHILE loop, or the host loop when per-launch timing is on).
+struct RoundCtl {
+  int* cur;          // this round's worklist
+  int* nxt;          // next round's worklist (written by k_commit)
+  int* stash;        // the list buffer parked during a verification sweep
+  int2* ss;          // per-voxel (site_of, src) of the classify in flight
+  double* dist;      // per-voxel distance
+  int n_cur;         // items in cur
+  int sweep_imp;     // improvements found by the last sweep
+  int tile_next;     // dynamic tile scheduler of the eval kernels (reset per round)
+  int pad_;
+  long long rounds, evals, commits, rounds_p1;
+};
+
 // Counter slots in the plan's small device array.
 enum { C_NIMP = 0, C_NNEXT = 1, C_BAD = 2, C_ASSIGNED = 3, C_NCOUNTERS = 8 };
 
@@ -174,24 +190,112 @@ __device__ __forceinline__ void mark_and_append(const Geo& g, const uint32_t* __
 // list. One thread per committed proposal: the compact proposal list keeps
 // every lane of a warp busy in the latency-bound enqueue.
 __global__ void __launch_bounds__(128) k_commit(const Prop* __restrict__ imp,
-                                                int* __restrict__ counters, Geo g,
-                                                const uint32_t* __restrict__ nbm,
-                                                int2* __restrict__ ss,
-                                                double* __restrict__ dist,
-                                                uint32_t* __restrict__ bm,
-                                                int* __restrict__ next) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+                                                int* __restrict__ counters, const RoundCtl* __restrict__ ctl,
+                                                Geo g, const uint32_t* __restrict__ nbm,
+                                                uint32_t* __restrict__ bm) {
   const int n_imp = *(volatile int*)(counters + C_NIMP);
-  if (blockIdx.x * blockDim.x >= n_imp) return;  // whole warp-uniform block exit
-  const bool active = i < n_imp;
-  int v = 0;
-  if (active) {
-    const Prop p = imp[i];
-    v = p.v;
-    ss[v] = make_int2(p.s, p.src);
-    dist[v] = p.d;
+  int* next = ctl->nxt;
+  int2* __restrict__ ss = ctl->ss;
+  double* __restrict__ dist = ctl->dist;
+  const int stride = gridDim.x * blockDim.x;
+  for (int base = blockIdx.x * blockDim.x; base < n_imp; base += stride) {  // warp-uniform
+    const int i = base + threadIdx.x;
+    const bool active = i < n_imp;
+    int v = 0;
+    if (active) {
+      const Prop p = imp[i];
+      v = p.v;
+      __stcg(ss + v, make_int2(p.s, p.src));  // explicit global stores: the
+      __stcg(dist + v, p.d);                  // pointers come from RoundCtl
+    }
+    mark_and_append(g, nbm, active, v, false, bm, next, counters + C_NNEXT);
   }
-  mark_and_append(g, nbm, active, v, false, bm, next, counters + C_NNEXT);
+}
+
+// end of a round (_kernels.py:370-384): counters -> statistics, swap lists,
+// next size; sets the graph loop condition when running inside a graph.
+__global__ void k_round_end(RoundCtl* ctl, int* counters, cudaGraphConditionalHandle h, int in_graph) {
+  const int n_imp = counters[C_NIMP], n_next = counters[C_NNEXT];
+  ctl->rounds++;
+  ctl->evals += ctl->n_cur;
+  ctl->commits += n_imp;
+  int* t = ctl->cur;
+  ctl->cur = ctl->nxt;
+  ctl->nxt = t;
+  ctl->n_cur = n_next;
+  ctl->tile_next = 0;
+  counters[C_NIMP] = 0;
+  counters[C_NNEXT] = 0;
+  if (in_graph) cudaGraphSetConditional(h, n_next > 0 ? 1u : 0u);
+}
+
+// Size classes of a round's worklist: class c covers (cap[c-1], cap[c]]
+// items, caps growing 4x from 2048; the graph launches the eval kernel of the
+// active class with cap[c] / BLOCK blocks (one tile per block).
+constexpr int MAX_CLASSES = 12;
+__host__ __device__ inline long long class_cap(int c) { return 2048ll << (2 * c); }
+
+__global__ void k_size_class(const RoundCtl* ctl, cudaGraphConditionalHandle* hs, int n_classes) {
+  const long long n = ctl->n_cur;
+  for (int c = 0; c < n_classes; c++) {
+    const long long lo = c == 0 ? 0 : class_cap(c - 1);
+    cudaGraphSetConditional(hs[c], (n > lo && (n <= class_cap(c) || c == n_classes - 1)) ? 1u : 0u);
+  }
+}
+
+__global__ void k_loop_init(const RoundCtl* ctl, cudaGraphConditionalHandle h) {
+  cudaGraphSetConditional(h, ctl->n_cur > 0 ? 1u : 0u);
+}
+
+// phase 1 starts from the seed worklist appended to `first` by k_seed_groups
+__global__ void k_phase1_start(RoundCtl* ctl, int* counters, int* first, int* second, int2* ss,
+                               double* dist) {
+  ctl->ss = ss;
+  ctl->dist = dist;
+  ctl->cur = first;
+  ctl->nxt = second;
+  ctl->stash = nullptr;
+  ctl->n_cur = counters[C_NNEXT];
+  ctl->rounds = ctl->evals = ctl->commits = ctl->rounds_p1 = 0;
+  ctl->sweep_imp = 0;
+  ctl->tile_next = 0;
+  counters[C_NIMP] = 0;
+  counters[C_NNEXT] = 0;
+}
+
+// phase 2 starts from a copy of the eligible list (tessellation.py:166-167)
+__global__ void k_phase2_copy(const int* __restrict__ eligible, const int* __restrict__ n_el,
+                              RoundCtl* ctl) {
+  const int n = *n_el;
+  int* dst = ctl->cur;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) dst[i] = eligible[i];
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    ctl->rounds_p1 = ctl->rounds;
+    ctl->n_cur = n;
+    ctl->tile_next = 0;
+  }
+}
+
+// verification sweep over the eligible list (tessellation.py:177-189): the
+// two list buffers are parked so the sweep's enqueue lands in a free one
+__global__ void k_sweep_start(RoundCtl* ctl, int* eligible, const int* n_el) {
+  ctl->stash = ctl->cur;
+  ctl->cur = eligible;
+  ctl->n_cur = *n_el;
+  ctl->tile_next = 0;
+}
+
+__global__ void k_sweep_end(RoundCtl* ctl, int* counters) {
+  const int n_imp = counters[C_NIMP], n_next = counters[C_NNEXT];
+  ctl->evals += ctl->n_cur;
+  ctl->commits += n_imp;
+  ctl->sweep_imp = n_imp;
+  ctl->cur = ctl->nxt;  // the sweep's enqueue
+  ctl->nxt = ctl->stash;
+  ctl->n_cur = n_imp ? n_next : 0;
+  ctl->tile_next = 0;
+  counters[C_NIMP] = 0;
+  counters[C_NNEXT] = 0;
 }
 
 // _kernels.py:399-422, site part: seed voxel, distance, validity.

@@ -30,7 +30,7 @@ constexpr int P1_TAB = 4;  // distinct-site distance table
 constexpr int P1_SPEC = 3;  // speculated rays per lane
 
 template <int BLOCK>
-__global__ void __launch_bounds__(BLOCK) k_eval_p1(const int* __restrict__ list, int n, Geo g,
+__device__ __forceinline__ void p1_tile(const int* __restrict__ list, int n, const int i, const Geo& g,
                                                    const int* __restrict__ comp,
                                                    const uint32_t* __restrict__ nbm,
                                                    const int2* __restrict__ ss,
@@ -49,7 +49,6 @@ __global__ void __launch_bounds__(BLOCK) k_eval_p1(const int* __restrict__ list,
   int* qs = q_s + wid * 32 * P1_SPEC;
   unsigned char* qok = q_ok + wid * 32 * P1_SPEC;
   if (lane == 0) q_n[wid] = 0;
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const bool active = i < n;
   const int v = active ? __ldg(list + i) : 0;
   int* row = &s_row[0][threadIdx.x];
@@ -72,7 +71,7 @@ __global__ void __launch_bounds__(BLOCK) k_eval_p1(const int* __restrict__ list,
 #pragma unroll
     for (int k = 0; k < 26; k++) {
       const int w = v + off_dx(k) + off_dy(k) * g.nx + off_dz(k) * g.nxy;
-      nw[k] = ((same >> k) & 1u) ? ss[w] : make_int2(-1, -1);
+      nw[k] = ((same >> k) & 1u) ? __ldg(ss + w) : make_int2(-1, -1);
     }
     int nt = 0;
 #pragma unroll
@@ -91,8 +90,8 @@ __global__ void __launch_bounds__(BLOCK) k_eval_p1(const int* __restrict__ list,
         nt++;
       }
     }
-    const int2 sv = ss[v];
-    best_d = dist[v];
+    const int2 sv = __ldg(ss + v);
+    best_d = __ldg(dist + v);
     best_s = sv.x; best_src = sv.y;
     orig_d = best_d; orig_s = best_s;
   }
@@ -188,6 +187,27 @@ __global__ void __launch_bounds__(BLOCK) k_eval_p1(const int* __restrict__ list,
   pr.d = best_d; pr.v = v; pr.s = best_s; pr.src = best_src; pr.pad = 0;
   const int slot = warp_append(counters + C_NIMP, improved);
   if (improved) imp[slot] = pr;
+}
+
+// Grid-stride over 128-voxel tiles of the worklist held in the round control
+// block (size and pointer read on device, so rounds need no host round trip).
+template <int BLOCK>
+__global__ void __launch_bounds__(BLOCK) k_eval_p1(RoundCtl* __restrict__ ctl, Geo g,
+                                                   const int* __restrict__ comp,
+                                                   const uint32_t* __restrict__ nbm,
+                                                   const double4* __restrict__ site_pos,
+                                                   uint32_t* __restrict__ bm,
+                                                   Prop* __restrict__ imp,
+                                                   int* __restrict__ counters) {
+  const int n = ctl->n_cur;
+  const int* list = ctl->cur;
+  const int2* __restrict__ ss = ctl->ss;
+  const double* __restrict__ dist = ctl->dist;
+  // one BLOCK-voxel tile per block: the launch grid always covers the list
+  // (exact grid on the host path, size-class grid >= n inside the graph)
+  const int base = blockIdx.x * BLOCK;
+  if (base >= n) return;
+  p1_tile<BLOCK>(list, n, base + (int)threadIdx.x, g, comp, nbm, ss, dist, site_pos, bm, imp, counters);
 }
 
 }  // namespace lrcvt

@@ -24,7 +24,7 @@ constexpr int P2_STAB = 4;  // distinct LOS sites
 constexpr int P2_NTAB = 6;  // distinct shortcut nodes
 
 template <int BLOCK, bool DYADIC>
-__global__ void __launch_bounds__(BLOCK, 512 / BLOCK) k_eval_p2(const int* __restrict__ list, int n, Geo g,
+__device__ __forceinline__ void p2_tile(const int* __restrict__ list, int n, const int i, const Geo& g,
                                                    const int* __restrict__ comp,
                                                    const uint32_t* __restrict__ nbm,
                                                    const int2* __restrict__ ss,
@@ -36,7 +36,6 @@ __global__ void __launch_bounds__(BLOCK, 512 / BLOCK) k_eval_p2(const int* __res
   __shared__ int s_site[26][BLOCK];    // site(w) or -1 (not a candidate source)
   __shared__ int s_node[26][BLOCK];    // -2: w is LOS; -1: no shortcut; else src(w)
   __shared__ double s_dw[26][BLOCK];   // dist[w] + |c_w - p| (path candidate)
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const bool active = i < n;
   const int v = active ? __ldg(list + i) : 0;
   const int t = threadIdx.x;
@@ -69,8 +68,8 @@ __global__ void __launch_bounds__(BLOCK, 512 / BLOCK) k_eval_p2(const int* __res
         const int k = 13 * h + q;
         const int w = v + off_dx(k) + off_dy(k) * g.nx + off_dz(k) * g.nxy;
         const bool ok = (same >> k) & 1u;
-        nw[q] = ok ? ss[w] : make_int2(-1, -1);
-        dw[q] = ok ? dist[w] : 0.0;
+        nw[q] = ok ? __ldg(ss + w) : make_int2(-1, -1);
+        dw[q] = ok ? __ldg(dist + w) : 0.0;
       }
 #pragma unroll
       for (int q = 0; q < 13; q++) {
@@ -117,8 +116,8 @@ __global__ void __launch_bounds__(BLOCK, 512 / BLOCK) k_eval_p2(const int* __res
         }
       }
     }
-    const int2 sv = ss[v];
-    best_d = dist[v];
+    const int2 sv = __ldg(ss + v);
+    best_d = __ldg(dist + v);
     best_s = sv.x; best_src = sv.y;
     orig_d = best_d; orig_s = best_s;
   }
@@ -133,12 +132,12 @@ __global__ void __launch_bounds__(BLOCK, 512 / BLOCK) k_eval_p2(const int* __res
   for (int j = 0; j < P2_NTAB; j++) {
     const int u = tu[j];
     if (u >= 0) {
-      const int2 nu = ss[u];
+      const int2 nu = __ldg(ss + u);
       if (nu.x >= 0 && __ldg(comp + u) == cv) {
         int ux, uy, uz;
         coords(g, u, ux, uy, uz);
         tus[j] = nu.x;
-        tud[j] = __dadd_rn(dist[u], dist3(px, py, pz, centre1(ux, g.sx), centre1(uy, g.sy),
+        tud[j] = __dadd_rn(__ldg(dist + u), dist3(px, py, pz, centre1(ux, g.sx), centre1(uy, g.sy),
                                           centre1(uz, g.sz)));
       }
     }
@@ -177,12 +176,12 @@ __global__ void __launch_bounds__(BLOCK, 512 / BLOCK) k_eval_p2(const int* __res
         for (int j = 0; j < P2_NTAB; j++)
           if (tu[j] == u) { su = tus[j]; d = tud[j]; hit = true; }
         if (!hit) {  // more than P2_NTAB distinct nodes (rare)
-          const int2 nu = ss[u];
+          const int2 nu = __ldg(ss + u);
           if (nu.x >= 0 && __ldg(comp + u) == cv) {
             int ux, uy, uz;
             coords(g, u, ux, uy, uz);
             su = nu.x;
-            d = __dadd_rn(dist[u], dist3(px, py, pz, centre1(ux, g.sx), centre1(uy, g.sy),
+            d = __dadd_rn(__ldg(dist + u), dist3(px, py, pz, centre1(ux, g.sx), centre1(uy, g.sy),
                                          centre1(uz, g.sz)));
           }
         }
@@ -211,6 +210,25 @@ __global__ void __launch_bounds__(BLOCK, 512 / BLOCK) k_eval_p2(const int* __res
   pr.d = best_d; pr.v = v; pr.s = best_s; pr.src = best_src; pr.pad = 0;
   const int slot = warp_append(counters + C_NIMP, improved);
   if (improved) imp[slot] = pr;
+}
+
+template <int BLOCK, bool DYADIC>
+__global__ void __launch_bounds__(BLOCK, 512 / BLOCK) k_eval_p2(RoundCtl* __restrict__ ctl, Geo g,
+                                                                const int* __restrict__ comp,
+                                                                const uint32_t* __restrict__ nbm,
+                                                                const double4* __restrict__ site_pos,
+                                                                uint32_t* __restrict__ bm,
+                                                                Prop* __restrict__ imp,
+                                                                int* __restrict__ counters) {
+  const int n = ctl->n_cur;
+  const int* list = ctl->cur;
+  const int2* __restrict__ ss = ctl->ss;
+  const double* __restrict__ dist = ctl->dist;
+  // one BLOCK-voxel tile per block: the launch grid always covers the list
+  // (exact grid on the host path, size-class grid >= n inside the graph)
+  const int base = blockIdx.x * BLOCK;
+  if (base >= n) return;
+  p2_tile<BLOCK, DYADIC>(list, n, base + (int)threadIdx.x, g, comp, nbm, ss, dist, site_pos, bm, imp, counters);
 }
 
 }  // namespace lrcvt

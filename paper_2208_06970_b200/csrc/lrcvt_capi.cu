@@ -198,6 +198,22 @@ struct lrcvt_plan {
   // cub
   void* cub_tmp = nullptr;
   size_t cub_bytes = 0;
+  // device-resident round control + CUDA-graph round loops (one per eval
+  // variant: phase 1, phase 2 dyadic, phase 2 general)
+  RoundCtl* ctl = nullptr;
+  RoundCtl* h_ctl = nullptr;  // pinned readback
+  int* d_nel = nullptr;       // eligible count (device)
+  cudaGraphExec_t graph[3] = {nullptr, nullptr, nullptr};
+  cudaGraphConditionalHandle* d_handles = nullptr;  // [3][MAX_CLASSES] size-class IF handles
+  int n_classes = 0;
+  cudaStream_t cap = nullptr;  // capture stream
+  int eval_blocks[3] = {0, 0, 0};
+  int commit_blocks = 0;
+  // eligible list of the last classify is reused by centroidal_update when
+  // the caller guarantees the site-component set is unchanged
+  bool reuse_eligible = false;
+  bool eligible_valid = false;
+  int64_t eligible_sites = -1;
   // optional per-launch timing of the dominant kernel (k_eval)
   bool timing = false;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr;
@@ -249,57 +265,147 @@ int prepare_eligible(lrcvt_plan* p, int n_sites, const int* site_comp, cudaStrea
   EligiblePred pred{p->comp, p->has_site};
   cub::CountingInputIterator<int> it(0);
   size_t bytes = p->cub_bytes;
-  CK(cub::DeviceSelect::If(p->cub_tmp, bytes, it, p->eligible, p->counters + C_ASSIGNED,
-                           (int)p->g.n, pred, st));
-  CKR(sync_counters(p, st));
-  p->n_eligible = p->h_counters[C_ASSIGNED];
+  CK(cub::DeviceSelect::If(p->cub_tmp, bytes, it, p->eligible, p->d_nel, (int)p->g.n, pred, st));
   return 0;
 }
 
-// eval launch over list[0..n): proposals -> p->imp
-int launch_eval(lrcvt_plan* p, bool phase2, const int* list, int n, int2* ss, double* dist,
-                cudaStream_t st) {
+// The eval kernel of variant `var` over ctl->cur with `blocks` blocks.
+int launch_eval_kernel(lrcvt_plan* p, int var, int blocks, cudaStream_t st) {
   const Geo& g = p->g;
-  if (!phase2)
-    k_eval_p1<128><<<grid_for(n, 128), 128, 0, st>>>(list, n, g, p->comp, p->nbm, ss, dist, p->site_pos,
-                                                     p->bm, p->imp, p->counters);
-  else if (g.dyadic)
-    k_eval_p2<64, true><<<grid_for(n, 64), 64, 0, st>>>(list, n, g, p->comp, p->nbm, ss, dist, p->site_pos,
-                                                        p->bm, p->imp, p->counters);
+  if (blocks < 1) blocks = 1;
+  if (var == 0)
+    k_eval_p1<128><<<blocks, 128, 0, st>>>(p->ctl, g, p->comp, p->nbm, p->site_pos, p->bm, p->imp, p->counters);
+  else if (var == 1)
+    k_eval_p2<64, true><<<blocks, 64, 0, st>>>(p->ctl, g, p->comp, p->nbm, p->site_pos, p->bm, p->imp,
+                                               p->counters);
   else
-    k_eval_p2<64, false><<<grid_for(n, 64), 64, 0, st>>>(list, n, g, p->comp, p->nbm, ss, dist, p->site_pos,
-                                                         p->bm, p->imp, p->counters);
+    k_eval_p2<64, false><<<blocks, 64, 0, st>>>(p->ctl, g, p->comp, p->nbm, p->site_pos, p->bm, p->imp,
+                                                p->counters);
   CKL("k_eval");
   return 0;
 }
 
-// commit + enqueue of up to n_upper proposals (count read on device)
-int launch_commit(lrcvt_plan* p, int n_upper, int2* ss, double* dist, int* next, cudaStream_t st) {
-  k_commit<<<grid_for(n_upper, 128), 128, 0, st>>>(p->imp, p->counters, p->g, p->nbm, ss, dist, p->bm, next);
+int eval_block_size(int var) { return var == 0 ? 128 : 64; }
+
+// Host-driven round (n known on the host): exact eval grid, commit, round end.
+int launch_round_kernels(lrcvt_plan* p, int var, int n, cudaStream_t st) {
+  CKR(launch_eval_kernel(p, var, (n + eval_block_size(var) - 1) / eval_block_size(var), st));
+  if (p->timing) CK(cudaEventRecord(p->ev1, st));
+  k_commit<<<p->commit_blocks, 128, 0, st>>>(p->imp, p->counters, p->ctl, p->g, p->nbm, p->bm);
   CKL("k_commit");
+  if (p->timing) CK(cudaEventRecord(p->ev2, st));
   return 0;
 }
 
-// one relaxation round loop (_kernels.py:337-385). list_in holds n items.
-int run_phase(lrcvt_plan* p, bool phase2, int** cur, int** nxt, int n, int2* ss, double* dist,
-              lrcvt_classify_stats* st_out, cudaStream_t st) {
-  while (n > 0) {
-    st_out->rounds++;
-    st_out->evaluations += n;
-    CK(cudaMemsetAsync(p->counters, 0, sizeof(int) * 2, st));
-    if (p->timing) CK(cudaEventRecord(p->ev0, st));
-    CKR(launch_eval(p, phase2, *cur, n, ss, dist, st));
-    if (p->timing) CK(cudaEventRecord(p->ev1, st));
-    CKR(launch_commit(p, n, ss, dist, *nxt, st));
-    LAUNCHED(2);
-    if (p->timing) CK(cudaEventRecord(p->ev2, st));
-    CKR(sync_counters(p, st, 2));
-    if (p->timing) CKR(note_eval(p, n, phase2, p->h_counters[C_NIMP]));
-    st_out->commits += p->h_counters[C_NIMP];
-    n = p->h_counters[C_NNEXT];
-    int* t = *cur; *cur = *nxt; *nxt = t;
-  }
+// Relaxation rounds until the worklist drains (_kernels.py:337-385): a
+// CUDA graph whose conditional WHILE node repeats eval -> commit -> round end
+// entirely on the device (instantiated once per plan and variant).
+int add_kernel_node(cudaGraphNode_t* node, cudaGraph_t g, const cudaGraphNode_t* dep, void* func, dim3 grid,
+                    dim3 block, void** args) {
+  cudaGraphNodeParams np = {};
+  np.type = cudaGraphNodeTypeKernel;
+  np.kernel.func = func;
+  np.kernel.gridDim = grid;
+  np.kernel.blockDim = block;
+  np.kernel.kernelParams = args;
+  CK(cudaGraphAddNode(node, g, dep, dep ? 1 : 0, &np));
   return 0;
+}
+
+int build_round_graph(lrcvt_plan* p, int var) {
+  if (!p->cap) CK(cudaStreamCreateWithFlags(&p->cap, cudaStreamNonBlocking));
+  cudaGraph_t g;
+  CK(cudaGraphCreate(&g, 0));
+  cudaGraphConditionalHandle h;
+  CK(cudaGraphConditionalHandleCreate(&h, g, 0, cudaGraphCondAssignDefault));
+  RoundCtl* ctl = p->ctl;
+  cudaGraphNode_t n_init, n_loop;
+  {
+    void* args[] = {&ctl, &h};
+    CKR(add_kernel_node(&n_init, g, nullptr, (void*)k_loop_init, dim3(1), dim3(1), args));
+  }
+  cudaGraphNodeParams pw = {};
+  pw.type = cudaGraphNodeTypeConditional;
+  pw.conditional.handle = h;
+  pw.conditional.type = cudaGraphCondTypeWhile;
+  pw.conditional.size = 1;
+  CK(cudaGraphAddNode(&n_loop, g, &n_init, 1, &pw));
+  cudaGraph_t body = pw.conditional.phGraph_out[0];
+  // body: size class -> IF(class c) eval with cap[c]/BLOCK blocks -> commit -> round end
+  std::vector<cudaGraphConditionalHandle> hs(p->n_classes);
+  for (int c = 0; c < p->n_classes; c++) CK(cudaGraphConditionalHandleCreate(&hs[c], g, 0, 0));
+  cudaGraphConditionalHandle* d_hs = p->d_handles + var * MAX_CLASSES;
+  CK(cudaMemcpy(d_hs, hs.data(), sizeof(cudaGraphConditionalHandle) * p->n_classes, cudaMemcpyHostToDevice));
+  cudaGraphNode_t prev;
+  {
+    int ncl = p->n_classes;
+    void* args[] = {&ctl, &d_hs, &ncl};
+    CKR(add_kernel_node(&prev, body, nullptr, (void*)k_size_class, dim3(1), dim3(1), args));
+  }
+  const int bs = eval_block_size(var);
+  for (int c = 0; c < p->n_classes; c++) {
+    cudaGraphNodeParams pi = {};
+    pi.type = cudaGraphNodeTypeConditional;
+    pi.conditional.handle = hs[c];
+    pi.conditional.type = cudaGraphCondTypeIf;
+    pi.conditional.size = 1;
+    cudaGraphNode_t nif;
+    CK(cudaGraphAddNode(&nif, body, &prev, 1, &pi));
+    cudaGraph_t ib = pi.conditional.phGraph_out[0];
+    long long cap = class_cap(c);
+    if (c == p->n_classes - 1 && cap < p->n_inband) cap = p->n_inband;
+    const int blocks = (int)((cap + bs - 1) / bs);
+    CK(cudaStreamBeginCaptureToGraph(p->cap, ib, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+    const int rc = launch_eval_kernel(p, var, blocks, p->cap);
+    cudaGraph_t captured;
+    const cudaError_t ee = cudaStreamEndCapture(p->cap, &captured);
+    if (rc) return rc;
+    if (ee != cudaSuccess) return set_error(LRCVT_E_CUDA, "eval capture", ee);
+    prev = nif;
+  }
+  cudaGraphNode_t n_commit, n_end;
+  {
+    Prop* imp = p->imp;
+    int* counters = p->counters;
+    Geo gg = p->g;
+    const uint32_t* nbm = p->nbm;
+    uint32_t* bm = p->bm;
+    void* args[] = {&imp, &counters, &ctl, &gg, &nbm, &bm};
+    CKR(add_kernel_node(&n_commit, body, &prev, (void*)k_commit, dim3(p->commit_blocks), dim3(128), args));
+  }
+  {
+    int* counters = p->counters;
+    int one = 1;
+    void* args[] = {&ctl, &counters, &h, &one};
+    CKR(add_kernel_node(&n_end, body, &n_commit, (void*)k_round_end, dim3(1), dim3(1), args));
+  }
+  CK(cudaGraphInstantiate(&p->graph[var], g, 0));
+  CK(cudaGraphDestroy(g));
+  return 0;
+}
+
+int run_rounds(lrcvt_plan* p, int var, cudaStream_t st) {
+  if (!p->timing) {
+    if (!p->graph[var]) CKR(build_round_graph(p, var));
+    CK(cudaGraphLaunch(p->graph[var], st));
+    LAUNCHED(1);  // k_loop_init; per-round kernels are counted from ctl->rounds
+    return 0;
+  }
+  // host-driven rounds with per-launch CUDA-event timing (bench breakdown)
+  CK(cudaMemcpyAsync(p->h_ctl, p->ctl, sizeof(RoundCtl), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  for (;;) {
+    const int n = p->h_ctl->n_cur;
+    const long long commits0 = p->h_ctl->commits;
+    if (n <= 0) return 0;
+    CK(cudaEventRecord(p->ev0, st));
+    CKR(launch_round_kernels(p, var, n, st));
+    k_round_end<<<1, 1, 0, st>>>(p->ctl, p->counters, cudaGraphConditionalHandle{}, 0);
+    CKL("k_round_end");
+    CK(cudaMemcpyAsync(p->h_ctl, p->ctl, sizeof(RoundCtl), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    CKR(note_eval(p, n, var != 0, p->h_ctl->commits - commits0));
+  }
 }
 
 }  // namespace
@@ -350,6 +456,9 @@ int lrcvt_plan_create(lrcvt_plan** plan, int64_t nx, int64_t ny, int64_t nz, dou
   rc |= dalloc(&p->imp, nin);
   rc |= dalloc(&p->bm, p->bm_words);
   rc |= dalloc(&p->nbm, n);
+  rc |= dalloc(&p->ctl, 1);
+  rc |= dalloc(&p->d_handles, 3 * MAX_CLASSES);
+  rc |= dalloc(&p->d_nel, 1);
   rc |= dalloc(&p->has_site, n_components > 0 ? n_components : 1);
   rc |= dalloc(&p->site_pos, S);
   rc |= dalloc(&p->new_pos, S);
@@ -383,6 +492,25 @@ int lrcvt_plan_create(lrcvt_plan** plan, int64_t nx, int64_t ny, int64_t nz, dou
     need = b > need ? b : need;
   }
   p->cub_bytes = need;
+  p->n_classes = 1;
+  while (p->n_classes < MAX_CLASSES && class_cap(p->n_classes - 1) < nin) p->n_classes++;
+  if (cudaMallocHost((void**)&p->h_ctl, sizeof(RoundCtl)) != cudaSuccess) {
+    lrcvt_plan_destroy(p);
+    return set_error(LRCVT_E_NOMEM, "pinned round control");
+  }
+  {
+    int dev = 0, sms = 148, nb = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_eval_p1<128>, 128, 0);
+    p->eval_blocks[0] = (nb > 0 ? nb : 1) * sms;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_eval_p2<64, true>, 64, 0);
+    p->eval_blocks[1] = (nb > 0 ? nb : 1) * sms;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_eval_p2<64, false>, 64, 0);
+    p->eval_blocks[2] = (nb > 0 ? nb : 1) * sms;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_commit, 128, 0);
+    p->commit_blocks = (nb > 0 ? nb : 1) * sms;
+  }
   if (dalloc((char**)&p->cub_tmp, (int64_t)need)) { lrcvt_plan_destroy(p); return LRCVT_E_NOMEM; }
   *plan = p;
   return 0;
@@ -390,7 +518,11 @@ int lrcvt_plan_create(lrcvt_plan** plan, int64_t nx, int64_t ny, int64_t nz, dou
 
 int lrcvt_plan_destroy(lrcvt_plan* p) {
   if (!p) return 0;
-  void* bufs[] = {p->counters, p->list_a, p->list_b, p->eligible, p->imp, p->bm, p->nbm, p->has_site,
+  for (auto& gx : p->graph)
+    if (gx) cudaGraphExecDestroy(gx);
+  if (p->cap) cudaStreamDestroy(p->cap);
+  if (p->h_ctl) cudaFreeHost(p->h_ctl);
+  void* bufs[] = {p->counters, p->ctl, p->d_handles, p->d_nel, p->list_a, p->list_b, p->eligible, p->imp, p->bm, p->nbm, p->has_site,
                   p->site_pos, p->new_pos, p->sk_key, p->sk_key2, p->sk_val, p->sk_val2, p->sk_d,
                   p->acc, p->sums, p->vt_key, p->vt_key2, p->vt_idx, p->vt_idx2, p->vt_terms,
                   p->seg_b, p->seg_e, p->cub_tmp};
@@ -429,6 +561,12 @@ int lrcvt_plan_timing(const lrcvt_plan* p, int64_t* launches, int64_t* items, do
   return 0;
 }
 
+int lrcvt_plan_reuse_eligible(lrcvt_plan* p, int enable) {
+  if (!p) return set_error(LRCVT_E_ARG, "lrcvt_plan_reuse_eligible");
+  p->reuse_eligible = enable != 0;
+  return 0;
+}
+
 int lrcvt_plan_profile(const lrcvt_plan* p, double* out6) {
   if (!p || !out6) return set_error(LRCVT_E_ARG, "lrcvt_plan_profile");
   for (int i = 0; i < 6; i++) out6[i] = p->prof[i];
@@ -464,59 +602,65 @@ int lrcvt_classify(lrcvt_plan* p, int64_t n_sites, const double* d_site_pos,
   k_site_voxel<<<grid_for(S, 256), 256, 0, st>>>(g, p->comp, p->site_pos, d_site_comp, S, p->sk_key,
                                                  p->sk_val, p->sk_d, p->counters);
   CKL("k_site_voxel"); LAUNCHED(1);
-  CKR(sync_counters(p, st, C_BAD + 1));
-  if (p->h_counters[C_BAD]) {
-    stats->bad_sites = p->h_counters[C_BAD];
-    return p->h_counters[C_BAD];
-  }
   {
     size_t bytes = p->cub_bytes;
     CK(cub::DeviceRadixSort::SortPairs(p->cub_tmp, bytes, p->sk_key, p->sk_key2, p->sk_val,
                                        p->sk_val2, S, 0, 32, st));
   }
-  // groups -> seeds, then the phase-1 worklist (tessellation.py:151)
-  CK(cudaMemsetAsync(p->counters, 0, sizeof(int) * 2, st));
+  // groups -> seeds, then the phase-1 worklist (tessellation.py:151); sites
+  // outside their component (key INT_MAX) are skipped and reported at the end
   k_seed_groups<<<grid_for(S, 128), 128, 0, st>>>(g, p->nbm, p->sk_key2, p->sk_val2, p->sk_d, S, ss,
                                                   d_dist, p->bm, p->list_a, p->counters);  // marks bm (round-1 frontier)
   CKL("k_seed_groups"); LAUNCHED(1);
-  CKR(sync_counters(p, st, 2));
-  int n_wl = p->h_counters[C_NNEXT];
-  int* cur = p->list_a;
-  int* nxt = p->list_b;
+  k_phase1_start<<<1, 1, 0, st>>>(p->ctl, p->counters, p->list_a, p->list_b, ss, d_dist);
+  CKL("k_phase1_start"); LAUNCHED(1);
   // phase 1 (tessellation.py:152-156)
-  if (run_phase(p, false, &cur, &nxt, n_wl, ss, d_dist, stats, st)) return LRCVT_E_CUDA;
-  stats->phase1_rounds = stats->rounds;
-  // phase 2 (tessellation.py:161-189)
+  CKR(run_rounds(p, 0, st));
+  // phase 2 (tessellation.py:161-189): eligible list, rounds, verification sweeps
   if (prepare_eligible(p, S, d_site_comp, st)) return LRCVT_E_CUDA;
-  stats->eligible = p->n_eligible;
-  const int n_el = (int)p->n_eligible;
-  CK(cudaMemcpyAsync(cur, p->eligible, sizeof(int) * n_el, cudaMemcpyDeviceToDevice, st));
-  n_wl = n_el;
+  p->eligible_valid = true;
+  p->eligible_sites = S;
+  k_phase2_copy<<<148 * 4, 256, 0, st>>>(p->eligible, p->d_nel, p->ctl);
+  CKL("k_phase2_copy"); LAUNCHED(1);
+  const int var2 = g.dyadic ? 1 : 2;
   for (;;) {
-    if (run_phase(p, true, &cur, &nxt, n_wl, ss, d_dist, stats, st)) return LRCVT_E_CUDA;
+    CKR(run_rounds(p, var2, st));
     stats->sweeps++;
-    stats->evaluations += n_el;
-    CK(cudaMemsetAsync(p->counters, 0, sizeof(int) * 2, st));
+    k_sweep_start<<<1, 1, 0, st>>>(p->ctl, p->eligible, p->d_nel);
+    CKL("k_sweep_start"); LAUNCHED(1);
     if (p->timing) CK(cudaEventRecord(p->ev0, st));
-    // verification sweep: full eval over eligible; improved voxels' neighbours
-    // become the next worklist (tessellation.py:179-189)
-    CKR(launch_eval(p, true, p->eligible, n_el, ss, d_dist, st));
-    if (p->timing) CK(cudaEventRecord(p->ev1, st));
-    CKR(launch_commit(p, n_el, ss, d_dist, cur, st));
-    LAUNCHED(2);
-    if (p->timing) CK(cudaEventRecord(p->ev2, st));
-    CKR(sync_counters(p, st, 2));
-    if (p->timing) CKR(note_eval(p, n_el, true, p->h_counters[C_NIMP]));
-    if (p->h_counters[C_NIMP] == 0) break;
-    stats->commits += p->h_counters[C_NIMP];
-    n_wl = p->h_counters[C_NNEXT];
+    CKR(launch_round_kernels(p, var2, (int)p->n_inband, st));  // sweep: n_el <= in-band
+    k_sweep_end<<<1, 1, 0, st>>>(p->ctl, p->counters);
+    CKL("k_sweep_end"); LAUNCHED(3);  // eval, commit, sweep end
+    CK(cudaMemcpyAsync(p->h_ctl, p->ctl, sizeof(RoundCtl), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (p->timing) {
+      CK(cudaMemcpyAsync(p->h_counters + 7, p->d_nel, sizeof(int), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      CKR(note_eval(p, p->h_counters[7], true, p->h_ctl->sweep_imp));
+    }
+    if (p->h_ctl->sweep_imp == 0) break;
   }
   // state bits + assigned (tessellation.py:191-204)
-  CK(cudaMemsetAsync(p->counters + C_ASSIGNED, 0, sizeof(int), st));
   k_state<<<grid_for(g.n, 256, 148 * 16), 256, 0, st>>>(ss, g.n, d_state, p->counters);
   CKL("k_state"); LAUNCHED(1);
+  CK(cudaMemcpyAsync(p->h_ctl, p->ctl, sizeof(RoundCtl), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(p->h_counters + 7, p->d_nel, sizeof(int), cudaMemcpyDeviceToHost, st));
   CKR(sync_counters(p, st, C_ASSIGNED + 1));
+  const RoundCtl& c = *p->h_ctl;
+  p->n_eligible = p->h_counters[7];
+  stats->eligible = p->n_eligible;
+  stats->rounds = c.rounds;
+  stats->phase1_rounds = c.rounds_p1;
+  stats->evaluations = c.evals;
+  stats->commits = c.commits;
   stats->assigned = p->h_counters[C_ASSIGNED];
+  stats->bad_sites = p->h_counters[C_BAD];
+  LAUNCHED(3 * c.rounds);  // eval, commit, round end per relaxation round
+  if (p->h_counters[C_BAD]) {
+    p->eligible_valid = false;
+    return p->h_counters[C_BAD];
+  }
   return 0;
 }
 
@@ -536,7 +680,14 @@ int lrcvt_centroidal_update(lrcvt_plan* p, int64_t n_sites, const double* d_site
   if (S == 0) return 0;
   k_pack_sites<<<grid_for(S, 256), 256, 0, st>>>(d_site_pos, S, p->site_pos);
   CKL("k_pack_sites"); LAUNCHED(1);
-  if (prepare_eligible(p, S, d_site_comp, st)) return LRCVT_E_CUDA;
+  if (!(p->reuse_eligible && p->eligible_valid && p->eligible_sites == S)) {
+    if (prepare_eligible(p, S, d_site_comp, st)) return LRCVT_E_CUDA;
+    CK(cudaMemcpyAsync(p->h_counters + 7, p->d_nel, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    p->n_eligible = p->h_counters[7];
+    p->eligible_valid = true;
+    p->eligible_sites = S;
+  }
   const int n_el = (int)p->n_eligible;
   const bool exact = weight_mode == LRCVT_W_ONES && g.dyadic && g.nx <= (1 << 20) &&
                      g.ny <= (1 << 20) && g.nz <= (1 << 20);

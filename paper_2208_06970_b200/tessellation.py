@@ -403,6 +403,22 @@ def lrcvt(grid: VoxelGrid, labels: LabelMap, seeding: SeedingParams,
     _, site_comp, pos_d, comp_d = _site_arrays(torch, sites)
     mode, w_d = lloyd_weight_mode(torch, grid, seeding, weights)
     vlen = voxel_length(grid.dims, grid.spacing)
+    eng.L.lrcvt_plan_reuse_eligible(eng.plan, 1)  # site components fixed for the whole loop
+    try:
+        trace = _lloyd_iterations(eng, pos_d, comp_d, mode, w_d, vlen, lloyd, trace)
+    finally:
+        eng.L.lrcvt_plan_reuse_eligible(eng.plan, 0)
+    pos_d = eng._last_pos
+    pos = pos_d.cpu().numpy()
+    final_sites = [Site(position=(float(p[0]), float(p[1]), float(p[2])), component_id=int(c))
+                   for p, c in zip(pos, site_comp)]
+    final = voronoi_classify(grid, labels, final_sites, weights)
+    final.report["seeding"] = seed_report
+    final.report["updates"] = len(trace)
+    return final, trace
+
+
+def _lloyd_iterations(eng, pos_d, comp_d, mode, w_d, vlen, lloyd, trace):
     for _ in range(lloyd.max_updates):
         eng.classify(pos_d, comp_d, want_state=False)
         pos_d, disp, _, _ = eng.centroidal(pos_d, comp_d, mode, w_d, 0.5 * vlen)
@@ -411,13 +427,8 @@ def lrcvt(grid: VoxelGrid, labels: LabelMap, seeding: SeedingParams,
         trace.append(mean_ds)
         if mean_ds < lloyd.ds_tolerance:
             break
-    pos = pos_d.cpu().numpy()
-    final_sites = [Site(position=(float(p[0]), float(p[1]), float(p[2])), component_id=int(c))
-                   for p, c in zip(pos, site_comp)]
-    final = voronoi_classify(grid, labels, final_sites, weights)
-    final.report["seeding"] = seed_report
-    final.report["updates"] = len(trace)
-    return final, trace
+    eng._last_pos = pos_d
+    return trace
 
 
 # ---------------------------------------------------------------------------
