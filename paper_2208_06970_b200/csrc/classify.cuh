@@ -142,23 +142,57 @@ __device__ __forceinline__ void mark_and_append(const Geo& g, const uint32_t* __
                                                 bool active, int v, bool self,
                                                 uint32_t* __restrict__ bm,
                                                 int* __restrict__ next, int* counter) {
+  // The 27-cube around v is 9 x-rows of 3 voxels (dx = -1, 0, +1); a row's
+  // three bits sit in one bitmap word (two when they straddle a word), so
+  // each row costs one cached precheck load and at most one atomicOr with a
+  // 3-bit mask. A stale cached word can only under-report set bits (bits are
+  // only set during a round), which merely sends that row to the atomic.
+  // newmask uses the 27-cube index j = (dz+1)*9 + (dy+1)*3 + (dx+1).
   unsigned newmask = 0;
   if (active) {
-    const unsigned same = __ldg(nbm + v) | (self ? (1u << 26) : 0u);
-    uint32_t words[27];
+    const unsigned same = __ldg(nbm + v);
 #pragma unroll
-    for (int k = 0; k < 27; k++) {
-      const int u = k < 26 ? v + off_dx(k) + off_dy(k) * g.nx + off_dz(k) * g.nxy : v;
-      words[k] = ((same >> k) & 1u) ? __ldcg(bm + (u >> 5)) : 0xffffffffu;
-    }
+    for (int r = 0; r < 9; r++) {
+      const int dy = r % 3 - 1, dz = r / 3 - 1;
+      // k of (dx=-1,dy,dz): j = 3r (+0), k = j < 13 ? j : j - 1
+      const int j0 = 3 * r;
+      unsigned want = 0;  // bit t <=> dx = t - 1
 #pragma unroll
-    for (int k = 0; k < 27; k++) {
-      const int u = k < 26 ? v + off_dx(k) + off_dy(k) * g.nx + off_dz(k) * g.nxy : v;
-      const uint32_t bit = 1u << (u & 31);
-      if (((same >> k) & 1u) && !(words[k] & bit)) {
-        const uint32_t old = atomicOr(bm + (u >> 5), bit);
-        if (!(old & bit)) newmask |= 1u << k;
+      for (int t = 0; t < 3; t++) {
+        const int j = j0 + t;
+        if (j == 13) {
+          if (self) want |= 1u << t;
+        } else {
+          const int k = j < 13 ? j : j - 1;
+          if ((same >> k) & 1u) want |= 1u << t;
+        }
       }
+      if (!want) continue;
+      // anchor the window at the first wanted voxel (always inside the grid)
+      const int f = __ffs(want) - 1;
+      const unsigned wv = want >> f;
+      const int base = v + (f - 1) + dy * g.nx + dz * g.nxy;
+      const int w0 = base >> 5;
+      const int sh = base & 31;
+      const unsigned lo = wv << sh;                           // bits in word w0
+      const unsigned hi = sh > 29 ? (wv >> (32 - sh)) : 0u;   // spill into w0 + 1
+      unsigned got = 0;  // newly set by this thread, in `wv` coordinates
+      if (lo) {
+        const uint32_t cur = __ldca(bm + w0);
+        if ((cur & lo) != lo) {
+          const uint32_t old = atomicOr(bm + w0, lo);
+          got |= ((~old) & lo) >> sh;
+        }
+      }
+      if (hi) {
+        const uint32_t cur = __ldca(bm + w0 + 1);
+        if ((cur & hi) != hi) {
+          const uint32_t old = atomicOr(bm + w0 + 1, hi);
+          got |= ((~old) & hi) << (32 - sh);
+        }
+      }
+      got <<= f;
+      newmask |= got << j0;
     }
   }
   const int cnt = __popc(newmask);
@@ -174,13 +208,11 @@ __device__ __forceinline__ void mark_and_append(const Geo& g, const uint32_t* __
   if (lane == 31 && total) base = atomicAdd(counter, total);
   base = __shfl_sync(0xffffffffu, base, 31);
   int pos = base + incl - cnt;
-  if (newmask & (1u << 26)) next[pos++] = v;
-  newmask &= ALL26;
   while (newmask) {
-    const int k = __ffs(newmask) - 1;
+    const int j = __ffs(newmask) - 1;
     newmask &= newmask - 1;
-    const char4 o = c_off[k];
-    next[pos++] = nbr_index(v, o, g.nx, g.nxy);
+    const int dx = j % 3 - 1, dy = (j / 3) % 3 - 1, dz = j / 9 - 1;
+    next[pos++] = v + dx + dy * g.nx + dz * g.nxy;
   }
 }
 
