@@ -28,6 +28,7 @@ constexpr int P1_TAB = 4;  // distinct-site distance table
 // Ray outcomes are pure functions of (voxel, site), so the decision sequence
 // is exactly the reference's in every case.
 constexpr int P1_SPEC = 3;  // speculated rays per lane
+constexpr int P1_MIN_BLOCKS = 5;  // caps registers at 102: +25% occupancy, few spills (measured best)
 
 template <int BLOCK>
 __device__ __forceinline__ void p1_tile(const int* __restrict__ list, int n, const int i, const Geo& g,
@@ -192,7 +193,7 @@ __device__ __forceinline__ void p1_tile(const int* __restrict__ list, int n, con
 // Grid-stride over 128-voxel tiles of the worklist held in the round control
 // block (size and pointer read on device, so rounds need no host round trip).
 template <int BLOCK>
-__global__ void __launch_bounds__(BLOCK) k_eval_p1(RoundCtl* __restrict__ ctl, Geo g,
+__global__ void __launch_bounds__(BLOCK, P1_MIN_BLOCKS) k_eval_p1(RoundCtl* __restrict__ ctl, Geo g,
                                                    const int* __restrict__ comp,
                                                    const uint32_t* __restrict__ nbm,
                                                    const double4* __restrict__ site_pos,
