@@ -45,7 +45,7 @@ struct RoundCtl {
 };
 
 // Counter slots in the plan's small device array.
-enum { C_NIMP = 0, C_NNEXT = 1, C_BAD = 2, C_ASSIGNED = 3, C_NCOUNTERS = 8 };
+enum { C_NIMP = 0, C_NNEXT = 1, C_BAD = 2, C_ASSIGNED = 3, C_DONE = 4, C_NCOUNTERS = 8 };
 
 __global__ void k_fill_state(int2* __restrict__ ss, double* __restrict__ dist, int64_t n) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -216,15 +216,53 @@ __device__ __forceinline__ void mark_and_append(const Geo& g, const uint32_t* __
   }
 }
 
+// Size classes of a round's worklist: class c covers (cap[c-1], cap[c]]
+// items, caps growing 4x from 2048; the graph launches the eval kernel of the
+// active class with cap[c] / BLOCK blocks (one tile per block).
+constexpr int MAX_CLASSES = 12;
+__host__ __device__ inline long long class_cap(int c) { return 2048ll << (2 * c); }
+
+// sets exactly one class handle (none when n == 0)
+__device__ __forceinline__ void set_size_class(long long n, const cudaGraphConditionalHandle* hs, int n_classes) {
+  for (int c = 0; c < n_classes; c++) {
+    const long long lo = c == 0 ? 0 : class_cap(c - 1);
+    cudaGraphSetConditional(hs[c], (n > lo && (n <= class_cap(c) || c == n_classes - 1)) ? 1u : 0u);
+  }
+}
+
 // _kernels.py:285-334: commit the round's proposals, then enqueue the
 // same-component neighbours of every improved voxel into the frontier bitmap
 // (cleared word by word by the eval kernel that consumed it) and the next
 // list. One thread per committed proposal: the compact proposal list keeps
 // every lane of a warp busy in the latency-bound enqueue.
+// round end (_kernels.py:370-384): statistics, list swap, next size; inside
+// the round graph it also arms the next round (size-class IF handles and the
+// WHILE condition). Runs on one thread.
+__device__ __forceinline__ void round_end(RoundCtl* ctl, int* counters, const cudaGraphConditionalHandle* hs,
+                                          int n_classes, cudaGraphConditionalHandle loop, int in_graph) {
+  const int n_imp = counters[C_NIMP], n_next = counters[C_NNEXT];
+  ctl->rounds++;
+  ctl->evals += ctl->n_cur;
+  ctl->commits += n_imp;
+  int* t = ctl->cur;
+  ctl->cur = ctl->nxt;
+  ctl->nxt = t;
+  ctl->n_cur = n_next;
+  ctl->tile_next = 0;
+  counters[C_NIMP] = 0;
+  counters[C_NNEXT] = 0;
+  if (in_graph) {
+    set_size_class(n_next, hs, n_classes);
+    cudaGraphSetConditional(loop, n_next > 0 ? 1u : 0u);
+  }
+}
+
 __global__ void __launch_bounds__(128) k_commit(const Prop* __restrict__ imp,
-                                                int* __restrict__ counters, const RoundCtl* __restrict__ ctl,
+                                                int* __restrict__ counters, RoundCtl* __restrict__ ctl,
                                                 Geo g, const uint32_t* __restrict__ nbm,
-                                                uint32_t* __restrict__ bm) {
+                                                uint32_t* __restrict__ bm,
+                                                const cudaGraphConditionalHandle* __restrict__ hs, int n_classes,
+                                                cudaGraphConditionalHandle loop, int end_mode) {
   const int n_imp = *(volatile int*)(counters + C_NIMP);
   int* next = ctl->nxt;
   int2* __restrict__ ss = ctl->ss;
@@ -242,40 +280,23 @@ __global__ void __launch_bounds__(128) k_commit(const Prop* __restrict__ imp,
     }
     mark_and_append(g, nbm, active, v, false, bm, next, counters + C_NNEXT);
   }
-}
-
-// end of a round (_kernels.py:370-384): counters -> statistics, swap lists,
-// next size; sets the graph loop condition when running inside a graph.
-__global__ void k_round_end(RoundCtl* ctl, int* counters, cudaGraphConditionalHandle h, int in_graph) {
-  const int n_imp = counters[C_NIMP], n_next = counters[C_NNEXT];
-  ctl->rounds++;
-  ctl->evals += ctl->n_cur;
-  ctl->commits += n_imp;
-  int* t = ctl->cur;
-  ctl->cur = ctl->nxt;
-  ctl->nxt = t;
-  ctl->n_cur = n_next;
-  ctl->tile_next = 0;
-  counters[C_NIMP] = 0;
-  counters[C_NNEXT] = 0;
-  if (in_graph) cudaGraphSetConditional(h, n_next > 0 ? 1u : 0u);
-}
-
-// Size classes of a round's worklist: class c covers (cap[c-1], cap[c]]
-// items, caps growing 4x from 2048; the graph launches the eval kernel of the
-// active class with cap[c] / BLOCK blocks (one tile per block).
-constexpr int MAX_CLASSES = 12;
-__host__ __device__ inline long long class_cap(int c) { return 2048ll << (2 * c); }
-
-__global__ void k_size_class(const RoundCtl* ctl, cudaGraphConditionalHandle* hs, int n_classes) {
-  const long long n = ctl->n_cur;
-  for (int c = 0; c < n_classes; c++) {
-    const long long lo = c == 0 ? 0 : class_cap(c - 1);
-    cudaGraphSetConditional(hs[c], (n > lo && (n <= class_cap(c) || c == n_classes - 1)) ? 1u : 0u);
+  if (end_mode < 0) return;  // sweep: k_sweep_end follows
+  // the last block to finish ends the round (no separate launch)
+  __shared__ bool last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(counters + C_DONE, 1) == (int)gridDim.x - 1;
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    __threadfence();
+    counters[C_DONE] = 0;
+    round_end(ctl, counters, hs, n_classes, loop, end_mode);
   }
 }
 
-__global__ void k_loop_init(const RoundCtl* ctl, cudaGraphConditionalHandle h) {
+__global__ void k_loop_init(const RoundCtl* ctl, cudaGraphConditionalHandle h,
+                            const cudaGraphConditionalHandle* hs, int n_classes) {
+  set_size_class(ctl->n_cur, hs, n_classes);
   cudaGraphSetConditional(h, ctl->n_cur > 0 ? 1u : 0u);
 }
 

@@ -287,12 +287,25 @@ int launch_eval_kernel(lrcvt_plan* p, int var, int blocks, cudaStream_t st) {
 
 int eval_block_size(int var) { return var == 0 ? 128 : 64; }
 
-// Host-driven round (n known on the host): exact eval grid, commit, round end.
-int launch_round_kernels(lrcvt_plan* p, int var, int n, cudaStream_t st) {
+// commit + enqueue (+ round end in its last block unless end_mode < 0)
+int launch_commit_kernel(lrcvt_plan* p, int blocks, cudaStream_t st, const cudaGraphConditionalHandle* hs,
+                         cudaGraphConditionalHandle loop, int end_mode) {
+  if (blocks < 1) blocks = 1;
+  // grid-stride: at most one resident wave (the last-block round end costs one
+  // same-address atomic per block)
+  if (blocks > p->commit_blocks) blocks = p->commit_blocks;
+  k_commit<<<blocks, 128, 0, st>>>(p->imp, p->counters, p->ctl, p->g, p->nbm, p->bm, hs, p->n_classes, loop,
+                                   end_mode);
+  CKL("k_commit");
+  return 0;
+}
+
+// Host-driven round (n known on the host): exact grids; end_mode 0 = round
+// end without graph conditionals, -1 = sweep (k_sweep_end follows).
+int launch_round_kernels(lrcvt_plan* p, int var, int n, cudaStream_t st, int end_mode = 0) {
   CKR(launch_eval_kernel(p, var, (n + eval_block_size(var) - 1) / eval_block_size(var), st));
   if (p->timing) CK(cudaEventRecord(p->ev1, st));
-  k_commit<<<p->commit_blocks, 128, 0, st>>>(p->imp, p->counters, p->ctl, p->g, p->nbm, p->bm);
-  CKL("k_commit");
+  CKR(launch_commit_kernel(p, (n + 127) / 128, st, nullptr, cudaGraphConditionalHandle{}, end_mode));
   if (p->timing) CK(cudaEventRecord(p->ev2, st));
   return 0;
 }
@@ -318,10 +331,15 @@ int build_round_graph(lrcvt_plan* p, int var) {
   CK(cudaGraphCreate(&g, 0));
   cudaGraphConditionalHandle h;
   CK(cudaGraphConditionalHandleCreate(&h, g, 0, cudaGraphCondAssignDefault));
+  std::vector<cudaGraphConditionalHandle> hs(p->n_classes);
+  for (int c = 0; c < p->n_classes; c++) CK(cudaGraphConditionalHandleCreate(&hs[c], g, 0, 0));
+  cudaGraphConditionalHandle* d_hs = p->d_handles + var * MAX_CLASSES;
+  CK(cudaMemcpy(d_hs, hs.data(), sizeof(cudaGraphConditionalHandle) * p->n_classes, cudaMemcpyHostToDevice));
   RoundCtl* ctl = p->ctl;
   cudaGraphNode_t n_init, n_loop;
   {
-    void* args[] = {&ctl, &h};
+    int ncl = p->n_classes;
+    void* args[] = {&ctl, &h, &d_hs, &ncl};
     CKR(add_kernel_node(&n_init, g, nullptr, (void*)k_loop_init, dim3(1), dim3(1), args));
   }
   cudaGraphNodeParams pw = {};
@@ -331,18 +349,11 @@ int build_round_graph(lrcvt_plan* p, int var) {
   pw.conditional.size = 1;
   CK(cudaGraphAddNode(&n_loop, g, &n_init, 1, &pw));
   cudaGraph_t body = pw.conditional.phGraph_out[0];
-  // body: size class -> IF(class c) eval with cap[c]/BLOCK blocks -> commit -> round end
-  std::vector<cudaGraphConditionalHandle> hs(p->n_classes);
-  for (int c = 0; c < p->n_classes; c++) CK(cudaGraphConditionalHandleCreate(&hs[c], g, 0, 0));
-  cudaGraphConditionalHandle* d_hs = p->d_handles + var * MAX_CLASSES;
-  CK(cudaMemcpy(d_hs, hs.data(), sizeof(cudaGraphConditionalHandle) * p->n_classes, cudaMemcpyHostToDevice));
-  cudaGraphNode_t prev;
-  {
-    int ncl = p->n_classes;
-    void* args[] = {&ctl, &d_hs, &ncl};
-    CKR(add_kernel_node(&prev, body, nullptr, (void*)k_size_class, dim3(1), dim3(1), args));
-  }
+  // body: IF(class c) { eval with cap[c]/BLOCK blocks; commit + round end with
+  // cap[c]/128 blocks } for each class; the last commit block arms the next
+  // round's class and the WHILE condition
   const int bs = eval_block_size(var);
+  cudaGraphNode_t prev = nullptr;
   for (int c = 0; c < p->n_classes; c++) {
     cudaGraphNodeParams pi = {};
     pi.type = cudaGraphNodeTypeConditional;
@@ -350,34 +361,18 @@ int build_round_graph(lrcvt_plan* p, int var) {
     pi.conditional.type = cudaGraphCondTypeIf;
     pi.conditional.size = 1;
     cudaGraphNode_t nif;
-    CK(cudaGraphAddNode(&nif, body, &prev, 1, &pi));
+    CK(cudaGraphAddNode(&nif, body, prev ? &prev : nullptr, prev ? 1 : 0, &pi));
     cudaGraph_t ib = pi.conditional.phGraph_out[0];
     long long cap = class_cap(c);
     if (c == p->n_classes - 1 && cap < p->n_inband) cap = p->n_inband;
-    const int blocks = (int)((cap + bs - 1) / bs);
     CK(cudaStreamBeginCaptureToGraph(p->cap, ib, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
-    const int rc = launch_eval_kernel(p, var, blocks, p->cap);
+    int rc = launch_eval_kernel(p, var, (int)((cap + bs - 1) / bs), p->cap);
+    if (!rc) rc = launch_commit_kernel(p, (int)((cap + 127) / 128), p->cap, d_hs, h, 1);
     cudaGraph_t captured;
     const cudaError_t ee = cudaStreamEndCapture(p->cap, &captured);
     if (rc) return rc;
-    if (ee != cudaSuccess) return set_error(LRCVT_E_CUDA, "eval capture", ee);
+    if (ee != cudaSuccess) return set_error(LRCVT_E_CUDA, "round capture", ee);
     prev = nif;
-  }
-  cudaGraphNode_t n_commit, n_end;
-  {
-    Prop* imp = p->imp;
-    int* counters = p->counters;
-    Geo gg = p->g;
-    const uint32_t* nbm = p->nbm;
-    uint32_t* bm = p->bm;
-    void* args[] = {&imp, &counters, &ctl, &gg, &nbm, &bm};
-    CKR(add_kernel_node(&n_commit, body, &prev, (void*)k_commit, dim3(p->commit_blocks), dim3(128), args));
-  }
-  {
-    int* counters = p->counters;
-    int one = 1;
-    void* args[] = {&ctl, &counters, &h, &one};
-    CKR(add_kernel_node(&n_end, body, &n_commit, (void*)k_round_end, dim3(1), dim3(1), args));
   }
   CK(cudaGraphInstantiate(&p->graph[var], g, 0));
   CK(cudaGraphDestroy(g));
@@ -400,8 +395,6 @@ int run_rounds(lrcvt_plan* p, int var, cudaStream_t st) {
     if (n <= 0) return 0;
     CK(cudaEventRecord(p->ev0, st));
     CKR(launch_round_kernels(p, var, n, st));
-    k_round_end<<<1, 1, 0, st>>>(p->ctl, p->counters, cudaGraphConditionalHandle{}, 0);
-    CKL("k_round_end");
     CK(cudaMemcpyAsync(p->h_ctl, p->ctl, sizeof(RoundCtl), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     CKR(note_eval(p, n, var != 0, p->h_ctl->commits - commits0));
@@ -629,7 +622,7 @@ int lrcvt_classify(lrcvt_plan* p, int64_t n_sites, const double* d_site_pos,
     k_sweep_start<<<1, 1, 0, st>>>(p->ctl, p->eligible, p->d_nel);
     CKL("k_sweep_start"); LAUNCHED(1);
     if (p->timing) CK(cudaEventRecord(p->ev0, st));
-    CKR(launch_round_kernels(p, var2, (int)p->n_inband, st));  // sweep: n_el <= in-band
+    CKR(launch_round_kernels(p, var2, (int)p->n_inband, st, -1));  // sweep: n_el <= in-band
     k_sweep_end<<<1, 1, 0, st>>>(p->ctl, p->counters);
     CKL("k_sweep_end"); LAUNCHED(3);  // eval, commit, sweep end
     CK(cudaMemcpyAsync(p->h_ctl, p->ctl, sizeof(RoundCtl), cudaMemcpyDeviceToHost, st));
@@ -656,7 +649,7 @@ int lrcvt_classify(lrcvt_plan* p, int64_t n_sites, const double* d_site_pos,
   stats->commits = c.commits;
   stats->assigned = p->h_counters[C_ASSIGNED];
   stats->bad_sites = p->h_counters[C_BAD];
-  LAUNCHED(3 * c.rounds);  // eval, commit, round end per relaxation round
+  LAUNCHED(2 * c.rounds);  // eval, commit (+ fused round end) per relaxation round
   if (p->h_counters[C_BAD]) {
     p->eligible_valid = false;
     return p->h_counters[C_BAD];
