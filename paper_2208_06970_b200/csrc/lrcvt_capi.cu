@@ -55,6 +55,23 @@ int set_error(int code, const char* what, cudaError_t e = cudaSuccess) {
     if (e_ != cudaSuccess) return set_error(LRCVT_E_CUDA, what, e_);    \
   } while (0)
 
+// The short-lived scratch of the standalone passes (CCL, aggregation, plan
+// setup) comes from the device's default stream-ordered pool. Its default
+// release threshold (0) hands memory back to the driver at every
+// synchronisation, which turned each large cudaMallocAsync into a fresh
+// page-mapping (~100x the kernels' time); keep it pooled instead.
+void retain_pool() {
+  static thread_local int done_dev = -1;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev == done_dev) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done_dev = dev;
+}
+
 bool is_pow2(double s) {
   int e;
   double m = frexp(s, &e);
@@ -412,6 +429,7 @@ const char* lrcvt_last_error(void) { return g_last_error.c_str(); }
 int lrcvt_plan_create(lrcvt_plan** plan, int64_t nx, int64_t ny, int64_t nz, double sx, double sy,
                       double sz, const int32_t* d_comp, int32_t n_components, int64_t max_sites,
                       void* stream) {
+  retain_pool();
   if (!plan || !d_comp || !geo_ok(nx, ny, nz, sx, sy, sz) || n_components < 0 || max_sites < 0)
     return set_error(LRCVT_E_ARG, "lrcvt_plan_create: bad arguments");
   cudaStream_t st = (cudaStream_t)stream;
@@ -772,6 +790,7 @@ int lrcvt_isobands(int64_t n, const float* d_field, const double* d_iso, int32_t
 
 int lrcvt_label_components(int64_t nx, int64_t ny, int64_t nz, const int32_t* d_layer, int32_t n_layers,
                            int32_t* d_component, int32_t* n_components, void* stream) {
+  retain_pool();
   if (!geo_ok(nx, ny, nz, 1, 1, 1) || !d_layer || !d_component || !n_components || n_layers < 0)
     return set_error(LRCVT_E_ARG, "lrcvt_label_components: bad arguments");
   cudaStream_t st = (cudaStream_t)stream;
@@ -851,6 +870,7 @@ int lrcvt_aggregate(int64_t n, int32_t n_fields, const float* const* field_ptrs,
                     const int32_t* d_site_of, int32_t n_sites, int32_t n_components, int32_t n_pairs,
                     const int32_t* pairs, int32_t n_bins, double* axes, int64_t* d_count, double* d_sums,
                     double* d_minmax, int64_t* d_hist, void* stream) {
+  retain_pool();
   if (n < 0 || n >= (int64_t(1) << 31) || n_fields < 1 || n_fields > 16 || !field_ptrs || !d_component ||
       !d_site_of || n_sites < 0 || n_components < 0 || n_pairs < 1 || n_pairs > 136 || !pairs || n_bins < 0 ||
       n_bins > 1024 || !d_count || !d_sums || !d_minmax || (n_bins > 0 && (!d_hist || !axes)))
