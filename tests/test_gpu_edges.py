@@ -1,0 +1,119 @@
+"""GPU edge cases against the CPU oracle (bit-exact): degenerate grids,
+contested seed voxels, components without sites, non-power-of-two spacing in
+3D, many small components, early Lloyd stop."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _labels(comp, dims):
+    from paper_2208_06970_b200.grid import ComponentInfo, LabelMap
+
+    comp = np.ascontiguousarray(comp, dtype=np.int32)
+    n = int(comp.max()) + 1 if (comp >= 0).any() else 0
+    counts = np.bincount(comp[comp >= 0], minlength=n)
+    table = [ComponentInfo(c, 0, int(counts[c]), (0,) * 6, (0.0, 1.0)) for c in range(n)]
+    return LabelMap(tuple(dims), np.where(comp >= 0, 0, -1).astype(np.int32), comp, table, [0.0, 1.0], "f")
+
+
+def _check(grid, labels, sites, oracle, weights=None):
+    from paper_2208_06970_b200 import centroidal_update, voronoi_classify
+
+    tess = voronoi_classify(grid, labels, sites, weights)
+    pos, sc = tess.site_positions(), tess.site_components()
+    ref = oracle.classify(grid.dims, grid.spacing, labels.component, pos, sc, labels.n_components)
+    for k in ("site_of", "dist", "src", "state"):
+        assert np.array_equal(getattr(tess, k), ref[k]), k
+    assert tess.report["rounds"] == ref["rounds"] and tess.report["sweeps"] == ref["sweeps"]
+    new_sites, mean_ds = centroidal_update(tess)
+    u = oracle.centroidal(grid.dims, grid.spacing, labels.component, ref["site_of"], ref["src"], weights, pos, sc)
+    assert np.array_equal(np.array([s.position for s in new_sites]).reshape(-1, 3), u["new_pos"])
+    assert mean_ds == u["mean_ds"]
+    assert tess.report["empty_regions"] == u["empty"]
+    return tess
+
+
+def test_single_voxel_grid(oracle_mod):
+    from paper_2208_06970_b200 import Site, VoxelGrid
+
+    grid = VoxelGrid((1, 1, 1), (1, 1, 1), {})
+    _check(grid, _labels(np.zeros(1), (1, 1, 1)), [Site((0.3, 0.7, 0.5), 0)], oracle_mod)
+
+
+def test_long_line_grid(oracle_mod):
+    from paper_2208_06970_b200 import Site, VoxelGrid
+
+    n = 5000
+    grid = VoxelGrid((n, 1, 1), (1, 1, 1), {})
+    comp = np.zeros(n, np.int32)
+    comp[2000:2100] = -1  # a gap splits the line into two components
+    comp[2100:] = 1
+    sites = [Site((10.5, 0.5, 0.5), 0), Site((1500.25, 0.5, 0.5), 0), Site((4999.5, 0.5, 0.5), 1)]
+    _check(grid, _labels(comp, (n, 1, 1)), sites, oracle_mod)
+
+
+def test_contested_seed_voxels_and_empty_regions(oracle_mod):
+    """Several sites in one voxel: the lexicographic (distance, id) winner
+    takes the voxel, the others keep empty regions and do not move."""
+    from paper_2208_06970_b200 import Site, VoxelGrid
+
+    dims = (24, 20, 6)
+    grid = VoxelGrid(dims, (1, 1, 1), {})
+    comp = np.zeros(int(np.prod(dims)), np.int32)
+    sites = [Site((5.5, 5.5, 2.5), 0), Site((5.2, 5.9, 2.1), 0), Site((5.5, 5.5, 2.5), 0),
+             Site((17.9, 12.1, 3.3), 0), Site((17.1, 12.9, 3.9), 0)]
+    tess = _check(grid, _labels(comp, dims), sites, oracle_mod)
+    assert tess.report["empty_regions"] >= 1
+
+
+def test_components_without_sites_and_many_components(oracle_mod):
+    from paper_2208_06970_b200 import (IsobandSpec, Site, VoxelGrid, classify_isobands, label_components)
+
+    rng = np.random.default_rng(4)
+    dims = (40, 30, 20)
+    f = rng.random(int(np.prod(dims))).astype(np.float32)
+    grid = VoxelGrid(dims, (1, 1, 1), {"f": f})
+    labels = label_components(classify_isobands(grid, IsobandSpec("f", [0.2, 0.6])))
+    assert labels.n_components > 100
+    nx, ny = dims[0], dims[1]
+    sites = []
+    for c in labels.component_table[::7][:60]:
+        v = int(np.flatnonzero(labels.component == c.id)[0])
+        sites.append(Site(((v % nx) + 0.25, ((v // nx) % ny) + 0.75, (v // (nx * ny)) + 0.5), c.id))
+    tess = _check(grid, labels, sites, oracle_mod)
+    assert len(tess.report["components_without_sites"]) == labels.n_components - len(sites)
+
+
+def test_non_dyadic_spacing_3d(oracle_mod):
+    from paper_2208_06970_b200 import IsobandSpec, SeedingParams, VoxelGrid, classify_isobands, label_components
+    from paper_2208_06970_b200 import seed_sites, synth_field, voxel_weights
+
+    base = synth_field("random-smooth", (30, 26, 22), 5)
+    grid = VoxelGrid(base.dims, (0.7, 1.3, 0.45), base.fields)
+    labels = label_components(classify_isobands(grid, IsobandSpec("f", [0.3, 0.6, 0.85])))
+    params = SeedingParams(alpha=50, seed=2, weight_field="g", gamma=1.5)
+    sites, _ = seed_sites(grid, labels, params)
+    _check(grid, labels, sites, oracle_mod, voxel_weights(grid, params))
+
+
+def test_lloyd_tolerance_stops_early():
+    from paper_2208_06970_b200 import LloydParams, SeedingParams, VoxelGrid, lrcvt
+
+    f = np.full(15 * 15, 0.5, np.float32)
+    grid = VoxelGrid((15, 15, 1), (1, 1, 1), {"f": f})
+    from paper_2208_06970_b200 import IsobandSpec, classify_isobands, label_components
+
+    labels = label_components(classify_isobands(grid, IsobandSpec("f", [0.0, 1.0])))
+    _, trace = lrcvt(grid, labels, SeedingParams(alpha=4, seed=1), LloydParams(max_updates=50, ds_tolerance=0.5))
+    assert len(trace) < 50 and trace[-1] < 0.5
+
+
+def test_zero_sites():
+    from paper_2208_06970_b200 import VoxelGrid, voronoi_classify
+
+    grid = VoxelGrid((4, 4, 1), (1, 1, 1), {})
+    tess = voronoi_classify(grid, _labels(np.zeros(16), (4, 4, 1)), [])
+    assert np.all(tess.site_of == -1) and np.all(np.isinf(tess.dist))
+    assert tess.report["components_without_sites"] == [0]
