@@ -361,7 +361,7 @@ def main():
         cur = [Site(tuple(p), int(c)) for p, c in zip(pos_start, sc_np)]
         ke = max(1, min(args.steps, 10))
         cur_sites = cur
-        for _ in range(1):
+        for _ in range(3):  # warm-up: first API calls build plans / graphs / pool
             t_ = voronoi_classify(grid, labels, cur_sites, weights if params.weight_field else None)
             cur_sites, _ = centroidal_update(t_)
         torch.cuda.synchronize()
