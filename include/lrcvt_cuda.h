@@ -142,6 +142,30 @@ int lrcvt_aggregate(int64_t n, int32_t n_fields, const float *const *field_ptrs,
                     double *axes, int64_t *d_count, double *d_sums, double *d_minmax,
                     int64_t *d_hist, void *stream);
 
+/* Multi-GPU global mode (z-slab partitioned evaluation over replicated
+ * state). A rank's plan owns planes [zlo, zhi); the caller
+ * drives rounds: begin -> { eval -> all-gather proposals -> commit }* ->
+ * phase2 -> { rounds, sweep (eval sweep=1, commit sweep=1) }* -> finish.
+ * Proposals are 24-byte records {f64 d; i32 v, site, src, pad} at
+ * lrcvt_mg_proposals(plan) after an eval; commit takes the concatenation of
+ * all ranks' proposals (any order). Counts are summed by the caller for
+ * report rounds/evaluations/commits; results are bit-identical to
+ * lrcvt_classify on one domain. */
+int lrcvt_mg_set_slab(lrcvt_plan *plan, int64_t zlo, int64_t zhi);
+int lrcvt_mg_begin(lrcvt_plan *plan, int64_t n_sites, const double *d_site_pos,
+                   const int32_t *d_site_comp, int32_t *d_site_src, double *d_dist,
+                   int64_t *n_frontier, void *stream);
+int lrcvt_mg_phase2(lrcvt_plan *plan, int64_t n_sites, const int32_t *d_site_comp,
+                    int64_t *n_frontier, void *stream);
+int lrcvt_mg_eval(lrcvt_plan *plan, int32_t phase, int32_t sweep, int64_t *n_evaluated,
+                  int64_t *n_prop, void *stream);
+void *lrcvt_mg_proposals(lrcvt_plan *plan);
+int lrcvt_mg_copy_proposals(lrcvt_plan *plan, void *d_dst, int64_t n, void *stream);
+int lrcvt_mg_commit(lrcvt_plan *plan, const void *d_props, int64_t n_props, int32_t sweep,
+                    int64_t *n_next, void *stream);
+int lrcvt_mg_finish(lrcvt_plan *plan, const int32_t *d_site_src, uint8_t *d_state,
+                    int64_t *assigned, void *stream);
+
 /* Instrumentation for bench.py: enable CUDA-event timing of every k_eval
  * launch (the dominant kernel) on the plan; read back launches, voxels
  * evaluated and summed device milliseconds. lrcvt_launch_count() counts this

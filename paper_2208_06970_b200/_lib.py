@@ -68,6 +68,15 @@ SIGNATURES = {
     "lrcvt_plan_timing": (c_int, [c_void_p, POINTER(c_int64), POINTER(c_int64), POINTER(c_double)]),
     "lrcvt_launch_count": (ctypes.c_ulonglong, []),
     "lrcvt_plan_profile": (c_int, [c_void_p, POINTER(c_double)]),
+    "lrcvt_mg_set_slab": (c_int, [c_void_p, c_int64, c_int64]),
+    "lrcvt_mg_begin": (c_int, [c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_void_p, POINTER(c_int64),
+                               c_void_p]),
+    "lrcvt_mg_phase2": (c_int, [c_void_p, c_int64, c_void_p, POINTER(c_int64), c_void_p]),
+    "lrcvt_mg_eval": (c_int, [c_void_p, c_int32, c_int32, POINTER(c_int64), POINTER(c_int64), c_void_p]),
+    "lrcvt_mg_proposals": (c_void_p, [c_void_p]),
+    "lrcvt_mg_copy_proposals": (c_int, [c_void_p, c_void_p, c_int64, c_void_p]),
+    "lrcvt_mg_commit": (c_int, [c_void_p, c_void_p, c_int64, c_int32, POINTER(c_int64), c_void_p]),
+    "lrcvt_mg_finish": (c_int, [c_void_p, c_void_p, c_void_p, POINTER(c_int64), c_void_p]),
     "lrcvt_isobands": (
         c_int,
         [c_int64, c_void_p, c_void_p, c_int32, c_void_p, c_void_p],

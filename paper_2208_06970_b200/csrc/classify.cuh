@@ -141,7 +141,8 @@ __global__ void k_eligible(const int* __restrict__ comp, const uint8_t* __restri
 __device__ __forceinline__ void mark_and_append(const Geo& g, const uint32_t* __restrict__ nbm,
                                                 bool active, int v, bool self,
                                                 uint32_t* __restrict__ bm,
-                                                int* __restrict__ next, int* counter) {
+                                                int* __restrict__ next, int* counter,
+                                                int zlo = 0, int zhi = 1 << 30) {
   // The 27-cube around v is 9 x-rows of 3 voxels (dx = -1, 0, +1); a row's
   // three bits sit in one bitmap word (two when they straddle a word), so
   // each row costs one cached precheck load and at most one atomicOr with a
@@ -149,11 +150,17 @@ __device__ __forceinline__ void mark_and_append(const Geo& g, const uint32_t* __
   // only set during a round), which merely sends that row to the atomic.
   // newmask uses the 27-cube index j = (dz+1)*9 + (dy+1)*3 + (dx+1).
   unsigned newmask = 0;
+  int vz = 0;
+  if (active && (zlo > 0 || zhi < g.nz)) {  // slab mode: only rows inside [zlo, zhi)
+    vz = (int)((unsigned)v / (unsigned)g.nxy);
+    if (vz < zlo - 1 || vz > zhi) active = false;
+  }
   if (active) {
     const unsigned same = __ldg(nbm + v);
 #pragma unroll
     for (int r = 0; r < 9; r++) {
       const int dy = r % 3 - 1, dz = r / 3 - 1;
+      if ((zlo > 0 || zhi < g.nz) && (vz + dz < zlo || vz + dz >= zhi)) continue;
       // k of (dx=-1,dy,dz): j = 3r (+0), k = j < 13 ? j : j - 1
       const int j0 = 3 * r;
       unsigned want = 0;  // bit t <=> dx = t - 1
@@ -262,7 +269,8 @@ __global__ void __launch_bounds__(128) k_commit(const Prop* __restrict__ imp,
                                                 Geo g, const uint32_t* __restrict__ nbm,
                                                 uint32_t* __restrict__ bm,
                                                 const cudaGraphConditionalHandle* __restrict__ hs, int n_classes,
-                                                cudaGraphConditionalHandle loop, int end_mode) {
+                                                cudaGraphConditionalHandle loop, int end_mode,
+                                                int zlo = 0, int zhi = 1 << 30) {
   const int n_imp = *(volatile int*)(counters + C_NIMP);
   int* next = ctl->nxt;
   int2* __restrict__ ss = ctl->ss;
@@ -278,9 +286,9 @@ __global__ void __launch_bounds__(128) k_commit(const Prop* __restrict__ imp,
       __stcg(ss + v, make_int2(p.s, p.src));  // explicit global stores: the
       __stcg(dist + v, p.d);                  // pointers come from RoundCtl
     }
-    mark_and_append(g, nbm, active, v, false, bm, next, counters + C_NNEXT);
+    mark_and_append(g, nbm, active, v, false, bm, next, counters + C_NNEXT, zlo, zhi);
   }
-  if (end_mode < 0) return;  // sweep: k_sweep_end follows
+  if (end_mode < 0) return;  // sweep / multi-GPU: the host ends the round
   // the last block to finish ends the round (no separate launch)
   __shared__ bool last;
   __threadfence();
@@ -385,7 +393,8 @@ __global__ void __launch_bounds__(128) k_seed_groups(Geo g, const uint32_t* __re
                                                      double* __restrict__ dist,
                                                      uint32_t* __restrict__ bm,
                                                      int* __restrict__ next,
-                                                     int* __restrict__ counters) {
+                                                     int* __restrict__ counters,
+                                                     int zlo = 0, int zhi = 1 << 30) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   bool head = false;
   int v = 0;
@@ -405,7 +414,7 @@ __global__ void __launch_bounds__(128) k_seed_groups(Geo g, const uint32_t* __re
     dist[v] = cur_d;
   }
   if (blockIdx.x * blockDim.x >= n_sites) return;
-  mark_and_append(g, nbm, head, v, true, bm, next, counters + C_NNEXT);
+  mark_and_append(g, nbm, head, v, true, bm, next, counters + C_NNEXT, zlo, zhi);
 }
 
 // tessellation.py:191-194 state bits, plus the `assigned` count.

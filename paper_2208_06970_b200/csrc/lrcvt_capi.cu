@@ -226,6 +226,9 @@ struct lrcvt_plan {
   cudaStream_t cap = nullptr;  // capture stream
   int eval_blocks[3] = {0, 0, 0};
   int commit_blocks = 0;
+  // multi-GPU global mode: own z-slab [zlo, zhi); zhi = 1<<30 disables it
+  int zlo = 0, zhi = 1 << 30;
+  int h_ncur = 0;  // host mirror of ctl->n_cur in multi-GPU stepping
   // eligible list of the last classify is reused by centroidal_update when
   // the caller guarantees the site-component set is unchanged
   bool reuse_eligible = false;
@@ -280,9 +283,12 @@ int prepare_eligible(lrcvt_plan* p, int n_sites, const int* site_comp, cudaStrea
     CKL("k_mark_site_comps"); LAUNCHED(1);
   }
   EligiblePred pred{p->comp, p->has_site};
-  cub::CountingInputIterator<int> it(0);
+  // own slab only in multi-GPU global mode (tessellation.py:163-164 restricted)
+  const int z0 = p->zlo;
+  const int z1 = p->zhi < p->g.nz ? p->zhi : p->g.nz;
+  cub::CountingInputIterator<int> it(z0 * p->g.nxy);
   size_t bytes = p->cub_bytes;
-  CK(cub::DeviceSelect::If(p->cub_tmp, bytes, it, p->eligible, p->d_nel, (int)p->g.n, pred, st));
+  CK(cub::DeviceSelect::If(p->cub_tmp, bytes, it, p->eligible, p->d_nel, (z1 - z0) * p->g.nxy, pred, st));
   return 0;
 }
 
@@ -976,6 +982,152 @@ int lrcvt_aggregate(int64_t n, int32_t n_fields, const float* const* field_ptrs,
                   (void*)sege, (void*)d_pairs, (void*)d_fields, (void*)d_axes, (void*)d_lohi, tmp})
     if (b) CK(cudaFreeAsync(b, st));
   CK(cudaStreamSynchronize(st));
+  return 0;
+}
+
+
+// ---------------------------------------------------------------------------
+// Multi-GPU global mode: replicated per-voxel state, each rank
+// evaluates only its z-slab's frontier; the round's proposals are all-gathered
+// by the caller and committed on every rank (which enqueues only own-slab
+// neighbours). The caller drives rounds with these steps.
+
+__global__ void k_mg_round_end(RoundCtl* ctl, int* counters, int sweep) {
+  const int n_next = counters[C_NNEXT];
+  if (sweep) {
+    ctl->cur = ctl->nxt;
+    ctl->nxt = ctl->stash;
+  } else {
+    int* t = ctl->cur;
+    ctl->cur = ctl->nxt;
+    ctl->nxt = t;
+  }
+  ctl->n_cur = n_next;
+  counters[C_NIMP] = 0;
+  counters[C_NNEXT] = 0;
+}
+
+int lrcvt_mg_set_slab(lrcvt_plan* p, int64_t zlo, int64_t zhi) {
+  if (!p || zlo < 0 || zhi <= zlo || zlo >= p->g.nz) return set_error(LRCVT_E_ARG, "lrcvt_mg_set_slab");
+  p->zlo = (int)zlo;
+  p->zhi = zhi >= p->g.nz ? p->g.nz : (int)zhi;  // kernels filter iff zlo > 0 || zhi < nz
+  p->eligible_valid = false;
+  return 0;
+}
+
+int lrcvt_mg_begin(lrcvt_plan* p, int64_t n_sites, const double* d_site_pos, const int32_t* d_site_comp,
+                   int32_t* d_site_src, double* d_dist, int64_t* n_frontier, void* stream) {
+  if (!p || n_sites < 1 || n_sites > p->max_sites || !d_site_pos || !d_site_comp || !d_site_src || !d_dist ||
+      !n_frontier)
+    return set_error(LRCVT_E_ARG, "lrcvt_mg_begin: bad arguments");
+  retain_pool();
+  cudaStream_t st = (cudaStream_t)stream;
+  const Geo& g = p->g;
+  const int S = (int)n_sites;
+  int2* ss = reinterpret_cast<int2*>(d_site_src);
+  k_fill_state<<<grid_for(g.n, 256, 148 * 32), 256, 0, st>>>(ss, d_dist, g.n);
+  CKL("k_fill_state");
+  CK(cudaMemsetAsync(p->counters, 0, sizeof(int) * C_NCOUNTERS, st));
+  k_pack_sites<<<grid_for(S, 256), 256, 0, st>>>(d_site_pos, S, p->site_pos);
+  CKL("k_pack_sites");
+  k_site_voxel<<<grid_for(S, 256), 256, 0, st>>>(g, p->comp, p->site_pos, d_site_comp, S, p->sk_key, p->sk_val,
+                                                 p->sk_d, p->counters);
+  CKL("k_site_voxel");
+  {
+    size_t bytes = p->cub_bytes;
+    CK(cub::DeviceRadixSort::SortPairs(p->cub_tmp, bytes, p->sk_key, p->sk_key2, p->sk_val, p->sk_val2, S, 0, 32,
+                                       st));
+  }
+  // every rank places every seed (replicated state); the phase-1 worklist
+  // holds the own slab's part only
+  k_seed_groups<<<grid_for(S, 128), 128, 0, st>>>(g, p->nbm, p->sk_key2, p->sk_val2, p->sk_d, S, ss, d_dist, p->bm,
+                                                  p->list_a, p->counters, p->zlo, p->zhi);
+  CKL("k_seed_groups");
+  k_phase1_start<<<1, 1, 0, st>>>(p->ctl, p->counters, p->list_a, p->list_b, ss, d_dist);
+  CKL("k_phase1_start");
+  CK(cudaMemcpyAsync(p->h_ctl, p->ctl, sizeof(RoundCtl), cudaMemcpyDeviceToHost, st));
+  CKR(sync_counters(p, st, C_NCOUNTERS));
+  if (p->h_counters[C_BAD]) return p->h_counters[C_BAD];
+  p->h_ncur = p->h_ctl->n_cur;
+  *n_frontier = p->h_ncur;
+  p->eligible_valid = false;
+  return 0;
+}
+
+int lrcvt_mg_phase2(lrcvt_plan* p, int64_t n_sites, const int32_t* d_site_comp, int64_t* n_frontier, void* stream) {
+  if (!p || !d_site_comp || !n_frontier) return set_error(LRCVT_E_ARG, "lrcvt_mg_phase2");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (prepare_eligible(p, (int)n_sites, d_site_comp, st)) return LRCVT_E_CUDA;
+  k_phase2_copy<<<148 * 4, 256, 0, st>>>(p->eligible, p->d_nel, p->ctl);
+  CKL("k_phase2_copy");
+  CK(cudaMemcpyAsync(p->h_counters + 7, p->d_nel, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  p->n_eligible = p->h_counters[7];
+  p->eligible_valid = true;
+  p->eligible_sites = n_sites;
+  p->h_ncur = (int)p->n_eligible;
+  *n_frontier = p->h_ncur;
+  return 0;
+}
+
+int lrcvt_mg_eval(lrcvt_plan* p, int32_t phase, int32_t sweep, int64_t* n_evaluated, int64_t* n_prop,
+                  void* stream) {
+  if (!p || phase < 1 || phase > 2 || !n_prop || !n_evaluated) return set_error(LRCVT_E_ARG, "lrcvt_mg_eval");
+  cudaStream_t st = (cudaStream_t)stream;
+  int n = p->h_ncur;
+  if (sweep) {
+    k_sweep_start<<<1, 1, 0, st>>>(p->ctl, p->eligible, p->d_nel);
+    CKL("k_sweep_start");
+    n = (int)p->n_eligible;
+  }
+  CK(cudaMemsetAsync(p->counters, 0, sizeof(int) * 2, st));
+  const int var = phase == 1 ? 0 : (p->g.dyadic ? 1 : 2);
+  if (n > 0) CKR(launch_eval_kernel(p, var, (n + eval_block_size(var) - 1) / eval_block_size(var), st));
+  CKR(sync_counters(p, st, 1));
+  *n_evaluated = n;
+  *n_prop = p->h_counters[C_NIMP];
+  return 0;
+}
+
+void* lrcvt_mg_proposals(lrcvt_plan* p) { return p ? (void*)p->imp : nullptr; }
+
+int lrcvt_mg_copy_proposals(lrcvt_plan* p, void* d_dst, int64_t n, void* stream) {
+  if (!p || n < 0 || (n > 0 && !d_dst)) return set_error(LRCVT_E_ARG, "lrcvt_mg_copy_proposals");
+  if (n > 0) CK(cudaMemcpyAsync(d_dst, p->imp, sizeof(Prop) * n, cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+  return 0;
+}
+
+int lrcvt_mg_commit(lrcvt_plan* p, const void* d_props, int64_t n_props, int32_t sweep, int64_t* n_next,
+                    void* stream) {
+  if (!p || n_props < 0 || (n_props > 0 && !d_props) || !n_next) return set_error(LRCVT_E_ARG, "lrcvt_mg_commit");
+  cudaStream_t st = (cudaStream_t)stream;
+  int hv[2] = {(int)n_props, 0};
+  CK(cudaMemcpyAsync(p->counters, hv, sizeof(int) * 2, cudaMemcpyHostToDevice, st));
+  if (n_props > 0) {
+    int blocks = (int)((n_props + 127) / 128);
+    if (blocks > p->commit_blocks) blocks = p->commit_blocks;
+    k_commit<<<blocks, 128, 0, st>>>((const Prop*)d_props, p->counters, p->ctl, p->g, p->nbm, p->bm, nullptr,
+                                     p->n_classes, cudaGraphConditionalHandle{}, -1, p->zlo, p->zhi);
+    CKL("k_commit");
+  }
+  CKR(sync_counters(p, st, 2));
+  const int nn = p->h_counters[C_NNEXT];
+  k_mg_round_end<<<1, 1, 0, st>>>(p->ctl, p->counters, sweep);
+  CKL("k_mg_round_end");
+  p->h_ncur = nn;
+  *n_next = nn;
+  return 0;
+}
+
+int lrcvt_mg_finish(lrcvt_plan* p, const int32_t* d_site_src, uint8_t* d_state, int64_t* assigned, void* stream) {
+  if (!p || !d_site_src || !assigned) return set_error(LRCVT_E_ARG, "lrcvt_mg_finish");
+  cudaStream_t st = (cudaStream_t)stream;
+  CK(cudaMemsetAsync(p->counters + C_ASSIGNED, 0, sizeof(int), st));
+  k_state<<<grid_for(p->g.n, 256, 148 * 16), 256, 0, st>>>(reinterpret_cast<const int2*>(d_site_src), p->g.n,
+                                                           d_state, p->counters);
+  CKL("k_state");
+  CKR(sync_counters(p, st, C_ASSIGNED + 1));
+  *assigned = p->h_counters[C_ASSIGNED];
   return 0;
 }
 
