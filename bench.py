@@ -242,6 +242,63 @@ def cpu_baseline(grid, labels, params, weights, pos, sc, budget_s=20.0, max_iter
             "sample": f"{it} Lloyd iteration(s) of the same workload from the timed region's starting sites"}
 
 
+def run_global(args, cfg, world, rank, local):
+    """--mode global: the same volume on every rank, evaluation partitioned in
+    z-slabs (paper_2208_06970_b200.multigpu), vote replicated; value = voxels x
+    steps / max-over-ranks device time (strong scaling)."""
+    import torch
+
+    from paper_2208_06970_b200 import _lib
+    from paper_2208_06970_b200.multigpu import Emulated, GlobalClassifier, TorchDist
+    from paper_2208_06970_b200.tessellation import lloyd_weight_mode, voxel_length
+
+    grid, labels, params, sites, weights = build_workload(cfg, 0)
+    coll = TorchDist() if world > 1 else Emulated(1)
+    S = len(sites)
+    gc = GlobalClassifier(grid.dims, grid.spacing, labels.component, labels.n_components, S, coll)
+    eng = gc.any_engine()
+    pos_d = torch.from_numpy(np.array([s.position for s in sites])).cuda()
+    sc_d = torch.from_numpy(np.array([s.component_id for s in sites], np.int32)).cuda()
+    mode, w_d = lloyd_weight_mode(torch, grid, params, weights)
+    vlen = voxel_length(grid.dims, grid.spacing)
+    L = _lib.lib()
+
+    def step(p):
+        gc.classify(p, sc_d)
+        _lib.check(L.lrcvt_mg_set_slab(eng.plan, 0, grid.dims[2]), "slab")
+        p2, _, _, _ = eng.centroidal(p, sc_d, mode, w_d, 0.5 * vlen)
+        return p2
+
+    for _ in range(args.warmup):
+        pos_d = step(pos_d)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        t0.record()
+        for _ in range(args.steps):
+            pos_d = step(pos_d)
+        t1.record()
+        torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1)
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    if rank == 0:
+        print(json.dumps({
+            "metric": "CVT-iteration voxels/s", "value": grid.size * args.steps / (ms / 1e3), "unit": "voxels/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "mode": "global",
+            "config": {"workload": cfg["label"], "dims": list(cfg["dims"]), "voxels": grid.size, "sites": S,
+                       "slabs": world},
+            "clocks": clk.summary()}), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -252,6 +309,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-passes", action="store_true")
+    ap.add_argument("--mode", default="blocks", choices=["blocks", "global"],
+                    help="blocks: one independent volume per rank (weak scaling, default); global: one volume "
+                         "z-slab partitioned over the ranks (strong scaling, proposal all-gather per round)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     cfg = CONFIGS[args.config]
@@ -270,6 +330,9 @@ def main():
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if args.mode == "global":
+        run_global(args, cfg, world, rank, local)
+        return
     grid, labels, params, sites, weights = build_workload(cfg, rank)
     n = grid.size
     S = len(sites)
@@ -366,11 +429,15 @@ def main():
             cur_sites, _ = centroidal_update(t_)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
+        marks = []
         for _ in range(ke):
             t_ = voronoi_classify(grid, labels, cur_sites, weights if params.weight_field else None)
             cur_sites, _ = centroidal_update(t_)
+            marks.append(time.perf_counter())
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
+        if os.environ.get("LRCVT_DEBUG_E2E"):
+            print("e2e step ms:", [round(1e3 * (b - a), 2) for a, b in zip([t0] + marks, marks)], file=sys.stderr)
         h2d = 2 * S * (24 + 4)
         d2h = S * (24 + 8) + 64
         e2e = {"value": n * ke * world / dt, "unit": "voxels/s", "h2d_bytes_per_step": h2d,
