@@ -142,6 +142,26 @@ int lrcvt_aggregate(int64_t n, int32_t n_fields, const float *const *field_ptrs,
                     double *axes, int64_t *d_count, double *d_sums, double *d_minmax,
                     int64_t *d_hist, void *stream);
 
+/* Seeding masses (seeding.py:71-107 component_masses; SURVEY.md §8(f) rank
+ * 1). In-band voxels (d_component >= 0) grouped by (component, block) --
+ * block = (x/bs) + nbx*((y/bs) + nby*(z/bs)), nbx = ceil(nx/bs), nby =
+ * ceil(ny/bs) -- voxels increasing inside a group, groups ordered by
+ * component then block (= np.lexsort((voxel, block, comp))). Weights m_v**gamma
+ * by weight_mode (LRCVT_W_*; d_weights NULL for ONES). Outputs (device):
+ * d_voxels int32[max_inband] the grouped voxel list, d_weights_sorted
+ * float64[max_inband] their weights (may be NULL), per group r < *n_runs:
+ * d_run_key int64 = comp * n_blocks + block, d_run_start int64, d_run_len
+ * int64, d_run_mass float64 = np.sum of the group's weights (numpy pairwise
+ * order, bit-exact). Host outputs: *n_inband, *n_runs, *total_mass = np.sum
+ * of all in-band weights in voxel order. Returns LRCVT_E_ARG (and the needed
+ * sizes in *n_inband / *n_runs) when max_inband or max_runs is too small. */
+int lrcvt_seed_masses(int64_t nx, int64_t ny, int64_t nz, int32_t block_size,
+                      const int32_t *d_component, int32_t n_components, int32_t weight_mode,
+                      const void *d_weights, int64_t max_inband, int64_t max_runs,
+                      int32_t *d_voxels, double *d_weights_sorted, int64_t *d_run_key,
+                      int64_t *d_run_start, int64_t *d_run_len, double *d_run_mass,
+                      int64_t *n_inband, int64_t *n_runs, double *total_mass, void *stream);
+
 /* Multi-GPU global mode (z-slab partitioned evaluation over replicated
  * state). A rank's plan owns planes [zlo, zhi); the caller
  * drives rounds: begin -> { eval -> all-gather proposals -> commit }* ->

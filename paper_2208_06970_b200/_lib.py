@@ -18,6 +18,7 @@ import os
 LIB_PATH = Path(os.environ.get("LRCVT_LIB") or Path(__file__).resolve().with_name("liblrcvt_cuda.so"))
 
 W_ONES, W_F64, W_F32_G1, W_F32_G2 = 0, 1, 2, 3
+E_CUDA, E_ARG, E_NOMEM = -1, -2, -3
 
 
 class ClassifyStats(ctypes.Structure):
@@ -94,6 +95,12 @@ SIGNATURES = {
         c_int,
         [c_int64, c_int32, c_void_p, c_void_p, c_void_p, c_int32, c_int32, c_int32, c_void_p,
          c_int32, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p],
+    ),
+    "lrcvt_seed_masses": (
+        c_int,
+        [c_int64, c_int64, c_int64, c_int32, c_void_p, c_int32, c_int32, c_void_p, c_int64, c_int64,
+         c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, POINTER(c_int64), POINTER(c_int64),
+         POINTER(c_double), c_void_p],
     ),
 }
 

@@ -16,6 +16,7 @@
 #include "eval_p1.cuh"
 #include "eval_p2.cuh"
 #include "aggregate.cuh"
+#include "seeding.cuh"
 
 using namespace lrcvt;
 
@@ -424,6 +425,48 @@ int run_rounds(lrcvt_plan* p, int var, cudaStream_t st) {
   }
 }
 
+}  // namespace
+
+namespace {
+// stream-ordered scratch released on every exit path
+struct Scratch {
+  cudaStream_t st;
+  std::vector<void*> ptrs;
+  explicit Scratch(cudaStream_t s) : st(s) {}
+  template <typename T>
+  cudaError_t get(T** p, int64_t count) {
+    *p = nullptr;
+    cudaError_t e = cudaMallocAsync((void**)p, sizeof(T) * (size_t)(count > 0 ? count : 1), st);
+    if (e == cudaSuccess) ptrs.push_back(*p);
+    return e;
+  }
+  ~Scratch() {
+    for (void* q : ptrs) cudaFreeAsync(q, st);
+  }
+};
+
+// numpy's pairwise split (seeding.cuh) cut into subtrees of at most kCut
+// elements, left to right, and the sum rebuilt in the same shape
+constexpr int64_t kSubtree = int64_t(1) << 14;
+void pw_split(int64_t lo, int64_t n, std::vector<int64_t>& L, std::vector<int64_t>& N) {
+  if (n <= kSubtree) {
+    L.push_back(lo);
+    N.push_back(n);
+    return;
+  }
+  int64_t n2 = n / 2;
+  n2 -= n2 % 8;
+  pw_split(lo, n2, L, N);
+  pw_split(lo + n2, n - n2, L, N);
+}
+double pw_join(int64_t n, const std::vector<double>& v, size_t& k) {
+  if (n <= kSubtree) return v[k++];
+  int64_t n2 = n / 2;
+  n2 -= n2 % 8;
+  const double a = pw_join(n2, v, k);
+  const double b = pw_join(n - n2, v, k);
+  return a + b;
+}
 }  // namespace
 
 extern "C" {
@@ -1128,6 +1171,111 @@ int lrcvt_mg_finish(lrcvt_plan* p, const int32_t* d_site_src, uint8_t* d_state, 
   CKL("k_state");
   CKR(sync_counters(p, st, C_ASSIGNED + 1));
   *assigned = p->h_counters[C_ASSIGNED];
+  return 0;
+}
+
+
+int lrcvt_seed_masses(int64_t nx, int64_t ny, int64_t nz, int32_t block_size, const int32_t* d_component,
+                      int32_t n_components, int32_t weight_mode, const void* d_weights, int64_t max_inband,
+                      int64_t max_runs, int32_t* d_voxels, double* d_weights_sorted, int64_t* d_run_key,
+                      int64_t* d_run_start, int64_t* d_run_len, double* d_run_mass, int64_t* n_inband,
+                      int64_t* n_runs, double* total_mass, void* stream) {
+  retain_pool();
+  const int64_t n = nx * ny * nz;
+  if (nx < 1 || ny < 1 || nz < 1 || n >= (int64_t(1) << 31) || block_size < 1 || !d_component ||
+      n_components < 0 || weight_mode < 0 || weight_mode > 3 || (weight_mode != LRCVT_W_ONES && !d_weights) ||
+      !d_voxels || !d_run_key || !d_run_start || !d_run_len || !d_run_mass || !n_inband || !n_runs ||
+      !total_mass)
+    return set_error(LRCVT_E_ARG, "lrcvt_seed_masses: bad arguments");
+  cudaStream_t st = (cudaStream_t)stream;
+  *n_inband = 0;
+  *n_runs = 0;
+  *total_mass = 0.0;
+  const int64_t bs = block_size;
+  const int64_t nbx = (nx + bs - 1) / bs, nby = (ny + bs - 1) / bs, nbz = (nz + bs - 1) / bs;
+  const int64_t n_blocks = nbx * nby * nbz;
+  SeedWeight w{weight_mode, (const double*)d_weights, (const float*)d_weights};
+  if (weight_mode == LRCVT_W_ONES) w.w64 = nullptr, w.w32 = nullptr;
+  Scratch sc(st);
+  int* list = nullptr;
+  int* cnt = nullptr;
+  void* tmp = nullptr;
+  size_t b = 0;
+  CK(sc.get(&list, n));
+  CK(sc.get(&cnt, 1));
+  cub::CountingInputIterator<int> it(0);
+  IsInband pred{d_component};
+  CK(cub::DeviceSelect::If(nullptr, b, it, list, cnt, (int)n, pred, st));
+  CK(sc.get((char**)&tmp, (int64_t)b));
+  CK(cub::DeviceSelect::If(tmp, b, it, list, cnt, (int)n, pred, st));
+  int h_cnt = 0;
+  CK(cudaMemcpyAsync(&h_cnt, cnt, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  const int64_t m = h_cnt;
+  *n_inband = m;
+  if (m > max_inband) return set_error(LRCVT_E_ARG, "lrcvt_seed_masses: max_inband too small");
+  if (m == 0) return 0;
+  unsigned long long *key = nullptr, *key2 = nullptr;
+  int64_t* nr = nullptr;
+  int64_t *rk = nullptr, *rl = nullptr;
+  double* ws = d_weights_sorted;
+  CK(sc.get(&key, m));
+  CK(sc.get(&key2, m));
+  CK(sc.get(&nr, 1));
+  CK(sc.get(&rk, m));
+  CK(sc.get(&rl, m));
+  if (!ws) CK(sc.get(&ws, m));
+  k_seed_keys<<<grid_for(m, 256, 148 * 16), 256, 0, st>>>(list, m, d_component, (int)nx, (int)ny, (int)bs, nbx,
+                                                          nby, n_blocks, key);
+  CKL("k_seed_keys"); LAUNCHED(1);
+  int bits = 1;
+  const unsigned long long kmax = (unsigned long long)(n_components > 0 ? n_components : 1) * n_blocks;
+  while (bits < 64 && (1ull << bits) < kmax) bits++;
+  b = 0;
+  CK(cub::DeviceRadixSort::SortPairs(nullptr, b, key, key2, list, d_voxels, (int)m, 0, bits, st));
+  void* tmp2 = nullptr;
+  CK(sc.get((char**)&tmp2, (int64_t)b));
+  CK(cub::DeviceRadixSort::SortPairs(tmp2, b, key, key2, list, d_voxels, (int)m, 0, bits, st));
+  // group boundaries (unique keys + lengths)
+  b = 0;
+  CK(cub::DeviceRunLengthEncode::Encode(nullptr, b, key2, (unsigned long long*)rk, rl, nr, (int)m, st));
+  void* tmp3 = nullptr;
+  CK(sc.get((char**)&tmp3, (int64_t)b));
+  CK(cub::DeviceRunLengthEncode::Encode(tmp3, b, key2, (unsigned long long*)rk, rl, nr, (int)m, st));
+  // total mass in voxel order: subtrees on the device, joined on the host
+  std::vector<int64_t> tl, tn;
+  pw_split(0, m, tl, tn);
+  const int nt = (int)tl.size();
+  int64_t *d_tl = nullptr, *d_tn = nullptr;
+  double* d_tv = nullptr;
+  CK(sc.get(&d_tl, nt));
+  CK(sc.get(&d_tn, nt));
+  CK(sc.get(&d_tv, nt));
+  CK(cudaMemcpyAsync(d_tl, tl.data(), sizeof(int64_t) * nt, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d_tn, tn.data(), sizeof(int64_t) * nt, cudaMemcpyHostToDevice, st));
+  k_seed_subtrees<<<grid_for(nt, 64), 64, 0, st>>>(list, w, d_tl, d_tn, nt, d_tv);
+  CKL("k_seed_subtrees"); LAUNCHED(1);
+  k_seed_weights<<<grid_for(m, 256, 148 * 16), 256, 0, st>>>(d_voxels, m, w, ws);
+  CKL("k_seed_weights"); LAUNCHED(1);
+  int64_t h_nr = 0;
+  std::vector<double> tv(nt);
+  CK(cudaMemcpyAsync(&h_nr, nr, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(tv.data(), d_tv, sizeof(double) * nt, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  size_t k = 0;
+  *total_mass = 0.0 + pw_join(m, tv, k);
+  *n_runs = h_nr;
+  if (h_nr > max_runs) return set_error(LRCVT_E_ARG, "lrcvt_seed_masses: max_runs too small");
+  b = 0;
+  CK(cub::DeviceScan::ExclusiveSum(nullptr, b, rl, d_run_start, (int)h_nr, st));
+  void* tmp4 = nullptr;
+  CK(sc.get((char**)&tmp4, (int64_t)b));
+  CK(cub::DeviceScan::ExclusiveSum(tmp4, b, rl, d_run_start, (int)h_nr, st));
+  CK(cudaMemcpyAsync(d_run_key, rk, sizeof(int64_t) * h_nr, cudaMemcpyDeviceToDevice, st));
+  CK(cudaMemcpyAsync(d_run_len, rl, sizeof(int64_t) * h_nr, cudaMemcpyDeviceToDevice, st));
+  k_seed_run_mass<<<grid_for(h_nr, 64), 64, 0, st>>>(ws, d_run_start, d_run_len, h_nr, d_run_mass);
+  CKL("k_seed_run_mass"); LAUNCHED(1);
+  CK(cudaStreamSynchronize(st));
   return 0;
 }
 
