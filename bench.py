@@ -171,6 +171,30 @@ def run_reference(args, cfg, world, rank):
     print(json.dumps(line), flush=True)
 
 
+def seeding_pass(grid, labels, params):
+    """Seeding stage: the GPU mass table alone and the
+    whole seed_sites (GPU table + host numpy draw), wall clock; the host numpy
+    table beside it on volumes where it takes seconds, not minutes."""
+    import torch
+
+    from paper_2208_06970_b200.seeding import component_masses, component_masses_device, seed_sites
+
+    def wall(fn):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        fn()
+        torch.cuda.synchronize()
+        return 1e3 * (time.perf_counter() - t0)
+
+    component_masses_device(grid, labels, params)  # warm-up (allocator, CUB)
+    out = {"masses_gpu_ms": wall(lambda: component_masses_device(grid, labels, params)),
+           "seed_sites_ms": wall(lambda: seed_sites(grid, labels, params, device=True))}
+    if grid.size <= (1 << 22):
+        out["masses_host_numpy_ms"] = wall(lambda: component_masses(grid, labels, params))
+    out["note"] = "wall clock incl. D2H of the grouped voxel/weight lists; the draw (Generator.choice) is host numpy"
+    return out
+
+
 def one_off_passes(grid, labels, eng, config, S, reps=3):
     """Device-resident timing of the passes reported beside the iteration
     metric: isoband + component masks, and the per-cell
@@ -415,6 +439,8 @@ def main():
 
     L.lrcvt_plan_reuse_eligible(eng.plan, 0)  # public-API e2e below takes the general path
     passes = one_off_passes(grid, labels, eng, args.config, S) if not args.no_passes else None
+    if passes is not None:
+        passes["seeding"] = seeding_pass(grid, labels, params)
 
     # end-to-end through the public API with host numpy in/out
     e2e = None

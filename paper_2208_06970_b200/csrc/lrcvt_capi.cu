@@ -854,10 +854,20 @@ int lrcvt_label_components(int64_t nx, int64_t ny, int64_t nz, const int32_t* d_
   cub::CountingInputIterator<int> it(0);
   CK(cudaMallocAsync((void**)&L, sizeof(int) * n, st));
   CK(cudaMallocAsync((void**)&cnt, sizeof(int), st));
-  k_ccl_init<<<grid_for(n, 256, 148 * 16), 256, 0, st>>>(d_layer, n, n_layers, L);
-  CKL("k_ccl_init"); LAUNCHED(1);
-  k_ccl_merge<<<grid_for(n, 256, 148 * 16), 256, 0, st>>>(g, d_layer, n_layers, L);
-  CKL("k_ccl_merge"); LAUNCHED(1);
+  // tile-local labelling in shared memory, then cross-tile unions on tile faces
+  if (nz > 1) {
+    const int64_t tiles = ((nx + 31) / 32) * ((ny + 3) / 4) * ((nz + 3) / 4);
+    k_ccl_tile<32, 4, 4><<<(unsigned)tiles, 512, 0, st>>>(g, d_layer, n_layers, L);
+    CKL("k_ccl_tile"); LAUNCHED(1);
+    k_ccl_faces<32, 4, 4><<<(unsigned)tiles, 256, 0, st>>>(g, d_layer, n_layers, L);
+    CKL("k_ccl_faces"); LAUNCHED(1);
+  } else {
+    const int64_t tiles = ((nx + 31) / 32) * ((ny + 15) / 16);
+    k_ccl_tile<32, 16, 1><<<(unsigned)tiles, 512, 0, st>>>(g, d_layer, n_layers, L);
+    CKL("k_ccl_tile"); LAUNCHED(1);
+    k_ccl_faces<32, 16, 1><<<(unsigned)tiles, 256, 0, st>>>(g, d_layer, n_layers, L);
+    CKL("k_ccl_faces"); LAUNCHED(1);
+  }
   k_ccl_compress<<<grid_for(n, 256, 148 * 16), 256, 0, st>>>(n, L);
   CKL("k_ccl_compress"); LAUNCHED(1);
   pred.L = L;

@@ -73,17 +73,114 @@ __global__ void k_ccl_init(const int* __restrict__ layer, int64_t n, int n_layer
     L[i] = in_layers(layer[i], n_layers) ? (int)i : -1;
 }
 
-__global__ void k_ccl_merge(Geo g, const int* __restrict__ layer, int n_layers, int* __restrict__ L) {
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < g.n; i += stride) {
-    const int v = (int)i;
-    const int l = layer[v];
-    if (!in_layers(l, n_layers)) continue;
-    int x, y, z;
-    coords(g, v, x, y, z);
-    if (x > 0 && layer[v - 1] == l) uf_union(L, v, v - 1);
-    if (y > 0 && layer[v - g.nx] == l) uf_union(L, v, v - g.nx);
-    if (z > 0 && layer[v - g.nxy] == l) uf_union(L, v, v - g.nxy);
+// Tile-local labelling: one CTA per TX x TY x TZ tile (TX = 32: a warp is one
+// x-row), one thread per voxel. Rows first, without atomics: a lane's run
+// start comes from a ballot of "layer differs from the left neighbour". Then
+// the y and z adjacencies unite run starts in a shared-memory union-find
+// (larger index linked under smaller, atomicMin), one union per distinct
+// (run, neighbour-run) pair in the warp. Local row-major order equals global
+// row-major order restricted to the tile, so a local root is also the
+// minimum global index of that tile component; every voxel then points at
+// its local root in global L.
+template <int TX, int TY, int TZ>
+__global__ void __launch_bounds__(TX * TY * TZ) k_ccl_tile(Geo g, const int* __restrict__ layer, int n_layers,
+                                                           int* __restrict__ L) {
+  static_assert(TX == 32, "a warp is one x-row of the tile");
+  constexpr int T = TX * TY * TZ;
+  __shared__ int s_par[T];
+  __shared__ signed char s_lay[T];
+  const int t = threadIdx.x;
+  const int lx = t % TX, ly = (t / TX) % TY, lz = t / (TX * TY);
+  const int64_t ntx = (g.nx + TX - 1) / TX, nty = (g.ny + TY - 1) / TY;
+  const int64_t b = blockIdx.x;
+  const int x = (int)(b % ntx) * TX + lx;
+  const int y = (int)((b / ntx) % nty) * TY + ly;
+  const int z = (int)(b / (ntx * nty)) * TZ + lz;
+  const bool in = x < g.nx && y < g.ny && z < g.nz;
+  const int v = in ? x + g.nx * (y + g.ny * z) : 0;
+  int l = in ? __ldcs(layer + v) : -1;
+  if (!in_layers(l, n_layers)) l = -1;
+  const int left = __shfl_up_sync(0xffffffffu, l, 1);
+  const unsigned starts = __ballot_sync(0xffffffffu, l >= 0 && (lx == 0 || left != l));
+  const int row = t - lx;
+  const int run = row + 31 - __clz(starts & (0xffffffffu >> (31 - lx)));
+  s_lay[t] = (signed char)l;
+  s_par[t] = l >= 0 ? run : t;
+  __syncthreads();
+  volatile int* vp = s_par;  // parents change under other threads' atomics
+  auto find = [&](int q) {
+    int p = vp[q];
+    while (p != q) { q = p; p = vp[q]; }
+    return q;
+  };
+  auto unite = [&](int p, int q) {
+    for (;;) {
+      p = find(p);
+      q = find(q);
+      if (p == q) return;
+      if (p < q) { const int w = p; p = q; q = w; }
+      const int old = atomicMin(&s_par[p], q);
+      if (old == p) return;
+      p = old;
+    }
+  };
+#pragma unroll
+  for (int dir = 0; dir < 2; ++dir) {
+    const int step = dir == 0 ? TX : TX * TY;
+    const bool edge = dir == 0 ? ly > 0 : lz > 0;
+    if (dir == 1 && TZ == 1) break;
+    int other = -1;
+    if (l >= 0 && edge && s_lay[t - step] == l) other = vp[t - step];  // a run start or its ancestor
+    const unsigned key = other >= 0 ? ((unsigned)run << 16) | (unsigned)other : 0xffffffffu;
+    const unsigned grp = __match_any_sync(0xffffffffu, key);
+    if (other >= 0 && lx == __ffs(grp) - 1) unite(run, other);
+  }
+  __syncthreads();
+  if (!in) return;
+  if (l < 0) {
+    L[v] = -1;
+    return;
+  }
+  int r = run;
+  while (s_par[r] != r) r = s_par[r];
+  const int rx = x - lx + r % TX, ry = y - ly + (r / TX) % TY, rz = z - lz + r / (TX * TY);
+  L[v] = rx + g.nx * (ry + g.ny * rz);
+}
+
+// Cross-tile merges: each CTA takes one tile's three lower faces and unites
+// every face voxel with its neighbour in the previous tile (same layer).
+// Lanes holding the same (root-hint, root-hint) pair elect one lane, so a
+// face shared by two tile components costs about one global union per warp.
+template <int TX, int TY, int TZ>
+__global__ void __launch_bounds__(256) k_ccl_faces(Geo g, const int* __restrict__ layer, int n_layers,
+                                                   int* __restrict__ L) {
+  constexpr int FX = TY * TZ, FY = TX * TZ, FZ = TX * TY;
+  const int64_t ntx = (g.nx + TX - 1) / TX, nty = (g.ny + TY - 1) / TY;
+  const int64_t b = blockIdx.x;
+  const int x0 = (int)(b % ntx) * TX, y0 = (int)((b / ntx) % nty) * TY, z0 = (int)(b / (ntx * nty)) * TZ;
+  for (int i = threadIdx.x; i < ((FX + FY + FZ + 31) / 32) * 32; i += blockDim.x) {
+    int x = -1, y = 0, z = 0, d = 0;
+    if (i < FX) {
+      if (x0 > 0) { x = x0; y = y0 + i % TY; z = z0 + i / TY; d = 1; }
+    } else if (i < FX + FY) {
+      const int k = i - FX;
+      if (y0 > 0) { x = x0 + k % TX; y = y0; z = z0 + k / TX; d = g.nx; }
+    } else if (i < FX + FY + FZ) {
+      const int k = i - FX - FY;
+      if (z0 > 0) { x = x0 + k % TX; y = y0 + k / TX; z = z0; d = g.nxy; }
+    }
+    int a = -1, c = -1;
+    if (x >= 0 && x < g.nx && y < g.ny && z < g.nz) {
+      const int v = x + g.nx * (y + g.ny * z);
+      const int l = layer[v];
+      if (in_layers(l, n_layers) && layer[v - d] == l) {
+        a = __ldcg(L + v);
+        c = __ldcg(L + v - d);
+      }
+    }
+    const unsigned long long key = ((unsigned long long)(unsigned)a << 32) | (unsigned)c;
+    const unsigned grp = __match_any_sync(0xffffffffu, key);
+    if (a >= 0 && (threadIdx.x & 31) == __ffs(grp) - 1) uf_union(L, a, c);
   }
 }
 
