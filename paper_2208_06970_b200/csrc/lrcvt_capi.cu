@@ -840,70 +840,61 @@ int lrcvt_isobands(int64_t n, const float* d_field, const double* d_iso, int32_t
 int lrcvt_label_components(int64_t nx, int64_t ny, int64_t nz, const int32_t* d_layer, int32_t n_layers,
                            int32_t* d_component, int32_t* n_components, void* stream) {
   retain_pool();
-  if (!geo_ok(nx, ny, nz, 1, 1, 1) || !d_layer || !d_component || !n_components || n_layers < 0)
+  if (!geo_ok(nx, ny, nz, 1, 1, 1) || !d_layer || !d_component || !n_components || n_layers < 0 ||
+      n_layers > 64)
     return set_error(LRCVT_E_ARG, "lrcvt_label_components: bad arguments");
   cudaStream_t st = (cudaStream_t)stream;
   Geo g = make_geo(nx, ny, nz, 1, 1, 1);
   const int64_t n = g.n;
-  int *L = nullptr, *roots = nullptr, *roots2 = nullptr, *keys = nullptr, *keys2 = nullptr, *cnt = nullptr;
-  void* tmp = nullptr;
-  int h_cnt = 0;
-  int rc = 0;
-  size_t b1 = 0, b2 = 0;
-  IsRoot pred{nullptr};
-  cub::CountingInputIterator<int> it(0);
-  CK(cudaMallocAsync((void**)&L, sizeof(int) * n, st));
-  CK(cudaMallocAsync((void**)&cnt, sizeof(int), st));
+  Scratch sc(st);
+  int *L = nullptr, *local = nullptr, *cnt = nullptr;
+  CK(sc.get(&L, n));
+  CK(sc.get(&local, n));
+  CK(sc.get(&cnt, 2));
+  CK(cudaMemsetAsync(cnt, 0, 2 * sizeof(int), st));
   // tile-local labelling in shared memory, then cross-tile unions on tile faces
   if (nz > 1) {
-    const int64_t tiles = ((nx + 31) / 32) * ((ny + 3) / 4) * ((nz + 3) / 4);
-    k_ccl_tile<32, 4, 4><<<(unsigned)tiles, 512, 0, st>>>(g, d_layer, n_layers, L);
+    const int64_t tiles = ((nx + 31) / 32) * ((ny + 3) / 4) * ((nz + 7) / 8);
+    k_ccl_tile<32, 4, 8><<<(unsigned)tiles, 128, 0, st>>>(g, d_layer, n_layers, L, local, cnt);
     CKL("k_ccl_tile"); LAUNCHED(1);
-    k_ccl_faces<32, 4, 4><<<(unsigned)tiles, 256, 0, st>>>(g, d_layer, n_layers, L);
+    k_ccl_faces<32, 4, 8><<<(unsigned)tiles, 256, 0, st>>>(g, d_layer, n_layers, L);
     CKL("k_ccl_faces"); LAUNCHED(1);
   } else {
     const int64_t tiles = ((nx + 31) / 32) * ((ny + 15) / 16);
-    k_ccl_tile<32, 16, 1><<<(unsigned)tiles, 512, 0, st>>>(g, d_layer, n_layers, L);
+    k_ccl_tile<32, 16, 1><<<(unsigned)tiles, 512, 0, st>>>(g, d_layer, n_layers, L, local, cnt);
     CKL("k_ccl_tile"); LAUNCHED(1);
     k_ccl_faces<32, 16, 1><<<(unsigned)tiles, 256, 0, st>>>(g, d_layer, n_layers, L);
     CKL("k_ccl_faces"); LAUNCHED(1);
   }
-  k_ccl_compress<<<grid_for(n, 256, 148 * 16), 256, 0, st>>>(n, L);
-  CKL("k_ccl_compress"); LAUNCHED(1);
-  pred.L = L;
-  CK(cub::DeviceSelect::If(nullptr, b1, it, (int*)nullptr, cnt, (int)n, pred, st));
-  CK(cudaMallocAsync((void**)&roots, sizeof(int) * n, st));
-  CK(cudaMallocAsync(&tmp, b1, st));
-  CK(cub::DeviceSelect::If(tmp, b1, it, roots, cnt, (int)n, pred, st));
-  CK(cudaMemcpyAsync(&h_cnt, cnt, sizeof(int), cudaMemcpyDeviceToHost, st));
+  int h_cnt[2] = {0, 0};
+  CK(cudaMemcpyAsync(h_cnt, cnt, sizeof(int), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
-  if (h_cnt > 0) {
-    CK(cudaMallocAsync((void**)&roots2, sizeof(int) * h_cnt, st));
-    CK(cudaMallocAsync((void**)&keys, sizeof(int) * h_cnt, st));
-    CK(cudaMallocAsync((void**)&keys2, sizeof(int) * h_cnt, st));
-    k_ccl_root_keys<<<grid_for(h_cnt, 256), 256, 0, st>>>(roots, h_cnt, d_layer, keys);
+  const int n_local = h_cnt[0];
+  if (n_local > 0) {
+    unsigned long long *key = nullptr, *key2 = nullptr;
+    void* tmp = nullptr;
+    size_t bytes = 0;
+    CK(sc.get(&key, n_local));
+    CK(sc.get(&key2, n_local));
+    k_ccl_root_keys<<<grid_for(n_local, 256), 256, 0, st>>>(local, n_local, L, d_layer, n_layers, key, cnt + 1);
     CKL("k_ccl_root_keys"); LAUNCHED(1);
-    int bits = 1;
-    while ((1ll << bits) <= n_layers) bits++;
-    CK(cub::DeviceRadixSort::SortPairs(nullptr, b2, keys, keys2, roots, roots2, h_cnt, 0, bits, st));
-    CK(cudaFreeAsync(tmp, st));
-    CK(cudaMallocAsync(&tmp, b2, st));
-    CK(cub::DeviceRadixSort::SortPairs(tmp, b2, keys, keys2, roots, roots2, h_cnt, 0, bits, st));
-    k_ccl_root_ids<<<grid_for(h_cnt, 256), 256, 0, st>>>(roots2, h_cnt, d_component);
+    int bits = 32;
+    while ((1ll << (bits - 31)) <= n_layers) bits++;
+    CK(cub::DeviceRadixSort::SortKeys(nullptr, bytes, key, key2, n_local, 0, bits, st));
+    CK(sc.get((char**)&tmp, (int64_t)bytes));
+    CK(cub::DeviceRadixSort::SortKeys(tmp, bytes, key, key2, n_local, 0, bits, st));
+    k_ccl_compress_roots<<<grid_for(n_local, 256), 256, 0, st>>>(local, n_local, L);
+    CKL("k_ccl_compress_roots"); LAUNCHED(1);
+    k_ccl_root_ids<<<grid_for(n_local, 256), 256, 0, st>>>(key2, n_local, n_layers, L);
     CKL("k_ccl_root_ids"); LAUNCHED(1);
   }
-  k_ccl_relabel<<<grid_for(n, 256, 148 * 16), 256, 0, st>>>(L, n, d_component);
+  k_ccl_relabel<<<grid_for(n, 256, 148 * 16), 256, 0, st>>>(L, n, d_component,
+                                                            ((uintptr_t)d_component & 15) == 0);
   CKL("k_ccl_relabel"); LAUNCHED(1);
-  CK(cudaFreeAsync(L, st));
-  CK(cudaFreeAsync(cnt, st));
-  CK(cudaFreeAsync(roots, st));
-  CK(cudaFreeAsync(tmp, st));
-  if (roots2) CK(cudaFreeAsync(roots2, st));
-  if (keys) CK(cudaFreeAsync(keys, st));
-  if (keys2) CK(cudaFreeAsync(keys2, st));
+  CK(cudaMemcpyAsync(h_cnt + 1, cnt + 1, sizeof(int), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
-  *n_components = h_cnt;
-  return rc;
+  *n_components = h_cnt[1];
+  return 0;
 }
 
 int lrcvt_component_table(int64_t nx, int64_t ny, int64_t nz, const int32_t* d_component,

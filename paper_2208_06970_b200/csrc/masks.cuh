@@ -5,10 +5,12 @@
 //   pass: 4 B read + 4 B write per voxel, 128-bit vectorised.
 // label_components (grid.py:166-220): 6-connected (4 in 2D) components per
 //   layer with dense ids ordered by (layer, first voxel in row-major order).
-//   Lock-free union-find where a union always links the larger root under
-//   the smaller one (atomicMin), so every tree's root is its component's
-//   minimum flat index -- the reference's "first occurrence" -- independent
-//   of thread timing. Ids: stable radix sort of roots by layer.
+//   Tile-local union-find in shared memory (k_ccl_tile), then a lock-free
+//   global union-find over tile faces (k_ccl_faces). Every union links the
+//   larger root under the smaller one (atomicMin), so every tree's root is
+//   its component's minimum flat index -- the reference's "first
+//   occurrence" -- independent of thread timing. Ids: radix sort of the
+//   global roots by (layer, voxel).
 #pragma once
 #include "common.cuh"
 
@@ -67,45 +69,52 @@ __device__ __forceinline__ void uf_union(int* L, int a, int b) {
 
 __device__ __forceinline__ bool in_layers(int l, int n_layers) { return l >= 0 && l < n_layers; }
 
-__global__ void k_ccl_init(const int* __restrict__ layer, int64_t n, int n_layers, int* __restrict__ L) {
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride)
-    L[i] = in_layers(layer[i], n_layers) ? (int)i : -1;
-}
-
-// Tile-local labelling: one CTA per TX x TY x TZ tile (TX = 32: a warp is one
-// x-row), one thread per voxel. Rows first, without atomics: a lane's run
-// start comes from a ballot of "layer differs from the left neighbour". Then
-// the y and z adjacencies unite run starts in a shared-memory union-find
-// (larger index linked under smaller, atomicMin), one union per distinct
-// (run, neighbour-run) pair in the warp. Local row-major order equals global
-// row-major order restricted to the tile, so a local root is also the
-// minimum global index of that tile component; every voxel then points at
-// its local root in global L.
+// Tile-local labelling: one CTA per TX x TY x TZ tile, TX*TY threads; a
+// warp is one x-row (TX = 32) and every thread walks its TZ voxels along z,
+// so TZ independent loads per thread are in flight. Rows first, without
+// atomics: a lane's run start comes from a ballot of "layer differs from the
+// left neighbour". Then the y and z adjacencies unite run starts in a
+// shared-memory union-find (larger index linked under smaller, atomicMin),
+// one union per distinct (run, neighbour-run) pair in the warp. Local
+// row-major order equals global row-major order restricted to the tile, so
+// a local root is also the minimum global index of that tile component;
+// every voxel then points at its local root in global L, and the local roots
+// (the only possible global roots) are appended to a compact list.
 template <int TX, int TY, int TZ>
-__global__ void __launch_bounds__(TX * TY * TZ) k_ccl_tile(Geo g, const int* __restrict__ layer, int n_layers,
-                                                           int* __restrict__ L) {
+__global__ void __launch_bounds__(TX * TY) k_ccl_tile(Geo g, const int* __restrict__ layer, int n_layers,
+                                                      int* __restrict__ L, int* __restrict__ local_roots,
+                                                      int* __restrict__ n_local) {
   static_assert(TX == 32, "a warp is one x-row of the tile");
-  constexpr int T = TX * TY * TZ;
+  constexpr int T = TX * TY * TZ, P = TX * TY;
   __shared__ int s_par[T];
   __shared__ signed char s_lay[T];
-  const int t = threadIdx.x;
-  const int lx = t % TX, ly = (t / TX) % TY, lz = t / (TX * TY);
+  __shared__ int s_root_list[T];
+  __shared__ int s_nroot, s_base;
+  const int t0 = threadIdx.x;  // position in a z-plane of the tile
+  const int lx = t0 % TX, ly = t0 / TX;
   const int64_t ntx = (g.nx + TX - 1) / TX, nty = (g.ny + TY - 1) / TY;
   const int64_t b = blockIdx.x;
   const int x = (int)(b % ntx) * TX + lx;
   const int y = (int)((b / ntx) % nty) * TY + ly;
-  const int z = (int)(b / (ntx * nty)) * TZ + lz;
-  const bool in = x < g.nx && y < g.ny && z < g.nz;
-  const int v = in ? x + g.nx * (y + g.ny * z) : 0;
-  int l = in ? __ldcs(layer + v) : -1;
-  if (!in_layers(l, n_layers)) l = -1;
-  const int left = __shfl_up_sync(0xffffffffu, l, 1);
-  const unsigned starts = __ballot_sync(0xffffffffu, l >= 0 && (lx == 0 || left != l));
-  const int row = t - lx;
-  const int run = row + 31 - __clz(starts & (0xffffffffu >> (31 - lx)));
-  s_lay[t] = (signed char)l;
-  s_par[t] = l >= 0 ? run : t;
+  const int z0 = (int)(b / (ntx * nty)) * TZ;
+  const int nzt = min(TZ, g.nz - z0);  // planes of this tile inside the grid
+  const bool in_xy = x < g.nx && y < g.ny;
+  const int v0 = x + g.nx * (y + g.ny * z0);
+  if (t0 == 0) s_nroot = 0;
+  {
+    int l[TZ];
+#pragma unroll
+    for (int k = 0; k < TZ; ++k) l[k] = in_xy && k < nzt ? __ldcs(layer + v0 + (int64_t)k * g.nxy) : -1;
+#pragma unroll
+    for (int k = 0; k < TZ; ++k) {
+      const int lk = in_layers(l[k], n_layers) ? l[k] : -1;
+      const int left = __shfl_up_sync(0xffffffffu, lk, 1);
+      const unsigned starts = __ballot_sync(0xffffffffu, lk >= 0 && (lx == 0 || left != lk));
+      const int t = k * P + t0;
+      s_lay[t] = (signed char)lk;
+      s_par[t] = lk >= 0 ? t - lx + 31 - __clz(starts & (0xffffffffu >> (31 - lx))) : t;
+    }
+  }
   __syncthreads();
   volatile int* vp = s_par;  // parents change under other threads' atomics
   auto find = [&](int q) {
@@ -124,27 +133,62 @@ __global__ void __launch_bounds__(TX * TY * TZ) k_ccl_tile(Geo g, const int* __r
       p = old;
     }
   };
-#pragma unroll
-  for (int dir = 0; dir < 2; ++dir) {
-    const int step = dir == 0 ? TX : TX * TY;
-    const bool edge = dir == 0 ? ly > 0 : lz > 0;
-    if (dir == 1 && TZ == 1) break;
-    int other = -1;
-    if (l >= 0 && edge && s_lay[t - step] == l) other = vp[t - step];  // a run start or its ancestor
-    const unsigned key = other >= 0 ? ((unsigned)run << 16) | (unsigned)other : 0xffffffffu;
-    const unsigned grp = __match_any_sync(0xffffffffu, key);
-    if (other >= 0 && lx == __ffs(grp) - 1) unite(run, other);
+  // y and z adjacencies between runs; a lane unites only where its
+  // (run, neighbour) pair differs from its left neighbour's. Shuffles first
+  // (warp-uniform trip count), unions after.
+#pragma unroll 1
+  for (int k = 0; k < TZ; ++k) {
+    const int t = k * P + t0;
+    const int l = k < nzt ? (int)s_lay[t] : -1;
+    const bool start = l >= 0 && (lx == 0 || s_lay[t - 1] != l);
+    const int run = start ? t : (l >= 0 ? vp[t] : -1);  // non-starts keep their run start as parent
+    int oy = -1, oz = -1;
+    if (l >= 0 && ly > 0 && s_lay[t - TX] == l) oy = vp[t - TX];
+    if (TZ > 1 && l >= 0 && k > 0 && s_lay[t - P] == l) oz = vp[t - P];
+    const int run_left = __shfl_up_sync(0xffffffffu, run, 1);
+    const int oy_left = __shfl_up_sync(0xffffffffu, oy, 1);
+    const int oz_left = __shfl_up_sync(0xffffffffu, oz, 1);
+    const bool fresh = lx == 0 || run != run_left;
+    if (oy >= 0 && (fresh || oy != oy_left)) unite(run, oy);
+    if (oz >= 0 && (fresh || oz != oz_left)) unite(run, oz);
+    __syncwarp();
   }
   __syncthreads();
-  if (!in) return;
-  if (l < 0) {
-    L[v] = -1;
-    return;
+  // run starts resolve their root once; every voxel then needs one hop.
+  // Roots are gathered in shared memory, then appended with one atomic.
+#pragma unroll 1
+  for (int k = 0; k < nzt; ++k) {
+    const int t = k * P + t0;
+    const int l = s_lay[t];
+    if (l >= 0 && (lx == 0 || s_lay[t - 1] != l)) {
+      int r = t;
+      while (vp[r] != r) r = vp[r];
+      if (r == t) {
+        if (in_xy) s_root_list[atomicAdd(&s_nroot, 1)] = v0 + k * g.nxy;
+      } else {
+        vp[t] = r;
+      }
+    }
   }
-  int r = run;
-  while (s_par[r] != r) r = s_par[r];
-  const int rx = x - lx + r % TX, ry = y - ly + (r / TX) % TY, rz = z - lz + r / (TX * TY);
-  L[v] = rx + g.nx * (ry + g.ny * rz);
+  __syncthreads();
+  if (t0 == 0) s_base = s_nroot ? atomicAdd(n_local, s_nroot) : 0;
+  __syncthreads();
+  for (int i = t0; i < s_nroot; i += P) local_roots[s_base + i] = s_root_list[i];
+#pragma unroll 1
+  for (int k = 0; k < nzt; ++k) {
+    if (!in_xy) break;
+    const int t = k * P + t0;
+    const int v = v0 + k * g.nxy;
+    const int l = s_lay[t];
+    if (l < 0) {
+      L[v] = -1;
+      continue;
+    }
+    int r = s_par[t];
+    if (r != t) r = s_par[r];  // voxel -> run start -> root
+    const int rz = r / P, rp = r % P;
+    L[v] = (x - lx + rp % TX) + g.nx * ((y - ly + rp / TX) + g.ny * (z0 + rz));
+  }
 }
 
 // Cross-tile merges: each CTA takes one tile's three lower faces and unites
@@ -184,34 +228,58 @@ __global__ void __launch_bounds__(256) k_ccl_faces(Geo g, const int* __restrict_
   }
 }
 
-__global__ void k_ccl_compress(int64_t n, int* __restrict__ L) {
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
-    const int p = L[i];
-    if (p >= 0 && p != (int)i) L[i] = uf_find(L, p);
-  }
-}
-
-// roots: key = layer, value = root voxel (input in increasing voxel order)
-__global__ void k_ccl_root_keys(const int* __restrict__ roots, int n_roots, const int* __restrict__ layer,
-                                int* __restrict__ key) {
+// sort key of each local root: (layer << 31 | voxel) if it is still a global
+// root after the face unions, else (n_layers << 31), which sorts last
+__global__ void k_ccl_root_keys(const int* __restrict__ local_roots, int n_local, const int* __restrict__ L,
+                                const int* __restrict__ layer, int n_layers,
+                                unsigned long long* __restrict__ key, int* __restrict__ n_roots) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n_roots) key[i] = layer[roots[i]];
-}
-
-// id of each root, written at the root's own slot of `comp`
-__global__ void k_ccl_root_ids(const int* __restrict__ sorted_roots, int n_roots, int* __restrict__ comp) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n_roots) comp[sorted_roots[i]] = i;
-}
-
-__global__ void k_ccl_relabel(const int* __restrict__ L, int64_t n, int* __restrict__ comp) {
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
-    const int r = L[i];
-    if (r < 0) comp[i] = LRCVT_NONE;
-    else if (r != (int)i) comp[i] = comp[r];  // roots already hold their id
+  bool root = false;
+  if (i < n_local) {
+    const int r = local_roots[i];
+    root = __ldcg(L + r) == r;
+    key[i] = root ? ((unsigned long long)layer[r] << 31) | (unsigned)r : (unsigned long long)n_layers << 31;
   }
+  const unsigned m = __ballot_sync(0xffffffffu, root);
+  if (m && (threadIdx.x & 31) == __ffs(m) - 1) atomicAdd(n_roots, __popc(m));
+}
+
+// local roots point straight at their global root afterwards
+__global__ void k_ccl_compress_roots(const int* __restrict__ local_roots, int n_local, int* __restrict__ L) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_local) return;
+  const int r = local_roots[i];
+  const int q = uf_find(L, r);
+  if (q != r) L[r] = q;
+}
+
+// dense id of every global root (keys sorted by (layer, voxel)), stored in
+// the root's own L slot as -(id) - 2 (-1 stays "not in a layer")
+__global__ void k_ccl_root_ids(const unsigned long long* __restrict__ sorted, int n_local, int n_layers,
+                               int* __restrict__ L) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n_local && (int)(sorted[i] >> 31) < n_layers) L[(int)(sorted[i] & 0x7fffffffu)] = -i - 2;
+}
+
+// every voxel takes its root's id: voxel -> local root -> global root, at
+// most two hops once the local roots are compressed. L is read-only here.
+__global__ void k_ccl_relabel(const int* __restrict__ L, int64_t n, int* __restrict__ comp, bool vec4) {
+  const int64_t n4 = vec4 ? n / 4 : 0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  auto one = [&](int p) {
+    if (p == -1) return (int)LRCVT_NONE;
+    if (p < -1) return -p - 2;
+    int q = __ldg(L + p);
+    if (q < -1) return -q - 2;
+    q = __ldg(L + q);
+    return -q - 2;
+  };
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += stride) {
+    const int4 p = __ldg(reinterpret_cast<const int4*>(L) + i);
+    __stcs(reinterpret_cast<int4*>(comp) + i, make_int4(one(p.x), one(p.y), one(p.z), one(p.w)));
+  }
+  for (int64_t i = 4 * n4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride)
+    comp[i] = one(__ldg(L + i));
 }
 
 // component table: count (u64), bbox (x0,y0,z0 via atomicMin, x1,y1,z1 via
