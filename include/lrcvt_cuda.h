@@ -162,6 +162,21 @@ int lrcvt_seed_masses(int64_t nx, int64_t ny, int64_t nz, int32_t block_size,
                       int64_t *d_run_start, int64_t *d_run_len, double *d_run_mass,
                       int64_t *n_inband, int64_t *n_runs, double *total_mass, void *stream);
 
+/* Record block of the .lrcvt layout (layout.py:123-200 build_and_write):
+ * in-band voxels ordered by (component, region = site_of with unassigned ->
+ * 0xFFFFFFFF, voxel), packed as records {u32 x, y, z; f32 field[n_fields]}
+ * (little-endian, 12 + 4 * n_fields bytes each) into d_records; field_ptrs
+ * is a HOST array of n_fields DEVICE float32[n] pointers. Also per record
+ * its region key (d_region_key, u32) and per component its first record and
+ * record count (d_comp_first / d_comp_count int64[n_components]; 0 / 0 when
+ * empty). *n_records = the in-band count; LRCVT_E_ARG when it exceeds
+ * max_records. */
+int lrcvt_layout_records(int64_t nx, int64_t ny, int64_t nz, int32_t n_fields,
+                         const float *const *field_ptrs, const int32_t *d_component,
+                         const int32_t *d_site_of, int32_t n_components, int64_t max_records,
+                         void *d_records, uint32_t *d_region_key, int64_t *d_comp_first,
+                         int64_t *d_comp_count, int64_t *n_records, void *stream);
+
 /* Multi-GPU global mode (z-slab partitioned evaluation over replicated
  * state). A rank's plan owns planes [zlo, zhi); the caller
  * drives rounds: begin -> { eval -> all-gather proposals -> commit }* ->

@@ -102,6 +102,11 @@ SIGNATURES = {
          c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, POINTER(c_int64), POINTER(c_int64),
          POINTER(c_double), c_void_p],
     ),
+    "lrcvt_layout_records": (
+        c_int,
+        [c_int64, c_int64, c_int64, c_int32, c_void_p, c_void_p, c_void_p, c_int32, c_int64, c_void_p,
+         c_void_p, c_void_p, c_void_p, POINTER(c_int64), c_void_p],
+    ),
 }
 
 _lib = None

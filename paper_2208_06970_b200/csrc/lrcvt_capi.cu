@@ -17,6 +17,7 @@
 #include "eval_p2.cuh"
 #include "aggregate.cuh"
 #include "seeding.cuh"
+#include "layout.cuh"
 
 using namespace lrcvt;
 
@@ -1276,6 +1277,74 @@ int lrcvt_seed_masses(int64_t nx, int64_t ny, int64_t nz, int32_t block_size, co
   CK(cudaMemcpyAsync(d_run_len, rl, sizeof(int64_t) * h_nr, cudaMemcpyDeviceToDevice, st));
   k_seed_run_mass<<<grid_for(h_nr, 64), 64, 0, st>>>(ws, d_run_start, d_run_len, h_nr, d_run_mass);
   CKL("k_seed_run_mass"); LAUNCHED(1);
+  CK(cudaStreamSynchronize(st));
+  return 0;
+}
+
+int lrcvt_layout_records(int64_t nx, int64_t ny, int64_t nz, int32_t n_fields, const float* const* field_ptrs,
+                         const int32_t* d_component, const int32_t* d_site_of, int32_t n_components,
+                         int64_t max_records, void* d_records, uint32_t* d_region_key, int64_t* d_comp_first,
+                         int64_t* d_comp_count, int64_t* n_records, void* stream) {
+  retain_pool();
+  const int64_t n = nx * ny * nz;
+  if (nx < 1 || ny < 1 || nz < 1 || n >= (int64_t(1) << 31) || n_fields < 0 || n_fields > 16 ||
+      (n_fields > 0 && !field_ptrs) || !d_component || !d_site_of || n_components < 0 || !d_records ||
+      !d_region_key || (n_components > 0 && (!d_comp_first || !d_comp_count)) || !n_records)
+    return set_error(LRCVT_E_ARG, "lrcvt_layout_records: bad arguments");
+  FieldPtrs fp{};
+  for (int i = 0; i < n_fields; i++) {
+    if (!field_ptrs[i]) return set_error(LRCVT_E_ARG, "lrcvt_layout_records: null field");
+    fp.f[i] = field_ptrs[i];
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  *n_records = 0;
+  Scratch sc(st);
+  int *list = nullptr, *cnt = nullptr, *vox = nullptr;
+  void* tmp = nullptr;
+  size_t b = 0;
+  CK(sc.get(&list, n));
+  CK(sc.get(&cnt, 1));
+  cub::CountingInputIterator<int> it(0);
+  IsInband pred{d_component};
+  CK(cub::DeviceSelect::If(nullptr, b, it, list, cnt, (int)n, pred, st));
+  CK(sc.get((char**)&tmp, (int64_t)b));
+  CK(cub::DeviceSelect::If(tmp, b, it, list, cnt, (int)n, pred, st));
+  int h_cnt = 0;
+  CK(cudaMemcpyAsync(&h_cnt, cnt, sizeof(int), cudaMemcpyDeviceToHost, st));
+  if (n_components > 0) {
+    CK(cudaMemsetAsync(d_comp_first, 0, sizeof(int64_t) * n_components, st));
+    CK(cudaMemsetAsync(d_comp_count, 0, sizeof(int64_t) * n_components, st));
+  }
+  CK(cudaStreamSynchronize(st));
+  const int64_t r = h_cnt;
+  *n_records = r;
+  if (r > max_records) return set_error(LRCVT_E_ARG, "lrcvt_layout_records: max_records too small");
+  if (r == 0) return 0;
+  unsigned long long *key = nullptr, *key2 = nullptr;
+  CK(sc.get(&key, r));
+  CK(sc.get(&key2, r));
+  CK(sc.get(&vox, r));
+  k_layout_keys<<<grid_for(r, 256, 148 * 16), 256, 0, st>>>(list, r, d_component, d_site_of, key);
+  CKL("k_layout_keys"); LAUNCHED(1);
+  int bits = 33;
+  while (bits < 64 && (1ll << (bits - 32)) < (int64_t)n_components) bits++;
+  b = 0;
+  CK(cub::DeviceRadixSort::SortPairs(nullptr, b, key, key2, list, vox, (int)r, 0, bits, st));
+  void* tmp2 = nullptr;
+  CK(sc.get((char**)&tmp2, (int64_t)b));
+  CK(cub::DeviceRadixSort::SortPairs(tmp2, b, key, key2, list, vox, (int)r, 0, bits, st));
+  k_layout_pack<<<grid_for(r * (3 + n_fields), 256, 148 * 32), 256, 0, st>>>(vox, r, n_fields, (int)nx, (int)ny,
+                                                                              fp, (unsigned*)d_records);
+  CKL("k_layout_pack"); LAUNCHED(1);
+  k_layout_index<<<grid_for(r, 256, 148 * 16), 256, 0, st>>>(key2, r, d_region_key, n_components,
+                                                              (long long*)d_comp_first,
+                                                              (long long*)d_comp_count);
+  CKL("k_layout_index"); LAUNCHED(1);
+  if (n_components > 0) {
+    k_layout_counts<<<grid_for(n_components, 256), 256, 0, st>>>(n_components, (const long long*)d_comp_first,
+                                                                 (long long*)d_comp_count);
+    CKL("k_layout_counts"); LAUNCHED(1);
+  }
   CK(cudaStreamSynchronize(st));
   return 0;
 }

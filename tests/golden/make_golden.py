@@ -388,6 +388,68 @@ def dump_blocks(G, S, T, P):
     (OUT / "blocks.json").write_text(json.dumps(meta))
 
 
+def dump_layout(G, S, T, P):
+    """.lrcvt files written by the reference's build_and_write (layout.py:123-219):
+    sha256 of the file, of its record block and of the manifest, the summary,
+    plus the inputs (arrays in layout.npz) so the tests can rebuild them."""
+    import tempfile
+
+    from lrcvt import layout as LY
+
+    cases = {}
+    grid = G.synth_field("spiral", (48, 48, 1), 0)
+    res = P.run_pipeline(grid, G.IsobandSpec("f", [0.3, 0.55, 0.8]), S.SeedingParams(alpha=40, seed=7),
+                         T.LloydParams(max_updates=4, ds_tolerance=0.05))
+    cases["explore"] = (grid, res.labels, res.tess, P.aggregate_moments(grid, res.labels, res.tess))
+    # unassigned voxels inside the record order (a component without sites)
+    nx, ny = 30, 12
+    f = np.zeros(nx * ny, dtype=np.float32)
+    f3 = f.reshape(ny, nx)
+    f3[2:5, 2:12] = 0.3
+    f3[2:5, 18:28] = 0.3
+    f3[7:10, 6:24] = 0.7
+    g2 = G.VoxelGrid((nx, ny, 1), (1.0, 1.0, 1.0), {"f": f, "g": np.linspace(0, 1, nx * ny, dtype=np.float32)})
+    l2 = G.label_components(G.classify_isobands(g2, G.IsobandSpec("f", [0.1, 0.5, 0.9])))
+    t2 = T.voronoi_classify(g2, l2, [S.Site((3.5, 3.5, 0.5), 0), S.Site((8.5, 3.5, 0.5), 0),
+                                     S.Site((10.5, 8.5, 0.5), 2)])
+    cases["stray"] = (g2, l2, t2, P.aggregate_moments(g2, l2, t2))
+    # 3D, anisotropic spacing, two bands, every site of component 1 dropped
+    g3 = G.VoxelGrid((24, 20, 16), (1.0, 0.5, 2.0), G.synth_field("random-smooth", (24, 20, 16), 0).fields)
+    l3 = G.label_components(G.classify_isobands(g3, G.IsobandSpec("f", [0.35, 0.5, 0.7])))
+    sites3, _ = S.seed_sites(g3, l3, S.SeedingParams(alpha=30, seed=2))
+    sites3 = [s for s in sites3 if s.component_id != 1]
+    t3 = T.voronoi_classify(g3, l3, sites3)
+    cases["smooth3d"] = (g3, l3, t3, [])
+    arrays, out = {}, {}
+    with tempfile.TemporaryDirectory() as d:
+        for name, (grid, labels, tess, blobs) in cases.items():
+            path = Path(d) / f"{name}.lrcvt"
+            summary = LY.build_and_write(grid, labels, tess, blobs, path)
+            data = path.read_bytes()
+            man = Path(str(path) + ".manifest.json").read_text()
+            h = LY.LayoutReader(path).header
+            for k, v in grid.fields.items():
+                arrays[f"{name}/field/{k}"] = v
+            arrays[f"{name}/layer"] = labels.layer
+            arrays[f"{name}/component"] = labels.component
+            arrays[f"{name}/site_of"] = tess.site_of
+            summary.pop("path")
+            out[name] = {
+                "dims": list(grid.dims), "spacing": list(grid.spacing), "fields": grid.field_names(),
+                "iso_field": labels.field_name, "iso_values": list(labels.iso_values),
+                "table": table_json(labels),
+                "sites": [[*s.position, s.component_id] for s in tess.sites],
+                "blobs": [{"scope": b.scope, "id": b.scope_id, "kind": b.kind, "payload": b.payload.decode()}
+                          for b in blobs],
+                "file_sha": hashlib.sha256(data).hexdigest(),
+                "data_sha": hashlib.sha256(data[h.data_off:h.agg_off]).hexdigest(),
+                "manifest_sha": hashlib.sha256(man.encode()).hexdigest(),
+                "file_bytes": len(data), "summary": summary,
+            }
+    np.savez_compressed(OUT / "layout.npz", **arrays)
+    (OUT / "layout.json").write_text(json.dumps(out))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--big", action="store_true", help="also record C2 128^3 and C3 256^3 trajectories")
@@ -395,7 +457,7 @@ def main():
     a = ap.parse_args()
     G, S, T, P, ST, K = ref()
     todo = a.only.split(",") if a.only else ["classify", "raycast", "masks", "aggregate", "seeding", "lloyd",
-                                             "blocks"]
+                                             "blocks", "layout"]
     if "classify" in todo:
         dump_classify(G, S, T, K)
     if "raycast" in todo:
@@ -410,6 +472,8 @@ def main():
         dump_lloyd(G, S, T, a.big)
     if "blocks" in todo:
         dump_blocks(G, S, T, P)
+    if "layout" in todo:
+        dump_layout(G, S, T, P)
 
 
 if __name__ == "__main__":
