@@ -244,6 +244,39 @@ def layout_pass(grid, labels, eng, S):
                     "bytes = component scan 4N + per record key/voxel/region 16 B + gathers 4m + record out"}
 
 
+def adjacency_pass(grid, eng, S):
+    """Site adjacency face scan, CUDA events."""
+    import ctypes
+
+    import torch
+
+    from paper_2208_06970_b200 import _lib
+
+    L = _lib.lib()
+    nx, ny, nz = grid.dims
+    site_of = eng.ss[:, 0].contiguous()
+    cap = 32 * S + 1024
+    edges = torch.empty((cap, 2), dtype=torch.int64, device="cuda")
+    got = ctypes.c_int64()
+    st = _lib.stream_handle(torch)
+
+    def run():
+        _lib.check(L.lrcvt_region_adjacency(nx, ny, nz, site_of.data_ptr(), eng.comp.data_ptr(), S, cap,
+                                            edges.data_ptr(), ctypes.byref(got), st), "adjacency")
+
+    run()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    run()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    return {"edges": int(got.value), "device_ms": ms, "voxels_per_s": grid.size / (ms / 1e3),
+            "algorithmic_GBps": 8.0 * grid.size / (ms / 1e3) / 1e9,
+            "note": "lrcvt_region_adjacency: face scan of site_of + component (8 B/voxel), hash-set dedup, sort"}
+
+
 def one_off_passes(grid, labels, eng, config, S, reps=3):
     """Device-resident timing of the passes reported beside the iteration
     metric: isoband + component masks, and the per-cell
@@ -491,6 +524,7 @@ def main():
     if passes is not None:
         passes["seeding"] = seeding_pass(grid, labels, params)
         passes["layout"] = layout_pass(grid, labels, eng, S)
+        passes["adjacency"] = adjacency_pass(grid, eng, S)
 
     # end-to-end through the public API with host numpy in/out
     e2e = None

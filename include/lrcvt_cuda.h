@@ -177,6 +177,15 @@ int lrcvt_layout_records(int64_t nx, int64_t ny, int64_t nz, int32_t n_fields,
                          void *d_records, uint32_t *d_region_key, int64_t *d_comp_first,
                          int64_t *d_comp_count, int64_t *n_records, void *stream);
 
+/* Site adjacency (sitegraph.py:46-82 region_adjacency): the sorted,
+ * de-duplicated (lo, hi) site pairs, lo < hi, of face-neighbouring voxels
+ * (+x, +y, +z) with different assigned sites in the same component.
+ * d_edges int64[max_edges][2] (device); *n_edges = the edge count
+ * (LRCVT_E_ARG when it exceeds max_edges; call again with room). */
+int lrcvt_region_adjacency(int64_t nx, int64_t ny, int64_t nz, const int32_t *d_site_of,
+                           const int32_t *d_component, int64_t n_sites, int64_t max_edges,
+                           int64_t *d_edges, int64_t *n_edges, void *stream);
+
 /* Multi-GPU global mode (z-slab partitioned evaluation over replicated
  * state). A rank's plan owns planes [zlo, zhi); the caller
  * drives rounds: begin -> { eval -> all-gather proposals -> commit }* ->

@@ -107,6 +107,10 @@ SIGNATURES = {
         [c_int64, c_int64, c_int64, c_int32, c_void_p, c_void_p, c_void_p, c_int32, c_int64, c_void_p,
          c_void_p, c_void_p, c_void_p, POINTER(c_int64), c_void_p],
     ),
+    "lrcvt_region_adjacency": (
+        c_int,
+        [c_int64, c_int64, c_int64, c_void_p, c_void_p, c_int64, c_int64, c_void_p, POINTER(c_int64), c_void_p],
+    ),
 }
 
 _lib = None

@@ -18,6 +18,7 @@
 #include "aggregate.cuh"
 #include "seeding.cuh"
 #include "layout.cuh"
+#include "adjacency.cuh"
 
 using namespace lrcvt;
 
@@ -1345,6 +1346,62 @@ int lrcvt_layout_records(int64_t nx, int64_t ny, int64_t nz, int32_t n_fields, c
                                                                  (long long*)d_comp_count);
     CKL("k_layout_counts"); LAUNCHED(1);
   }
+  CK(cudaStreamSynchronize(st));
+  return 0;
+}
+
+int lrcvt_region_adjacency(int64_t nx, int64_t ny, int64_t nz, const int32_t* d_site_of,
+                           const int32_t* d_component, int64_t n_sites, int64_t max_edges, int64_t* d_edges,
+                           int64_t* n_edges, void* stream) {
+  retain_pool();
+  if (!geo_ok(nx, ny, nz, 1, 1, 1) || !d_site_of || !d_component || n_sites < 0 || max_edges < 0 ||
+      (max_edges > 0 && !d_edges) || !n_edges)
+    return set_error(LRCVT_E_ARG, "lrcvt_region_adjacency: bad arguments");
+  cudaStream_t st = (cudaStream_t)stream;
+  *n_edges = 0;
+  Geo g = make_geo(nx, ny, nz, 1, 1, 1);
+  // 3D Voronoi cells have ~14 face neighbours: 16 slots per site keeps the
+  // set under half full
+  unsigned long long slots = 1024;
+  while (slots < (unsigned long long)(16 * n_sites) && slots < (1ull << 34)) slots <<= 1;
+  Scratch sc(st);
+  unsigned long long *table = nullptr, *keys = nullptr, *keys2 = nullptr;
+  int* cnt = nullptr;
+  CK(sc.get(&cnt, 2));
+  for (;;) {
+    CK(sc.get(&table, (int64_t)slots));
+    CK(cudaMemsetAsync(table, 0xff, sizeof(unsigned long long) * slots, st));
+    CK(cudaMemsetAsync(cnt + 1, 0, sizeof(int), st));
+    k_adjacency<<<grid_for(g.n, 256, 148 * 8), 256, 0, st>>>(g, d_site_of, d_component, table, slots - 1,
+                                                             cnt + 1);
+    CKL("k_adjacency"); LAUNCHED(1);
+    int overflow = 0;
+    CK(cudaMemcpyAsync(&overflow, cnt + 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (!overflow) break;
+    if (slots >= (1ull << 34)) return set_error(LRCVT_E_NOMEM, "lrcvt_region_adjacency: edge set too large");
+    slots <<= 2;
+  }
+  size_t b = 0;
+  void* tmp = nullptr;
+  CK(sc.get(&keys, (int64_t)slots));
+  CK(cub::DeviceSelect::If(nullptr, b, table, keys, cnt, (int64_t)slots, NotEmpty{}, st));
+  CK(sc.get((char**)&tmp, (int64_t)b));
+  CK(cub::DeviceSelect::If(tmp, b, table, keys, cnt, (int64_t)slots, NotEmpty{}, st));
+  int h_cnt = 0;
+  CK(cudaMemcpyAsync(&h_cnt, cnt, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  *n_edges = h_cnt;
+  if (h_cnt > max_edges) return set_error(LRCVT_E_ARG, "lrcvt_region_adjacency: max_edges too small");
+  if (h_cnt == 0) return 0;
+  CK(sc.get(&keys2, h_cnt));
+  b = 0;
+  CK(cub::DeviceRadixSort::SortKeys(nullptr, b, keys, keys2, h_cnt, 0, 64, st));
+  void* tmp2 = nullptr;
+  CK(sc.get((char**)&tmp2, (int64_t)b));
+  CK(cub::DeviceRadixSort::SortKeys(tmp2, b, keys, keys2, h_cnt, 0, 64, st));
+  k_split_edges<<<grid_for(h_cnt, 256), 256, 0, st>>>(keys2, h_cnt, (long long*)d_edges);
+  CKL("k_split_edges"); LAUNCHED(1);
   CK(cudaStreamSynchronize(st));
   return 0;
 }

@@ -450,6 +450,38 @@ def dump_layout(G, S, T, P):
     (OUT / "layout.json").write_text(json.dumps(out))
 
 
+def dump_sitegraph(G, S, T):
+    """sitegraph.py region_adjacency / all_pairs_paths / fold_metric on the
+    layout cases (inputs from layout.npz/json) and a 3D Lloyd result."""
+    from lrcvt import sitegraph as SG
+
+    meta = json.loads((OUT / "layout.json").read_text())
+    arr = np.load(OUT / "layout.npz")
+    tess = {}
+    for name, m in meta.items():
+        sites = [S.Site(tuple(s[:3]), int(s[3])) for s in m["sites"]]
+        n = int(np.prod(m["dims"]))
+        tess[name] = T.Tessellation(tuple(m["dims"]), tuple(m["spacing"]), arr[f"{name}/site_of"], np.zeros(n),
+                                    np.zeros(n, np.int32), np.zeros(n, np.uint8), arr[f"{name}/component"], sites)
+    grid = G.synth_field("gaussian-mix", (32, 30, 28), 0)
+    labels = G.label_components(G.classify_isobands(grid, G.IsobandSpec("f", [0.25, 0.5, 0.75])))
+    t, _ = T.lrcvt(grid, labels, S.SeedingParams(alpha=80, weight_field="g", seed=4), T.LloydParams(max_updates=3))
+    tess["gmix3d"] = t
+    out, arrays = {}, {}
+    for name, tt in tess.items():
+        gr = SG.region_adjacency(tt)
+        paths = SG.all_pairs_paths(gr)
+        fm = SG.fold_metric(gr.positions, paths, c=1.5)
+        if name == "gmix3d":
+            arrays["gmix3d/site_of"] = tt.site_of
+            arrays["gmix3d/component"] = tt.component
+            arrays["gmix3d/sites"] = np.array([[*s.position, s.component_id] for s in tt.sites])
+        out[name] = {"edges": gr.edges.tolist(), "weights": [w.hex() for w in gr.weights],
+                     "paths_sha": sha(paths), "fold_sha": sha(fm.matrix), "dims": list(tt.dims)}
+    np.savez_compressed(OUT / "sitegraph.npz", **arrays)
+    (OUT / "sitegraph.json").write_text(json.dumps(out))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--big", action="store_true", help="also record C2 128^3 and C3 256^3 trajectories")
@@ -457,7 +489,7 @@ def main():
     a = ap.parse_args()
     G, S, T, P, ST, K = ref()
     todo = a.only.split(",") if a.only else ["classify", "raycast", "masks", "aggregate", "seeding", "lloyd",
-                                             "blocks", "layout"]
+                                             "blocks", "layout", "sitegraph"]
     if "classify" in todo:
         dump_classify(G, S, T, K)
     if "raycast" in todo:
@@ -474,6 +506,8 @@ def main():
         dump_blocks(G, S, T, P)
     if "layout" in todo:
         dump_layout(G, S, T, P)
+    if "sitegraph" in todo:
+        dump_sitegraph(G, S, T)
 
 
 if __name__ == "__main__":
