@@ -58,8 +58,52 @@ __device__ __forceinline__ void powers(double x, double* xp) {
 
 // one warp per (cell, pair); out layout: sums[cell][pair][15],
 // minmax[cell][pair][4] = (min_x, max_x, min_y, max_y), count[cell]
-__global__ void __launch_bounds__(128) k_agg_moments(const int* __restrict__ sorted_v,
-                                                     const int* __restrict__ seg_b,
+// Per-lane compensated accumulation of the terms of one (cell, pair). Only
+// the work that changes a result is done: S_00 is the count (exact); terms
+// with p == 0 or q == 0 are plain powers (the product with 1.0 is exact);
+// for a pair of one field with itself (x == y) the sums S_pq and S_qp are
+// identical (IEEE products commute), so only p <= q is accumulated.
+template <bool SAME>
+__device__ __forceinline__ void agg_lane(const float* __restrict__ fx, const float* __restrict__ fy, int b, int e,
+                                         int lane, double* s, double* c, double& mnx, double& mxx, double& mny,
+                                         double& mxy) {
+  for (int j = b + lane; j < e; j += 32) {
+    const double x = (double)__ldg(fx + j);
+    const double y = SAME ? x : (double)__ldg(fy + j);
+    mnx = fmin(mnx, x); mxx = fmax(mxx, x);
+    if (!SAME) { mny = fmin(mny, y); mxy = fmax(mxy, y); }
+    double xp[5], yq[5];
+    powers(x, xp);
+    if (SAME) {
+#pragma unroll
+      for (int k = 0; k < 5; k++) yq[k] = xp[k];
+    } else {
+      powers(y, yq);
+    }
+#pragma unroll
+    for (int t = 1; t < AGG_NSUMS; t++) {
+      const int p = ord_p(t), q = ord_q(t);
+      if (SAME && p > q) continue;
+      const double term = p == 0 ? yq[q] : q == 0 ? xp[p] : __dmul_rn(xp[p], yq[q]);
+      double hi, lo;
+      two_sum(s[t], term, hi, lo);
+      s[t] = hi;
+      c[t] = __dadd_rn(c[t], lo);
+    }
+  }
+  if (SAME) { mny = mnx; mxy = mxx; }
+}
+
+// index of the (q, p) term of ORDERS
+__host__ __device__ constexpr int ord_mirror(int t) {
+  const int p = ord_p(t), q = ord_q(t);
+  int k = 0;
+  for (int u = 0; u < AGG_NSUMS; u++)
+    if (ord_p(u) == q && ord_q(u) == p) k = u;
+  return k;
+}
+
+__global__ void __launch_bounds__(128) k_agg_moments(const int* __restrict__ seg_b,
                                                      const int* __restrict__ seg_e, int n_cells,
                                                      const float* const* __restrict__ fields,
                                                      const int* __restrict__ pairs, int n_pairs,
@@ -70,36 +114,22 @@ __global__ void __launch_bounds__(128) k_agg_moments(const int* __restrict__ sor
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (gw >= n_cells * n_pairs) return;
   const int cell = gw / n_pairs, pr = gw - cell * n_pairs;
-  const float* __restrict__ fx = fields[pairs[2 * pr]];
-  const float* __restrict__ fy = fields[pairs[2 * pr + 1]];
+  const int ix = pairs[2 * pr], iy = pairs[2 * pr + 1];
+  const float* __restrict__ fx = fields[ix];  // columns in cell order
+  const float* __restrict__ fy = fields[iy];
   const int b = seg_b[cell], e = seg_e[cell];
   double s[AGG_NSUMS], c[AGG_NSUMS];
 #pragma unroll
   for (int j = 0; j < AGG_NSUMS; j++) { s[j] = 0.0; c[j] = 0.0; }
   double mnx = __longlong_as_double(0x7ff0000000000000LL), mny = mnx;
   double mxx = -mnx, mxy = -mnx;
-  for (int j = b + lane; j < e; j += 32) {
-    const int v = sorted_v[j];
-    const double x = (double)__ldg(fx + v), y = (double)__ldg(fy + v);
-    mnx = fmin(mnx, x); mxx = fmax(mxx, x);
-    mny = fmin(mny, y); mxy = fmax(mxy, y);
-    double xp[5], yq[5];
-    powers(x, xp);
-    powers(y, yq);
-#pragma unroll
-    for (int t = 0; t < AGG_NSUMS; t++) {
-      const double term = __dmul_rn(xp[ord_p(t)], yq[ord_q(t)]);
-      double hi, lo;
-      two_sum(s[t], term, hi, lo);
-      s[t] = hi;
-      c[t] = __dadd_rn(c[t], lo);
-    }
-  }
+  if (ix == iy) agg_lane<true>(fx, fy, b, e, lane, s, c, mnx, mxx, mny, mxy);
+  else agg_lane<false>(fx, fy, b, e, lane, s, c, mnx, mxx, mny, mxy);
   // fixed-order double-double tree across lanes
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
 #pragma unroll
-    for (int t = 0; t < AGG_NSUMS; t++) {
+    for (int t = 1; t < AGG_NSUMS; t++) {
       const double os = __shfl_down_sync(0xffffffffu, s[t], o);
       const double oc = __shfl_down_sync(0xffffffffu, c[t], o);
       double hi, lo;
@@ -114,8 +144,17 @@ __global__ void __launch_bounds__(128) k_agg_moments(const int* __restrict__ sor
   }
   if (lane == 0) {
     double* out = sums + ((int64_t)cell * n_pairs + pr) * AGG_NSUMS;
+    out[0] = (double)(e - b);
+    if (ix == iy) {
 #pragma unroll
-    for (int t = 0; t < AGG_NSUMS; t++) out[t] = __dadd_rn(s[t], c[t]);
+      for (int t = 1; t < AGG_NSUMS; t++) {
+        const int src = ord_p(t) > ord_q(t) ? ord_mirror(t) : t;
+        out[t] = __dadd_rn(s[src], c[src]);
+      }
+    } else {
+#pragma unroll
+      for (int t = 1; t < AGG_NSUMS; t++) out[t] = __dadd_rn(s[t], c[t]);
+    }
     double* mm = minmax + ((int64_t)cell * n_pairs + pr) * 4;
     mm[0] = mnx; mm[1] = mxx; mm[2] = mny; mm[3] = mxy;
     if (pr == 0) count[cell] = e - b;
@@ -165,12 +204,14 @@ __device__ __forceinline__ int np_bin(double a, double lo, double hi, double den
   return idx;
 }
 
-// one warp per (cell, field); hist[cell][field][B + 2] (bins, under, over)
+// one warp per (cell, field); hist[cell][field][B + 2] (bins, under, over).
+// The first bin guess uses a reciprocal multiply instead of numpy's division:
+// both guesses are within one bin of the edge-defined bin, and numpy's +-1
+// edge fix-ups (histograms.py) map any such guess to that same bin.
 template <int MAXB>
-__global__ void __launch_bounds__(128) k_agg_hist(const int* __restrict__ sorted_v,
-                                                  const int* __restrict__ seg_b,
+__global__ void __launch_bounds__(128) k_agg_hist(const int* __restrict__ seg_b,
                                                   const int* __restrict__ seg_e, int n_cells,
-                                                  const float* const* __restrict__ fields,
+                                                  const float* const* __restrict__ cols,
                                                   int n_fields, const double* __restrict__ axes,
                                                   int B, long long* __restrict__ hist) {
   __shared__ int bins[4][MAXB + 2];
@@ -181,22 +222,47 @@ __global__ void __launch_bounds__(128) k_agg_hist(const int* __restrict__ sorted
   __syncwarp();
   if (live) {
     const int cell = gw / n_fields, fi = gw - cell * n_fields;
-    const float* __restrict__ f = fields[fi];
+    const float* __restrict__ f = cols[fi];
     const double lo = axes[2 * fi], hi = axes[2 * fi + 1];
     const double denom = __dsub_rn(hi, lo);
     const double step = __ddiv_rn(denom, (double)B);
+    const double scale = __ddiv_rn((double)B, denom);
     const int b = seg_b[cell], e = seg_e[cell];
-    for (int j = b + lane; j < e; j += 32) {
-      const double a = (double)__ldg(f + sorted_v[j]);
-      int slot;
-      if (a < lo) slot = B;
-      else if (a > hi) slot = B + 1;
-      else slot = np_bin(a, lo, hi, denom, step, B);
-      atomicAdd(&bins[wid][slot], 1);
+    const int end = b + ((e - b + 31) & ~31);  // warp-uniform trip count
+    for (int j = b + lane; j < end; j += 32) {
+      int slot = -1;
+      if (j < e) {
+        const double a = (double)__ldg(f + j);
+        if (a < lo) slot = B;
+        else if (a > hi) slot = B + 1;
+        else {
+          int idx = (int)__dmul_rn(__dsub_rn(a, lo), scale);
+          if (idx >= B) idx = B - 1;
+          if (idx < 0) idx = 0;
+          const double e_lo = __dadd_rn(__dmul_rn((double)idx, step), lo);
+          if (a < e_lo) idx -= 1;
+          const double e_hi = idx + 1 == B ? hi : __dadd_rn(__dmul_rn((double)(idx + 1), step), lo);
+          if (a >= e_hi && idx != B - 1) idx += 1;
+          slot = idx;
+        }
+      }
+      const unsigned grp = __match_any_sync(0xffffffffu, slot);
+      if (slot >= 0 && lane == __ffs(grp) - 1) atomicAdd(&bins[wid][slot], __popc(grp));
     }
     __syncwarp();
     long long* out = hist + ((int64_t)cell * n_fields + fi) * (B + 2);
     for (int j = lane; j < B + 2; j += 32) out[j] = bins[wid][j];
+  }
+}
+
+// in-band field values gathered into cell order, one contiguous column per
+// field, so the moment and histogram warps stream instead of chasing indices
+__global__ void k_agg_gather(const int* __restrict__ sorted_v, int m, const float* const* __restrict__ fields,
+                             int n_fields, float* __restrict__ cols) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < m; j += stride) {
+    const int v = sorted_v[j];
+    for (int fi = 0; fi < n_fields; ++fi) __stcg(cols + (int64_t)fi * m + j, __ldg(fields[fi] + v));
   }
 }
 

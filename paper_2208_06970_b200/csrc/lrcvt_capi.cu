@@ -935,6 +935,8 @@ int lrcvt_aggregate(int64_t n, int32_t n_fields, const float* const* field_ptrs,
   int *inband = nullptr, *cnt = nullptr, *key = nullptr, *key2 = nullptr, *val = nullptr, *val2 = nullptr;
   int *segb = nullptr, *sege = nullptr, *d_pairs = nullptr;
   const float** d_fields = nullptr;
+  const float** d_cols = nullptr;
+  float* d_colbuf = nullptr;
   double* d_axes = nullptr;
   unsigned long long* d_lohi = nullptr;
   void* tmp = nullptr;
@@ -977,8 +979,21 @@ int lrcvt_aggregate(int64_t n, int32_t n_fields, const float* const* field_ptrs,
     CKL("k_segments"); LAUNCHED(1);
   }
   {
+    // field columns in cell order (contiguous streams for the moment/histogram warps)
+    CK(cudaMallocAsync((void**)&d_colbuf, sizeof(float) * (size_t)n_fields * (m > 0 ? m : 1), st));
+    CK(cudaMallocAsync((void**)&d_cols, sizeof(float*) * n_fields, st));
+    {
+      std::vector<const float*> cp(n_fields);
+      for (int f = 0; f < n_fields; f++) cp[f] = d_colbuf + (size_t)f * (m > 0 ? m : 1);
+      // pageable source: the copy is staged before cudaMemcpyAsync returns
+      CK(cudaMemcpyAsync(d_cols, cp.data(), sizeof(float*) * n_fields, cudaMemcpyHostToDevice, st));
+    }
+    if (m > 0) {
+      k_agg_gather<<<grid_for(m, 256, 148 * 16), 256, 0, st>>>(val2, m, d_fields, n_fields, d_colbuf);
+      CKL("k_agg_gather"); LAUNCHED(1);
+    }
     const int64_t warps = (int64_t)n_cells * n_pairs;
-    k_agg_moments<<<grid_for(warps * 32, 128), 128, 0, st>>>(val2, segb, sege, n_cells, d_fields, d_pairs,
+    k_agg_moments<<<grid_for(warps * 32, 128), 128, 0, st>>>(segb, sege, n_cells, d_cols, d_pairs,
                                                              n_pairs, (long long*)d_count, d_sums, d_minmax);
     CKL("k_agg_moments"); LAUNCHED(1);
   }
@@ -1020,12 +1035,13 @@ int lrcvt_aggregate(int64_t n, int32_t n_fields, const float* const* field_ptrs,
     }
     CK(cudaMemcpyAsync(d_axes, axes, sizeof(double) * 2 * n_fields, cudaMemcpyHostToDevice, st));
     const int64_t warps = (int64_t)n_cells * n_fields;
-    k_agg_hist<1024><<<grid_for(warps * 32, 128), 128, 0, st>>>(val2, segb, sege, n_cells, d_fields, n_fields,
+    k_agg_hist<1024><<<grid_for(warps * 32, 128), 128, 0, st>>>(segb, sege, n_cells, d_cols, n_fields,
                                                                 d_axes, n_bins, (long long*)d_hist);
     CKL("k_agg_hist"); LAUNCHED(1);
   }
   for (void* b : {(void*)inband, (void*)cnt, (void*)key, (void*)key2, (void*)val, (void*)val2, (void*)segb,
-                  (void*)sege, (void*)d_pairs, (void*)d_fields, (void*)d_axes, (void*)d_lohi, tmp})
+                  (void*)sege, (void*)d_pairs, (void*)d_fields, (void*)d_axes, (void*)d_lohi, tmp,
+                  (void*)d_cols, (void*)d_colbuf})
     if (b) CK(cudaFreeAsync(b, st));
   CK(cudaStreamSynchronize(st));
   return 0;
