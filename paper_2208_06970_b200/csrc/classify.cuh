@@ -80,6 +80,44 @@ __global__ void k_nbr_mask(Geo g, const int* __restrict__ comp, uint32_t* __rest
   }
 }
 
+// Clearance layers (see ray_clear_by_clearance): clr = 1 where a 26-neighbour
+// is foreign or outside the grid, then layer r + 1 = unknown voxels next to
+// layer r (for the L-infinity metric D(v) = 1 + min over 26-neighbours),
+// finally stored in nbm bits 26..31. 0 for out-of-band voxels.
+constexpr unsigned char CLR_UNKNOWN = 0xFF;
+constexpr int CLR_MAX = 31;
+__global__ void k_clear_init(Geo g, const int* __restrict__ comp, const uint32_t* __restrict__ nbm,
+                             unsigned char* __restrict__ clr) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < g.n; i += stride) {
+    const int v = (int)i;
+    if (comp[v] < 0) { clr[v] = 0; continue; }
+    clr[v] = (nbm[v] & ((1u << 26) - 1)) == ((1u << 26) - 1) ? CLR_UNKNOWN : 1;
+  }
+}
+__global__ void k_clear_layer(Geo g, unsigned char* __restrict__ clr, int r) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < g.n; i += stride) {
+    const int v = (int)i;
+    if (clr[v] != CLR_UNKNOWN) continue;  // unknown => all 26 neighbours inside, same component
+    bool hit = false;
+#pragma unroll
+    for (int k = 0; k < 26; k++) {
+      const int w = v + off_dx(k) + off_dy(k) * g.nx + off_dz(k) * g.nxy;
+      hit |= clr[w] == (unsigned char)r;
+    }
+    if (hit) clr[v] = (unsigned char)(r + 1);
+  }
+}
+__global__ void k_clear_store(int64_t n, const unsigned char* __restrict__ clr, uint32_t* __restrict__ nbm) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+    unsigned c = clr[i];
+    if (c == CLR_UNKNOWN) c = CLR_MAX + 1;  // D > CLR_MAX: a safe lower bound
+    nbm[i] = (nbm[i] & ((1u << 26) - 1)) | (c << NBM_CLR_SHIFT);
+  }
+}
+
 // has_site[c] = 1 for every component that owns a site (tessellation.py:161-162)
 __global__ void k_mark_site_comps(const int* __restrict__ site_comp, int n_sites,
                                   uint8_t* __restrict__ has_site) {

@@ -242,6 +242,27 @@ __device__ __forceinline__ bool segment_clear(const int* __restrict__ comp, cons
   return segment_hit_t(comp, g, ax, ay, az, bx, by, bz, want) >= 1.0;
 }
 
+// Clearance shortcut for a ray from the centre c of voxel v to a point p.
+// nbm bits 26..31 hold clr(v) = min(D(v), 32), D(v) = Chebyshev distance from
+// v to the nearest voxel of another component or outside the grid, so every
+// voxel within Chebyshev radius clr(v) - 1 of v shares v's component. The
+// DDA only visits cells inside the index box spanned by v and cell(p),
+// widened by at most one cell where a rounded crossing parameter oversteps;
+// along each axis |cell(p) - v| <= |p - c| / s + 1/2, so with
+// t = max_a |p_a - c_a| / s_a, t + 2.5 <= clr(v) proves every visited cell is
+// in v's component (_segment_clear is true) without walking the ray. Tested
+// in float with a further 0.5 cell of slack for its rounding.
+constexpr int NBM_CLR_SHIFT = 26;
+__device__ __forceinline__ bool ray_clear_by_clearance(unsigned nbm_v, float tx, float ty, float tz) {
+  return fmaxf(tx, fmaxf(ty, tz)) + 3.0f <= (float)(nbm_v >> NBM_CLR_SHIFT);
+}
+// |p - c| per axis in cells (inv = 1 / spacing, float)
+__device__ __forceinline__ bool ray_clear_near(unsigned nbm_v, double px, double py, double pz, double cx,
+                                               double cy, double cz, float isx, float isy, float isz) {
+  return ray_clear_by_clearance(nbm_v, fabsf((float)(px - cx)) * isx, fabsf((float)(py - cy)) * isy,
+                                fabsf((float)(pz - cz)) * isz);
+}
+
 // Warp-aggregated append of `take` (0/1) items; returns this lane's slot
 // (valid only when take). All 32 lanes must call it.
 __device__ __forceinline__ int warp_append(int* counter, bool take) {

@@ -54,6 +54,7 @@ __device__ __forceinline__ void p1_tile(const int* __restrict__ list, int n, con
   const int v = active ? __ldg(list + i) : 0;
   int* row = &s_row[0][threadIdx.x];
   int x = 0, y = 0, z = 0, cv = -3;
+  unsigned nbv = 0;  // this voxel's nbm word (neighbour bits + clearance)
   double px = 0, py = 0, pz = 0;
   int ts[P1_TAB];
   double td[P1_TAB];
@@ -67,6 +68,7 @@ __device__ __forceinline__ void p1_tile(const int* __restrict__ list, int n, con
     cv = __ldg(comp + v);
     px = centre1(x, g.sx); py = centre1(y, g.sy); pz = centre1(z, g.sz);
     const unsigned same = __ldg(nbm + v);
+    nbv = same;
     // ---- A
     int2 nw[26];
 #pragma unroll
@@ -139,13 +141,15 @@ __device__ __forceinline__ void p1_tile(const int* __restrict__ list, int n, con
   __syncwarp();
   // ---- D: the warp traces its queued rays, one per lane
   const int nq = q_n[wid];
+  const float isx = (float)(1.0 / g.sx), isy = (float)(1.0 / g.sy), isz = (float)(1.0 / g.sz);
   for (int j = lane; j < nq; j += 32) {
     const int rv = qv[j];
     int rx, ry, rz;
     coords(g, rv, rx, ry, rz);
     const double4 sp = ld_d4(site_pos + qs[j]);
-    qok[j] = segment_clear(comp, g, centre1(rx, g.sx), centre1(ry, g.sy), centre1(rz, g.sz), sp.x, sp.y,
-                           sp.z, __ldg(comp + rv))
+    const double cx = centre1(rx, g.sx), cy = centre1(ry, g.sy), cz = centre1(rz, g.sz);
+    qok[j] = ray_clear_near(__ldg(nbm + rv), sp.x, sp.y, sp.z, cx, cy, cz, isx, isy, isz) ||
+                     segment_clear(comp, g, cx, cy, cz, sp.x, sp.y, sp.z, __ldg(comp + rv))
                  ? 1 : 0;
   }
   __syncwarp();
@@ -175,7 +179,8 @@ __device__ __forceinline__ void p1_tile(const int* __restrict__ list, int n, con
       }
       if (beats(d, s, best_d, best_s) && s != failed) {
         const double4 sp = ld_d4(site_pos + s);
-        if (segment_clear(comp, g, px, py, pz, sp.x, sp.y, sp.z, cv)) {
+        if (ray_clear_near(nbv, sp.x, sp.y, sp.z, px, py, pz, isx, isy, isz) ||
+            segment_clear(comp, g, px, py, pz, sp.x, sp.y, sp.z, cv)) {
           best_d = d; best_s = s; best_src = v;
         } else {
           failed = s;

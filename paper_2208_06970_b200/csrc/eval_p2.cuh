@@ -40,6 +40,7 @@ __device__ __forceinline__ void p2_tile(const int* __restrict__ list, int n, con
   const int v = active ? __ldg(list + i) : 0;
   const int t = threadIdx.x;
   int x = 0, y = 0, z = 0, cv = -3;
+  unsigned nbv = 0;  // this voxel's nbm word (neighbour bits + clearance)
   double px = 0, py = 0, pz = 0;
   int ts[P2_STAB];
   double td[P2_STAB];
@@ -58,6 +59,7 @@ __device__ __forceinline__ void p2_tile(const int* __restrict__ list, int n, con
     cv = __ldg(comp + v);
     px = centre1(x, g.sx); py = centre1(y, g.sy); pz = centre1(z, g.sz);
     const unsigned same = __ldg(nbm + v);
+    nbv = same;
     // ---- A: gather (two batches of 13 to bound register pressure)
 #pragma unroll
     for (int h = 0; h < 2; h++) {
@@ -198,7 +200,9 @@ __device__ __forceinline__ void p2_tile(const int* __restrict__ list, int n, con
       coords(g, rsrc, ux, uy, uz);
       qx = centre1(ux, g.sx); qy = centre1(uy, g.sy); qz = centre1(uz, g.sz);
     }
-    if (segment_clear(comp, g, px, py, pz, qx, qy, qz, cv)) {
+    if (ray_clear_near(nbv, qx, qy, qz, px, py, pz, (float)(1.0 / g.sx), (float)(1.0 / g.sy),
+                       (float)(1.0 / g.sz)) ||
+        segment_clear(comp, g, px, py, pz, qx, qy, qz, cv)) {
       best_d = rd; best_s = rs; best_src = rsrc;
     } else if (los) {
       failed = rs;

@@ -535,6 +535,19 @@ int lrcvt_plan_create(lrcvt_plan** plan, int64_t nx, int64_t ny, int64_t nz, dou
   rc |= dalloc(&p->seg_e, S);
   if (rc) { lrcvt_plan_destroy(p); return LRCVT_E_NOMEM; }
   k_nbr_mask<<<grid_for(n, 256, 148 * 16), 256, 0, st>>>(p->g, d_comp, p->nbm);
+  {  // clearance layers into nbm bits 26..31 (exact ray shortcut, common.cuh)
+    unsigned char* clr = nullptr;
+    CK(cudaMallocAsync((void**)&clr, (size_t)n, st));
+    k_clear_init<<<grid_for(n, 256, 148 * 16), 256, 0, st>>>(p->g, d_comp, p->nbm, clr);
+    CKL("k_clear_init"); LAUNCHED(1);
+    for (int r = 1; r <= CLR_MAX; r++) {
+      k_clear_layer<<<grid_for(n, 256, 148 * 16), 256, 0, st>>>(p->g, clr, r);
+      CKL("k_clear_layer"); LAUNCHED(1);
+    }
+    k_clear_store<<<grid_for(n, 256, 148 * 16), 256, 0, st>>>(n, clr, p->nbm);
+    CKL("k_clear_store"); LAUNCHED(1);
+    CK(cudaFreeAsync(clr, st));
+  }
   if (cudaMemsetAsync(p->bm, 0, sizeof(uint32_t) * p->bm_words, st) != cudaSuccess) {
     lrcvt_plan_destroy(p);
     return set_error(LRCVT_E_CUDA, "bitmap clear");
