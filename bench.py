@@ -43,6 +43,10 @@ CONFIGS = {
     "c4": dict(kind="random-smooth", dims=(512, 512, 512), iso=[0.35, 0.5, 0.65, 0.8],
                seeding=dict(alpha=32768, weight_field="g", seed=0),
                label="C4 3D 512^3 random-smooth, 3 bands, 32k g-weighted sites"),
+    # north-star volume on ONE B200; fields generated on the GPU (synth_c5)
+    "c5": dict(kind="c5-helix", dims=(1024, 1024, 1024), iso=[0.55, 0.75, 0.95],
+               seeding=dict(alpha=262144, weight_field="g", seed=0),
+               label="C5 3D 1024^3 helical two-field, 2 bands, 256k g-weighted sites"),
 }
 L2_BYTES = 126 * 2**20
 
@@ -55,11 +59,54 @@ def peaks():
     return 6650.0, "fallback"
 
 
+def synth_c5(dims, seed):
+    """C5 input: f = the 3D helical spiral formula of
+    synth_field (grid.py:268-275) and g = smooth value noise (a 17^3 lattice of
+    uniform randoms, trilinear), both computed on the GPU in float64 and stored
+    as float32 -- the numpy generator would need ~100 GB of host temporaries
+    at 1024^3. Synthetic input generation only; not part of any timed region."""
+    import torch
+
+    from paper_2208_06970_b200.grid import VoxelGrid
+
+    nx, ny, nz = dims
+    dev = "cuda"
+    f = torch.empty((nz, ny, nx), dtype=torch.float32, device=dev)
+    xs = torch.arange(nx, dtype=torch.float64, device=dev) + 0.5
+    ys = torch.arange(ny, dtype=torch.float64, device=dev) + 0.5
+    yy, xx = torch.meshgrid(ys - ny / 2, xs - nx / 2, indexing="ij")
+    theta = torch.atan2(yy, xx)
+    r = torch.sqrt(xx * xx + yy * yy)
+    base = 2.0 * theta + (10.0 / max(nx, ny)) * 2 * np.pi * r / 4.0
+    amp = torch.clamp(r / (0.55 * min(nx, ny)), 0, 1.2)
+    for z in range(nz):
+        f[z] = (0.5 * (1.0 + torch.cos(base + 2 * np.pi * (z + 0.5) / nz)) * amp).to(torch.float32)
+    del xs, ys, yy, xx, theta, r, base, amp
+    lat = torch.from_numpy(np.random.default_rng(seed + 1).random((1, 1, 17, 17, 17))).to(dev)
+    g = torch.empty((nz, ny, nx), dtype=torch.float32, device=dev)
+    step = 64
+    for z0 in range(0, nz, step):
+        zc = min(step, nz - z0)
+        # trilinear value noise on a lattice with one node every nx/16 voxels
+        zz = (torch.arange(z0, z0 + zc, dtype=torch.float64, device=dev) + 0.5) * 16.0 / nz
+        yv = (torch.arange(ny, dtype=torch.float64, device=dev) + 0.5) * 16.0 / ny
+        xv = (torch.arange(nx, dtype=torch.float64, device=dev) + 0.5) * 16.0 / nx
+        grid = torch.stack(torch.meshgrid(zz, yv, xv, indexing="ij")[::-1], dim=-1) / 8.0 - 1.0
+        g[z0:z0 + zc] = torch.nn.functional.grid_sample(lat, grid[None], mode="bilinear",
+                                                         align_corners=True)[0, 0].to(torch.float32)
+        del grid
+    out = VoxelGrid(dims=tuple(dims), spacing=(1.0, 1.0, 1.0),
+                    fields={"f": f.reshape(-1).cpu().numpy(), "g": g.reshape(-1).cpu().numpy()})
+    del f, g
+    torch.cuda.empty_cache()
+    return out
+
+
 def build_workload(cfg, rank, use_gpu_masks=True):
     from paper_2208_06970_b200 import (IsobandSpec, SeedingParams, classify_isobands, label_components,
                                        seed_sites, synth_field, voxel_weights)
 
-    grid = synth_field(cfg["kind"], cfg["dims"], rank)
+    grid = synth_c5(cfg["dims"], rank) if cfg["kind"] == "c5-helix" else synth_field(cfg["kind"], cfg["dims"], rank)
     spec = IsobandSpec("f", cfg["iso"])
     if use_gpu_masks:
         labels = label_components(classify_isobands(grid, spec))
@@ -74,7 +121,8 @@ def build_workload(cfg, rank, use_gpu_masks=True):
                            for t in table], spec.iso_values, "f")
     params = SeedingParams(**cfg["seeding"])
     sites, _ = seed_sites(grid, labels, params)
-    return grid, labels, params, sites, voxel_weights(grid, params)
+    weights = voxel_weights(grid, params) if grid.size <= (1 << 28) else None  # host f64 copy: e2e / CPU arm only
+    return grid, labels, params, sites, weights
 
 
 class ClockSampler:
