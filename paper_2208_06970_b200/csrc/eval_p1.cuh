@@ -55,6 +55,7 @@ __device__ __forceinline__ void p1_tile(const int* __restrict__ list, int n, con
   int* row = &s_row[0][threadIdx.x];
   int x = 0, y = 0, z = 0, cv = -3;
   unsigned nbv = 0;  // this voxel's nbm word (neighbour bits + clearance)
+  bool ovf = false;  // more distinct neighbour sites than the table holds
   double px = 0, py = 0, pz = 0;
   int ts[P1_TAB];
   double td[P1_TAB];
@@ -91,6 +92,8 @@ __device__ __forceinline__ void p1_tile(const int* __restrict__ list, int n, con
         for (int j = 0; j < P1_TAB; j++)
           if (j == nt) ts[j] = s;
         nt++;
+      } else if (!seen) {
+        ovf = true;
       }
     }
     const int2 sv = __ldg(ss + v);
@@ -105,15 +108,64 @@ __device__ __forceinline__ void p1_tile(const int* __restrict__ list, int n, con
       td[j] = dist3(px, py, pz, sp.x, sp.y, sp.z);
     }
   }
+  // ---- strict-order fast path. When every two distinct (distance, site)
+  // elements among the current state and the table differ in distance by
+  // more than 2.5e-9 + |d|*1e-15, `_beats` between them is decided by the
+  // distance alone (neither of its EPS tie clauses can fire) and is a strict
+  // order, so the reference's sequential fold ends at the minimum-distance
+  // element among {current} and the LOS candidates whose ray is clear:
+  // repeated sites are no-ops, failed_site only skips rays that would fail
+  // again, and a clear candidate of smaller distance than the running best
+  // always beats it. Only the winner's ray is needed; if it is blocked the
+  // lane takes the exact non-speculative fold below.
+  bool strict = false;
+  int jwin = -1;
+  if (active && !ovf) {
+    strict = true;
+#pragma unroll
+    for (int a = 0; a <= P1_TAB; a++) {
+#pragma unroll
+      for (int b = a + 1; b <= P1_TAB; b++) {
+        const bool va = a == 0 || ts[a - 1] >= 0, vb = ts[b - 1] >= 0;
+        const double da = a == 0 ? orig_d : td[a - 1], db = td[b - 1];
+        const int sa = a == 0 ? orig_s : ts[a - 1], sb = ts[b - 1];
+        if (va && vb && !(da == db && sa == sb)) {
+          const bool ia = isinf(da), ib = isinf(db);
+          const double tol = __dadd_rn(2.5e-9, __dmul_rn(fmax(fabs(da), fabs(db)), 1e-15));
+          if (!((ia != ib) || (!ia && fabs(__dsub_rn(da, db)) > tol))) strict = false;
+        }
+      }
+    }
+    if (strict) {
+      double dmin = orig_d;
+#pragma unroll
+      for (int j = 0; j < P1_TAB; j++)
+        if (ts[j] >= 0 && td[j] < dmin) { dmin = td[j]; jwin = j; }
+    }
+  }
   __syncwarp();  // q_n initialised
-  // ---- C: speculative fold
+  const float isx = (float)(1.0 / g.sx), isy = (float)(1.0 / g.sy), isz = (float)(1.0 / g.sz);
+  int win_slot = -1;   // queue slot of the strict winner's ray (-1: none or proven clear)
+  int win_s = -1;
+  double win_d = 0.0;
+  if (jwin >= 0) {
+#pragma unroll
+    for (int j = 0; j < P1_TAB; j++)
+      if (j == jwin) { win_s = ts[j]; win_d = td[j]; }
+    const double4 sp = ld_d4(site_pos + win_s);
+    if (!ray_clear_near(nbv, sp.x, sp.y, sp.z, px, py, pz, isx, isy, isz)) {
+      win_slot = atomicAdd(&q_n[wid], 1);
+      qv[win_slot] = v; qs[win_slot] = win_s;
+    }
+  }
+  // ---- C: speculative fold (lanes without a strict order)
   int failed = -1;
   int nspec = 0, kstop = 26;
   int sp_slot[P1_SPEC], sp_k[P1_SPEC], sp_s[P1_SPEC], sp_src[P1_SPEC];
   double sp_d[P1_SPEC];
 #pragma unroll
   for (int q = 0; q < P1_SPEC; q++) { sp_slot[q] = 0; sp_k[q] = 0; sp_s[q] = 0; sp_src[q] = 0; sp_d[q] = 0; }
-  if (active) {
+  if (active && !strict) {
     for (int k = 0; k < 26; k++) {
       const int s = row[k * BLOCK];
       if (s < 0) continue;
@@ -141,7 +193,6 @@ __device__ __forceinline__ void p1_tile(const int* __restrict__ list, int n, con
   __syncwarp();
   // ---- D: the warp traces its queued rays, one per lane
   const int nq = q_n[wid];
-  const float isx = (float)(1.0 / g.sx), isy = (float)(1.0 / g.sy), isz = (float)(1.0 / g.sz);
   for (int j = lane; j < nq; j += 32) {
     const int rv = qv[j];
     int rx, ry, rz;
@@ -153,9 +204,16 @@ __device__ __forceinline__ void p1_tile(const int* __restrict__ list, int n, con
                  ? 1 : 0;
   }
   __syncwarp();
-  // ---- E: replay outcomes; rewind at the first blocked ray
+  // ---- E: strict lanes take their winner (or fall back); the others replay
+  // their speculated outcomes and rewind at the first blocked ray
   int kres = 26;  // resume point of the non-speculative tail
-  if (active) {
+  if (active && strict) {
+    if (jwin >= 0 && (win_slot < 0 || qok[win_slot])) {
+      best_d = win_d; best_s = win_s; best_src = v;
+    } else if (jwin >= 0) {
+      kres = 0;  // winner blocked: exact fold from the start (best = current state)
+    }
+  } else if (active) {
 #pragma unroll
     for (int q = 0; q < P1_SPEC; q++) {
       if (q < nspec && kres == 26 && !qok[sp_slot[q]]) {
@@ -165,6 +223,8 @@ __device__ __forceinline__ void p1_tile(const int* __restrict__ list, int n, con
       }
     }
     if (kres == 26 && kstop < 26) kres = kstop;  // window overflow, all clear
+  }
+  if (active) {
     for (int k = kres; k < 26; k++) {
       const int s = row[k * BLOCK];
       if (s < 0) continue;

@@ -435,6 +435,12 @@ struct Scratch {
   cudaStream_t st;
   std::vector<void*> ptrs;
   explicit Scratch(cudaStream_t s) : st(s) {}
+  cudaError_t raw(void** p, size_t bytes) {
+    *p = nullptr;
+    cudaError_t e = cudaMallocAsync(p, bytes > 0 ? bytes : 1, st);
+    if (e == cudaSuccess) ptrs.push_back(*p);
+    return e;
+  }
   template <typename T>
   cudaError_t get(T** p, int64_t count) {
     *p = nullptr;
@@ -945,6 +951,7 @@ int lrcvt_aggregate(int64_t n, int32_t n_fields, const float* const* field_ptrs,
   cudaStream_t st = (cudaStream_t)stream;
   const int n_cells = n_sites + n_components;
   if (n_cells == 0) return 0;
+  Scratch sc(st);  // every scratch buffer is released on all exit paths
   int *inband = nullptr, *cnt = nullptr, *key = nullptr, *key2 = nullptr, *val = nullptr, *val2 = nullptr;
   int *segb = nullptr, *sege = nullptr, *d_pairs = nullptr;
   const float** d_fields = nullptr;
@@ -957,25 +964,24 @@ int lrcvt_aggregate(int64_t n, int32_t n_fields, const float* const* field_ptrs,
   int h_cnt = 0;
   IsInband pred{d_component};
   cub::CountingInputIterator<int> it(0);
-  CK(cudaMallocAsync((void**)&inband, sizeof(int) * (n > 0 ? n : 1), st));
-  CK(cudaMallocAsync((void**)&cnt, sizeof(int), st));
+  CK(sc.raw((void**)&inband, sizeof(int) * (n > 0 ? n : 1)));
+  CK(sc.raw((void**)&cnt, sizeof(int)));
   CK(cub::DeviceSelect::If(nullptr, b1, it, inband, cnt, (int)n, pred, st));
-  CK(cudaMallocAsync(&tmp, b1, st));
+  CK(sc.raw((void**)&tmp, b1));
   CK(cub::DeviceSelect::If(tmp, b1, it, inband, cnt, (int)n, pred, st));
   CK(cudaMemcpyAsync(&h_cnt, cnt, sizeof(int), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
-  CK(cudaFreeAsync(tmp, st));
   tmp = nullptr;
   const int m = h_cnt;
   const int mm = m > 0 ? m : 1;
-  CK(cudaMallocAsync((void**)&key, sizeof(int) * mm, st));
-  CK(cudaMallocAsync((void**)&key2, sizeof(int) * mm, st));
-  CK(cudaMallocAsync((void**)&val, sizeof(int) * mm, st));
-  CK(cudaMallocAsync((void**)&val2, sizeof(int) * mm, st));
-  CK(cudaMallocAsync((void**)&segb, sizeof(int) * n_cells, st));
-  CK(cudaMallocAsync((void**)&sege, sizeof(int) * n_cells, st));
-  CK(cudaMallocAsync((void**)&d_pairs, sizeof(int) * 2 * n_pairs, st));
-  CK(cudaMallocAsync((void**)&d_fields, sizeof(float*) * n_fields, st));
+  CK(sc.raw((void**)&key, sizeof(int) * mm));
+  CK(sc.raw((void**)&key2, sizeof(int) * mm));
+  CK(sc.raw((void**)&val, sizeof(int) * mm));
+  CK(sc.raw((void**)&val2, sizeof(int) * mm));
+  CK(sc.raw((void**)&segb, sizeof(int) * n_cells));
+  CK(sc.raw((void**)&sege, sizeof(int) * n_cells));
+  CK(sc.raw((void**)&d_pairs, sizeof(int) * 2 * n_pairs));
+  CK(sc.raw((void**)&d_fields, sizeof(float*) * n_fields));
   CK(cudaMemcpyAsync(d_pairs, pairs, sizeof(int) * 2 * n_pairs, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(d_fields, field_ptrs, sizeof(float*) * n_fields, cudaMemcpyHostToDevice, st));
   CK(cudaMemsetAsync(segb, 0, sizeof(int) * n_cells, st));
@@ -986,15 +992,15 @@ int lrcvt_aggregate(int64_t n, int32_t n_fields, const float* const* field_ptrs,
     int bits = 1;
     while ((1ll << bits) <= n_cells) bits++;
     CK(cub::DeviceRadixSort::SortPairs(nullptr, b2, key, key2, val, val2, m, 0, bits, st));
-    CK(cudaMallocAsync(&tmp, b2, st));
+    CK(sc.raw((void**)&tmp, b2));
     CK(cub::DeviceRadixSort::SortPairs(tmp, b2, key, key2, val, val2, m, 0, bits, st));
     k_segments<<<grid_for(m, 256, 148 * 16), 256, 0, st>>>(key2, m, n_cells, segb, sege);
     CKL("k_segments"); LAUNCHED(1);
   }
   {
     // field columns in cell order (contiguous streams for the moment/histogram warps)
-    CK(cudaMallocAsync((void**)&d_colbuf, sizeof(float) * (size_t)n_fields * (m > 0 ? m : 1), st));
-    CK(cudaMallocAsync((void**)&d_cols, sizeof(float*) * n_fields, st));
+    CK(sc.raw((void**)&d_colbuf, sizeof(float) * (size_t)n_fields * (m > 0 ? m : 1)));
+    CK(sc.raw((void**)&d_cols, sizeof(float*) * n_fields));
     {
       std::vector<const float*> cp(n_fields);
       for (int f = 0; f < n_fields; f++) cp[f] = d_colbuf + (size_t)f * (m > 0 ? m : 1);
@@ -1011,11 +1017,11 @@ int lrcvt_aggregate(int64_t n, int32_t n_fields, const float* const* field_ptrs,
     CKL("k_agg_moments"); LAUNCHED(1);
   }
   if (n_bins > 0) {
-    CK(cudaMallocAsync((void**)&d_axes, sizeof(double) * 2 * n_fields, st));
+    CK(sc.raw((void**)&d_axes, sizeof(double) * 2 * n_fields));
     bool any_auto = false;
     for (int f = 0; f < n_fields; f++) any_auto |= !(axes[2 * f] == axes[2 * f]) || !(axes[2 * f + 1] == axes[2 * f + 1]);
     if (any_auto) {  // stats.py:186-191 auto range over in-band values
-      CK(cudaMallocAsync((void**)&d_lohi, sizeof(unsigned long long) * 2 * n_fields, st));
+      CK(sc.raw((void**)&d_lohi, sizeof(unsigned long long) * 2 * n_fields));
       std::vector<unsigned long long> init(2 * n_fields);
       for (int f = 0; f < n_fields; f++) { init[2 * f] = ~0ull; init[2 * f + 1] = 0ull; }
       CK(cudaMemcpyAsync(d_lohi, init.data(), sizeof(unsigned long long) * 2 * n_fields, cudaMemcpyHostToDevice, st));
@@ -1052,10 +1058,6 @@ int lrcvt_aggregate(int64_t n, int32_t n_fields, const float* const* field_ptrs,
                                                                 d_axes, n_bins, (long long*)d_hist);
     CKL("k_agg_hist"); LAUNCHED(1);
   }
-  for (void* b : {(void*)inband, (void*)cnt, (void*)key, (void*)key2, (void*)val, (void*)val2, (void*)segb,
-                  (void*)sege, (void*)d_pairs, (void*)d_fields, (void*)d_axes, (void*)d_lohi, tmp,
-                  (void*)d_cols, (void*)d_colbuf})
-    if (b) CK(cudaFreeAsync(b, st));
   CK(cudaStreamSynchronize(st));
   return 0;
 }
