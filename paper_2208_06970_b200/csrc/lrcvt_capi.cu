@@ -455,7 +455,7 @@ struct Scratch {
 
 // numpy's pairwise split (seeding.cuh) cut into subtrees of at most kCut
 // elements, left to right, and the sum rebuilt in the same shape
-constexpr int64_t kSubtree = int64_t(1) << 14;
+constexpr int64_t kSubtree = 128;  // = numpy's leaf size: one thread per leaf
 void pw_split(int64_t lo, int64_t n, std::vector<int64_t>& L, std::vector<int64_t>& N) {
   if (n <= kSubtree) {
     L.push_back(lo);
@@ -1287,7 +1287,7 @@ int lrcvt_seed_masses(int64_t nx, int64_t ny, int64_t nz, int32_t block_size, co
   CK(sc.get(&d_tv, nt));
   CK(cudaMemcpyAsync(d_tl, tl.data(), sizeof(int64_t) * nt, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(d_tn, tn.data(), sizeof(int64_t) * nt, cudaMemcpyHostToDevice, st));
-  k_seed_subtrees<<<grid_for(nt, 64), 64, 0, st>>>(list, w, d_tl, d_tn, nt, d_tv);
+  k_seed_subtrees<<<grid_for(nt, 128), 128, 0, st>>>(list, w, d_tl, d_tn, nt, d_tv);
   CKL("k_seed_subtrees"); LAUNCHED(1);
   k_seed_weights<<<grid_for(m, 256, 148 * 16), 256, 0, st>>>(d_voxels, m, w, ws);
   CKL("k_seed_weights"); LAUNCHED(1);
@@ -1307,8 +1307,8 @@ int lrcvt_seed_masses(int64_t nx, int64_t ny, int64_t nz, int32_t block_size, co
   CK(cub::DeviceScan::ExclusiveSum(tmp4, b, rl, d_run_start, (int)h_nr, st));
   CK(cudaMemcpyAsync(d_run_key, rk, sizeof(int64_t) * h_nr, cudaMemcpyDeviceToDevice, st));
   CK(cudaMemcpyAsync(d_run_len, rl, sizeof(int64_t) * h_nr, cudaMemcpyDeviceToDevice, st));
-  k_seed_run_mass<<<grid_for(h_nr, 64), 64, 0, st>>>(ws, d_run_start, d_run_len, h_nr, d_run_mass);
-  CKL("k_seed_run_mass"); LAUNCHED(1);
+  k_seed_run_mass_warp<4><<<grid_for(h_nr, 4), 128, 0, st>>>(ws, d_run_start, d_run_len, h_nr, d_run_mass);
+  CKL("k_seed_run_mass_warp"); LAUNCHED(1);
   CK(cudaStreamSynchronize(st));
   return 0;
 }

@@ -150,6 +150,92 @@ __global__ void k_seed_run_mass(const double* __restrict__ w_sorted, const int64
   mass[r] = __dadd_rn(0.0, pw_sum(SeqDirect{w_sorted}, start[r], len[r]));
 }
 
+// One warp per run: lane 0 lists the run's pairwise leaves (<= 128 elements)
+// in depth-first order, the lanes sum the leaves in parallel (pw_leaf), and
+// lane 0 rebuilds the same tree over the leaf sums -- the identical
+// operation sequence of pw_sum, with the element loads spread over the warp.
+// Runs with more than WARP_LEAVES leaves fall back to one thread (pw_sum).
+constexpr int WARP_LEAVES = 128;
+template <int WARPS>
+__global__ void __launch_bounds__(32 * WARPS) k_seed_run_mass_warp(const double* __restrict__ w_sorted,
+                                                                    const int64_t* __restrict__ start,
+                                                                    const int64_t* __restrict__ len,
+                                                                    int64_t n_runs, double* __restrict__ mass) {
+  __shared__ int64_t s_lo[WARPS][WARP_LEAVES];
+  __shared__ int s_n[WARPS][WARP_LEAVES];
+  __shared__ double s_sum[WARPS][WARP_LEAVES];
+  __shared__ int s_cnt[WARPS];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t r = blockIdx.x * (int64_t)WARPS + wid;
+  if (r >= n_runs) return;
+  const int64_t lo0 = start[r], n0 = len[r];
+  const SeqDirect seq{w_sorted};
+  if (lane == 0) {
+    // depth-first leaf list (explicit stack of pending ranges, left first)
+    int64_t st_lo[40], st_n[40];
+    int top = 0, cnt = 0;
+    st_lo[0] = lo0; st_n[0] = n0;
+    while (top >= 0 && cnt <= WARP_LEAVES) {
+      const int64_t lo = st_lo[top], n = st_n[top];
+      --top;
+      if (n <= 128) {
+        if (cnt < WARP_LEAVES) { s_lo[wid][cnt] = lo; s_n[wid][cnt] = (int)n; }
+        ++cnt;
+        continue;
+      }
+      int64_t n2 = n / 2;
+      n2 -= n2 % 8;
+      ++top; st_lo[top] = lo + n2; st_n[top] = n - n2;  // right half pops after the left
+      ++top; st_lo[top] = lo; st_n[top] = n2;
+    }
+    s_cnt[wid] = cnt;
+  }
+  __syncwarp();
+  const int cnt = s_cnt[wid];
+  if (cnt > WARP_LEAVES) {  // very long run: single-thread tree
+    if (lane == 0) mass[r] = __dadd_rn(0.0, pw_sum(seq, lo0, n0));
+    return;
+  }
+  for (int j = lane; j < cnt; j += 32) s_sum[wid][j] = pw_leaf(seq, s_lo[wid][j], s_n[wid][j]);
+  __syncwarp();
+  if (lane == 0) {
+    // rebuild: the same recursion, consuming leaf sums in depth-first order
+    int64_t st_n[40];
+    double st_left[40];
+    unsigned char st_state[40];
+    int top = 0, next = 0;
+    st_n[0] = n0; st_state[0] = 0;
+    double ret = 0.0;
+    bool have = false;
+    if (n0 <= 128) {
+      ret = s_sum[wid][0];
+      top = -1;
+    }
+    while (top >= 0) {
+      const int64_t n = st_n[top];
+      int64_t n2 = n / 2;
+      n2 -= n2 % 8;
+      if (have) {
+        have = false;
+        if (st_state[top] == 0) {
+          st_left[top] = ret;
+          st_state[top] = 1;
+          if (n - n2 <= 128) { ret = s_sum[wid][next++]; have = true; continue; }
+          ++top; st_n[top] = n - n2; st_state[top] = 0;
+          continue;
+        }
+        ret = __dadd_rn(st_left[top], ret);
+        have = true;
+        --top;
+        continue;
+      }
+      if (n2 <= 128) { ret = s_sum[wid][next++]; have = true; continue; }
+      ++top; st_n[top] = n2; st_state[top] = 0;
+    }
+    mass[r] = __dadd_rn(0.0, ret);
+  }
+}
+
 // subtree sums of the total in-band mass (voxel order); the host splits the
 // tree into these subtrees and adds them back in the same shape
 __global__ void k_seed_subtrees(const int* __restrict__ list, SeedWeight w, const int64_t* __restrict__ lo,
