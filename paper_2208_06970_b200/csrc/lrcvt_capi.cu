@@ -930,9 +930,15 @@ int lrcvt_component_table(int64_t nx, int64_t ny, int64_t nz, const int32_t* d_c
   k_ccl_table_init<<<grid_for(n_components, 256), 256, 0, st>>>(n_components, (unsigned long long*)d_count,
                                                                 d_bbox);
   CKL("k_ccl_table_init"); LAUNCHED(1);
-  k_ccl_table<<<grid_for(g.n, 256, 148 * 16), 256, 0, st>>>(g, d_component, d_layer,
-                                                            (unsigned long long*)d_count, d_bbox, d_layer_of);
-  CKL("k_ccl_table"); LAUNCHED(1);
+  if (n_components <= TABLE_SMEM_COMP) {
+    k_ccl_table_smem<<<grid_for(g.n, 256, 148 * 8), 256, 0, st>>>(
+        g, d_component, d_layer, n_components, (unsigned long long*)d_count, d_bbox, d_layer_of);
+    CKL("k_ccl_table_smem"); LAUNCHED(1);
+  } else {
+    k_ccl_table<<<grid_for(g.n, 256, 148 * 16), 256, 0, st>>>(g, d_component, d_layer,
+                                                              (unsigned long long*)d_count, d_bbox, d_layer_of);
+    CKL("k_ccl_table"); LAUNCHED(1);
+  }
   return 0;
 }
 

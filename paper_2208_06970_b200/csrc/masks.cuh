@@ -314,6 +314,61 @@ __global__ void k_ccl_table(Geo g, const int* __restrict__ comp, const int* __re
   }
 }
 
+// Same table with the per-warp partials merged in shared memory first (one
+// global atomic per component per CTA instead of per warp): few components
+// otherwise serialise every warp on the same six addresses. n_comp <= SMEM_COMP.
+constexpr int TABLE_SMEM_COMP = 512;
+__global__ void __launch_bounds__(256) k_ccl_table_smem(Geo g, const int* __restrict__ comp,
+                                                        const int* __restrict__ layer, int n_comp,
+                                                        unsigned long long* __restrict__ count,
+                                                        int* __restrict__ bbox, int* __restrict__ layer_of) {
+  __shared__ unsigned long long s_cnt[TABLE_SMEM_COMP];
+  __shared__ int s_box[TABLE_SMEM_COMP][6];
+  __shared__ int s_lay[TABLE_SMEM_COMP];
+  for (int c = threadIdx.x; c < n_comp; c += blockDim.x) {
+    s_cnt[c] = 0;
+    s_box[c][0] = s_box[c][1] = s_box[c][2] = 0x7fffffff;
+    s_box[c][3] = s_box[c][4] = s_box[c][5] = -1;
+    s_lay[c] = -1;
+  }
+  __syncthreads();
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x; i0 < g.n; i0 += stride) {
+    const int64_t i = i0 + threadIdx.x;
+    int c = -1, x = 0, y = 0, z = 0;
+    if (i < g.n) {
+      c = comp[i];
+      if (c >= 0) coords(g, (int)i, x, y, z);
+    }
+    const unsigned grp = __match_any_sync(0xffffffffu, c);
+    const unsigned cnt = __popc(grp);
+    const int xmin = __reduce_min_sync(grp, x), xmax = __reduce_max_sync(grp, x);
+    const int ymin = __reduce_min_sync(grp, y), ymax = __reduce_max_sync(grp, y);
+    const int zmin = __reduce_min_sync(grp, z), zmax = __reduce_max_sync(grp, z);
+    if (c >= 0 && (threadIdx.x & 31) == __ffs(grp) - 1) {
+      atomicAdd(&s_cnt[c], (unsigned long long)cnt);
+      atomicMin(&s_box[c][0], xmin);
+      atomicMin(&s_box[c][1], ymin);
+      atomicMin(&s_box[c][2], zmin);
+      atomicMax(&s_box[c][3], xmax);
+      atomicMax(&s_box[c][4], ymax);
+      atomicMax(&s_box[c][5], zmax);
+      s_lay[c] = layer[i];
+    }
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < n_comp; c += blockDim.x) {
+    if (!s_cnt[c]) continue;
+    atomicAdd(count + c, s_cnt[c]);
+#pragma unroll
+    for (int a = 0; a < 3; a++) {
+      atomicMin(bbox + 6 * c + a, s_box[c][a]);
+      atomicMax(bbox + 6 * c + 3 + a, s_box[c][3 + a]);
+    }
+    layer_of[c] = s_lay[c];
+  }
+}
+
 __global__ void k_ccl_table_init(int n_comp, unsigned long long* count, int* bbox) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= n_comp) return;

@@ -47,7 +47,10 @@ def shares(ls):
 
 
 def full(rep):
-    out = subprocess.run(["ncu", "-i", str(rep), "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    if str(rep).endswith(".csv"):  # raw page exported on the GPU box (ncu -i rep --page raw --csv)
+        out = Path(rep).read_text()
+    else:
+        out = subprocess.run(["ncu", "-i", str(rep), "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     h = rows[0]
     want = {"grid": "launch__grid_size", "block": "launch__block_size", "regs": "launch__registers_per_thread",
