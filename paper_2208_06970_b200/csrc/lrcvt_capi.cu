@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -15,6 +16,7 @@
 #include "masks.cuh"
 #include "eval_p1.cuh"
 #include "eval_p2.cuh"
+#include "eval_warp.cuh"
 #include "aggregate.cuh"
 #include "seeding.cuh"
 #include "layout.cuh"
@@ -235,6 +237,8 @@ struct lrcvt_plan {
   // eligible list of the last classify is reused by centroidal_update when
   // the caller guarantees the site-component set is unchanged
   bool reuse_eligible = false;
+  bool warp_eval = true;  // warp-per-voxel kernels for small frontiers (LRCVT_WARP_EVAL=0 disables)
+  bool warp_eval_all = false;
   bool eligible_valid = false;
   int64_t eligible_sites = -1;
   // optional per-launch timing of the dominant kernel (k_eval)
@@ -296,9 +300,26 @@ int prepare_eligible(lrcvt_plan* p, int n_sites, const int* site_comp, cudaStrea
 }
 
 // The eval kernel of variant `var` over ctl->cur with `blocks` blocks.
-int launch_eval_kernel(lrcvt_plan* p, int var, int blocks, cudaStream_t st) {
+// Frontiers up to EW_SMALL voxels: warp-per-voxel kernels (eval_warp.cuh),
+// whose round latency is one voxel's parallel evaluation instead of its
+// serial one; larger frontiers: the thread-per-voxel tile kernels.
+constexpr int EW_SMALL = 2048;
+int launch_eval_kernel(lrcvt_plan* p, int var, int items, cudaStream_t st) {
   const Geo& g = p->g;
-  if (blocks < 1) blocks = 1;
+  if (items < 1) items = 1;
+  if ((items <= EW_SMALL && p->warp_eval) || p->warp_eval_all) {
+    const int blocks = (items + EW_WARPS - 1) / EW_WARPS;
+    if (var == 0)
+      k_eval_warp<false><<<blocks, 32 * EW_WARPS, 0, st>>>(p->ctl, g, p->comp, p->nbm, p->site_pos, p->bm, p->imp,
+                                                            p->counters);
+    else
+      k_eval_warp<true><<<blocks, 32 * EW_WARPS, 0, st>>>(p->ctl, g, p->comp, p->nbm, p->site_pos, p->bm, p->imp,
+                                                           p->counters);
+    CKL("k_eval_warp");
+    return 0;
+  }
+  const int bs = var == 0 ? 128 : 64;
+  const int blocks = (items + bs - 1) / bs;
   if (var == 0)
     k_eval_p1<128><<<blocks, 128, 0, st>>>(p->ctl, g, p->comp, p->nbm, p->site_pos, p->bm, p->imp, p->counters);
   else if (var == 1)
@@ -310,7 +331,6 @@ int launch_eval_kernel(lrcvt_plan* p, int var, int blocks, cudaStream_t st) {
   CKL("k_eval");
   return 0;
 }
-
 int eval_block_size(int var) { return var == 0 ? 128 : 64; }
 
 // commit + enqueue (+ round end in its last block unless end_mode < 0)
@@ -329,7 +349,7 @@ int launch_commit_kernel(lrcvt_plan* p, int blocks, cudaStream_t st, const cudaG
 // Host-driven round (n known on the host): exact grids; end_mode 0 = round
 // end without graph conditionals, -1 = sweep (k_sweep_end follows).
 int launch_round_kernels(lrcvt_plan* p, int var, int n, cudaStream_t st, int end_mode = 0) {
-  CKR(launch_eval_kernel(p, var, (n + eval_block_size(var) - 1) / eval_block_size(var), st));
+  CKR(launch_eval_kernel(p, var, n, st));
   if (p->timing) CK(cudaEventRecord(p->ev1, st));
   CKR(launch_commit_kernel(p, (n + 127) / 128, st, nullptr, cudaGraphConditionalHandle{}, end_mode));
   if (p->timing) CK(cudaEventRecord(p->ev2, st));
@@ -392,7 +412,7 @@ int build_round_graph(lrcvt_plan* p, int var) {
     long long cap = class_cap(c);
     if (c == p->n_classes - 1 && cap < p->n_inband) cap = p->n_inband;
     CK(cudaStreamBeginCaptureToGraph(p->cap, ib, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
-    int rc = launch_eval_kernel(p, var, (int)((cap + bs - 1) / bs), p->cap);
+    int rc = launch_eval_kernel(p, var, (int)cap, p->cap);
     if (!rc) rc = launch_commit_kernel(p, (int)((cap + 127) / 128), p->cap, d_hs, h, 1);
     cudaGraph_t captured;
     const cudaError_t ee = cudaStreamEndCapture(p->cap, &captured);
@@ -491,6 +511,10 @@ int lrcvt_plan_create(lrcvt_plan** plan, int64_t nx, int64_t ny, int64_t nz, dou
     return set_error(LRCVT_E_ARG, "lrcvt_plan_create: bad arguments");
   cudaStream_t st = (cudaStream_t)stream;
   lrcvt_plan* p = new lrcvt_plan();
+  if (const char* e = getenv("LRCVT_WARP_EVAL")) {  // 0: never, 2: every frontier size (tests)
+    p->warp_eval = e[0] != '0';
+    p->warp_eval_all = e[0] == '2';
+  }
   p->g = make_geo(nx, ny, nz, sx, sy, sz);
   p->comp = d_comp;
   p->n_components = n_components;
@@ -1165,7 +1189,7 @@ int lrcvt_mg_eval(lrcvt_plan* p, int32_t phase, int32_t sweep, int64_t* n_evalua
   }
   CK(cudaMemsetAsync(p->counters, 0, sizeof(int) * 2, st));
   const int var = phase == 1 ? 0 : (p->g.dyadic ? 1 : 2);
-  if (n > 0) CKR(launch_eval_kernel(p, var, (n + eval_block_size(var) - 1) / eval_block_size(var), st));
+  if (n > 0) CKR(launch_eval_kernel(p, var, n, st));
   CKR(sync_counters(p, st, 1));
   *n_evaluated = n;
   *n_prop = p->h_counters[C_NIMP];

@@ -1,0 +1,26 @@
+"""The warp-per-voxel evaluation kernels (eval_warp.cuh) normally serve only
+small frontiers; LRCVT_WARP_EVAL=2 routes EVERY round through them, so the
+reference-pinned classify tests (golden cases, fresh volumes vs the oracle,
+20-iteration Lloyd trajectories) exercise their strict-order rule and exact
+fallback on millions of evaluations. LRCVT_WARP_EVAL=0 checks the tile
+kernels alone the same way."""
+
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = Path(__file__).resolve().parents[1]
+
+
+@pytest.mark.parametrize("mode", ["2", "0"])
+def test_classify_suite_under_forced_kernel_choice(mode):
+    env = dict(os.environ, LRCVT_WARP_EVAL=mode)
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider",
+                        str(ROOT / "tests" / "test_gpu_classify.py"), str(ROOT / "tests" / "test_gpu_edges.py"),
+                        str(ROOT / "tests" / "test_gpu_blocks.py")],
+                       cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
