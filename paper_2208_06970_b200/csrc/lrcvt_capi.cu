@@ -181,6 +181,7 @@ bool geo_ok(int64_t nx, int64_t ny, int64_t nz, double sx, double sy, double sz)
 
 }  // namespace
 
+constexpr int EW_SMALL_DEFAULT = 2048;  // frontier size served by the warp-per-voxel kernels
 struct lrcvt_plan {
   Geo g;
   const int* comp = nullptr;
@@ -239,6 +240,7 @@ struct lrcvt_plan {
   bool reuse_eligible = false;
   bool warp_eval = true;  // warp-per-voxel kernels for small frontiers (LRCVT_WARP_EVAL=0 disables)
   bool warp_eval_all = false;
+  int ew_small = EW_SMALL_DEFAULT;
   bool eligible_valid = false;
   int64_t eligible_sites = -1;
   // optional per-launch timing of the dominant kernel (k_eval)
@@ -303,11 +305,10 @@ int prepare_eligible(lrcvt_plan* p, int n_sites, const int* site_comp, cudaStrea
 // Frontiers up to EW_SMALL voxels: warp-per-voxel kernels (eval_warp.cuh),
 // whose round latency is one voxel's parallel evaluation instead of its
 // serial one; larger frontiers: the thread-per-voxel tile kernels.
-constexpr int EW_SMALL = 2048;
 int launch_eval_kernel(lrcvt_plan* p, int var, int items, cudaStream_t st) {
   const Geo& g = p->g;
   if (items < 1) items = 1;
-  if ((items <= EW_SMALL && p->warp_eval) || p->warp_eval_all) {
+  if ((items <= p->ew_small && p->warp_eval) || p->warp_eval_all) {
     const int blocks = (items + EW_WARPS - 1) / EW_WARPS;
     if (var == 0)
       k_eval_warp<false><<<blocks, 32 * EW_WARPS, 0, st>>>(p->ctl, g, p->comp, p->nbm, p->site_pos, p->bm, p->imp,
@@ -515,6 +516,7 @@ int lrcvt_plan_create(lrcvt_plan** plan, int64_t nx, int64_t ny, int64_t nz, dou
     p->warp_eval = e[0] != '0';
     p->warp_eval_all = e[0] == '2';
   }
+  if (const char* e = getenv("LRCVT_EW_SMALL")) p->ew_small = atoi(e);
   p->g = make_geo(nx, ny, nz, sx, sy, sz);
   p->comp = d_comp;
   p->n_components = n_components;
