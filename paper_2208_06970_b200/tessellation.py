@@ -145,6 +145,7 @@ class Engine:
         self.dist = torch.empty(self.n, dtype=torch.float64, device="cuda")
         self.state = torch.empty(self.n, dtype=torch.uint8, device="cuda")
         self.version = 0  # bumps on every classify; guards host<->device reuse
+        self.classify_seq = 0  # bumps on every classify call (the plan's eligible list follows it)
         self.stats = _lib.ClassifyStats()
         self._fin = weakref.finalize(self, Engine._destroy, self.L, self.plan)
 
@@ -179,6 +180,7 @@ class Engine:
         S = int(site_pos.shape[0])
         self.reserve(S)
         ss, dist, state = out if out is not None else (self.ss, self.dist, self.state)
+        self.classify_seq += 1
         rc = _lib.check(self.L.lrcvt_classify(
             self.plan, S, _lib.ptr(site_pos), _lib.ptr(site_comp), ss.data_ptr(),
             dist.data_ptr(), state.data_ptr() if want_state else None,
@@ -309,7 +311,7 @@ def voronoi_classify(grid: VoxelGrid, labels: LabelMap, sites: list[Site],
                             weights)
     torch = _lib.require_cuda()
     eng = engine_for(labels, grid.spacing, len(sites))
-    _, site_comp, pos_d, comp_d = _site_arrays(torch, sites)
+    pos_h, site_comp, pos_d, comp_d = _site_arrays(torch, sites)
     dev = eng.new_state()
     st = eng.classify(pos_d, comp_d, out=dev)
     report = {"rounds": st["rounds"], "sweeps": st["sweeps"],
@@ -317,6 +319,9 @@ def voronoi_classify(grid: VoxelGrid, labels: LabelMap, sites: list[Site],
               "assigned": st["assigned"]}
     tess = DeviceTessellation(grid.dims, grid.spacing, comp, list(sites), report, weights, eng, dev)
     tess._b200_stats = st
+    # the site arrays this classification used: centroidal_update reuses them (and the plan's
+    # eligible-voxel list) while no other classification ran on the plan and the sites are unchanged
+    tess._b200_sites = (eng.classify_seq, pos_h, site_comp, pos_d, comp_d)
     return tess
 
 
@@ -357,15 +362,29 @@ def centroidal_update(tess: Tessellation, weights: np.ndarray | None = None) -> 
                      len(tess.sites))
         eng.upload(tess.site_of, tess.src)
         del labels
-    pos, _, pos_d, comp_d = _site_arrays(torch, tess.sites)
+    pos = np.array([s.position for s in tess.sites], dtype=np.float64).reshape(-1, 3)
+    cached = getattr(tess, "_b200_sites", None) if dev is not None else None
+    reuse = (cached is not None and cached[0] == eng.classify_seq and np.array_equal(cached[2], site_comp)
+             and np.array_equal(cached[1], pos))
+    if reuse:
+        pos_d, comp_d = cached[3], cached[4]
+    else:
+        pos_d = torch.from_numpy(pos).to("cuda")
+        comp_d = torch.from_numpy(np.ascontiguousarray(site_comp, dtype=np.int32)).to("cuda")
     mode, w_d = _weights_mode(torch, weights, eng)
     vlen = voxel_length(tess.dims, tess.spacing)
-    new_pos, disp, empty, _ = eng.centroidal(pos_d, comp_d, mode, w_d, 0.5 * vlen, ss=ss)
+    if reuse:  # same site components as the classification that built the eligible list
+        eng.L.lrcvt_plan_reuse_eligible(eng.plan, 1)
+    try:
+        new_pos, disp, empty, _ = eng.centroidal(pos_d, comp_d, mode, w_d, 0.5 * vlen, ss=ss)
+    finally:
+        if reuse:
+            eng.L.lrcvt_plan_reuse_eligible(eng.plan, 0)
     tess.report["empty_regions"] = int(empty)
-    new_pos = new_pos.cpu().numpy()
-    disp = disp.cpu().numpy()
-    new_sites = [Site(position=(float(p[0]), float(p[1]), float(p[2])), component_id=int(c))
-                 for p, c in zip(new_pos, site_comp)]
+    both = torch.cat([new_pos, disp[:, None]], dim=1).cpu().numpy()  # one device->host read
+    disp = np.ascontiguousarray(both[:, 3])
+    new_sites = [Site(position=(a, b, c), component_id=k)
+                 for (a, b, c), k in zip(both[:, :3].tolist(), site_comp.tolist())]
     mean_ds = float(disp.mean() / vlen) if disp.size else 0.0
     return new_sites, mean_ds
 
