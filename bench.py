@@ -120,7 +120,7 @@ def build_workload(cfg, rank, use_gpu_masks=True):
                           [ComponentInfo(t["id"], t["layer"], t["voxel_count"], tuple(t["bbox"]), (0, 0))
                            for t in table], spec.iso_values, "f")
     params = SeedingParams(**cfg["seeding"])
-    sites, _ = seed_sites(grid, labels, params)
+    sites, _ = seed_sites(grid, labels, params, device=use_gpu_masks)
     weights = voxel_weights(grid, params) if grid.size <= (1 << 28) else None  # host f64 copy: e2e / CPU arm only
     return grid, labels, params, sites, weights
 
@@ -187,6 +187,7 @@ def run_reference(args, cfg, world, rank):
     from oracle import oracle
 
     oracle.build()
+    oracle.set_num_threads(os.cpu_count() or 1)  # all host threads, whatever OMP_NUM_THREADS says
     grid, labels, params, sites, weights = build_workload(cfg, 0, use_gpu_masks=False)
     n = grid.size
     pos = np.array([s.position for s in sites])
@@ -382,6 +383,7 @@ def cpu_baseline(grid, labels, params, weights, pos, sc, budget_s=20.0, max_iter
     from oracle import oracle
 
     oracle.build()
+    oracle.set_num_threads(os.cpu_count() or 1)
     w = None if params.weight_field is None else weights
     comp = labels.component
     t0 = time.perf_counter()
@@ -429,7 +431,7 @@ def run_global(args, cfg, world, rank, local):
         torch.distributed.barrier()
     torch.cuda.synchronize()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
+    with ClockSampler(int(os.environ.get("LRCVT_BENCH_DEVICE", local))) as clk:
         t0.record()
         for _ in range(args.steps):
             pos_d = step(pos_d)
@@ -437,7 +439,8 @@ def run_global(args, cfg, world, rank, local):
         torch.cuda.synchronize()
     ms = t0.elapsed_time(t1)
     if world > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        t = torch.tensor([ms], dtype=torch.float64,
+                         device="cuda" if torch.distributed.get_backend() == "nccl" else "cpu")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t.item())
     if rank == 0:
@@ -479,11 +482,18 @@ def main():
     from paper_2208_06970_b200 import _lib, centroidal_update, voronoi_classify
     from paper_2208_06970_b200.tessellation import engine_for, lloyd_weight_mode, voxel_length
 
-    torch.cuda.set_device(local)
+    # LRCVT_BENCH_DEVICE / LRCVT_BENCH_BACKEND exist only to smoke-test the multi-rank code path on a
+    # one-GPU box (ranks sharing device 0 over gloo; block-mode ranks never wait on each other's kernels)
+    dev_index = int(os.environ.get("LRCVT_BENCH_DEVICE", local))
+    torch.cuda.set_device(dev_index)
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("LRCVT_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev_index))
+        else:
+            dist.init_process_group(backend)
     if args.mode == "global":
         run_global(args, cfg, world, rank, local)
         return
@@ -520,7 +530,7 @@ def main():
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
+    with ClockSampler(int(os.environ.get("LRCVT_BENCH_DEVICE", local))) as clk:
         for k in range(args.steps):
             if flush:
                 scratch.zero_()
@@ -546,7 +556,8 @@ def main():
         pos_b, _ = step(pos_b)
     torch.cuda.synchronize()
     if world > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        t = torch.tensor([ms], dtype=torch.float64,
+                         device="cuda" if torch.distributed.get_backend() == "nccl" else "cpu")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t.item())
     el, eitems, ems = _lib.ctypes.c_int64(), _lib.ctypes.c_int64(), _lib.ctypes.c_double()

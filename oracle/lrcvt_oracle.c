@@ -520,3 +520,14 @@ int orc_num_threads(void) {
   return 1;
 #endif
 }
+
+/* thread count of the eval loops (torchrun exports OMP_NUM_THREADS=1 to every
+ * rank; the CPU arm sets all host threads explicitly) */
+void orc_set_num_threads(int n) {
+#ifdef _OPENMP
+  extern void omp_set_num_threads(int);
+  if (n > 0) omp_set_num_threads(n);
+#else
+  (void)n;
+#endif
+}
