@@ -82,3 +82,21 @@ def test_no_cpu_fallback():
     g = VoxelGrid((4, 1, 1), (1, 1, 1), {"f": np.zeros(4, np.float32)})
     with pytest.raises(LrcvtCudaError):
         classify_isobands(g, IsobandSpec("f", [0.0, 1.0]))
+
+
+def test_new_entry_points_validate_arguments_without_device():
+    """§8(f) entry points reject bad arguments before touching the device."""
+    import ctypes
+
+    from paper_2208_06970_b200 import _lib
+
+    L = _lib.lib()
+    n_in, n_runs, tot = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_double()
+    rc = L.lrcvt_seed_masses(4, 4, 4, 2, None, 1, 0, None, 10, 10, None, None, None, None, None, None,
+                             ctypes.byref(n_in), ctypes.byref(n_runs), ctypes.byref(tot), None)
+    assert rc == -2 and b"lrcvt_seed_masses" in L.lrcvt_last_error()
+    got = ctypes.c_int64()
+    rc = L.lrcvt_layout_records(4, 4, 4, 1, None, None, None, 1, 10, None, None, None, None, ctypes.byref(got), None)
+    assert rc == -2 and b"lrcvt_layout_records" in L.lrcvt_last_error()
+    rc = L.lrcvt_region_adjacency(4, 4, 4, None, None, 3, 10, None, ctypes.byref(got), None)
+    assert rc == -2 and b"lrcvt_region_adjacency" in L.lrcvt_last_error()
