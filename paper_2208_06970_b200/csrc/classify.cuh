@@ -37,6 +37,7 @@ struct RoundCtl {
   int* stash;        // the list buffer parked during a verification sweep
   int2* ss;          // per-voxel (site_of, src) of the classify in flight
   double* dist;      // per-voxel distance
+  int* site1;        // phase 1 only: per-voxel LOS site (site if src == self, else -1); null in phase 2
   int n_cur;         // items in cur
   int sweep_imp;     // improvements found by the last sweep
   int tile_next;     // dynamic tile scheduler of the eval kernels (reset per round)
@@ -47,11 +48,13 @@ struct RoundCtl {
 // Counter slots in the plan's small device array.
 enum { C_NIMP = 0, C_NNEXT = 1, C_BAD = 2, C_ASSIGNED = 3, C_DONE = 4, C_NCOUNTERS = 8 };
 
-__global__ void k_fill_state(int2* __restrict__ ss, double* __restrict__ dist, int64_t n) {
+__global__ void k_fill_state(int2* __restrict__ ss, double* __restrict__ dist, int* __restrict__ site1,
+                             int64_t n) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (; i < n; i += stride) {
     ss[i] = make_int2(LRCVT_NONE, LRCVT_NONE);
+    site1[i] = LRCVT_NONE;
     dist[i] = __longlong_as_double(0x7ff0000000000000LL);  // +inf
   }
 }
@@ -313,6 +316,7 @@ __global__ void __launch_bounds__(128) k_commit(const Prop* __restrict__ imp,
   int* next = ctl->nxt;
   int2* __restrict__ ss = ctl->ss;
   double* __restrict__ dist = ctl->dist;
+  int* __restrict__ site1 = ctl->site1;
   const int stride = gridDim.x * blockDim.x;
   for (int base = blockIdx.x * blockDim.x; base < n_imp; base += stride) {  // warp-uniform
     const int i = base + threadIdx.x;
@@ -323,6 +327,7 @@ __global__ void __launch_bounds__(128) k_commit(const Prop* __restrict__ imp,
       v = p.v;
       __stcg(ss + v, make_int2(p.s, p.src));  // explicit global stores: the
       __stcg(dist + v, p.d);                  // pointers come from RoundCtl
+      if (site1) __stcg(site1 + v, p.src == p.v ? p.s : (int)LRCVT_NONE);
     }
     mark_and_append(g, nbm, active, v, false, bm, next, counters + C_NNEXT, zlo, zhi);
   }
@@ -348,9 +353,10 @@ __global__ void k_loop_init(const RoundCtl* ctl, cudaGraphConditionalHandle h,
 
 // phase 1 starts from the seed worklist appended to `first` by k_seed_groups
 __global__ void k_phase1_start(RoundCtl* ctl, int* counters, int* first, int* second, int2* ss,
-                               double* dist) {
+                               double* dist, int* site1) {
   ctl->ss = ss;
   ctl->dist = dist;
+  ctl->site1 = site1;
   ctl->cur = first;
   ctl->nxt = second;
   ctl->stash = nullptr;
@@ -370,6 +376,7 @@ __global__ void k_phase2_copy(const int* __restrict__ eligible, const int* __res
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) dst[i] = eligible[i];
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     ctl->rounds_p1 = ctl->rounds;
+    ctl->site1 = nullptr;  // phase 2 commits non-LOS states; its kernels read ss
     ctl->n_cur = n;
     ctl->tile_next = 0;
   }
@@ -428,7 +435,7 @@ __global__ void __launch_bounds__(128) k_seed_groups(Geo g, const uint32_t* __re
                                                      const int* __restrict__ val,
                                                      const double* __restrict__ sd_by_site,
                                                      int n_sites, int2* __restrict__ ss,
-                                                     double* __restrict__ dist,
+                                                     double* __restrict__ dist, int* __restrict__ site1,
                                                      uint32_t* __restrict__ bm,
                                                      int* __restrict__ next,
                                                      int* __restrict__ counters,
@@ -449,6 +456,7 @@ __global__ void __launch_bounds__(128) k_seed_groups(Geo g, const uint32_t* __re
       if (beats(d, s, cur_d, cur_s)) { cur_s = s; cur_d = d; }
     }
     ss[v] = make_int2(cur_s, v);
+    site1[v] = cur_s;
     dist[v] = cur_d;
   }
   if (blockIdx.x * blockDim.x >= n_sites) return;

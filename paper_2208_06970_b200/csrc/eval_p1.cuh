@@ -34,7 +34,7 @@ template <int BLOCK>
 __device__ __forceinline__ void p1_tile(const int* __restrict__ list, int n, const int i, const Geo& g,
                                                    const int* __restrict__ comp,
                                                    const uint32_t* __restrict__ nbm,
-                                                   const int2* __restrict__ ss,
+                                                   const int* __restrict__ site1,
                                                    const double* __restrict__ dist,
                                                    const double4* __restrict__ site_pos,
                                                    uint32_t* __restrict__ bm,
@@ -71,17 +71,17 @@ __device__ __forceinline__ void p1_tile(const int* __restrict__ list, int n, con
     const unsigned same = __ldg(nbm + v);
     nbv = same;
     // ---- A
-    int2 nw[26];
+    // phase 1: site1[w] is site_of[w] when src[w] == w (every phase-1 assignment), else -1
+    int nw[26];
 #pragma unroll
     for (int k = 0; k < 26; k++) {
       const int w = v + off_dx(k) + off_dy(k) * g.nx + off_dz(k) * g.nxy;
-      nw[k] = ((same >> k) & 1u) ? __ldg(ss + w) : make_int2(-1, -1);
+      nw[k] = ((same >> k) & 1u) ? __ldg(site1 + w) : -1;
     }
     int nt = 0;
 #pragma unroll
     for (int k = 0; k < 26; k++) {
-      const int w = v + off_dx(k) + off_dy(k) * g.nx + off_dz(k) * g.nxy;
-      const int s = (nw[k].x >= 0 && nw[k].y == w) ? nw[k].x : -1;
+      const int s = nw[k];
       row[k * BLOCK] = s;
       // ---- B: distinct-site table
       bool seen = s < 0;
@@ -96,9 +96,8 @@ __device__ __forceinline__ void p1_tile(const int* __restrict__ list, int n, con
         ovf = true;
       }
     }
-    const int2 sv = __ldg(ss + v);
     best_d = __ldg(dist + v);
-    best_s = sv.x; best_src = sv.y;
+    best_s = __ldg(site1 + v); best_src = v;  // phase-1 states are LOS (src == v)
     orig_d = best_d; orig_s = best_s;
   }
 #pragma unroll
@@ -267,13 +266,13 @@ __global__ void __launch_bounds__(BLOCK, P1_MIN_BLOCKS) k_eval_p1(RoundCtl* __re
                                                    int* __restrict__ counters) {
   const int n = ctl->n_cur;
   const int* list = ctl->cur;
-  const int2* __restrict__ ss = ctl->ss;
+  const int* __restrict__ site1 = ctl->site1;
   const double* __restrict__ dist = ctl->dist;
   // one BLOCK-voxel tile per block: the launch grid always covers the list
   // (exact grid on the host path, size-class grid >= n inside the graph)
   const int base = blockIdx.x * BLOCK;
   if (base >= n) return;
-  p1_tile<BLOCK>(list, n, base + (int)threadIdx.x, g, comp, nbm, ss, dist, site_pos, bm, imp, counters);
+  p1_tile<BLOCK>(list, n, base + (int)threadIdx.x, g, comp, nbm, site1, dist, site_pos, bm, imp, counters);
 }
 
 }  // namespace lrcvt

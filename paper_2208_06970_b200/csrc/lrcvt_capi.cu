@@ -197,6 +197,7 @@ struct lrcvt_plan {
   uint32_t* bm = nullptr;  // frontier bitmap (1 bit per voxel)
   int64_t bm_words = 0;
   uint32_t* nbm = nullptr;  // static same-component neighbour masks
+  int* site1 = nullptr;     // phase-1 LOS site per voxel (RoundCtl::site1)
   int* counters = nullptr;
   int* h_counters = nullptr;  // pinned
   uint8_t* has_site = nullptr;
@@ -550,6 +551,7 @@ int lrcvt_plan_create(lrcvt_plan** plan, int64_t nx, int64_t ny, int64_t nz, dou
   rc |= dalloc(&p->imp, nin);
   rc |= dalloc(&p->bm, p->bm_words);
   rc |= dalloc(&p->nbm, n);
+  rc |= dalloc(&p->site1, n);
   rc |= dalloc(&p->ctl, 1);
   rc |= dalloc(&p->d_handles, 3 * MAX_CLASSES);
   rc |= dalloc(&p->d_nel, 1);
@@ -629,7 +631,7 @@ int lrcvt_plan_destroy(lrcvt_plan* p) {
     if (gx) cudaGraphExecDestroy(gx);
   if (p->cap) cudaStreamDestroy(p->cap);
   if (p->h_ctl) cudaFreeHost(p->h_ctl);
-  void* bufs[] = {p->counters, p->ctl, p->d_handles, p->d_nel, p->list_a, p->list_b, p->eligible, p->imp, p->bm, p->nbm, p->has_site,
+  void* bufs[] = {p->counters, p->ctl, p->d_handles, p->d_nel, p->list_a, p->list_b, p->eligible, p->imp, p->bm, p->nbm, p->site1, p->has_site,
                   p->site_pos, p->new_pos, p->sk_key, p->sk_key2, p->sk_val, p->sk_val2, p->sk_d,
                   p->acc, p->sums, p->vt_key, p->vt_key2, p->vt_idx, p->vt_idx2, p->vt_terms,
                   p->seg_b, p->seg_e, p->cub_tmp};
@@ -695,7 +697,7 @@ int lrcvt_classify(lrcvt_plan* p, int64_t n_sites, const double* d_site_pos,
   int2* ss = reinterpret_cast<int2*>(d_site_src);
   memset(stats, 0, sizeof *stats);
   // tessellation.py:120-122
-  k_fill_state<<<grid_for(g.n, 256, 148 * 32), 256, 0, st>>>(ss, d_dist, g.n);
+  k_fill_state<<<grid_for(g.n, 256, 148 * 32), 256, 0, st>>>(ss, d_dist, p->site1, g.n);
   CKL("k_fill_state"); LAUNCHED(1);
   CK(cudaMemsetAsync(p->counters, 0, sizeof(int) * C_NCOUNTERS, st));
   if (S == 0) {  // tessellation.py:126-134
@@ -717,9 +719,9 @@ int lrcvt_classify(lrcvt_plan* p, int64_t n_sites, const double* d_site_pos,
   // groups -> seeds, then the phase-1 worklist (tessellation.py:151); sites
   // outside their component (key INT_MAX) are skipped and reported at the end
   k_seed_groups<<<grid_for(S, 128), 128, 0, st>>>(g, p->nbm, p->sk_key2, p->sk_val2, p->sk_d, S, ss,
-                                                  d_dist, p->bm, p->list_a, p->counters);  // marks bm (round-1 frontier)
+                                                  d_dist, p->site1, p->bm, p->list_a, p->counters);  // marks bm (round-1 frontier)
   CKL("k_seed_groups"); LAUNCHED(1);
-  k_phase1_start<<<1, 1, 0, st>>>(p->ctl, p->counters, p->list_a, p->list_b, ss, d_dist);
+  k_phase1_start<<<1, 1, 0, st>>>(p->ctl, p->counters, p->list_a, p->list_b, ss, d_dist, p->site1);
   CKL("k_phase1_start"); LAUNCHED(1);
   // phase 1 (tessellation.py:152-156)
   CKR(run_rounds(p, 0, st));
@@ -1134,7 +1136,7 @@ int lrcvt_mg_begin(lrcvt_plan* p, int64_t n_sites, const double* d_site_pos, con
   const Geo& g = p->g;
   const int S = (int)n_sites;
   int2* ss = reinterpret_cast<int2*>(d_site_src);
-  k_fill_state<<<grid_for(g.n, 256, 148 * 32), 256, 0, st>>>(ss, d_dist, g.n);
+  k_fill_state<<<grid_for(g.n, 256, 148 * 32), 256, 0, st>>>(ss, d_dist, p->site1, g.n);
   CKL("k_fill_state");
   CK(cudaMemsetAsync(p->counters, 0, sizeof(int) * C_NCOUNTERS, st));
   k_pack_sites<<<grid_for(S, 256), 256, 0, st>>>(d_site_pos, S, p->site_pos);
@@ -1149,10 +1151,10 @@ int lrcvt_mg_begin(lrcvt_plan* p, int64_t n_sites, const double* d_site_pos, con
   }
   // every rank places every seed (replicated state); the phase-1 worklist
   // holds the own slab's part only
-  k_seed_groups<<<grid_for(S, 128), 128, 0, st>>>(g, p->nbm, p->sk_key2, p->sk_val2, p->sk_d, S, ss, d_dist, p->bm,
+  k_seed_groups<<<grid_for(S, 128), 128, 0, st>>>(g, p->nbm, p->sk_key2, p->sk_val2, p->sk_d, S, ss, d_dist, p->site1, p->bm,
                                                   p->list_a, p->counters, p->zlo, p->zhi);
   CKL("k_seed_groups");
-  k_phase1_start<<<1, 1, 0, st>>>(p->ctl, p->counters, p->list_a, p->list_b, ss, d_dist);
+  k_phase1_start<<<1, 1, 0, st>>>(p->ctl, p->counters, p->list_a, p->list_b, ss, d_dist, p->site1);
   CKL("k_phase1_start");
   CK(cudaMemcpyAsync(p->h_ctl, p->ctl, sizeof(RoundCtl), cudaMemcpyDeviceToHost, st));
   CKR(sync_counters(p, st, C_NCOUNTERS));
