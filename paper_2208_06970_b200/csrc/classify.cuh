@@ -251,11 +251,26 @@ __device__ __forceinline__ void mark_and_append(const Geo& g, const uint32_t* __
     const int t = __shfl_up_sync(0xffffffffu, incl, o);
     if (lane >= o) incl += t;
   }
-  const int total = __shfl_sync(0xffffffffu, incl, 31);
-  int base = 0;
-  if (lane == 31 && total) base = atomicAdd(counter, total);
-  base = __shfl_sync(0xffffffffu, base, 31);
-  int pos = base + incl - cnt;
+  // one list reservation per CTA (a per-warp atomic on the single counter
+  // serialised ~4 M same-address atomics per 512^3 iteration); every thread
+  // of the CTA reaches this point the same number of times
+  __shared__ int s_wbase[32];
+  __shared__ int s_cbase;
+  const int wid = threadIdx.x >> 5;
+  if (lane == 31) s_wbase[wid] = incl;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int sum = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); w++) {
+      const int t = s_wbase[w];
+      s_wbase[w] = sum;
+      sum += t;
+    }
+    s_cbase = sum ? atomicAdd(counter, sum) : 0;
+  }
+  __syncthreads();
+  int pos = s_cbase + s_wbase[wid] + incl - cnt;
+  __syncthreads();  // the next call may overwrite s_wbase / s_cbase
   while (newmask) {
     const int j = __ffs(newmask) - 1;
     newmask &= newmask - 1;
