@@ -265,6 +265,28 @@ __device__ __forceinline__ bool ray_clear_near(unsigned nbm_v, double px, double
 
 // Warp-aggregated append of `take` (0/1) items; returns this lane's slot
 // (valid only when take). All 32 lanes must call it.
+// CTA-aggregated append: one atomic per CTA. Every thread of the CTA must
+// call it (uses __syncthreads).
+__device__ __forceinline__ int block_append(int* counter, bool take) {
+  __shared__ int s_w[32];
+  __shared__ int s_b;
+  const unsigned m = __ballot_sync(0xffffffffu, take);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) s_w[wid] = __popc(m);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int sum = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); w++) {
+      const int t = s_w[w];
+      s_w[w] = sum;
+      sum += t;
+    }
+    s_b = sum ? atomicAdd(counter, sum) : 0;
+  }
+  __syncthreads();
+  return s_b + s_w[wid] + __popc(m & ((1u << lane) - 1u));
+}
+
 __device__ __forceinline__ int warp_append(int* counter, bool take) {
   unsigned m = __ballot_sync(0xffffffffu, take);
   int lane = threadIdx.x & 31;

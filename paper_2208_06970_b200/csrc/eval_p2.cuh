@@ -212,7 +212,7 @@ __device__ __forceinline__ void p2_tile(const int* __restrict__ list, int n, con
   const bool improved = active && ((best_s != orig_s) || (best_d < __dsub_rn(orig_d, LRCVT_EPS)));
   Prop pr;
   pr.d = best_d; pr.v = v; pr.s = best_s; pr.src = best_src; pr.pad = 0;
-  const int slot = warp_append(counters + C_NIMP, improved);
+  const int slot = block_append(counters + C_NIMP, improved);
   if (improved) imp[slot] = pr;
 }
 
