@@ -11,6 +11,8 @@ Lloyd loop and only the final tessellation is copied back.
 from __future__ import annotations
 
 import ctypes
+import itertools
+import operator
 import weakref
 from dataclasses import dataclass, field
 
@@ -57,10 +59,10 @@ class Tessellation:
         return len(self.sites)
 
     def site_positions(self) -> np.ndarray:
-        return np.array([s.position for s in self.sites], dtype=np.float64).reshape(-1, 3)
+        return _positions(self.sites)
 
     def site_components(self) -> np.ndarray:
-        return np.array([s.component_id for s in self.sites], dtype=np.int32)
+        return _components(self.sites)
 
 
 class DeviceTessellation(Tessellation):
@@ -247,9 +249,23 @@ def engine_for(labels: LabelMap, spacing, n_sites: int) -> Engine:
     return eng
 
 
+_get_pos = operator.attrgetter("position")
+_get_comp = operator.attrgetter("component_id")
+
+
+def _positions(sites) -> np.ndarray:
+    """float64[S, 3] site positions (C-level iteration; same values as np.array)."""
+    return np.fromiter(itertools.chain.from_iterable(map(_get_pos, sites)), dtype=np.float64,
+                       count=3 * len(sites)).reshape(-1, 3)
+
+
+def _components(sites) -> np.ndarray:
+    return np.fromiter(map(_get_comp, sites), dtype=np.int32, count=len(sites))
+
+
 def _site_arrays(torch, sites):
-    pos = np.array([s.position for s in sites], dtype=np.float64).reshape(-1, 3)
-    comp = np.array([s.component_id for s in sites], dtype=np.int32)
+    pos = _positions(sites)
+    comp = _components(sites)
     return pos, comp, torch.from_numpy(pos).to("cuda"), torch.from_numpy(comp).to("cuda")
 
 
@@ -362,7 +378,7 @@ def centroidal_update(tess: Tessellation, weights: np.ndarray | None = None) -> 
                      len(tess.sites))
         eng.upload(tess.site_of, tess.src)
         del labels
-    pos = np.array([s.position for s in tess.sites], dtype=np.float64).reshape(-1, 3)
+    pos = _positions(tess.sites)
     cached = getattr(tess, "_b200_sites", None) if dev is not None else None
     reuse = (cached is not None and cached[0] == eng.classify_seq and np.array_equal(cached[2], site_comp)
              and np.array_equal(cached[1], pos))
@@ -383,8 +399,7 @@ def centroidal_update(tess: Tessellation, weights: np.ndarray | None = None) -> 
     tess.report["empty_regions"] = int(empty)
     both = torch.cat([new_pos, disp[:, None]], dim=1).cpu().numpy()  # one device->host read
     disp = np.ascontiguousarray(both[:, 3])
-    new_sites = [Site(position=(a, b, c), component_id=k)
-                 for (a, b, c), k in zip(both[:, :3].tolist(), site_comp.tolist())]
+    new_sites = list(map(Site, map(tuple, both[:, :3].tolist()), site_comp.tolist()))
     mean_ds = float(disp.mean() / vlen) if disp.size else 0.0
     return new_sites, mean_ds
 
