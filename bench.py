@@ -274,7 +274,7 @@ def layout_pass(grid, labels, eng, S):
 
     def run():
         _lib.check(L.lrcvt_layout_records(nx, ny, nz, len(names), ptrs, eng.comp.data_ptr(), site_of.data_ptr(),
-                                          labels.n_components, r_cap, rec.data_ptr(), key.data_ptr(),
+                                          labels.n_components, S, r_cap, rec.data_ptr(), key.data_ptr(),
                                           first.data_ptr(), count.data_ptr(), ctypes.byref(got), st), "layout")
 
     run()

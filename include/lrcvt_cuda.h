@@ -170,10 +170,11 @@ int lrcvt_seed_masses(int64_t nx, int64_t ny, int64_t nz, int32_t block_size,
  * its region key (d_region_key, u32) and per component its first record and
  * record count (d_comp_first / d_comp_count int64[n_components]; 0 / 0 when
  * empty). *n_records = the in-band count; LRCVT_E_ARG when it exceeds
- * max_records. */
+ * max_records or a site_of entry is >= n_sites. */
 int lrcvt_layout_records(int64_t nx, int64_t ny, int64_t nz, int32_t n_fields,
                          const float *const *field_ptrs, const int32_t *d_component,
-                         const int32_t *d_site_of, int32_t n_components, int64_t max_records,
+                         const int32_t *d_site_of, int32_t n_components, int32_t n_sites,
+                         int64_t max_records,
                          void *d_records, uint32_t *d_region_key, int64_t *d_comp_first,
                          int64_t *d_comp_count, int64_t *n_records, void *stream);
 

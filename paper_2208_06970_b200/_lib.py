@@ -104,7 +104,7 @@ SIGNATURES = {
     ),
     "lrcvt_layout_records": (
         c_int,
-        [c_int64, c_int64, c_int64, c_int32, c_void_p, c_void_p, c_void_p, c_int32, c_int64, c_void_p,
+        [c_int64, c_int64, c_int64, c_int32, c_void_p, c_void_p, c_void_p, c_int32, c_int32, c_int64, c_void_p,
          c_void_p, c_void_p, c_void_p, POINTER(c_int64), c_void_p],
     ),
     "lrcvt_region_adjacency": (

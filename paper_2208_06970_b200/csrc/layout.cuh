@@ -16,13 +16,20 @@ namespace lrcvt {
 
 constexpr unsigned kUnassignedRegion = 0xFFFFFFFFu;
 
+// key = component << rbits | region code; code = site, or n_sites for an
+// unassigned voxel (so it closes its component's range like 0xFFFFFFFF does);
+// 32-bit keys whenever the two fields fit. A site id >= n_sites sets *bad.
+template <typename K>
 __global__ void k_layout_keys(const int* __restrict__ list, int64_t n, const int* __restrict__ comp,
-                              const int* __restrict__ site_of, unsigned long long* __restrict__ key) {
+                              const int* __restrict__ site_of, int n_sites, int rbits, K* __restrict__ key,
+                              int* __restrict__ bad) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
     const int v = list[i];
-    const int s = site_of[v];
-    key[i] = ((unsigned long long)(unsigned)comp[v] << 32) | (s >= 0 ? (unsigned)s : kUnassignedRegion);
+    int s = site_of[v];
+    if (s >= n_sites) { atomicExch(bad, 1); s = n_sites; }
+    const unsigned code = s >= 0 ? (unsigned)s : (unsigned)n_sites;
+    key[i] = ((K)(unsigned)comp[v] << rbits) | (K)code;
   }
 }
 
@@ -49,18 +56,22 @@ __global__ void k_layout_pack(const int* __restrict__ vox, int64_t r, int m, int
   }
 }
 
-// region key per record, and each component's [first, first + count) range
-__global__ void k_layout_index(const unsigned long long* __restrict__ key, int64_t r,
+// region key per record (the reference's u32 key: site or 0xFFFFFFFF), and
+// each component's [first, first + count) range
+template <typename K>
+__global__ void k_layout_index(const K* __restrict__ key, int64_t r, int rbits, int n_sites,
                                unsigned* __restrict__ region_key, int n_comp,
                                long long* __restrict__ comp_first, long long* __restrict__ comp_count) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const K rmask = ((K)1 << rbits) - 1;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < r; i += stride) {
-    const unsigned long long k = key[i];
-    region_key[i] = (unsigned)(k & 0xFFFFFFFFull);
-    const unsigned c = (unsigned)(k >> 32);
+    const K k = key[i];
+    const unsigned code = (unsigned)(k & rmask);
+    region_key[i] = code == (unsigned)n_sites ? kUnassignedRegion : code;
+    const unsigned c = (unsigned)(k >> rbits);
     if (c >= (unsigned)n_comp) continue;
-    if (i == 0 || (unsigned)(key[i - 1] >> 32) != c) comp_first[c] = i;
-    if (i == r - 1 || (unsigned)(key[i + 1] >> 32) != c) comp_count[c] = i + 1;  // end; count fixed below
+    if (i == 0 || (unsigned)(key[i - 1] >> rbits) != c) comp_first[c] = i;
+    if (i == r - 1 || (unsigned)(key[i + 1] >> rbits) != c) comp_count[c] = i + 1;  // end; count fixed below
   }
 }
 

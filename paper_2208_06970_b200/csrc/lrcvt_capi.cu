@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "../../include/lrcvt_cuda.h"
@@ -1349,12 +1350,12 @@ int lrcvt_seed_masses(int64_t nx, int64_t ny, int64_t nz, int32_t block_size, co
 
 int lrcvt_layout_records(int64_t nx, int64_t ny, int64_t nz, int32_t n_fields, const float* const* field_ptrs,
                          const int32_t* d_component, const int32_t* d_site_of, int32_t n_components,
-                         int64_t max_records, void* d_records, uint32_t* d_region_key, int64_t* d_comp_first,
+                         int32_t n_sites, int64_t max_records, void* d_records, uint32_t* d_region_key, int64_t* d_comp_first,
                          int64_t* d_comp_count, int64_t* n_records, void* stream) {
   retain_pool();
   const int64_t n = nx * ny * nz;
   if (nx < 1 || ny < 1 || nz < 1 || n >= (int64_t(1) << 31) || n_fields < 0 || n_fields > 16 ||
-      (n_fields > 0 && !field_ptrs) || !d_component || !d_site_of || n_components < 0 || !d_records ||
+      (n_fields > 0 && !field_ptrs) || !d_component || !d_site_of || n_components < 0 || n_sites < 0 || !d_records ||
       !d_region_key || (n_components > 0 && (!d_comp_first || !d_comp_count)) || !n_records)
     return set_error(LRCVT_E_ARG, "lrcvt_layout_records: bad arguments");
   FieldPtrs fp{};
@@ -1386,32 +1387,52 @@ int lrcvt_layout_records(int64_t nx, int64_t ny, int64_t nz, int32_t n_fields, c
   *n_records = r;
   if (r > max_records) return set_error(LRCVT_E_ARG, "lrcvt_layout_records: max_records too small");
   if (r == 0) return 0;
-  unsigned long long *key = nullptr, *key2 = nullptr;
-  CK(sc.get(&key, r));
-  CK(sc.get(&key2, r));
   CK(sc.get(&vox, r));
-  k_layout_keys<<<grid_for(r, 256, 148 * 16), 256, 0, st>>>(list, r, d_component, d_site_of, key);
-  CKL("k_layout_keys"); LAUNCHED(1);
-  int bits = 33;
-  while (bits < 64 && (1ll << (bits - 32)) < (int64_t)n_components) bits++;
-  b = 0;
-  CK(cub::DeviceRadixSort::SortPairs(nullptr, b, key, key2, list, vox, (int)r, 0, bits, st));
-  void* tmp2 = nullptr;
-  CK(sc.get((char**)&tmp2, (int64_t)b));
-  CK(cub::DeviceRadixSort::SortPairs(tmp2, b, key, key2, list, vox, (int)r, 0, bits, st));
-  k_layout_pack<<<grid_for(r * (3 + n_fields), 256, 148 * 32), 256, 0, st>>>(vox, r, n_fields, (int)nx, (int)ny,
-                                                                              fp, (unsigned*)d_records);
-  CKL("k_layout_pack"); LAUNCHED(1);
-  k_layout_index<<<grid_for(r, 256, 148 * 16), 256, 0, st>>>(key2, r, d_region_key, n_components,
-                                                              (long long*)d_comp_first,
-                                                              (long long*)d_comp_count);
-  CKL("k_layout_index"); LAUNCHED(1);
+  int rbits = 1, cbits = 1;
+  while ((1ll << rbits) <= (int64_t)n_sites) rbits++;  // codes 0..n_sites
+  while ((1ll << cbits) < (int64_t)n_components) cbits++;
+  int* bad = nullptr;
+  CK(sc.get(&bad, 1));
+  CK(cudaMemsetAsync(bad, 0, sizeof(int), st));
+  auto run = [&](auto* key, auto* key2) -> int {
+    using K = std::remove_pointer_t<decltype(key)>;
+    k_layout_keys<K><<<grid_for(r, 256, 148 * 16), 256, 0, st>>>(list, r, d_component, d_site_of, n_sites, rbits,
+                                                                  key, bad);
+    CKL("k_layout_keys"); LAUNCHED(1);
+    size_t bb = 0;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, bb, key, key2, list, vox, (int)r, 0, rbits + cbits, st));
+    void* t2 = nullptr;
+    CK(sc.get((char**)&t2, (int64_t)bb));
+    CK(cub::DeviceRadixSort::SortPairs(t2, bb, key, key2, list, vox, (int)r, 0, rbits + cbits, st));
+    k_layout_pack<<<grid_for(r * (3 + n_fields), 256, 148 * 32), 256, 0, st>>>(vox, r, n_fields, (int)nx, (int)ny,
+                                                                                fp, (unsigned*)d_records);
+    CKL("k_layout_pack"); LAUNCHED(1);
+    k_layout_index<K><<<grid_for(r, 256, 148 * 16), 256, 0, st>>>(key2, r, rbits, n_sites, d_region_key,
+                                                                   n_components, (long long*)d_comp_first,
+                                                                   (long long*)d_comp_count);
+    CKL("k_layout_index"); LAUNCHED(1);
+    return 0;
+  };
+  if (rbits + cbits <= 32) {
+    unsigned *key = nullptr, *key2 = nullptr;
+    CK(sc.get(&key, r));
+    CK(sc.get(&key2, r));
+    CKR(run(key, key2));
+  } else {
+    unsigned long long *key = nullptr, *key2 = nullptr;
+    CK(sc.get(&key, r));
+    CK(sc.get(&key2, r));
+    CKR(run(key, key2));
+  }
   if (n_components > 0) {
     k_layout_counts<<<grid_for(n_components, 256), 256, 0, st>>>(n_components, (const long long*)d_comp_first,
                                                                  (long long*)d_comp_count);
     CKL("k_layout_counts"); LAUNCHED(1);
   }
+  int h_bad = 0;
+  CK(cudaMemcpyAsync(&h_bad, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
+  if (h_bad) return set_error(LRCVT_E_ARG, "lrcvt_layout_records: site_of holds an id >= n_sites");
   return 0;
 }
 

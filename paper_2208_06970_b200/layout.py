@@ -126,7 +126,7 @@ class Header:
 # device pass
 
 
-def device_records(grid: VoxelGrid, labels: LabelMap, site_of_dev, names: list[str]):
+def device_records(grid: VoxelGrid, labels: LabelMap, site_of_dev, names: list[str], n_sites: int):
     """(records [structured, host], region keys u32 [host], comp first int64,
     comp count int64) from one ``lrcvt_layout_records`` call."""
     from . import _lib
@@ -150,7 +150,7 @@ def device_records(grid: VoxelGrid, labels: LabelMap, site_of_dev, names: list[s
         key_d = torch.empty(max(cap, 1), dtype=torch.int32, device="cuda")
         got = ctypes.c_int64()
         rc = L.lrcvt_layout_records(nx, ny, nz, len(names), ptrs, comp_d.data_ptr(), site_of_dev.data_ptr(), n_comp,
-                                    cap, rec_d.data_ptr(), key_d.data_ptr(), first.data_ptr(), count.data_ptr(),
+                                    n_sites, cap, rec_d.data_ptr(), key_d.data_ptr(), first.data_ptr(), count.data_ptr(),
                                     ctypes.byref(got), _lib.stream_handle(torch))
         if rc == _lib.E_ARG and got.value > cap:
             cap = int(got.value)
@@ -274,7 +274,7 @@ def build_and_write(grid: VoxelGrid, labels: LabelMap, tess, aggregates: list[Ag
     path = Path(path)
     names = grid.field_names()
     m = len(names)
-    records, region, first, count = device_records(grid, labels, _site_of_device(tess), names)
+    records, region, first, count = device_records(grid, labels, _site_of_device(tess), names, len(tess.sites))
     layers, components, regions = _index_tables(labels, tess, region, first, count)
     r = int(records.size)
     h = Header(tuple(grid.dims), tuple(grid.spacing), names, labels.field_name, list(labels.iso_values), r,

@@ -96,7 +96,8 @@ def test_new_entry_points_validate_arguments_without_device():
                              ctypes.byref(n_in), ctypes.byref(n_runs), ctypes.byref(tot), None)
     assert rc == -2 and b"lrcvt_seed_masses" in L.lrcvt_last_error()
     got = ctypes.c_int64()
-    rc = L.lrcvt_layout_records(4, 4, 4, 1, None, None, None, 1, 10, None, None, None, None, ctypes.byref(got), None)
+    rc = L.lrcvt_layout_records(4, 4, 4, 1, None, None, None, 1, 1, 10, None, None, None, None, ctypes.byref(got),
+                                None)
     assert rc == -2 and b"lrcvt_layout_records" in L.lrcvt_last_error()
     rc = L.lrcvt_region_adjacency(4, 4, 4, None, None, 3, 10, None, ctypes.byref(got), None)
     assert rc == -2 and b"lrcvt_region_adjacency" in L.lrcvt_last_error()

@@ -134,7 +134,8 @@ def test_gpu_layout_pipeline_vs_oracle(oracle_mod, tmp_path):
     grid = synth_field("gaussian-mix", (40, 36, 28), 0)
     labels = label_components(classify_isobands(grid, IsobandSpec("f", [0.2, 0.45, 0.7])))
     tess, _ = lrcvt(grid, labels, SeedingParams(alpha=60, weight_field="g", seed=1), LloydParams(max_updates=2))
-    rec, region, first, count = device_records(grid, labels, _site_of_device(tess), grid.field_names())
+    rec, region, first, count = device_records(grid, labels, _site_of_device(tess), grid.field_names(),
+                                               len(tess.sites))
     orec, okey, ofirst, ocount = oracle_mod.layout_records(grid.dims, labels.component, tess.site_of,
                                                            [grid.fields[k] for k in grid.field_names()],
                                                            labels.n_components)
