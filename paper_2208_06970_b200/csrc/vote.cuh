@@ -130,27 +130,33 @@ __global__ void __launch_bounds__(WARPS * 32) k_vote_warp(const int* __restrict_
                                                          const int* __restrict__ seg_begin,
                                                          const int* __restrict__ seg_end,
                                                          int n_sites, double* __restrict__ sums) {
+  // terms are staged 32 at a time through shared memory; DEPTH batches are
+  // loaded ahead so the four serial chains (x, y, z, w) never wait on memory
+  constexpr int DEPTH = 4;
   __shared__ double buf[WARPS][32][4];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int s = blockIdx.x * WARPS + wid;
   if (s >= n_sites) return;
   const int b = seg_begin[s], e = seg_end[s];
   double acc = 0.0;
-  int j0 = b;
-  double4 t = make_double4(0, 0, 0, 0);
-  if (j0 + lane < e) t = terms[sidx[j0 + lane]];
-  while (j0 < e) {
-    buf[wid][lane][0] = t.x; buf[wid][lane][1] = t.y; buf[wid][lane][2] = t.z; buf[wid][lane][3] = t.w;
+  double4 t[DEPTH];
+#pragma unroll
+  for (int q = 0; q < DEPTH; q++) {
+    const int j = b + 32 * q + lane;
+    t[q] = j < e ? terms[sidx[j]] : make_double4(0, 0, 0, 0);
+  }
+  for (int j0 = b; j0 < e; j0 += 32) {
+    buf[wid][lane][0] = t[0].x; buf[wid][lane][1] = t[0].y; buf[wid][lane][2] = t[0].z; buf[wid][lane][3] = t[0].w;
     __syncwarp();
+#pragma unroll
+    for (int q = 0; q < DEPTH - 1; q++) t[q] = t[q + 1];
+    const int jn = j0 + 32 * DEPTH + lane;
+    t[DEPTH - 1] = jn < e ? terms[sidx[jn]] : make_double4(0, 0, 0, 0);
     const int cnt = min(32, e - j0);
-    const int jn = j0 + 32;
-    t = make_double4(0, 0, 0, 0);
-    if (jn + lane < e) t = terms[sidx[jn + lane]];
     if (lane < 4) {
       for (int q = 0; q < cnt; q++) acc = __dadd_rn(acc, buf[wid][q][lane]);
     }
     __syncwarp();
-    j0 = jn;
   }
   if (lane < 4) sums[lane * n_sites + s] = acc;
 }
