@@ -340,9 +340,12 @@ __global__ void __launch_bounds__(128) k_commit(const Prop* __restrict__ imp,
     if (active) {
       const Prop p = imp[i];
       v = p.v;
-      __stcg(ss + v, make_int2(p.s, p.src));  // explicit global stores: the
-      __stcg(dist + v, p.d);                  // pointers come from RoundCtl
+      // explicit global stores (the pointers come from RoundCtl). Phase 1
+      // keeps only the compact LOS site; ss is rebuilt from it once when
+      // phase 2 starts (k_site1_to_ss), saving a scattered 8-byte store here.
       if (site1) __stcg(site1 + v, p.src == p.v ? p.s : (int)LRCVT_NONE);
+      else __stcg(ss + v, make_int2(p.s, p.src));
+      __stcg(dist + v, p.d);
     }
     mark_and_append(g, nbm, active, v, false, bm, next, counters + C_NNEXT, zlo, zhi);
   }
@@ -384,6 +387,15 @@ __global__ void k_phase1_start(RoundCtl* ctl, int* counters, int* first, int* se
 }
 
 // phase 2 starts from a copy of the eligible list (tessellation.py:166-167)
+// phase-1 states are LOS (src == v): (site_of, src) from the compact array
+__global__ void k_site1_to_ss(const int* __restrict__ site1, int2* __restrict__ ss, int64_t n) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+    const int s = __ldcs(site1 + i);
+    __stcs(ss + i, make_int2(s, s >= 0 ? (int)i : (int)LRCVT_NONE));
+  }
+}
+
 __global__ void k_phase2_copy(const int* __restrict__ eligible, const int* __restrict__ n_el,
                               RoundCtl* ctl) {
   const int n = *n_el;

@@ -186,6 +186,7 @@ __global__ void __launch_bounds__(32 * EW_WARPS) k_eval_warp(RoundCtl* __restric
   if (i >= n) return;  // warp-uniform
   const int* __restrict__ list = ctl->cur;
   const int2* __restrict__ ss = ctl->ss;
+  const int* __restrict__ site1 = ctl->site1;
   const double* __restrict__ dist = ctl->dist;
   const int v = __ldg(list + i);
   int x, y, z;
@@ -193,7 +194,13 @@ __global__ void __launch_bounds__(32 * EW_WARPS) k_eval_warp(RoundCtl* __restric
   const int cv = __ldg(comp + v);
   const double px = centre1(x, g.sx), py = centre1(y, g.sy), pz = centre1(z, g.sz);
   const unsigned nbv = __ldg(nbm + v);
-  const int2 sv = __ldg(ss + v);
+  int2 sv;
+  if (PHASE2) {
+    sv = __ldg(ss + v);
+  } else {
+    const int s1 = __ldg(site1 + v);
+    sv = make_int2(s1, s1 >= 0 ? v : -1);
+  }
   const double orig_d = __ldg(dist + v);
   const int orig_s = sv.x, orig_src = sv.y;
   if (lane == 0) bm[v >> 5] = 0u;  // consume this round's frontier word
@@ -202,7 +209,14 @@ __global__ void __launch_bounds__(32 * EW_WARPS) k_eval_warp(RoundCtl* __restric
   if (lane < 26 && ((nbv >> lane) & 1u)) {
     const char4 o = c_off[lane];
     const int w = nbr_index(v, o, g.nx, g.nxy);
-    const int2 nw = __ldg(ss + w);
+    // phase 1 keeps only the compact LOS site (src == w implied); phase 2 reads (site, src)
+    int2 nw;
+    if (PHASE2) {
+      nw = __ldg(ss + w);
+    } else {
+      const int s1 = __ldg(site1 + w);
+      nw = make_int2(s1, s1 >= 0 ? w : -1);
+    }
     if (nw.x >= 0) {
       if (PHASE2) {
         double len;
