@@ -117,3 +117,38 @@ def test_zero_sites():
     tess = voronoi_classify(grid, _labels(np.zeros(16), (4, 4, 1)), [])
     assert np.all(tess.site_of == -1) and np.all(np.isinf(tess.dist))
     assert tess.report["components_without_sites"] == [0]
+
+
+@pytest.mark.parametrize("spacing", [(1.0, 1.0, 1.0), (0.7, 1.3, 2.1)])
+def test_labyrinth_thin_walls_and_thick_chambers(spacing, oracle_mod):
+    """Thick chambers (clearance shortcut proves most rays) separated by
+    one-voxel walls with pinholes (rays graze walls and thread the holes):
+    exercises the clearance bound, the strict-order rule and the exact
+    fallbacks against the oracle, in dyadic and non-dyadic spacing."""
+    from paper_2208_06970_b200 import Site, VoxelGrid
+
+    dims = (56, 44, 36)
+    nx, ny, nz = dims
+    comp = np.zeros((nz, ny, nx), np.int32)
+    comp[:, :, 18] = -1
+    comp[:, :, 37] = -1
+    comp[:, 20, :] = -1
+    comp[17, :, :] = -1
+    rng = np.random.default_rng(11)
+    for _ in range(40):  # pinholes through the walls
+        z, y = rng.integers(1, nz - 1), rng.integers(1, ny - 1)
+        comp[z, y, rng.choice([18, 37])] = 0
+        comp[rng.integers(1, nz - 1), 20, rng.integers(1, nx - 1)] = 0
+        comp[17, rng.integers(1, ny - 1), rng.integers(1, nx - 1)] = 0
+    comp = comp.reshape(-1)
+    grid = VoxelGrid(dims, spacing, {})
+    labels = _labels(comp, dims)
+    sx, sy, sz = spacing
+    sites = []
+    for _ in range(70):
+        while True:
+            x, y, z = rng.integers(0, nx), rng.integers(0, ny), rng.integers(0, nz)
+            if comp[x + nx * (y + ny * z)] == 0:
+                break
+        sites.append(Site(((x + rng.random()) * sx, (y + rng.random()) * sy, (z + rng.random()) * sz), 0))
+    _check(grid, labels, sites, oracle_mod)
