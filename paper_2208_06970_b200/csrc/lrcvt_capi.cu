@@ -216,9 +216,8 @@ struct lrcvt_plan {
   double* sums = nullptr;
   int* vt_key = nullptr;
   int* vt_key2 = nullptr;
-  int* vt_idx = nullptr;
-  int* vt_idx2 = nullptr;
-  double4* vt_terms = nullptr;
+  unsigned long long* vt_pv = nullptr;   // (phi(v), v) per eligible voxel
+  unsigned long long* vt_pv2 = nullptr;
   int* seg_b = nullptr;
   int* seg_e = nullptr;
   // cub
@@ -601,6 +600,10 @@ int lrcvt_plan_create(lrcvt_plan** plan, int64_t nx, int64_t ny, int64_t nz, dou
     b = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, b, p->list_a, p->list_b, p->list_a, p->list_b, (int)nin, 0, 32, st);
     need = b > need ? b : need;
+    b = 0;  // the ordered vote sorts (site, (phi, v)) pairs: 8-byte values
+    cub::DeviceRadixSort::SortPairs(nullptr, b, p->list_a, p->list_b, (unsigned long long*)nullptr,
+                                    (unsigned long long*)nullptr, (int)nin, 0, 32, st);
+    need = b > need ? b : need;
   }
   p->cub_bytes = need;
   p->n_classes = 1;
@@ -635,7 +638,7 @@ int lrcvt_plan_destroy(lrcvt_plan* p) {
   if (p->h_ctl) cudaFreeHost(p->h_ctl);
   void* bufs[] = {p->counters, p->ctl, p->d_handles, p->d_nel, p->list_a, p->list_b, p->eligible, p->imp, p->bm, p->nbm, p->site1, p->has_site,
                   p->site_pos, p->new_pos, p->sk_key, p->sk_key2, p->sk_val, p->sk_val2, p->sk_d,
-                  p->acc, p->sums, p->vt_key, p->vt_key2, p->vt_idx, p->vt_idx2, p->vt_terms,
+                  p->acc, p->sums, p->vt_key, p->vt_key2, p->vt_pv, p->vt_pv2,
                   p->seg_b, p->seg_e, p->cub_tmp};
   for (void* b : bufs)
     if (b) cudaFree(b);
@@ -819,28 +822,26 @@ int lrcvt_centroidal_update(lrcvt_plan* p, int64_t n_sites, const double* d_site
     if (!p->vt_key) {
       rc |= dalloc(&p->vt_key, nin);
       rc |= dalloc(&p->vt_key2, nin);
-      rc |= dalloc(&p->vt_idx, nin);
-      rc |= dalloc(&p->vt_idx2, nin);
-      rc |= dalloc(&p->vt_terms, nin);
+      rc |= dalloc(&p->vt_pv, nin);
+      rc |= dalloc(&p->vt_pv2, nin);
       if (rc) return LRCVT_E_NOMEM;
     }
     CK(cudaMemsetAsync(p->seg_b, 0, sizeof(int) * S, st));
     CK(cudaMemsetAsync(p->seg_e, 0, sizeof(int) * S, st));
     if (n_el > 0) {
-      k_vote_terms<<<grid_for(n_el, 256, 148 * 8), 256, 0, st>>>(
-          p->eligible, n_el, g, ss, (const double*)d_weights, (const float*)d_weights, weight_mode, S,
-          p->vt_key, p->vt_idx, p->vt_terms);
-      CKL("k_vote_terms"); LAUNCHED(1);
+      k_vote_pairs<<<grid_for(n_el, 256, 148 * 8), 256, 0, st>>>(p->eligible, n_el, ss, S, p->vt_key, p->vt_pv);
+      CKL("k_vote_pairs"); LAUNCHED(1);
       int bits = 1;
       while ((1ll << bits) <= S) bits++;
       size_t bytes = p->cub_bytes;
-      CK(cub::DeviceRadixSort::SortPairs(p->cub_tmp, bytes, p->vt_key, p->vt_key2, p->vt_idx, p->vt_idx2,
+      CK(cub::DeviceRadixSort::SortPairs(p->cub_tmp, bytes, p->vt_key, p->vt_key2, p->vt_pv, p->vt_pv2,
                                          n_el, 0, bits, st));
       k_segments<<<grid_for(n_el, 256, 148 * 8), 256, 0, st>>>(p->vt_key2, n_el, S, p->seg_b, p->seg_e);
       CKL("k_segments"); LAUNCHED(1);
     }
-    k_vote_warp<4><<<grid_for(S, 4), 128, 0, st>>>(p->vt_idx2, p->vt_terms, p->seg_b, p->seg_e, S, p->sums);
-    CKL("k_vote_warp"); LAUNCHED(1);
+    k_vote_sum<4><<<grid_for(S, 4), 128, 0, st>>>(p->vt_pv2, p->seg_b, p->seg_e, S, g, (const double*)d_weights,
+                                                   (const float*)d_weights, weight_mode, p->sums);
+    CKL("k_vote_sum"); LAUNCHED(1);
   }
   CK(cudaMemsetAsync(p->counters + C_BAD, 0, sizeof(int), st));
   k_move_sites<<<grid_for(S, 128), 128, 0, st>>>(g, p->comp, p->site_pos, d_site_comp, p->sums, S, backoff,

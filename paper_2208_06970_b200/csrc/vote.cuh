@@ -11,9 +11,10 @@
 //     the sequential fp64 sum equals the exact integer sum. Kernels reduce
 //     (2x+1) integers with warp match/reduce + 64-bit integer atomics and
 //     scale once: order-independent AND identical to the reference.
-//   * ORDERED path (any f64 weights): terms RN(w*a) are formed in parallel,
-//     a stable radix sort groups them by site in voxel order, and one thread
-//     per site adds them in exactly the reference order.
+//   * ORDERED path (any weights): a stable radix sort groups (phi(v), v)
+//     pairs by site in voxel order; one warp per site forms the terms
+//     (w, RN(w*ax), RN(w*ay), RN(w*az)) 32 at a time and four lanes add them
+//     in exactly the reference order.
 #pragma once
 #include "common.cuh"
 
@@ -77,33 +78,79 @@ __global__ void k_vote_exact_finish(const unsigned long long* __restrict__ acc, 
   sums[3 * n_sites + s] = __dmul_rn((double)acc[3 * n_sites + s], hz);
 }
 
-// ORDERED path, step 1: per eligible voxel (list sorted by voxel), the key
-// (site, or n_sites for unassigned) and the four products w, RN(w*ax), ...
-__global__ void __launch_bounds__(256) k_vote_terms(const int* __restrict__ list, int n, Geo g,
-                                                    const int2* __restrict__ ss,
-                                                    const double* __restrict__ w64,
-                                                    const float* __restrict__ w32, int w_mode,
-                                                    int n_sites, int* __restrict__ key,
-                                                    int* __restrict__ idx,
-                                                    double4* __restrict__ terms) {
+// ordered path, step 1 without a term array: key = site (n_sites when
+// unassigned) and the (phi(v), v) pair; the terms are formed again inside
+// the summing warps from the voxel's weight and its LOS ancestor's centre
+__global__ void __launch_bounds__(256) k_vote_pairs(const int* __restrict__ list, int n,
+                                                    const int2* __restrict__ ss, int n_sites,
+                                                    int* __restrict__ key, unsigned long long* __restrict__ pv) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
     const int v = list[i];
     const int2 a = ss[v];
-    idx[i] = (int)i;
-    if (a.x < 0) { key[i] = n_sites; continue; }
+    if (a.x < 0) {
+      key[i] = n_sites;
+      pv[i] = 0ull;
+      continue;
+    }
     key[i] = a.x;
     const int u = phi_chase(ss, v, a);
-    int x, y, z;
-    coords(g, u, x, y, z);
-    double w;
-    if (w_mode == 0) w = 1.0;
-    else if (w_mode == 1) w = w64[v];
-    else if (w_mode == 2) w = (double)w32[v];                            // m**1.0
-    else { const double m = (double)w32[v]; w = __dmul_rn(m, m); }     // m**2.0
-    terms[i] = make_double4(w, __dmul_rn(w, centre1(x, g.sx)), __dmul_rn(w, centre1(y, g.sy)),
-                            __dmul_rn(w, centre1(z, g.sz)));
+    pv[i] = ((unsigned long long)(unsigned)u << 32) | (unsigned)v;
   }
+}
+
+// the term of voxel v with LOS ancestor u: (w, RN(w*ax), RN(w*ay), RN(w*az)) (_kernels.py:520-531)
+__device__ __forceinline__ double4 vote_term(const Geo& g, unsigned long long p, const double* __restrict__ w64,
+                                             const float* __restrict__ w32, int w_mode) {
+  const int v = (int)(unsigned)(p & 0xffffffffull), u = (int)(unsigned)(p >> 32);
+  int x, y, z;
+  coords(g, u, x, y, z);
+  double w;
+  if (w_mode == 0) w = 1.0;
+  else if (w_mode == 1) w = __ldg(w64 + v);
+  else if (w_mode == 2) w = (double)__ldg(w32 + v);                          // m**1.0
+  else { const double m = (double)__ldg(w32 + v); w = __dmul_rn(m, m); }   // m**2.0
+  return make_double4(w, __dmul_rn(w, centre1(x, g.sx)), __dmul_rn(w, centre1(y, g.sy)),
+                      __dmul_rn(w, centre1(z, g.sz)));
+}
+
+// ordered path, step 3: one warp per site; lanes form 32 terms at a time
+// (DEPTH batches ahead), lanes 0-3 add them in voxel order (x, y, z, w chains)
+template <int WARPS>
+__global__ void __launch_bounds__(WARPS * 32) k_vote_sum(const unsigned long long* __restrict__ pv,
+                                                         const int* __restrict__ seg_begin,
+                                                         const int* __restrict__ seg_end, int n_sites, Geo g,
+                                                         const double* __restrict__ w64,
+                                                         const float* __restrict__ w32, int w_mode,
+                                                         double* __restrict__ sums) {
+  constexpr int DEPTH = 4;
+  __shared__ double buf[WARPS][32][4];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int s = blockIdx.x * WARPS + wid;
+  if (s >= n_sites) return;
+  const int b = seg_begin[s], e = seg_end[s];
+  double acc = 0.0;
+  unsigned long long q[DEPTH];
+#pragma unroll
+  for (int k = 0; k < DEPTH; k++) {
+    const int j = b + 32 * k + lane;
+    q[k] = j < e ? pv[j] : 0ull;
+  }
+  for (int j0 = b; j0 < e; j0 += 32) {
+    const double4 t = j0 + lane < e ? vote_term(g, q[0], w64, w32, w_mode) : make_double4(0, 0, 0, 0);
+    buf[wid][lane][0] = t.x; buf[wid][lane][1] = t.y; buf[wid][lane][2] = t.z; buf[wid][lane][3] = t.w;
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < DEPTH - 1; k++) q[k] = q[k + 1];
+    const int jn = j0 + 32 * DEPTH + lane;
+    q[DEPTH - 1] = jn < e ? pv[jn] : 0ull;
+    const int cnt = min(32, e - j0);
+    if (lane < 4) {
+      for (int k = 0; k < cnt; k++) acc = __dadd_rn(acc, buf[wid][k][lane]);
+    }
+    __syncwarp();
+  }
+  if (lane < 4) sums[lane * n_sites + s] = acc;
 }
 
 // step 2 (after the stable sort by key): segment starts/ends per site.
@@ -116,49 +163,6 @@ __global__ void k_segments(const int* __restrict__ skey, int n, int n_sites,
     if (i == 0 || skey[i - 1] != k) seg_begin[k] = (int)i;
     if (i == n - 1 || skey[i + 1] != k) seg_end[k] = (int)i + 1;
   }
-}
-
-// step 3: one warp per site. Lanes gather 32 consecutive terms of the
-// site's segment (coalesced: sorted indices are increasing) into shared
-// memory; lanes 0-3 then each run one of the four sequential fp64 chains
-// (w, tx, ty, tz) over them in increasing voxel order -- the reference's
-// exact accumulation order. The next chunk's gather is issued before the
-// adds so its latency overlaps the serial chain.
-template <int WARPS>
-__global__ void __launch_bounds__(WARPS * 32) k_vote_warp(const int* __restrict__ sidx,
-                                                         const double4* __restrict__ terms,
-                                                         const int* __restrict__ seg_begin,
-                                                         const int* __restrict__ seg_end,
-                                                         int n_sites, double* __restrict__ sums) {
-  // terms are staged 32 at a time through shared memory; DEPTH batches are
-  // loaded ahead so the four serial chains (x, y, z, w) never wait on memory
-  constexpr int DEPTH = 4;
-  __shared__ double buf[WARPS][32][4];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int s = blockIdx.x * WARPS + wid;
-  if (s >= n_sites) return;
-  const int b = seg_begin[s], e = seg_end[s];
-  double acc = 0.0;
-  double4 t[DEPTH];
-#pragma unroll
-  for (int q = 0; q < DEPTH; q++) {
-    const int j = b + 32 * q + lane;
-    t[q] = j < e ? terms[sidx[j]] : make_double4(0, 0, 0, 0);
-  }
-  for (int j0 = b; j0 < e; j0 += 32) {
-    buf[wid][lane][0] = t[0].x; buf[wid][lane][1] = t[0].y; buf[wid][lane][2] = t[0].z; buf[wid][lane][3] = t[0].w;
-    __syncwarp();
-#pragma unroll
-    for (int q = 0; q < DEPTH - 1; q++) t[q] = t[q + 1];
-    const int jn = j0 + 32 * DEPTH + lane;
-    t[DEPTH - 1] = jn < e ? terms[sidx[jn]] : make_double4(0, 0, 0, 0);
-    const int cnt = min(32, e - j0);
-    if (lane < 4) {
-      for (int q = 0; q < cnt; q++) acc = __dadd_rn(acc, buf[wid][q][lane]);
-    }
-    __syncwarp();
-  }
-  if (lane < 4) sums[lane * n_sites + s] = acc;
 }
 
 // _kernels.py:535-582, one thread per site. counters[0] += empty regions.
