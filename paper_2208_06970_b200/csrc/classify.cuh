@@ -340,12 +340,17 @@ __global__ void __launch_bounds__(128) k_commit(const Prop* __restrict__ imp,
     if (active) {
       const Prop p = imp[i];
       v = p.v;
-      // explicit global stores (the pointers come from RoundCtl). Phase 1
-      // keeps only the compact LOS site; ss is rebuilt from it once when
-      // phase 2 starts (k_site1_to_ss), saving a scattered 8-byte store here.
-      if (site1) __stcg(site1 + v, p.src == p.v ? p.s : (int)LRCVT_NONE);
-      else __stcg(ss + v, make_int2(p.s, p.src));
-      __stcg(dist + v, p.d);
+      // explicit global stores (the pointers come from RoundCtl); ss and dist
+      // are rebuilt from site1 once when phase 2 starts (k_site1_to_state),
+      // saving two scattered 8-byte stores per phase-1 commit.
+      // Phase 1 keeps only the compact LOS site: its distance is a pure
+      // function of (voxel, site) and is recomputed where needed.
+      if (site1) {
+        __stcg(site1 + v, p.src == p.v ? p.s : (int)LRCVT_NONE);
+      } else {
+        __stcg(ss + v, make_int2(p.s, p.src));
+        __stcg(dist + v, p.d);
+      }
     }
     mark_and_append(g, nbm, active, v, false, bm, next, counters + C_NNEXT, zlo, zhi);
   }
@@ -387,12 +392,19 @@ __global__ void k_phase1_start(RoundCtl* ctl, int* counters, int* first, int* se
 }
 
 // phase 2 starts from a copy of the eligible list (tessellation.py:166-167)
-// phase-1 states are LOS (src == v): (site_of, src) from the compact array
-__global__ void k_site1_to_ss(const int* __restrict__ site1, int2* __restrict__ ss, int64_t n) {
+// phase-1 states are LOS (src == v): (site_of, src) and dist = |c_v - p_site|
+// (the very dist3 the phase-1 kernels and the seeds compute) from site1
+__global__ void k_site1_to_state(Geo g, const int* __restrict__ site1, const double4* __restrict__ site_pos,
+                                 int2* __restrict__ ss, double* __restrict__ dist) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < g.n; i += stride) {
     const int s = __ldcs(site1 + i);
-    __stcs(ss + i, make_int2(s, s >= 0 ? (int)i : (int)LRCVT_NONE));
+    if (s < 0) continue;  // still the fill values (-1, -1) / inf
+    int x, y, z;
+    coords(g, (int)i, x, y, z);
+    const double4 p = ld_d4(site_pos + s);
+    __stcs(ss + i, make_int2(s, (int)i));
+    __stcs(dist + i, dist3(centre1(x, g.sx), centre1(y, g.sy), centre1(z, g.sz), p.x, p.y, p.z));
   }
 }
 

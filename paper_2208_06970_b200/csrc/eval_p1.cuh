@@ -96,8 +96,14 @@ __device__ __forceinline__ void p1_tile(const int* __restrict__ list, int n, con
         ovf = true;
       }
     }
-    best_d = __ldg(dist + v);
-    best_s = __ldg(site1 + v); best_src = v;  // phase-1 states are LOS (src == v)
+    // phase-1 states are LOS (src == v) and their distance is |c_v - p_site|
+    best_s = __ldg(site1 + v); best_src = v;
+    if (best_s >= 0) {
+      const double4 sp = ld_d4(site_pos + best_s);
+      best_d = dist3(px, py, pz, sp.x, sp.y, sp.z);
+    } else {
+      best_d = __longlong_as_double(0x7ff0000000000000LL);
+    }
     orig_d = best_d; orig_s = best_s;
   }
 #pragma unroll

@@ -195,13 +195,20 @@ __global__ void __launch_bounds__(32 * EW_WARPS) k_eval_warp(RoundCtl* __restric
   const double px = centre1(x, g.sx), py = centre1(y, g.sy), pz = centre1(z, g.sz);
   const unsigned nbv = __ldg(nbm + v);
   int2 sv;
+  double orig_d;
   if (PHASE2) {
     sv = __ldg(ss + v);
-  } else {
+    orig_d = __ldg(dist + v);
+  } else {  // phase 1: LOS state, distance |c_v - p_site| recomputed
     const int s1 = __ldg(site1 + v);
     sv = make_int2(s1, s1 >= 0 ? v : -1);
+    if (s1 >= 0) {
+      const double4 sp = ld_d4(site_pos + s1);
+      orig_d = dist3(px, py, pz, sp.x, sp.y, sp.z);
+    } else {
+      orig_d = __longlong_as_double(0x7ff0000000000000LL);
+    }
   }
-  const double orig_d = __ldg(dist + v);
   const int orig_s = sv.x, orig_src = sv.y;
   if (lane == 0) bm[v >> 5] = 0u;  // consume this round's frontier word
   double ed[2] = {0.0, 0.0};

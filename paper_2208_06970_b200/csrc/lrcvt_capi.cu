@@ -200,6 +200,7 @@ struct lrcvt_plan {
   uint32_t* nbm = nullptr;  // static same-component neighbour masks
   int* site1 = nullptr;     // phase-1 LOS site per voxel (RoundCtl::site1)
   int2* mg_ss = nullptr;    // (site_of, src) buffer of the multi-GPU classify in flight
+  double* mg_dist = nullptr;
   int* counters = nullptr;
   int* h_counters = nullptr;  // pinned
   uint8_t* has_site = nullptr;
@@ -734,8 +735,8 @@ int lrcvt_classify(lrcvt_plan* p, int64_t n_sites, const double* d_site_pos,
   if (prepare_eligible(p, S, d_site_comp, st)) return LRCVT_E_CUDA;
   p->eligible_valid = true;
   p->eligible_sites = S;
-  k_site1_to_ss<<<grid_for(g.n, 256, 148 * 16), 256, 0, st>>>(p->site1, ss, g.n);
-  CKL("k_site1_to_ss"); LAUNCHED(1);
+  k_site1_to_state<<<grid_for(g.n, 256, 148 * 16), 256, 0, st>>>(g, p->site1, p->site_pos, ss, d_dist);
+  CKL("k_site1_to_state"); LAUNCHED(1);
   k_phase2_copy<<<148 * 4, 256, 0, st>>>(p->eligible, p->d_nel, p->ctl);
   CKL("k_phase2_copy"); LAUNCHED(1);
   const int var2 = g.dyadic ? 1 : 2;
@@ -1142,6 +1143,7 @@ int lrcvt_mg_begin(lrcvt_plan* p, int64_t n_sites, const double* d_site_pos, con
   const int S = (int)n_sites;
   int2* ss = reinterpret_cast<int2*>(d_site_src);
   p->mg_ss = ss;
+  p->mg_dist = d_dist;
   k_fill_state<<<grid_for(g.n, 256, 148 * 32), 256, 0, st>>>(ss, d_dist, p->site1, g.n);
   CKL("k_fill_state");
   CK(cudaMemsetAsync(p->counters, 0, sizeof(int) * C_NCOUNTERS, st));
@@ -1175,8 +1177,9 @@ int lrcvt_mg_phase2(lrcvt_plan* p, int64_t n_sites, const int32_t* d_site_comp, 
   if (!p || !d_site_comp || !n_frontier) return set_error(LRCVT_E_ARG, "lrcvt_mg_phase2");
   cudaStream_t st = (cudaStream_t)stream;
   if (prepare_eligible(p, (int)n_sites, d_site_comp, st)) return LRCVT_E_CUDA;
-  k_site1_to_ss<<<grid_for(p->g.n, 256, 148 * 16), 256, 0, st>>>(p->site1, p->mg_ss, p->g.n);
-  CKL("k_site1_to_ss");
+  k_site1_to_state<<<grid_for(p->g.n, 256, 148 * 16), 256, 0, st>>>(p->g, p->site1, p->site_pos, p->mg_ss,
+                                                                     p->mg_dist);
+  CKL("k_site1_to_state");
   k_phase2_copy<<<148 * 4, 256, 0, st>>>(p->eligible, p->d_nel, p->ctl);
   CKL("k_phase2_copy");
   CK(cudaMemcpyAsync(p->h_counters + 7, p->d_nel, sizeof(int), cudaMemcpyDeviceToHost, st));
