@@ -128,51 +128,6 @@ __global__ void k_mark_site_comps(const int* __restrict__ site_comp, int n_sites
   if (s < n_sites) has_site[site_comp[s]] = 1;
 }
 
-// Ordered compaction of eligible voxels (in-band, component has a site),
-// tessellation.py:163-164. Each block owns a contiguous range; within it
-// order is preserved, block ranges are placed by a decoupled counter, so the
-// list is a permutation of sorted chunks (order never affects results).
-template <int BLOCK, int PER_THREAD>
-__global__ void k_eligible(const int* __restrict__ comp, const uint8_t* __restrict__ has_site,
-                           int64_t n, int* __restrict__ out, int* __restrict__ counter) {
-  __shared__ int warp_tot[BLOCK / 32];
-  __shared__ int base_s;
-  const int64_t chunk0 = (int64_t)blockIdx.x * BLOCK * PER_THREAD;
-  // thread t owns voxels chunk0 + t*PER_THREAD .. +PER_THREAD-1
-  int64_t v0 = chunk0 + (int64_t)threadIdx.x * PER_THREAD;
-  unsigned flags = 0;
-#pragma unroll
-  for (int j = 0; j < PER_THREAD; j++) {
-    int64_t v = v0 + j;
-    if (v < n) {
-      int c = comp[v];
-      if (c >= 0 && has_site[c]) flags |= 1u << j;
-    }
-  }
-  int cnt = __popc(flags);
-  int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  int incl = cnt;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    int t = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += t;
-  }
-  if (lane == 31) warp_tot[wid] = incl;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int acc = 0;
-    for (int w = 0; w < BLOCK / 32; w++) { int t = warp_tot[w]; warp_tot[w] = acc; acc += t; }
-    base_s = acc ? atomicAdd(counter, acc) : 0;
-  }
-  __syncthreads();
-  int pos = base_s + warp_tot[wid] + incl - cnt;
-  while (flags) {
-    int j = __ffs(flags) - 1;
-    flags &= flags - 1;
-    out[pos++] = (int)(v0 + j);
-  }
-}
-
 // Mark same-component neighbours of v (and v itself when `self`) in the
 // frontier bitmap; newly set bits are appended to `next`. Reproduces the
 // stamp-deduplicated enqueue of _kernels.py:313-333 (self=false) and
