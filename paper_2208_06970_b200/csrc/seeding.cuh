@@ -141,15 +141,6 @@ __global__ void k_seed_weights(const int* __restrict__ list, int64_t n, SeedWeig
     out[i] = w(list[i]);
 }
 
-// one thread per (component, block) run: mass = 0.0 + pw(run)
-__global__ void k_seed_run_mass(const double* __restrict__ w_sorted, const int64_t* __restrict__ start,
-                                const int64_t* __restrict__ len, int64_t n_runs,
-                                double* __restrict__ mass) {
-  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (r >= n_runs) return;
-  mass[r] = __dadd_rn(0.0, pw_sum(SeqDirect{w_sorted}, start[r], len[r]));
-}
-
 // One warp per run: lane 0 lists the run's pairwise leaves (<= 128 elements)
 // in depth-first order, the lanes sum the leaves in parallel (pw_leaf), and
 // lane 0 rebuilds the same tree over the leaf sums -- the identical
