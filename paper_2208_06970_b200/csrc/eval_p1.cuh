@@ -13,21 +13,23 @@ namespace lrcvt {
 constexpr int P1_TAB = 4;  // distinct-site distance table
 
 // Phase-1 evaluation (LOS candidates only):
-//   A  gather the 26 neighbours' candidate sites (immediate offsets, all
-//      loads in flight together) into a per-thread shared-memory row;
+//   A  gather the 26 neighbours' LOS sites from the compact site1 array
+//      (immediate offsets, all loads in flight) into a per-thread
+//      shared-memory row;
 //   B  compute the distance to each distinct neighbour site once;
-//   C  SPECULATIVE fold in OFFSETS order over the row with table lookups
-//      only, assuming every ray it needs is clear (96% are); each assumed
-//      ray (voxel, site) goes into a block-wide shared-memory queue together
-//      with the fold state before it;
-//   D  the whole block traces the queued rays, one per thread;
-//   E  each lane replays its rays' outcomes in order: if all were clear the
-//      speculative fold IS the reference's fold; at the first blocked ray the
-//      lane rewinds to the state before it, records failed_site and finishes
-//      the fold non-speculatively (rays traced inline; rare).
+//   C  strict-order rule: when no two distinct elements of
+//      {current state} + table are within the EPS tie band, the reference's
+//      fold ends at the minimum-distance element whose ray is clear, so only
+//      the winner's ray is needed: proven clear by the voxel's clearance, or
+//      queued per warp and D traced by the warp one ray per lane;
+//   E  a blocked winner, a near-tie or a table overflow takes the exact
+//      sequential fold in OFFSETS order with rays traced inline (rare once
+//      sites have left voxel centres).
 // Ray outcomes are pure functions of (voxel, site), so the decision sequence
-// is exactly the reference's in every case.
-constexpr int P1_SPEC = 3;  // speculated rays per lane
+// is exactly the reference's in every case. (A speculative fold that queued
+// up to three rays per lane preceded the strict rule; with the rule in place
+// it only cost registers and spills and was removed: p1 -7% at 512^3.)
+constexpr int P1_SPEC = 1;  // queued rays per lane (the strict winner's)
 constexpr int P1_MIN_BLOCKS = 5;  // caps registers at 102: +25% occupancy, few spills (measured best)
 
 template <int BLOCK>
@@ -163,38 +165,9 @@ __device__ __forceinline__ void p1_tile(const int* __restrict__ list, int n, con
       qv[win_slot] = v; qs[win_slot] = win_s;
     }
   }
-  // ---- C: speculative fold (lanes without a strict order)
+  // lanes without a strict order (near-ties: rare once sites have moved off
+  // voxel centres) take the exact fold below with rays traced inline
   int failed = -1;
-  int nspec = 0, kstop = 26;
-  int sp_slot[P1_SPEC], sp_k[P1_SPEC], sp_s[P1_SPEC], sp_src[P1_SPEC];
-  double sp_d[P1_SPEC];
-#pragma unroll
-  for (int q = 0; q < P1_SPEC; q++) { sp_slot[q] = 0; sp_k[q] = 0; sp_s[q] = 0; sp_src[q] = 0; sp_d[q] = 0; }
-  if (active && !strict) {
-    for (int k = 0; k < 26; k++) {
-      const int s = row[k * BLOCK];
-      if (s < 0) continue;
-      double d;
-      if (s == ts[0]) d = td[0];
-      else if (s == ts[1]) d = td[1];
-      else if (s == ts[2]) d = td[2];
-      else if (s == ts[3]) d = td[3];
-      else {  // more than P1_TAB distinct sites around v (rare)
-        const double4 sp = ld_d4(site_pos + s);
-        d = dist3(px, py, pz, sp.x, sp.y, sp.z);
-      }
-      if (beats(d, s, best_d, best_s) && s != failed) {
-        if (nspec == P1_SPEC) { kstop = k; break; }  // window full: finish after replay
-        const int slot = atomicAdd(&q_n[wid], 1);
-        qv[slot] = v; qs[slot] = s;
-#pragma unroll
-        for (int q = 0; q < P1_SPEC; q++)
-          if (q == nspec) { sp_slot[q] = slot; sp_k[q] = k; sp_s[q] = best_s; sp_src[q] = best_src; sp_d[q] = best_d; }
-        nspec++;
-        best_d = d; best_s = s; best_src = v;  // assume clear
-      }
-    }
-  }
   __syncwarp();
   // ---- D: the warp traces its queued rays, one per lane
   const int nq = q_n[wid];
@@ -209,9 +182,8 @@ __device__ __forceinline__ void p1_tile(const int* __restrict__ list, int n, con
                  ? 1 : 0;
   }
   __syncwarp();
-  // ---- E: strict lanes take their winner (or fall back); the others replay
-  // their speculated outcomes and rewind at the first blocked ray
-  int kres = 26;  // resume point of the non-speculative tail
+  // ---- E: strict lanes take their winner (or fall back to the exact fold)
+  int kres = 26;  // start of the exact sequential fold (26: not needed)
   if (active && strict) {
     if (jwin >= 0 && (win_slot < 0 || qok[win_slot])) {
       best_d = win_d; best_s = win_s; best_src = v;
@@ -219,15 +191,7 @@ __device__ __forceinline__ void p1_tile(const int* __restrict__ list, int n, con
       kres = 0;  // winner blocked: exact fold from the start (best = current state)
     }
   } else if (active) {
-#pragma unroll
-    for (int q = 0; q < P1_SPEC; q++) {
-      if (q < nspec && kres == 26 && !qok[sp_slot[q]]) {
-        best_d = sp_d[q]; best_s = sp_s[q]; best_src = sp_src[q];
-        failed = row[sp_k[q] * BLOCK];
-        kres = sp_k[q] + 1;
-      }
-    }
-    if (kres == 26 && kstop < 26) kres = kstop;  // window overflow, all clear
+    kres = 0;
   }
   if (active) {
     for (int k = kres; k < 26; k++) {
