@@ -99,23 +99,28 @@ __global__ void __launch_bounds__(256) k_vote_pairs(const int* __restrict__ list
   }
 }
 
-// the term of voxel v with LOS ancestor u: (w, RN(w*ax), RN(w*ay), RN(w*az)) (_kernels.py:520-531)
-__device__ __forceinline__ double4 vote_term(const Geo& g, unsigned long long p, const double* __restrict__ w64,
-                                             const float* __restrict__ w32, int w_mode) {
-  const int v = (int)(unsigned)(p & 0xffffffffull), u = (int)(unsigned)(p >> 32);
+// weight m_v**gamma of voxel v (seeding.py:68 for the modes the device forms)
+__device__ __forceinline__ double vote_weight(int v, const double* __restrict__ w64, const float* __restrict__ w32,
+                                              int w_mode) {
+  if (w_mode == 0) return 1.0;
+  if (w_mode == 1) return __ldg(w64 + v);
+  const double m = (double)__ldg(w32 + v);
+  return w_mode == 2 ? m : __dmul_rn(m, m);  // m**1.0 / m**2.0
+}
+
+// the term of voxel v (weight w) with LOS ancestor u: (w, RN(w*ax), RN(w*ay),
+// RN(w*az)) (_kernels.py:520-531)
+__device__ __forceinline__ double4 vote_term(const Geo& g, int u, double w) {
   int x, y, z;
   coords(g, u, x, y, z);
-  double w;
-  if (w_mode == 0) w = 1.0;
-  else if (w_mode == 1) w = __ldg(w64 + v);
-  else if (w_mode == 2) w = (double)__ldg(w32 + v);                          // m**1.0
-  else { const double m = (double)__ldg(w32 + v); w = __dmul_rn(m, m); }   // m**2.0
   return make_double4(w, __dmul_rn(w, centre1(x, g.sx)), __dmul_rn(w, centre1(y, g.sy)),
                       __dmul_rn(w, centre1(z, g.sz)));
 }
 
-// ordered path, step 3: one warp per site; lanes form 32 terms at a time
-// (DEPTH batches ahead), lanes 0-3 add them in voxel order (x, y, z, w chains)
+// ordered path, step 3: one warp per site. A three-stage software pipeline
+// per lane -- (phi, v) pairs two batches ahead, the weight one batch ahead,
+// the term for the batch being summed -- keeps loads off the critical path;
+// lanes 0-3 add the staged terms in voxel order (x, y, z, w chains).
 template <int WARPS>
 __global__ void __launch_bounds__(WARPS * 32) k_vote_sum(const unsigned long long* __restrict__ pv,
                                                          const int* __restrict__ seg_begin,
@@ -123,32 +128,28 @@ __global__ void __launch_bounds__(WARPS * 32) k_vote_sum(const unsigned long lon
                                                          const double* __restrict__ w64,
                                                          const float* __restrict__ w32, int w_mode,
                                                          double* __restrict__ sums) {
-  constexpr int DEPTH = 4;
   __shared__ double buf[WARPS][32][4];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int s = blockIdx.x * WARPS + wid;
   if (s >= n_sites) return;
   const int b = seg_begin[s], e = seg_end[s];
   double acc = 0.0;
-  unsigned long long q[DEPTH];
-#pragma unroll
-  for (int k = 0; k < DEPTH; k++) {
-    const int j = b + 32 * k + lane;
-    q[k] = j < e ? pv[j] : 0ull;
-  }
+  auto pair_at = [&](int j) { return j < e ? pv[j] : 0ull; };
+  unsigned long long q1 = pair_at(b + lane), q2 = pair_at(b + 32 + lane);  // batches j0, j0 + 32
+  double w1 = b + lane < e ? vote_weight((int)(unsigned)(q1 & 0xffffffffull), w64, w32, w_mode) : 0.0;
   for (int j0 = b; j0 < e; j0 += 32) {
-    const double4 t = j0 + lane < e ? vote_term(g, q[0], w64, w32, w_mode) : make_double4(0, 0, 0, 0);
+    const double4 t = j0 + lane < e ? vote_term(g, (int)(unsigned)(q1 >> 32), w1) : make_double4(0, 0, 0, 0);
+    // advance the pipeline before the serial adds so its loads overlap them
+    const unsigned long long q3 = pair_at(j0 + 64 + lane);
+    const double w2 = j0 + 32 + lane < e ? vote_weight((int)(unsigned)(q2 & 0xffffffffull), w64, w32, w_mode) : 0.0;
     buf[wid][lane][0] = t.x; buf[wid][lane][1] = t.y; buf[wid][lane][2] = t.z; buf[wid][lane][3] = t.w;
     __syncwarp();
-#pragma unroll
-    for (int k = 0; k < DEPTH - 1; k++) q[k] = q[k + 1];
-    const int jn = j0 + 32 * DEPTH + lane;
-    q[DEPTH - 1] = jn < e ? pv[jn] : 0ull;
     const int cnt = min(32, e - j0);
     if (lane < 4) {
       for (int k = 0; k < cnt; k++) acc = __dadd_rn(acc, buf[wid][k][lane]);
     }
     __syncwarp();
+    q1 = q2; q2 = q3; w1 = w2;
   }
   if (lane < 4) sums[lane * n_sites + s] = acc;
 }
