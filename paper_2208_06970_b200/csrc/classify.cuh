@@ -41,7 +41,7 @@ struct RoundCtl {
   int n_cur;         // items in cur
   int sweep_imp;     // improvements found by the last sweep
   int tile_next;     // dynamic tile scheduler of the eval kernels (reset per round)
-  int pad_;
+  int loop_min;      // the round graph loops while n_cur > loop_min (small frontiers: k_rounds_small)
   long long rounds, evals, commits, rounds_p1;
 };
 
@@ -134,11 +134,14 @@ __global__ void k_mark_site_comps(const int* __restrict__ site_comp, int n_sites
 // _kernels.py:425-454 (self=true). All 32 lanes must call it.
 // Three unrolled stages keep every load/atomic of a stage independent (26
 // requests in flight per thread instead of 26 dependent round trips).
+template <bool COH = false>
 __device__ __forceinline__ void mark_and_append(const Geo& g, const uint32_t* __restrict__ nbm,
                                                 bool active, int v, bool self,
                                                 uint32_t* __restrict__ bm,
                                                 int* __restrict__ next, int* counter,
                                                 int zlo = 0, int zhi = 1 << 30) {
+  // COH: inside the persistent small-round kernel the precheck must not see a
+  // stale L1 copy of a word cleared since (it would skip a needed enqueue)
   // The 27-cube around v is 9 x-rows of 3 voxels (dx = -1, 0, +1); a row's
   // three bits sit in one bitmap word (two when they straddle a word), so
   // each row costs one cached precheck load and at most one atomicOr with a
@@ -181,14 +184,14 @@ __device__ __forceinline__ void mark_and_append(const Geo& g, const uint32_t* __
       const unsigned hi = sh > 29 ? (wv >> (32 - sh)) : 0u;   // spill into w0 + 1
       unsigned got = 0;  // newly set by this thread, in `wv` coordinates
       if (lo) {
-        const uint32_t cur = __ldca(bm + w0);
+        const uint32_t cur = COH ? __ldcg(bm + w0) : __ldca(bm + w0);
         if ((cur & lo) != lo) {
           const uint32_t old = atomicOr(bm + w0, lo);
           got |= ((~old) & lo) >> sh;
         }
       }
       if (hi) {
-        const uint32_t cur = __ldca(bm + w0 + 1);
+        const uint32_t cur = COH ? __ldcg(bm + w0 + 1) : __ldca(bm + w0 + 1);
         if ((cur & hi) != hi) {
           const uint32_t old = atomicOr(bm + w0 + 1, hi);
           got |= ((~old) & hi) << (32 - sh);
@@ -271,7 +274,7 @@ __device__ __forceinline__ void round_end(RoundCtl* ctl, int* counters, const cu
   counters[C_NNEXT] = 0;
   if (in_graph) {
     set_size_class(n_next, hs, n_classes);
-    cudaGraphSetConditional(loop, n_next > 0 ? 1u : 0u);
+    cudaGraphSetConditional(loop, n_next > ctl->loop_min ? 1u : 0u);
   }
 }
 
@@ -326,7 +329,7 @@ __global__ void __launch_bounds__(128) k_commit(const Prop* __restrict__ imp,
 __global__ void k_loop_init(const RoundCtl* ctl, cudaGraphConditionalHandle h,
                             const cudaGraphConditionalHandle* hs, int n_classes) {
   set_size_class(ctl->n_cur, hs, n_classes);
-  cudaGraphSetConditional(h, ctl->n_cur > 0 ? 1u : 0u);
+  cudaGraphSetConditional(h, ctl->n_cur > ctl->loop_min ? 1u : 0u);
 }
 
 // phase 1 starts from the seed worklist appended to `first` by k_seed_groups

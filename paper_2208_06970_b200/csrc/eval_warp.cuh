@@ -171,24 +171,30 @@ __device__ __forceinline__ void ew_exact(const double (*ed)[2], const int (*es)[
 }
 
 // PHASE2 = false: LOS candidates only (phase 1); true: path + LOS/shortcut.
-template <bool PHASE2>
-__global__ void __launch_bounds__(32 * EW_WARPS) k_eval_warp(RoundCtl* __restrict__ ctl, Geo g,
-                                                             const int* __restrict__ comp,
-                                                             const uint32_t* __restrict__ nbm,
-                                                             const double4* __restrict__ site_pos,
-                                                             uint32_t* __restrict__ bm, Prop* __restrict__ imp,
-                                                             int* __restrict__ counters) {
-  __shared__ double s_d[EW_WARPS][26][2];
-  __shared__ int s_s[EW_WARPS][26][2], s_src[EW_WARPS][26][2], s_t[EW_WARPS][26][2];
-  const int n = ctl->n_cur;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int i = blockIdx.x * EW_WARPS + wid;
-  if (i >= n) return;  // warp-uniform
-  const int* __restrict__ list = ctl->cur;
-  const int2* __restrict__ ss = ctl->ss;
-  const int* __restrict__ site1 = ctl->site1;
-  const double* __restrict__ dist = ctl->dist;
-  const int v = __ldg(list + i);
+// shared staging of one warp's elements for the exact replay
+struct EwStage {
+  double d[26][2];
+  int s[26][2], src[26][2], t[26][2];
+};
+
+// loads of per-round state: read-only cache across launches, L2 (coherent)
+// inside the persistent small-round kernel where earlier rounds' writes by
+// other SMs must be seen
+template <bool COH, typename T>
+__device__ __forceinline__ T ldst(const T* p) {
+  if (COH) return __ldcg(p);
+  return __ldg(p);
+}
+
+// evaluate frontier item i of `list` with the calling warp (all 32 lanes)
+template <bool PHASE2, bool COH>
+__device__ __forceinline__ void ew_voxel(const int* list, const int2* ss, const int* site1, const double* dist,
+                                         const int i, const Geo& g, const int* __restrict__ comp,
+                                         const uint32_t* __restrict__ nbm, const double4* __restrict__ site_pos,
+                                         uint32_t* __restrict__ bm, Prop* __restrict__ imp,
+                                         int* __restrict__ counters, EwStage& st) {
+  const int lane = threadIdx.x & 31;
+  const int v = ldst<COH>(list + i);
   int x, y, z;
   coords(g, v, x, y, z);
   const int cv = __ldg(comp + v);
@@ -197,10 +203,10 @@ __global__ void __launch_bounds__(32 * EW_WARPS) k_eval_warp(RoundCtl* __restric
   int2 sv;
   double orig_d;
   if (PHASE2) {
-    sv = __ldg(ss + v);
-    orig_d = __ldg(dist + v);
+    sv = ldst<COH>(ss + v);
+    orig_d = ldst<COH>(dist + v);
   } else {  // phase 1: LOS state, distance |c_v - p_site| recomputed
-    const int s1 = __ldg(site1 + v);
+    const int s1 = ldst<COH>(site1 + v);
     sv = make_int2(s1, s1 >= 0 ? v : -1);
     if (s1 >= 0) {
       const double4 sp = ld_d4(site_pos + s1);
@@ -219,9 +225,9 @@ __global__ void __launch_bounds__(32 * EW_WARPS) k_eval_warp(RoundCtl* __restric
     // phase 1 keeps only the compact LOS site (src == w implied); phase 2 reads (site, src)
     int2 nw;
     if (PHASE2) {
-      nw = __ldg(ss + w);
+      nw = ldst<COH>(ss + w);
     } else {
-      const int s1 = __ldg(site1 + w);
+      const int s1 = ldst<COH>(site1 + w);
       nw = make_int2(s1, s1 >= 0 ? w : -1);
     }
     if (nw.x >= 0) {
@@ -232,18 +238,18 @@ __global__ void __launch_bounds__(32 * EW_WARPS) k_eval_warp(RoundCtl* __restric
         } else {
           len = dist3(px, py, pz, centre1(x + o.x, g.sx), centre1(y + o.y, g.sy), centre1(z + o.z, g.sz));
         }
-        ed[0] = __dadd_rn(__ldg(dist + w), len); es[0] = nw.x; esrc[0] = w; et[0] = EW_PATH;
+        ed[0] = __dadd_rn(ldst<COH>(dist + w), len); es[0] = nw.x; esrc[0] = w; et[0] = EW_PATH;
       }
       if (nw.y == w) {
         const double4 sp = ld_d4(site_pos + nw.x);
         ed[1] = dist3(px, py, pz, sp.x, sp.y, sp.z); es[1] = nw.x; esrc[1] = v; et[1] = EW_LOS;
       } else if (PHASE2 && nw.y >= 0) {
         const int u = nw.y;
-        const int2 nu = __ldg(ss + u);
+        const int2 nu = ldst<COH>(ss + u);
         if (nu.x >= 0 && __ldg(comp + u) == cv) {
           int ux, uy, uz;
           coords(g, u, ux, uy, uz);
-          ed[1] = __dadd_rn(__ldg(dist + u), dist3(px, py, pz, centre1(ux, g.sx), centre1(uy, g.sy),
+          ed[1] = __dadd_rn(ldst<COH>(dist + u), dist3(px, py, pz, centre1(ux, g.sx), centre1(uy, g.sy),
                                                    centre1(uz, g.sz)));
           es[1] = nu.x; esrc[1] = u; et[1] = EW_SHORT;
         }
@@ -258,16 +264,16 @@ __global__ void __launch_bounds__(32 * EW_WARPS) k_eval_warp(RoundCtl* __restric
     if (lane < 26) {
 #pragma unroll
       for (int e = 0; e < 2; e++) {
-        s_d[wid][lane][e] = ed[e]; s_s[wid][lane][e] = es[e];
-        s_src[wid][lane][e] = esrc[e]; s_t[wid][lane][e] = et[e];
+        st.d[lane][e] = ed[e]; st.s[lane][e] = es[e];
+        st.src[lane][e] = esrc[e]; st.t[lane][e] = et[e];
       }
     }
     __syncwarp();
     if (lane == 0) {
       best_d = orig_d; best_s = orig_s; best_src = orig_src;
-      ew_exact(s_d[wid], s_s[wid], s_src[wid], s_t[wid], g, comp, site_pos, nbv, px, py, pz, cv, best_d, best_s,
-               best_src);
+      ew_exact(st.d, st.s, st.src, st.t, g, comp, site_pos, nbv, px, py, pz, cv, best_d, best_s, best_src);
     }
+    __syncwarp();  // st is reused by this warp's next item
   }
   if (lane == 0) {
     const bool improved = (best_s != orig_s) || (best_d < __dsub_rn(orig_d, LRCVT_EPS));
@@ -277,6 +283,21 @@ __global__ void __launch_bounds__(32 * EW_WARPS) k_eval_warp(RoundCtl* __restric
       imp[atomicAdd(counters + C_NIMP, 1)] = pr;
     }
   }
+}
+
+template <bool PHASE2>
+__global__ void __launch_bounds__(32 * EW_WARPS) k_eval_warp(RoundCtl* __restrict__ ctl, Geo g,
+                                                             const int* __restrict__ comp,
+                                                             const uint32_t* __restrict__ nbm,
+                                                             const double4* __restrict__ site_pos,
+                                                             uint32_t* __restrict__ bm, Prop* __restrict__ imp,
+                                                             int* __restrict__ counters) {
+  __shared__ EwStage stage[EW_WARPS];
+  const int wid = threadIdx.x >> 5;
+  const int i = blockIdx.x * EW_WARPS + wid;
+  if (i >= ctl->n_cur) return;  // warp-uniform
+  ew_voxel<PHASE2, false>(ctl->cur, ctl->ss, ctl->site1, ctl->dist, i, g, comp, nbm, site_pos, bm, imp, counters,
+                          stage[wid]);
 }
 
 }  // namespace lrcvt

@@ -18,6 +18,7 @@
 #include "eval_p1.cuh"
 #include "eval_p2.cuh"
 #include "eval_warp.cuh"
+#include "rounds_small.cuh"
 #include "aggregate.cuh"
 #include "seeding.cuh"
 #include "layout.cuh"
@@ -244,6 +245,9 @@ struct lrcvt_plan {
   bool warp_eval = true;  // warp-per-voxel kernels for small frontiers (LRCVT_WARP_EVAL=0 disables)
   bool warp_eval_all = false;
   int ew_small = EW_SMALL_DEFAULT;
+  bool coop = false;    // small frontiers: all their rounds in one cooperative kernel (default: 2D grids;
+                        // LRCVT_COOP=1/0 forces it on/off)
+  int coop_blocks = 0;  // co-resident CTAs of k_rounds_small
   bool eligible_valid = false;
   int64_t eligible_sites = -1;
   // optional per-launch timing of the dominant kernel (k_eval)
@@ -429,12 +433,43 @@ int build_round_graph(lrcvt_plan* p, int var) {
   return 0;
 }
 
+int launch_rounds_small(lrcvt_plan* p, int var, cudaStream_t st) {
+  RoundCtl* ctl = p->ctl;
+  Geo g = p->g;
+  const int* comp = p->comp;
+  const uint32_t* nbm = p->nbm;
+  const double4* sp = p->site_pos;
+  uint32_t* bm = p->bm;
+  Prop* imp = p->imp;
+  int* counters = p->counters;
+  int small = p->ew_small, max_rounds = 1 << 20;
+  void* args[] = {&ctl, &g, &comp, &nbm, &sp, &bm, &imp, &counters, &small, &max_rounds};
+  void* fn = var == 0 ? (void*)k_rounds_small<false> : (void*)k_rounds_small<true>;
+  CK(cudaLaunchCooperativeKernel(fn, dim3(p->coop_blocks), dim3(32 * EW_WARPS), args, 0, st));
+  LAUNCHED(1);
+  return 0;
+}
+
 int run_rounds(lrcvt_plan* p, int var, cudaStream_t st) {
   if (!p->timing) {
     if (!p->graph[var]) CKR(build_round_graph(p, var));
-    CK(cudaGraphLaunch(p->graph[var], st));
-    LAUNCHED(1);  // k_loop_init; per-round kernels are counted from ctl->rounds
-    return 0;
+    if (!p->coop) {
+      CK(cudaGraphLaunch(p->graph[var], st));
+      LAUNCHED(1);  // k_loop_init; per-round kernels are counted from ctl->rounds
+      return 0;
+    }
+    // small frontiers in the cooperative kernel, large ones in the graph (which
+    // loops while n_cur > loop_min); alternate until the frontier is empty
+    for (int it = 0; it < 1000; ++it) {
+      CKR(launch_rounds_small(p, var, st));
+      CK(cudaGraphLaunch(p->graph[var], st));
+      LAUNCHED(1);
+      CKR(launch_rounds_small(p, var, st));
+      CK(cudaMemcpyAsync(p->h_ctl, p->ctl, sizeof(RoundCtl), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      if (p->h_ctl->n_cur <= 0) return 0;
+    }
+    return set_error(LRCVT_E_CUDA, "run_rounds: no convergence");
   }
   // host-driven rounds with per-launch CUDA-event timing (bench breakdown)
   CK(cudaMemcpyAsync(p->h_ctl, p->ctl, sizeof(RoundCtl), cudaMemcpyDeviceToHost, st));
@@ -520,6 +555,12 @@ int lrcvt_plan_create(lrcvt_plan** plan, int64_t nx, int64_t ny, int64_t nz, dou
     p->warp_eval_all = e[0] == '2';
   }
   if (const char* e = getenv("LRCVT_EW_SMALL")) p->ew_small = atoi(e);
+  // 2D bands run ~100 tiny rounds per classify: there the cooperative
+  // small-round kernel wins (C1 -13%); 3D configs are neutral to -3% and the
+  // extra host check per phase costs the 128^3 headline ~1%, so 3D stays on
+  // the graph unless asked
+  p->coop = nz == 1;
+  if (const char* e = getenv("LRCVT_COOP")) p->coop = e[0] == '1';
   p->g = make_geo(nx, ny, nz, sx, sy, sz);
   p->comp = d_comp;
   p->n_components = n_components;
@@ -625,6 +666,21 @@ int lrcvt_plan_create(lrcvt_plan** plan, int64_t nx, int64_t ny, int64_t nz, dou
     p->eval_blocks[2] = (nb > 0 ? nb : 1) * sms;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_commit, 128, 0);
     p->commit_blocks = (nb > 0 ? nb : 1) * sms;
+    int nb0 = 0, nb1 = 0;  // cooperative kernel: every CTA co-resident
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb0, k_rounds_small<false>, 32 * EW_WARPS, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb1, k_rounds_small<true>, 32 * EW_WARPS, 0);
+    const int nbc = nb0 < nb1 ? nb0 : nb1;
+    p->coop_blocks = sms;  // one CTA per SM: the three grid barriers per round stay cheap (measured best)
+    if (nbc <= 0) p->coop = false;
+    if (const char* e = getenv("LRCVT_COOP_BLOCKS")) {
+      const int want = atoi(e);
+      if (want > 0 && want < p->coop_blocks) p->coop_blocks = want;
+    }
+    int coop_ok = 0;
+    cudaDeviceGetAttribute(&coop_ok, cudaDevAttrCooperativeLaunch, dev);
+    if (!coop_ok || nbc <= 0) p->coop = false;
+    const int loop_min = p->coop ? p->ew_small : 0;
+    cudaMemcpy(&p->ctl->loop_min, &loop_min, sizeof(int), cudaMemcpyHostToDevice);
   }
   if (dalloc((char**)&p->cub_tmp, (int64_t)need)) { lrcvt_plan_destroy(p); return LRCVT_E_NOMEM; }
   *plan = p;

@@ -1,5 +1,5 @@
 """The warp-per-voxel evaluation kernels (eval_warp.cuh) normally serve only
-small frontiers; LRCVT_WARP_EVAL=2 routes EVERY round through them, so the
+small frontiers (and the cooperative small-round kernel, default for 2D); LRCVT_WARP_EVAL=2 routes EVERY round through them, so the
 reference-pinned classify tests (golden cases, fresh volumes vs the oracle,
 20-iteration Lloyd trajectories) exercise their strict-order rule and exact
 fallback on millions of evaluations. LRCVT_WARP_EVAL=0 checks the tile
@@ -16,9 +16,12 @@ pytestmark = pytest.mark.gpu
 ROOT = Path(__file__).resolve().parents[1]
 
 
-@pytest.mark.parametrize("mode", ["2", "0"])
+@pytest.mark.parametrize("mode", ["2", "0", "coop"])
 def test_classify_suite_under_forced_kernel_choice(mode):
-    env = dict(os.environ, LRCVT_WARP_EVAL=mode)
+    """mode "coop": every small frontier of every config goes through the
+    persistent cooperative round kernel (rounds_small.cuh)."""
+    env = dict(os.environ, LRCVT_COOP="1") if mode == "coop" else dict(os.environ, LRCVT_WARP_EVAL=mode,
+                                                                            LRCVT_COOP="0")
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider",
                         str(ROOT / "tests" / "test_gpu_classify.py"), str(ROOT / "tests" / "test_gpu_edges.py"),
                         str(ROOT / "tests" / "test_gpu_blocks.py")],
