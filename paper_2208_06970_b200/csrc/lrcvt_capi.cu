@@ -245,9 +245,9 @@ struct lrcvt_plan {
   bool warp_eval = true;  // warp-per-voxel kernels for small frontiers (LRCVT_WARP_EVAL=0 disables)
   bool warp_eval_all = false;
   int ew_small = EW_SMALL_DEFAULT;
-  bool coop = false;    // small frontiers: all their rounds in one cooperative kernel (default: 2D grids;
-                        // LRCVT_COOP=1/0 forces it on/off)
+  bool coop = false;    // small frontiers: all their rounds in one cooperative kernel
   int coop_blocks = 0;  // co-resident CTAs of k_rounds_small
+  bool coop_in_graph = false;  // k_rounds_small as the class-0 node of the round graph (LRCVT_COOP=2)
   bool eligible_valid = false;
   int64_t eligible_sites = -1;
   // optional per-launch timing of the dominant kernel (k_eval)
@@ -379,6 +379,38 @@ int add_kernel_node(cudaGraphNode_t* node, cudaGraph_t g, const cudaGraphNode_t*
   return 0;
 }
 
+int launch_rounds_small(lrcvt_plan* p, int var, cudaStream_t st, const cudaGraphConditionalHandle* hs = nullptr,
+                        cudaGraphConditionalHandle loop = cudaGraphConditionalHandle{}, int in_graph = 0) {
+  RoundCtl* ctl = p->ctl;
+  Geo g = p->g;
+  const int* comp = p->comp;
+  const uint32_t* nbm = p->nbm;
+  const double4* sp = p->site_pos;
+  uint32_t* bm = p->bm;
+  Prop* imp = p->imp;
+  int* counters = p->counters;
+  int small = p->ew_small, max_rounds = 1 << 20, ncl = p->n_classes;
+  void* args[] = {&ctl, &g, &comp, &nbm, &sp, &bm, &imp, &counters, &small, &max_rounds, &hs, &ncl, &loop,
+                  &in_graph};
+  void* fn = var == 0 ? (void*)k_rounds_small<false> : (void*)k_rounds_small<true>;
+  if (!in_graph) {
+    CK(cudaLaunchCooperativeKernel(fn, dim3(p->coop_blocks), dim3(32 * EW_WARPS), args, 0, st));
+  } else {  // captured into the round graph as a cooperative kernel node
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(p->coop_blocks);
+    cfg.blockDim = dim3(32 * EW_WARPS);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    CK(cudaLaunchKernelExC(&cfg, fn, args));
+  }
+  LAUNCHED(1);
+  return 0;
+}
+
 int build_round_graph(lrcvt_plan* p, int var) {
   if (!p->cap) CK(cudaStreamCreateWithFlags(&p->cap, cudaStreamNonBlocking));
   cudaGraph_t g;
@@ -420,8 +452,13 @@ int build_round_graph(lrcvt_plan* p, int var) {
     long long cap = class_cap(c);
     if (c == p->n_classes - 1 && cap < p->n_inband) cap = p->n_inband;
     CK(cudaStreamBeginCaptureToGraph(p->cap, ib, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
-    int rc = launch_eval_kernel(p, var, (int)cap, p->cap);
-    if (!rc) rc = launch_commit_kernel(p, (int)((cap + 127) / 128), p->cap, d_hs, h, 1);
+    int rc = 0;
+    if (c == 0 && p->coop_in_graph && cap <= p->ew_small) {
+      rc = launch_rounds_small(p, var, p->cap, d_hs, h, 1);  // all small rounds in one cooperative node
+    } else {
+      rc = launch_eval_kernel(p, var, (int)cap, p->cap);
+      if (!rc) rc = launch_commit_kernel(p, (int)((cap + 127) / 128), p->cap, d_hs, h, 1);
+    }
     cudaGraph_t captured;
     const cudaError_t ee = cudaStreamEndCapture(p->cap, &captured);
     if (rc) return rc;
@@ -433,27 +470,10 @@ int build_round_graph(lrcvt_plan* p, int var) {
   return 0;
 }
 
-int launch_rounds_small(lrcvt_plan* p, int var, cudaStream_t st) {
-  RoundCtl* ctl = p->ctl;
-  Geo g = p->g;
-  const int* comp = p->comp;
-  const uint32_t* nbm = p->nbm;
-  const double4* sp = p->site_pos;
-  uint32_t* bm = p->bm;
-  Prop* imp = p->imp;
-  int* counters = p->counters;
-  int small = p->ew_small, max_rounds = 1 << 20;
-  void* args[] = {&ctl, &g, &comp, &nbm, &sp, &bm, &imp, &counters, &small, &max_rounds};
-  void* fn = var == 0 ? (void*)k_rounds_small<false> : (void*)k_rounds_small<true>;
-  CK(cudaLaunchCooperativeKernel(fn, dim3(p->coop_blocks), dim3(32 * EW_WARPS), args, 0, st));
-  LAUNCHED(1);
-  return 0;
-}
-
 int run_rounds(lrcvt_plan* p, int var, cudaStream_t st) {
   if (!p->timing) {
     if (!p->graph[var]) CKR(build_round_graph(p, var));
-    if (!p->coop) {
+    if (!p->coop || p->coop_in_graph) {
       CK(cudaGraphLaunch(p->graph[var], st));
       LAUNCHED(1);  // k_loop_init; per-round kernels are counted from ctl->rounds
       return 0;
@@ -555,12 +575,15 @@ int lrcvt_plan_create(lrcvt_plan** plan, int64_t nx, int64_t ny, int64_t nz, dou
     p->warp_eval_all = e[0] == '2';
   }
   if (const char* e = getenv("LRCVT_EW_SMALL")) p->ew_small = atoi(e);
-  // 2D bands run ~100 tiny rounds per classify: there the cooperative
-  // small-round kernel wins (C1 -13%); 3D configs are neutral to -3% and the
-  // extra host check per phase costs the 128^3 headline ~1%, so 3D stays on
-  // the graph unless asked
-  p->coop = nz == 1;
-  if (const char* e = getenv("LRCVT_COOP")) p->coop = e[0] == '1';
+  // small frontiers: every round inside one cooperative kernel node of the
+  // round graph (C1 2D -14%, C3 -1.5%, C2 neutral; LRCVT_COOP=0 off, =1 host-
+  // alternated variant, =2 in-graph)
+  p->coop = true;
+  p->coop_in_graph = true;
+  if (const char* e = getenv("LRCVT_COOP")) {
+    p->coop = e[0] == '1' || e[0] == '2';
+    p->coop_in_graph = e[0] == '2';
+  }
   p->g = make_geo(nx, ny, nz, sx, sy, sz);
   p->comp = d_comp;
   p->n_components = n_components;
@@ -679,7 +702,8 @@ int lrcvt_plan_create(lrcvt_plan** plan, int64_t nx, int64_t ny, int64_t nz, dou
     int coop_ok = 0;
     cudaDeviceGetAttribute(&coop_ok, cudaDevAttrCooperativeLaunch, dev);
     if (!coop_ok || nbc <= 0) p->coop = false;
-    const int loop_min = p->coop ? p->ew_small : 0;
+    if (!p->coop) p->coop_in_graph = false;
+    const int loop_min = (p->coop && !p->coop_in_graph) ? p->ew_small : 0;
     cudaMemcpy(&p->ctl->loop_min, &loop_min, sizeof(int), cudaMemcpyHostToDevice);
   }
   if (dalloc((char**)&p->cub_tmp, (int64_t)need)) { lrcvt_plan_destroy(p); return LRCVT_E_NOMEM; }

@@ -25,7 +25,9 @@ __global__ void __launch_bounds__(32 * EW_WARPS) k_rounds_small(RoundCtl* __rest
                                                                 const double4* __restrict__ site_pos,
                                                                 uint32_t* __restrict__ bm, Prop* __restrict__ imp,
                                                                 int* __restrict__ counters, int small,
-                                                                int max_rounds) {
+                                                                int max_rounds,
+                                                                const cudaGraphConditionalHandle* hs, int n_classes,
+                                                                cudaGraphConditionalHandle loop, int in_graph) {
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
   __shared__ EwStage stage[EW_WARPS];
@@ -87,6 +89,13 @@ __global__ void __launch_bounds__(32 * EW_WARPS) k_rounds_small(RoundCtl* __rest
       __threadfence();
     }
     grid.sync();
+  }
+  // inside the round graph: arm the next size class and the WHILE condition
+  // (the frontier is empty, or too large for this kernel)
+  if (in_graph && blockIdx.x == 0 && threadIdx.x == 0) {
+    const int n = vctl->n_cur;
+    set_size_class(n, hs, n_classes);
+    cudaGraphSetConditional(loop, n > 0 ? 1u : 0u);
   }
 }
 
