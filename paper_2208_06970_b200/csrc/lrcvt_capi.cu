@@ -595,16 +595,19 @@ int lrcvt_plan_create(lrcvt_plan** plan, int64_t nx, int64_t ny, int64_t nz, dou
   if (rc) { lrcvt_plan_destroy(p); return set_error(LRCVT_E_NOMEM, "plan counters"); }
   // count in-band voxels
   {
-    CountInband op{d_comp};
-    cub::CountingInputIterator<int> it(0);
-    cub::TransformInputIterator<int, CountInband, cub::CountingInputIterator<int>> tin(it, op);
-    size_t bytes = 0;
-    CK(cub::DeviceReduce::Sum(nullptr, bytes, tin, p->counters, (int)n, st));
-    void* tmp = nullptr;
-    CK(cudaMallocAsync(&tmp, bytes, st));
-    CK(cub::DeviceReduce::Sum(tmp, bytes, tin, p->counters, (int)n, st));
-    CK(cudaFreeAsync(tmp, st));
-    if (sync_counters(p, st, 1)) { lrcvt_plan_destroy(p); return LRCVT_E_CUDA; }
+    auto count = [&]() -> int {
+      CountInband op{d_comp};
+      cub::CountingInputIterator<int> it(0);
+      cub::TransformInputIterator<int, CountInband, cub::CountingInputIterator<int>> tin(it, op);
+      size_t bytes = 0;
+      CK(cub::DeviceReduce::Sum(nullptr, bytes, tin, p->counters, (int)n, st));
+      Scratch sc(st);
+      char* tmp = nullptr;
+      CK(sc.get(&tmp, (int64_t)bytes));
+      CK(cub::DeviceReduce::Sum(tmp, bytes, tin, p->counters, (int)n, st));
+      return sync_counters(p, st, 1);
+    };
+    if (const int e = count()) { lrcvt_plan_destroy(p); return e; }  // no partial plan on failure
     p->n_inband = p->h_counters[0];
   }
   const int64_t nin = p->n_inband > 0 ? p->n_inband : 1;
@@ -634,19 +637,24 @@ int lrcvt_plan_create(lrcvt_plan** plan, int64_t nx, int64_t ny, int64_t nz, dou
   rc |= dalloc(&p->seg_b, S);
   rc |= dalloc(&p->seg_e, S);
   if (rc) { lrcvt_plan_destroy(p); return LRCVT_E_NOMEM; }
-  k_nbr_mask<<<grid_for(n, 256, 148 * 16), 256, 0, st>>>(p->g, d_comp, p->nbm);
-  {  // clearance layers into nbm bits 26..31 (exact ray shortcut, common.cuh)
-    unsigned char* clr = nullptr;
-    CK(cudaMallocAsync((void**)&clr, (size_t)n, st));
-    k_clear_init<<<grid_for(n, 256, 148 * 16), 256, 0, st>>>(p->g, d_comp, p->nbm, clr);
-    CKL("k_clear_init"); LAUNCHED(1);
-    for (int r = 1; r <= CLR_MAX; r++) {
-      k_clear_layer<<<grid_for(n, 256, 148 * 16), 256, 0, st>>>(p->g, clr, r);
-      CKL("k_clear_layer"); LAUNCHED(1);
-    }
-    k_clear_store<<<grid_for(n, 256, 148 * 16), 256, 0, st>>>(n, clr, p->nbm);
-    CKL("k_clear_store"); LAUNCHED(1);
-    CK(cudaFreeAsync(clr, st));
+  {  // static neighbour words + clearance layers in bits 26..31 (exact ray shortcut, common.cuh)
+    auto build = [&]() -> int {
+      k_nbr_mask<<<grid_for(n, 256, 148 * 16), 256, 0, st>>>(p->g, d_comp, p->nbm);
+      CKL("k_nbr_mask"); LAUNCHED(1);
+      Scratch sc(st);
+      unsigned char* clr = nullptr;
+      CK(sc.get(&clr, n));
+      k_clear_init<<<grid_for(n, 256, 148 * 16), 256, 0, st>>>(p->g, d_comp, p->nbm, clr);
+      CKL("k_clear_init"); LAUNCHED(1);
+      for (int r = 1; r <= CLR_MAX; r++) {
+        k_clear_layer<<<grid_for(n, 256, 148 * 16), 256, 0, st>>>(p->g, clr, r);
+        CKL("k_clear_layer"); LAUNCHED(1);
+      }
+      k_clear_store<<<grid_for(n, 256, 148 * 16), 256, 0, st>>>(n, clr, p->nbm);
+      CKL("k_clear_store"); LAUNCHED(1);
+      return 0;
+    };
+    if (const int e = build()) { lrcvt_plan_destroy(p); return e; }
   }
   if (cudaMemsetAsync(p->bm, 0, sizeof(uint32_t) * p->bm_words, st) != cudaSuccess) {
     lrcvt_plan_destroy(p);
