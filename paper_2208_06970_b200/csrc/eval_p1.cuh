@@ -30,7 +30,12 @@ constexpr int P1_TAB = 4;  // distinct-site distance table
 // up to three rays per lane preceded the strict rule; with the rule in place
 // it only cost registers and spills and was removed: p1 -7% at 512^3.)
 constexpr int P1_SPEC = 1;  // queued rays per lane (the strict winner's)
-constexpr int P1_MIN_BLOCKS = 5;  // caps registers at 102: +25% occupancy, few spills (measured best)
+// CTAs per SM the register budget is sized for: 5 (102 registers) is best for
+// rounds up to a few million voxels, 6 (85 registers, more spills but more
+// warps to hide the gathers) for the largest rounds (measured: 128^3 -5% / 512^3 +3% for 6)
+constexpr int P1_MIN_BLOCKS = 5;
+constexpr int P1_MIN_BLOCKS_BIG = 6;
+constexpr int P1_BIG_ROUND = 1 << 22;
 
 template <int BLOCK>
 __device__ __forceinline__ void p1_tile(const int* __restrict__ list, int n, const int i, const Geo& g,
@@ -226,8 +231,8 @@ __device__ __forceinline__ void p1_tile(const int* __restrict__ list, int n, con
 
 // Grid-stride over 128-voxel tiles of the worklist held in the round control
 // block (size and pointer read on device, so rounds need no host round trip).
-template <int BLOCK>
-__global__ void __launch_bounds__(BLOCK, P1_MIN_BLOCKS) k_eval_p1(RoundCtl* __restrict__ ctl, Geo g,
+template <int BLOCK, int MINB = P1_MIN_BLOCKS>
+__global__ void __launch_bounds__(BLOCK, MINB) k_eval_p1(RoundCtl* __restrict__ ctl, Geo g,
                                                    const int* __restrict__ comp,
                                                    const uint32_t* __restrict__ nbm,
                                                    const double4* __restrict__ site_pos,

@@ -328,7 +328,10 @@ int launch_eval_kernel(lrcvt_plan* p, int var, int items, cudaStream_t st) {
   }
   const int bs = var == 0 ? 128 : 64;
   const int blocks = (items + bs - 1) / bs;
-  if (var == 0)
+  if (var == 0 && items >= P1_BIG_ROUND)
+    k_eval_p1<128, P1_MIN_BLOCKS_BIG><<<blocks, 128, 0, st>>>(p->ctl, g, p->comp, p->nbm, p->site_pos, p->bm,
+                                                              p->imp, p->counters);
+  else if (var == 0)
     k_eval_p1<128><<<blocks, 128, 0, st>>>(p->ctl, g, p->comp, p->nbm, p->site_pos, p->bm, p->imp, p->counters);
   else if (var == 1)
     k_eval_p2<64, true><<<blocks, 64, 0, st>>>(p->ctl, g, p->comp, p->nbm, p->site_pos, p->bm, p->imp,
