@@ -30,12 +30,14 @@ constexpr int P1_TAB = 4;  // distinct-site distance table
 // up to three rays per lane preceded the strict rule; with the rule in place
 // it only cost registers and spills and was removed: p1 -7% at 512^3.)
 constexpr int P1_SPEC = 1;  // queued rays per lane (the strict winner's)
-// CTAs per SM the register budget is sized for: 5 (102 registers) is best for
-// rounds up to a few million voxels, 6 (85 registers, more spills but more
-// warps to hide the gathers) for the largest rounds (measured: 128^3 -5% / 512^3 +3% for 6)
+// CTAs per SM the register budget is sized for: 5 (102 registers) for rounds
+// below a million voxels; 8 (64 registers: more spills, but twice the warps
+// to hide the dependent gathers) for larger ones. Measured on phase-1 time:
+// 512^3 -10% and 256^3 -5% with 8 for the large rounds (6, 7, 10 in between
+// or equal, 12 worse); 128^3 rounds stay below the threshold (5 is 2% faster there).
 constexpr int P1_MIN_BLOCKS = 5;
-constexpr int P1_MIN_BLOCKS_BIG = 6;
-constexpr int P1_BIG_ROUND = 1 << 22;
+constexpr int P1_MIN_BLOCKS_BIG = 8;
+constexpr int P1_BIG_ROUND = 1 << 20;
 
 template <int BLOCK>
 __device__ __forceinline__ void p1_tile(const int* __restrict__ list, int n, const int i, const Geo& g,
