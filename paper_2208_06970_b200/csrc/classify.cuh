@@ -243,8 +243,19 @@ __device__ __forceinline__ void mark_and_append(const Geo& g, const uint32_t* __
 constexpr int MAX_CLASSES = 12;
 __host__ __device__ inline long long class_cap(int c) { return 2048ll << (2 * c); }
 
-// sets exactly one class handle (none when n == 0)
+// sets exactly one class handle (none when n == 0); n_classes < 0: one SWITCH
+// handle hs[0] over -n_classes bodies takes the class index (-n_classes = none)
 __device__ __forceinline__ void set_size_class(long long n, const cudaGraphConditionalHandle* hs, int n_classes) {
+  if (n_classes < 0) {
+    const int ncl = -n_classes;
+    int c = ncl;
+    if (n > 0) {
+      c = 0;
+      while (c < ncl - 1 && n > class_cap(c)) c++;
+    }
+    cudaGraphSetConditional(hs[0], (unsigned)c);
+    return;
+  }
   for (int c = 0; c < n_classes; c++) {
     const long long lo = c == 0 ? 0 : class_cap(c - 1);
     cudaGraphSetConditional(hs[c], (n > lo && (n <= class_cap(c) || c == n_classes - 1)) ? 1u : 0u);

@@ -248,6 +248,10 @@ struct lrcvt_plan {
   bool coop = false;    // small frontiers: all their rounds in one cooperative kernel
   int coop_blocks = 0;  // co-resident CTAs of k_rounds_small
   bool coop_in_graph = false;  // k_rounds_small as the class-0 node of the round graph (LRCVT_COOP=2)
+  // one SWITCH node selects the round's size class (LRCVT_SWITCH=0: a chain of
+  // IF nodes, one per class, every one of them visited each round)
+  bool class_switch = true;
+  int ncl_arg() const { return class_switch ? -n_classes : n_classes; }
   bool eligible_valid = false;
   int64_t eligible_sites = -1;
   // optional per-launch timing of the dominant kernel (k_eval)
@@ -351,7 +355,7 @@ int launch_commit_kernel(lrcvt_plan* p, int blocks, cudaStream_t st, const cudaG
   // grid-stride: at most one resident wave (the last-block round end costs one
   // same-address atomic per block)
   if (blocks > p->commit_blocks) blocks = p->commit_blocks;
-  k_commit<<<blocks, 128, 0, st>>>(p->imp, p->counters, p->ctl, p->g, p->nbm, p->bm, hs, p->n_classes, loop,
+  k_commit<<<blocks, 128, 0, st>>>(p->imp, p->counters, p->ctl, p->g, p->nbm, p->bm, hs, p->ncl_arg(), loop,
                                    end_mode);
   CKL("k_commit");
   return 0;
@@ -392,7 +396,7 @@ int launch_rounds_small(lrcvt_plan* p, int var, cudaStream_t st, const cudaGraph
   uint32_t* bm = p->bm;
   Prop* imp = p->imp;
   int* counters = p->counters;
-  int small = p->ew_small, max_rounds = 1 << 20, ncl = p->n_classes;
+  int small = p->ew_small, max_rounds = 1 << 20, ncl = p->ncl_arg();
   void* args[] = {&ctl, &g, &comp, &nbm, &sp, &bm, &imp, &counters, &small, &max_rounds, &hs, &ncl, &loop,
                   &in_graph};
   void* fn = var == 0 ? (void*)k_rounds_small<false> : (void*)k_rounds_small<true>;
@@ -420,14 +424,15 @@ int build_round_graph(lrcvt_plan* p, int var) {
   CK(cudaGraphCreate(&g, 0));
   cudaGraphConditionalHandle h;
   CK(cudaGraphConditionalHandleCreate(&h, g, 0, cudaGraphCondAssignDefault));
-  std::vector<cudaGraphConditionalHandle> hs(p->n_classes);
-  for (int c = 0; c < p->n_classes; c++) CK(cudaGraphConditionalHandleCreate(&hs[c], g, 0, 0));
+  const int n_handles = p->class_switch ? 1 : p->n_classes;
+  std::vector<cudaGraphConditionalHandle> hs(n_handles);
+  for (int c = 0; c < n_handles; c++) CK(cudaGraphConditionalHandleCreate(&hs[c], g, 0, 0));
   cudaGraphConditionalHandle* d_hs = p->d_handles + var * MAX_CLASSES;
-  CK(cudaMemcpy(d_hs, hs.data(), sizeof(cudaGraphConditionalHandle) * p->n_classes, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(d_hs, hs.data(), sizeof(cudaGraphConditionalHandle) * n_handles, cudaMemcpyHostToDevice));
   RoundCtl* ctl = p->ctl;
   cudaGraphNode_t n_init, n_loop;
   {
-    int ncl = p->n_classes;
+    int ncl = p->ncl_arg();
     void* args[] = {&ctl, &h, &d_hs, &ncl};
     CKR(add_kernel_node(&n_init, g, nullptr, (void*)k_loop_init, dim3(1), dim3(1), args));
   }
@@ -438,20 +443,36 @@ int build_round_graph(lrcvt_plan* p, int var) {
   pw.conditional.size = 1;
   CK(cudaGraphAddNode(&n_loop, g, &n_init, 1, &pw));
   cudaGraph_t body = pw.conditional.phGraph_out[0];
-  // body: IF(class c) { eval with cap[c]/BLOCK blocks; commit + round end with
-  // cap[c]/128 blocks } for each class; the last commit block arms the next
-  // round's class and the WHILE condition
+  // body: SWITCH(class) { case c: eval with cap[c]/BLOCK blocks; commit + round
+  // end with cap[c]/128 blocks } (or one IF node per class); the last commit
+  // block arms the next round's class and the WHILE condition
   const int bs = eval_block_size(var);
   cudaGraphNode_t prev = nullptr;
+  cudaGraph_t* sw_bodies = nullptr;  // SWITCH: body c runs when the handle holds c
+  if (p->class_switch) {
+    cudaGraphNodeParams ps = {};
+    ps.type = cudaGraphNodeTypeConditional;
+    ps.conditional.handle = hs[0];
+    ps.conditional.type = cudaGraphCondTypeSwitch;
+    ps.conditional.size = (unsigned)p->n_classes;
+    cudaGraphNode_t nsw;
+    CK(cudaGraphAddNode(&nsw, body, nullptr, 0, &ps));
+    sw_bodies = ps.conditional.phGraph_out;
+  }
   for (int c = 0; c < p->n_classes; c++) {
-    cudaGraphNodeParams pi = {};
-    pi.type = cudaGraphNodeTypeConditional;
-    pi.conditional.handle = hs[c];
-    pi.conditional.type = cudaGraphCondTypeIf;
-    pi.conditional.size = 1;
-    cudaGraphNode_t nif;
-    CK(cudaGraphAddNode(&nif, body, prev ? &prev : nullptr, prev ? 1 : 0, &pi));
-    cudaGraph_t ib = pi.conditional.phGraph_out[0];
+    cudaGraph_t ib;
+    cudaGraphNode_t nif = nullptr;
+    if (sw_bodies) {
+      ib = sw_bodies[c];
+    } else {
+      cudaGraphNodeParams pi = {};
+      pi.type = cudaGraphNodeTypeConditional;
+      pi.conditional.handle = hs[c];
+      pi.conditional.type = cudaGraphCondTypeIf;
+      pi.conditional.size = 1;
+      CK(cudaGraphAddNode(&nif, body, prev ? &prev : nullptr, prev ? 1 : 0, &pi));
+      ib = pi.conditional.phGraph_out[0];
+    }
     long long cap = class_cap(c);
     if (c == p->n_classes - 1 && cap < p->n_inband) cap = p->n_inband;
     CK(cudaStreamBeginCaptureToGraph(p->cap, ib, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
@@ -578,6 +599,7 @@ int lrcvt_plan_create(lrcvt_plan** plan, int64_t nx, int64_t ny, int64_t nz, dou
     p->warp_eval_all = e[0] == '2';
   }
   if (const char* e = getenv("LRCVT_EW_SMALL")) p->ew_small = atoi(e);
+  if (const char* e = getenv("LRCVT_SWITCH")) p->class_switch = e[0] != '0';
   // small frontiers: every round inside one cooperative kernel node of the
   // round graph (C1 2D -14%, C3 -1.5%, C2 neutral; LRCVT_COOP=0 off, =1 host-
   // alternated variant, =2 in-graph)
