@@ -241,7 +241,10 @@ __device__ __forceinline__ void mark_and_append(const Geo& g, const uint32_t* __
 // items, caps growing 4x from 2048; the graph launches the eval kernel of the
 // active class with cap[c] / BLOCK blocks (one tile per block).
 constexpr int MAX_CLASSES = 12;
-__host__ __device__ inline long long class_cap(int c) { return 2048ll << (2 * c); }
+#ifndef LRCVT_CLASS0
+#define LRCVT_CLASS0 2048  // cap of the smallest class (served by k_rounds_small)
+#endif
+__host__ __device__ inline long long class_cap(int c) { return (long long)LRCVT_CLASS0 << (2 * c); }
 
 // sets exactly one class handle (none when n == 0); n_classes < 0: one SWITCH
 // handle hs[0] over -n_classes bodies takes the class index (-n_classes = none)

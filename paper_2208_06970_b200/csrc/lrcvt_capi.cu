@@ -183,7 +183,7 @@ bool geo_ok(int64_t nx, int64_t ny, int64_t nz, double sx, double sy, double sz)
 
 }  // namespace
 
-constexpr int EW_SMALL_DEFAULT = 2048;  // frontier size served by the warp-per-voxel kernels
+constexpr int EW_SMALL_DEFAULT = LRCVT_CLASS0;  // frontier size served by the warp-per-voxel kernels
 struct lrcvt_plan {
   Geo g;
   const int* comp = nullptr;
