@@ -16,12 +16,18 @@ pytestmark = pytest.mark.gpu
 ROOT = Path(__file__).resolve().parents[1]
 
 
-@pytest.mark.parametrize("mode", ["2", "0", "coop"])
+@pytest.mark.parametrize("mode", ["2", "0", "coop", "ifchain"])
 def test_classify_suite_under_forced_kernel_choice(mode):
     """mode "coop": every small frontier of every config goes through the
-    persistent cooperative round kernel (rounds_small.cuh)."""
-    env = dict(os.environ, LRCVT_COOP="1") if mode == "coop" else dict(os.environ, LRCVT_WARP_EVAL=mode,
-                                                                            LRCVT_COOP="0")
+    persistent cooperative round kernel (rounds_small.cuh); mode "ifchain":
+    the round graph selects the size class with one IF node per class
+    instead of the SWITCH node (LRCVT_SWITCH=0)."""
+    if mode == "coop":
+        env = dict(os.environ, LRCVT_COOP="1")
+    elif mode == "ifchain":
+        env = dict(os.environ, LRCVT_SWITCH="0")
+    else:
+        env = dict(os.environ, LRCVT_WARP_EVAL=mode, LRCVT_COOP="0")
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider",
                         str(ROOT / "tests" / "test_gpu_classify.py"), str(ROOT / "tests" / "test_gpu_edges.py"),
                         str(ROOT / "tests" / "test_gpu_blocks.py")],
