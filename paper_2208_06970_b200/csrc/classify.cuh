@@ -271,7 +271,7 @@ __device__ __forceinline__ void set_size_class(long long n, const cudaGraphCondi
 // list. One thread per committed proposal: the compact proposal list keeps
 // every lane of a warp busy in the latency-bound enqueue.
 // round end (_kernels.py:370-384): statistics, list swap, next size; inside
-// the round graph it also arms the next round (size-class IF handles and the
+// the round graph it also arms the next round (size-class SWITCH/IF handles and the
 // WHILE condition). Runs on one thread.
 __device__ __forceinline__ void round_end(RoundCtl* ctl, int* counters, const cudaGraphConditionalHandle* hs,
                                           int n_classes, cudaGraphConditionalHandle loop, int in_graph) {

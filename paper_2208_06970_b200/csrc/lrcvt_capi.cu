@@ -231,7 +231,7 @@ struct lrcvt_plan {
   RoundCtl* h_ctl = nullptr;  // pinned readback
   int* d_nel = nullptr;       // eligible count (device)
   cudaGraphExec_t graph[3] = {nullptr, nullptr, nullptr};
-  cudaGraphConditionalHandle* d_handles = nullptr;  // [3][MAX_CLASSES] size-class IF handles
+  cudaGraphConditionalHandle* d_handles = nullptr;  // [3][MAX_CLASSES] size-class handles (SWITCH: slot 0 only)
   int n_classes = 0;
   cudaStream_t cap = nullptr;  // capture stream
   int eval_blocks[3] = {0, 0, 0};
