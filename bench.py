@@ -1,16 +1,23 @@
 """Benchmark: CVT-iteration voxels/s of the geodesic LSRCVT hot path.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl b200|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4] [--impl b200|reference]
 
 A step is one Lloyd iteration (voronoi_classify + centroidal_update: LOS
 classification, phi-propagated vote, clamped site move) over the whole volume;
-value = voxels x steps / device time. Default workload is
-BASELINE.json configs[1] (C2: 128^3 gaussian-mix, 1 band, 512 'g'-weighted
-sites). Under torchrun each rank runs its own volume instance (independent
-objects, no data-path collective): "scaling": "weak".
+value = voxels x steps / device time. The default workload
+is C4 (BASELINE.json configs[3], the largest configuration quoted for ONE
+GPU: 512^3 random-smooth, 3 bands, 32 776 'g'-weighted sites); c1-c3 and c5
+(1024^3 on one B200) are selectable with --config.
+
+--gpus N > 1 outside torchrun re-launches this script under
+torch.distributed.run (one rank per GPU, 127.0.0.1). --mode global (the
+default for N > 1) splits ONE volume into z-slabs (strong scaling); --mode
+blocks runs one independent volume per rank (weak scaling).
 
 --impl reference times the reference algorithm's CPU implementation (the C
-oracle port in oracle/, all host threads) on the same config; rank 0 only.
+oracle port in oracle/, all host threads) on the same config: one Lloyd
+iteration per step, timed until K steps or --ref-budget seconds (a bounded
+sample); rank 0 only.
 """
 
 from __future__ import annotations
@@ -49,6 +56,16 @@ CONFIGS = {
                label="C5 3D 1024^3 helical two-field, 2 bands, 256k g-weighted sites"),
 }
 L2_BYTES = 126 * 2**20
+
+
+def bench_config(cfg, n, S, inband):
+    """The `config` object of the JSON line -- identical in both arms."""
+    state_bytes = n * (8 + 8 + 4 + 1)
+    l2 = ("flushed between steps (256 MiB write)" if state_bytes < 2 * L2_BYTES
+          else f"inputs larger than L2 (per-voxel state {state_bytes / 2**20:.0f} MiB > 126 MiB)")
+    return {"workload": cfg["label"], "dims": list(cfg["dims"]), "voxels": int(n), "sites": int(S),
+            "inband": int(inband), "step": "one Lloyd iteration (voronoi_classify + centroidal_update)",
+            "l2": l2}
 
 
 def peaks():
@@ -181,7 +198,12 @@ def dist_setup(args):
 
 
 def run_reference(args, cfg, world, rank):
-    """CPU arm: the oracle port of the reference algorithm, all host threads."""
+    """CPU arm: the oracle port of the reference algorithm (oracle/lrcvt_oracle.c:
+    the numba kernels restated in C, OpenMP eval + serial commit like the
+    reference), all host threads, on the same workload. One step = one full
+    Lloyd iteration from the previous step's sites; warm-up is one iteration
+    (a CPU port has no JIT or allocator warm-up beyond the first touch), then
+    steps are timed until K are done or --ref-budget seconds have elapsed."""
     if rank != 0:
         return
     from oracle import oracle
@@ -194,27 +216,35 @@ def run_reference(args, cfg, world, rank):
     sc = np.array([s.component_id for s in sites], np.int32)
     w = None if params.weight_field is None else weights
     comp = labels.component
+    inband = int(np.count_nonzero(comp >= 0))
 
     def step(p):
         c = oracle.classify(grid.dims, grid.spacing, comp, p, sc, labels.n_components)
         return oracle.centroidal(grid.dims, grid.spacing, comp, c["site_of"], c["src"], w, p, sc)["new_pos"]
 
-    for _ in range(args.warmup):
+    warm = min(args.warmup, 1)
+    for _ in range(warm):
         pos = step(pos)
     t0 = time.perf_counter()
-    for _ in range(args.steps):
+    done = 0
+    while done < args.steps:
         pos = step(pos)
+        done += 1
+        el = time.perf_counter() - t0
+        if el + el / done > args.ref_budget:  # the next step would overrun the budget
+            break
     dt = time.perf_counter() - t0
-    value = n * args.steps / dt
+    value = n * done / dt
     threads = oracle.num_threads()
+    sample = (f"{done} full Lloyd iteration(s) of the workload after {warm} warm-up iteration(s), timed "
+              f"{'(all ' + str(args.steps) + ' steps)' if done == args.steps else f'(budget {args.ref_budget:.0f} s reached)'}")
     line = {
         "impl": "reference", "metric": "CVT-iteration voxels/s", "value": value, "unit": "voxels/s",
-        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": {"workload": cfg["label"], "dims": list(cfg["dims"]), "sites": len(sites)},
-        "cpu_baseline": {"value": value, "unit": "voxels/s", "cores": threads, "kind": "port",
-                         "sample": f"{args.steps} full Lloyd iterations after {args.warmup} warm-up, C oracle "
-                                   f"(restated numba kernels, OpenMP eval + serial commit)"},
+        "n_gpus": world, "steps": args.steps, "steps_timed": done, "warmup": args.warmup, "warmup_timed": warm,
+        "ms_per_step": 1e3 * dt / done, "higher_is_better": True,
+        "scaling": "weak" if world == 1 else "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": bench_config(cfg, n, len(sites), inband),
+        "cpu_baseline": {"value": value, "unit": "voxels/s", "cores": threads, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": "voxels/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -379,7 +409,7 @@ def one_off_passes(grid, labels, eng, config, S, reps=3):
     return out
 
 
-def cpu_baseline(grid, labels, params, weights, pos, sc, budget_s=20.0, max_iters=3):
+def cpu_baseline(grid, labels, params, weights, pos, sc, budget_s=45.0, max_iters=3):
     from oracle import oracle
 
     oracle.build()
@@ -456,30 +486,94 @@ def run_global(args, cfg, world, rank, local):
         torch.distributed.destroy_process_group()
 
 
+def relaunch(args) -> int:
+    """--gpus N > 1 outside torchrun: run this script under
+    torch.distributed.run with one rank per GPU on 127.0.0.1."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(args.gpus),
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(ROOT / "bench.py")] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def e2e_public_api(grid, labels, params, weights, pos_start, sc_np, steps, world):
+    """End to end through the public API, honouring the reference's output
+    contract: per step voronoi_classify(grid, labels, sites, weights) with host
+    Site lists in, the four per-voxel arrays materialised as numpy
+    (site_of/dist/src/state, tessellation.py:120-122, :205-208), then
+    centroidal_update(tess) with host Site lists out. Also the same loop
+    without reading the arrays (they stay in HBM; `lazy`)."""
+    import torch
+
+    from paper_2208_06970_b200 import centroidal_update, voronoi_classify
+    from paper_2208_06970_b200.seeding import Site
+
+    n, S = grid.size, len(sc_np)
+    w = weights if params.weight_field else None
+
+    def run(k, full):
+        cur = [Site(tuple(p), int(c)) for p, c in zip(pos_start, sc_np)]
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(k):
+            t_ = voronoi_classify(grid, labels, cur, w)
+            if full:
+                _ = (t_.site_of, t_.dist, t_.src, t_.state)
+            cur, _ = centroidal_update(t_)
+            del t_
+        torch.cuda.synchronize()
+        return time.perf_counter() - t0
+
+    run(2, True)  # warm-up: plans, graphs, pinned host pool
+    ke = max(1, min(steps, 10))
+    dt_full = run(ke, True)
+    dt_lazy = run(ke, False)
+    h2d = 2 * S * (24 + 4)
+    d2h_small = S * (24 + 8) + 64
+    return {"value": n * ke * world / dt_full, "unit": "voxels/s", "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h_small + n * (4 + 8 + 4 + 1), "steps": ke,
+            "note": "public API per step: voronoi_classify(grid, labels, sites, weights) + reading tess.site_of/"
+                    "dist/src/state as numpy (the reference's Tessellation output) + centroidal_update(tess); "
+                    "host Site lists in and out; labels/weights uploaded once",
+            "lazy": {"value": n * ke * world / dt_lazy, "unit": "voxels/s", "h2d_bytes_per_step": h2d,
+                     "d2h_bytes_per_step": d2h_small,
+                     "note": "same loop without reading the per-voxel arrays (they stay in HBM)"}}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--ref-budget", type=float, default=420.0,
+                    help="--impl reference: seconds of timed CPU work before the sample stops")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-passes", action="store_true")
-    ap.add_argument("--mode", default="blocks", choices=["blocks", "global"],
-                    help="blocks: one independent volume per rank (weak scaling, default); global: one volume "
-                         "z-slab partitioned over the ranks (strong scaling, proposal all-gather per round)")
+    ap.add_argument("--mode", default=None, choices=["blocks", "global"],
+                    help="global (default for N > 1): one volume z-slab partitioned over the ranks (strong "
+                         "scaling); blocks: one independent volume per rank (weak scaling)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     cfg = CONFIGS[args.config]
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch(args))
     world, rank, local = dist_setup(args)
+    if args.gpus != world:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    args.mode = args.mode or ("global" if world > 1 else "blocks")
     if args.impl == "reference":
         run_reference(args, cfg, world, rank)
         return
 
     import torch
 
-    from paper_2208_06970_b200 import _lib, centroidal_update, voronoi_classify
+    from paper_2208_06970_b200 import _lib
     from paper_2208_06970_b200.tessellation import engine_for, lloyd_weight_mode, voxel_length
 
     # LRCVT_BENCH_DEVICE / LRCVT_BENCH_BACKEND exist only to smoke-test the multi-rank code path on a
@@ -494,7 +588,7 @@ def main():
             dist.init_process_group("nccl", device_id=torch.device("cuda", dev_index))
         else:
             dist.init_process_group(backend)
-    if args.mode == "global":
+    if args.mode == "global" and world > 1:
         run_global(args, cfg, world, rank, local)
         return
     grid, labels, params, sites, weights = build_workload(cfg, rank)
@@ -508,8 +602,8 @@ def main():
     sc_d = torch.from_numpy(sc_np).cuda()
     mode, w_d = lloyd_weight_mode(torch, grid, params, weights)
     backoff = 0.5 * voxel_length(grid.dims, grid.spacing)
-    state_bytes = n * (8 + 8 + 4 + 1)
-    flush = state_bytes < 2 * L2_BYTES
+    config = bench_config(cfg, n, S, eng.inband)
+    flush = config["l2"].startswith("flushed")
     scratch = torch.empty(2 * L2_BYTES // 4, dtype=torch.float32, device="cuda") if flush else None
 
     def step(p):
@@ -524,7 +618,7 @@ def main():
     pos_start = pos_d.cpu().numpy()
 
     # timed region: device-side round loops (CUDA graphs), no per-launch events
-    E = C = 0
+    E = C = R = 0
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     launches0 = L.lrcvt_launch_count()
     if world > 1:
@@ -540,6 +634,7 @@ def main():
             st = eng.stats
             E += st.evaluations
             C += st.commits
+            R += st.rounds
         torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
@@ -567,16 +662,23 @@ def main():
     _lib.check(L.lrcvt_plan_set_timing(eng.plan, 0), "set_timing")
     value = n * args.steps * world / (ms / 1e3)
     hbm, peak_kind = peaks()
+    clocks = clk.summary()
     # dominant kernel: k_eval; algorithmic bytes = 20 B per evaluated voxel
     eval_bytes = 20.0 * eitems.value
     achieved = eval_bytes / (ems.value / 1e3) / 1e9 if ems.value > 0 else 0.0
     b_iter = 29.0 * n + 20.0 * E / args.steps + 16.0 * C / args.steps
-    traffic = None
+    traffic = issue = None
     prof_path = ROOT / "profiles" / f"ncu_{args.config}_k_eval.json"
     if prof_path.exists() and el.value:
-        per_item = json.loads(prof_path.read_text()).get("dram_bytes_per_item")
-        if per_item:
-            traffic = per_item * eitems.value / el.value
+        pj = json.loads(prof_path.read_text())
+        if pj.get("dram_bytes_per_item"):
+            traffic = pj["dram_bytes_per_item"] * eitems.value / el.value
+        # issue roof: warp instructions the eval launches execute (ncu, per evaluated voxel) over what 148 SMs x
+        # 4 schedulers issue in the measured eval time at the sampled SM clock
+        if pj.get("warp_inst_per_item") and clocks.get("sm_mhz"):
+            inst = pj["warp_inst_per_item"] * eitems.value
+            issue = {"warp_inst_per_item": pj["warp_inst_per_item"],
+                     "frac": inst / (148 * 4 * clocks["sm_mhz"] * 1e6 * ems.value / 1e3)}
 
     L.lrcvt_plan_reuse_eligible(eng.plan, 0)  # public-API e2e below takes the general path
     passes = one_off_passes(grid, labels, eng, args.config, S) if not args.no_passes else None
@@ -584,48 +686,17 @@ def main():
         passes["seeding"] = seeding_pass(grid, labels, params)
         passes["layout"] = layout_pass(grid, labels, eng, S)
         passes["adjacency"] = adjacency_pass(grid, eng, S)
-
-    # end-to-end through the public API with host numpy in/out
-    e2e = None
-    if not args.no_e2e:
-        from paper_2208_06970_b200.seeding import Site
-
-        cur = [Site(tuple(p), int(c)) for p, c in zip(pos_start, sc_np)]
-        ke = max(1, min(args.steps, 10))
-        cur_sites = cur
-        for _ in range(3):  # warm-up: first API calls build plans / graphs / pool
-            t_ = voronoi_classify(grid, labels, cur_sites, weights if params.weight_field else None)
-            cur_sites, _ = centroidal_update(t_)
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        marks = []
-        for _ in range(ke):
-            t_ = voronoi_classify(grid, labels, cur_sites, weights if params.weight_field else None)
-            cur_sites, _ = centroidal_update(t_)
-            marks.append(time.perf_counter())
-        torch.cuda.synchronize()
-        dt = time.perf_counter() - t0
-        if os.environ.get("LRCVT_DEBUG_E2E"):
-            print("e2e step ms:", [round(1e3 * (b - a), 2) for a, b in zip([t0] + marks, marks)], file=sys.stderr)
-        h2d = 2 * S * (24 + 4)
-        d2h = S * (24 + 8) + 64
-        e2e = {"value": n * ke * world / dt, "unit": "voxels/s", "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": d2h,
-               "note": "public API per step: voronoi_classify(grid, labels, sites, weights) + "
-                       "centroidal_update(tess) with host Site lists in and out (sites + comps H2D, new "
-                       "positions + displacements D2H); per-voxel tessellation arrays stay in HBM until read; "
-                       "labels/weights uploaded once"}
+    e2e = None if args.no_e2e else e2e_public_api(grid, labels, params, weights, pos_start, sc_np, args.steps,
+                                                  world)
 
     line = {
         "metric": "CVT-iteration voxels/s", "value": value, "unit": "voxels/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": cfg["label"], "dims": list(cfg["dims"]), "voxels": n, "sites": S,
-                   "inband": eng.inband, "l2": "flushed between steps (256 MiB write)" if flush
-                   else f"state {state_bytes / 2**20:.0f} MiB > L2", "E_per_step": E / args.steps,
-                   "C_per_step": C / args.steps},
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config,
+        "counters": {"E_per_step": E / args.steps, "C_per_step": C / args.steps, "rounds_per_step": R / args.steps},
         "roofline": {"bound": "hbm", "kernel": "k_eval", "achieved": achieved, "peak": hbm,
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / hbm, "traffic": traffic,
+                     "issue": issue,
                      "launches": el.value, "avg_launch_us": 1e3 * ems.value / max(el.value, 1),
                      "bytes_per_launch": eval_bytes / max(el.value, 1),
                      "eval_share_of_step": ems.value / ms if ms else None,
@@ -634,7 +705,7 @@ def main():
                                                "commit": prof[2] / args.steps},
                      "iteration_B": b_iter, "iteration_frac": b_iter / (ms / args.steps / 1e3) / 1e9 / hbm},
         "gpu_launches": launches,
-        "clocks": clk.summary(),
+        "clocks": clocks,
     }
     if e2e:
         line["e2e"] = e2e

@@ -222,6 +222,12 @@ unsigned long long lrcvt_launch_count(void);
  * phase-1 voxels evaluated, phase-2 voxels evaluated, proposals committed} */
 int lrcvt_plan_profile(const lrcvt_plan *plan, double *out6);
 
+/* Size classes of the device-side relaxation round loop (host-only, no GPU
+ * needed): returns the number of classes for a plan of n_inband in-band
+ * voxels and writes each class's launch size (voxels its eval launch covers,
+ * clamped to [1, n_inband], < 2^31) into launch_items[0..max_classes). */
+int32_t lrcvt_round_classes(int64_t n_inband, int64_t *launch_items, int32_t max_classes);
+
 const char *lrcvt_last_error(void);
 int lrcvt_version(void);
 

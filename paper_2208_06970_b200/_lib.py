@@ -69,6 +69,7 @@ SIGNATURES = {
     "lrcvt_plan_timing": (c_int, [c_void_p, POINTER(c_int64), POINTER(c_int64), POINTER(c_double)]),
     "lrcvt_launch_count": (ctypes.c_ulonglong, []),
     "lrcvt_plan_profile": (c_int, [c_void_p, POINTER(c_double)]),
+    "lrcvt_round_classes": (c_int32, [c_int64, POINTER(c_int64), c_int32]),
     "lrcvt_mg_set_slab": (c_int, [c_void_p, c_int64, c_int64]),
     "lrcvt_mg_begin": (c_int, [c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_void_p, POINTER(c_int64),
                                c_void_p]),

@@ -121,11 +121,19 @@ __global__ void k_clear_store(int64_t n, const unsigned char* __restrict__ clr, 
   }
 }
 
-// has_site[c] = 1 for every component that owns a site (tessellation.py:161-162)
-__global__ void k_mark_site_comps(const int* __restrict__ site_comp, int n_sites,
+// has_site[c] = 1 for every component that owns a site (tessellation.py:161-162:
+// `comps_with_sites[site_comp] = True` on an array of max(n_components, 1)
+// entries). Ids are taken with numpy's index rule -- a negative id counts
+// from the end (a site of id -1 in an out-of-band voxel passes _place_seeds)
+// -- and ids outside [-n, n) are never written (the reference would raise
+// IndexError; such a site is also a bad site, reported by the caller).
+__global__ void k_mark_site_comps(const int* __restrict__ site_comp, int n_sites, int n_slots,
                                   uint8_t* __restrict__ has_site) {
   int s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s < n_sites) has_site[site_comp[s]] = 1;
+  if (s >= n_sites) return;
+  int c = site_comp[s];
+  if (c < 0) c += n_slots;
+  if (c >= 0 && c < n_slots) has_site[c] = 1;
 }
 
 // Mark same-component neighbours of v (and v itself when `self`) in the
@@ -348,7 +356,8 @@ __global__ void k_loop_init(const RoundCtl* ctl, cudaGraphConditionalHandle h,
 
 // phase 1 starts from the seed worklist appended to `first` by k_seed_groups
 __global__ void k_phase1_start(RoundCtl* ctl, int* counters, int* first, int* second, int2* ss,
-                               double* dist, int* site1) {
+                               double* dist, int* site1, int loop_min) {
+  ctl->loop_min = loop_min;
   ctl->ss = ss;
   ctl->dist = dist;
   ctl->site1 = site1;
@@ -381,8 +390,9 @@ __global__ void k_site1_to_state(Geo g, const int* __restrict__ site1, const dou
 }
 
 __global__ void k_phase2_copy(const int* __restrict__ eligible, const int* __restrict__ n_el,
-                              RoundCtl* ctl) {
-  const int n = *n_el;
+                              RoundCtl* ctl, const int* __restrict__ counters) {
+  // bad sites (tessellation.py:139-140 raises before any relaxation): no work
+  const int n = counters[C_BAD] ? 0 : *n_el;
   int* dst = ctl->cur;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) dst[i] = eligible[i];
   if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -395,10 +405,10 @@ __global__ void k_phase2_copy(const int* __restrict__ eligible, const int* __res
 
 // verification sweep over the eligible list (tessellation.py:177-189): the
 // two list buffers are parked so the sweep's enqueue lands in a free one
-__global__ void k_sweep_start(RoundCtl* ctl, int* eligible, const int* n_el) {
+__global__ void k_sweep_start(RoundCtl* ctl, int* eligible, const int* n_el, const int* counters) {
   ctl->stash = ctl->cur;
   ctl->cur = eligible;
-  ctl->n_cur = *n_el;
+  ctl->n_cur = counters[C_BAD] ? 0 : *n_el;
   ctl->tile_next = 0;
 }
 
@@ -452,6 +462,9 @@ __global__ void __launch_bounds__(128) k_seed_groups(Geo g, const uint32_t* __re
                                                      int* __restrict__ counters,
                                                      int zlo = 0, int zhi = 1 << 30) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  // a bad site (k_site_voxel, the previous launch) aborts the classify before
+  // any relaxation as the reference's ValueError does: no seeds, no frontier
+  if (*(volatile int*)(counters + C_BAD)) return;
   bool head = false;
   int v = 0;
   if (i < n_sites) {

@@ -248,6 +248,7 @@ struct lrcvt_plan {
   bool coop = false;    // small frontiers: all their rounds in one cooperative kernel
   int coop_blocks = 0;  // co-resident CTAs of k_rounds_small
   bool coop_in_graph = false;  // k_rounds_small as the class-0 node of the round graph (LRCVT_COOP=2)
+  int loop_min = 0;            // RoundCtl::loop_min
   // one SWITCH node selects the round's size class (LRCVT_SWITCH=0: a chain of
   // IF nodes, one per class, every one of them visited each round)
   bool class_switch = true;
@@ -299,7 +300,8 @@ int sync_counters(lrcvt_plan* p, cudaStream_t st, int n = C_NCOUNTERS) {
 int prepare_eligible(lrcvt_plan* p, int n_sites, const int* site_comp, cudaStream_t st) {
   CK(cudaMemsetAsync(p->has_site, 0, p->n_components > 0 ? p->n_components : 1, st));
   if (n_sites > 0) {
-    k_mark_site_comps<<<grid_for(n_sites, 256), 256, 0, st>>>(site_comp, n_sites, p->has_site);
+    k_mark_site_comps<<<grid_for(n_sites, 256), 256, 0, st>>>(site_comp, n_sites,
+                                                            p->n_components > 0 ? p->n_components : 1, p->has_site);
     CKL("k_mark_site_comps"); LAUNCHED(1);
   }
   EligiblePred pred{p->comp, p->has_site};
@@ -320,7 +322,7 @@ int launch_eval_kernel(lrcvt_plan* p, int var, int items, cudaStream_t st) {
   const Geo& g = p->g;
   if (items < 1) items = 1;
   if ((items <= p->ew_small && p->warp_eval) || p->warp_eval_all) {
-    const int blocks = (items + EW_WARPS - 1) / EW_WARPS;
+    const int blocks = (int)(((int64_t)items + EW_WARPS - 1) / EW_WARPS);
     if (var == 0)
       k_eval_warp<false><<<blocks, 32 * EW_WARPS, 0, st>>>(p->ctl, g, p->comp, p->nbm, p->site_pos, p->bm, p->imp,
                                                             p->counters);
@@ -331,7 +333,7 @@ int launch_eval_kernel(lrcvt_plan* p, int var, int items, cudaStream_t st) {
     return 0;
   }
   const int bs = var == 0 ? 128 : 64;
-  const int blocks = (items + bs - 1) / bs;
+  const int blocks = (int)(((int64_t)items + bs - 1) / bs);
   if (var == 0 && items >= P1_BIG_ROUND)
     k_eval_p1<128, P1_MIN_BLOCKS_BIG><<<blocks, 128, 0, st>>>(p->ctl, g, p->comp, p->nbm, p->site_pos, p->bm,
                                                               p->imp, p->counters);
@@ -418,10 +420,35 @@ int launch_rounds_small(lrcvt_plan* p, int var, cudaStream_t st, const cudaGraph
   return 0;
 }
 
+// launch size of size class c: its cap, clamped to the in-band count (every
+// frontier, list and sweep holds at most n_inband voxels); the last class
+// covers everything up to n_inband. Always in [1, 2^31).
+long long class_launch_items(int c, int n_classes, int64_t n_inband) {
+  const long long nin = n_inband > 0 ? n_inband : 1;
+  long long cap = class_cap(c);
+  if (cap > nin || c == n_classes - 1) cap = nin;
+  return cap;
+}
+
+int count_classes(int64_t n_inband) {
+  const int64_t nin = n_inband > 0 ? n_inband : 1;
+  int n = 1;
+  while (n < MAX_CLASSES && class_cap(n - 1) < nin) n++;
+  return n;
+}
+
+struct GraphGuard {  // destroys the graph under construction on every exit path
+  cudaGraph_t g = nullptr;
+  ~GraphGuard() {
+    if (g) cudaGraphDestroy(g);
+  }
+};
+
 int build_round_graph(lrcvt_plan* p, int var) {
   if (!p->cap) CK(cudaStreamCreateWithFlags(&p->cap, cudaStreamNonBlocking));
-  cudaGraph_t g;
-  CK(cudaGraphCreate(&g, 0));
+  GraphGuard guard;
+  CK(cudaGraphCreate(&guard.g, 0));
+  cudaGraph_t g = guard.g;
   cudaGraphConditionalHandle h;
   CK(cudaGraphConditionalHandleCreate(&h, g, 0, cudaGraphCondAssignDefault));
   const int n_handles = p->class_switch ? 1 : p->n_classes;
@@ -473,8 +500,7 @@ int build_round_graph(lrcvt_plan* p, int var) {
       CK(cudaGraphAddNode(&nif, body, prev ? &prev : nullptr, prev ? 1 : 0, &pi));
       ib = pi.conditional.phGraph_out[0];
     }
-    long long cap = class_cap(c);
-    if (c == p->n_classes - 1 && cap < p->n_inband) cap = p->n_inband;
+    const long long cap = class_launch_items(c, p->n_classes, p->n_inband);
     CK(cudaStreamBeginCaptureToGraph(p->cap, ib, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
     int rc = 0;
     if (c == 0 && p->coop_in_graph && cap <= p->ew_small) {
@@ -490,7 +516,6 @@ int build_round_graph(lrcvt_plan* p, int var) {
     prev = nif;
   }
   CK(cudaGraphInstantiate(&p->graph[var], g, 0));
-  CK(cudaGraphDestroy(g));
   return 0;
 }
 
@@ -583,6 +608,14 @@ double pw_join(int64_t n, const std::vector<double>& v, size_t& k) {
 extern "C" {
 
 int lrcvt_version(void) { return 1; }
+
+int32_t lrcvt_round_classes(int64_t n_inband, int64_t* launch_items, int32_t max_classes) {
+  if (n_inband < 0 || n_inband >= (int64_t(1) << 31) || (max_classes > 0 && !launch_items))
+    return set_error(LRCVT_E_ARG, "lrcvt_round_classes: bad arguments");
+  const int n = count_classes(n_inband);
+  for (int c = 0; c < n && c < max_classes; c++) launch_items[c] = class_launch_items(c, n, n_inband);
+  return n;
+}
 
 const char* lrcvt_last_error(void) { return g_last_error.c_str(); }
 
@@ -704,8 +737,7 @@ int lrcvt_plan_create(lrcvt_plan** plan, int64_t nx, int64_t ny, int64_t nz, dou
     need = b > need ? b : need;
   }
   p->cub_bytes = need;
-  p->n_classes = 1;
-  while (p->n_classes < MAX_CLASSES && class_cap(p->n_classes - 1) < nin) p->n_classes++;
+  p->n_classes = count_classes(nin);
   if (cudaMallocHost((void**)&p->h_ctl, sizeof(RoundCtl)) != cudaSuccess) {
     lrcvt_plan_destroy(p);
     return set_error(LRCVT_E_NOMEM, "pinned round control");
@@ -736,8 +768,8 @@ int lrcvt_plan_create(lrcvt_plan** plan, int64_t nx, int64_t ny, int64_t nz, dou
     cudaDeviceGetAttribute(&coop_ok, cudaDevAttrCooperativeLaunch, dev);
     if (!coop_ok || nbc <= 0) p->coop = false;
     if (!p->coop) p->coop_in_graph = false;
-    const int loop_min = (p->coop && !p->coop_in_graph) ? p->ew_small : 0;
-    cudaMemcpy(&p->ctl->loop_min, &loop_min, sizeof(int), cudaMemcpyHostToDevice);
+    // set on the device by k_phase1_start at the start of every classify
+    p->loop_min = (p->coop && !p->coop_in_graph) ? p->ew_small : 0;
   }
   if (dalloc((char**)&p->cub_tmp, (int64_t)need)) { lrcvt_plan_destroy(p); return LRCVT_E_NOMEM; }
   *plan = p;
@@ -840,7 +872,7 @@ int lrcvt_classify(lrcvt_plan* p, int64_t n_sites, const double* d_site_pos,
   k_seed_groups<<<grid_for(S, 128), 128, 0, st>>>(g, p->nbm, p->sk_key2, p->sk_val2, p->sk_d, S, ss,
                                                   d_dist, p->site1, p->bm, p->list_a, p->counters);  // marks bm (round-1 frontier)
   CKL("k_seed_groups"); LAUNCHED(1);
-  k_phase1_start<<<1, 1, 0, st>>>(p->ctl, p->counters, p->list_a, p->list_b, ss, d_dist, p->site1);
+  k_phase1_start<<<1, 1, 0, st>>>(p->ctl, p->counters, p->list_a, p->list_b, ss, d_dist, p->site1, p->loop_min);
   CKL("k_phase1_start"); LAUNCHED(1);
   // phase 1 (tessellation.py:152-156)
   CKR(run_rounds(p, 0, st));
@@ -850,13 +882,13 @@ int lrcvt_classify(lrcvt_plan* p, int64_t n_sites, const double* d_site_pos,
   p->eligible_sites = S;
   k_site1_to_state<<<grid_for(g.n, 256, 148 * 16), 256, 0, st>>>(g, p->site1, p->site_pos, ss, d_dist);
   CKL("k_site1_to_state"); LAUNCHED(1);
-  k_phase2_copy<<<148 * 4, 256, 0, st>>>(p->eligible, p->d_nel, p->ctl);
+  k_phase2_copy<<<148 * 4, 256, 0, st>>>(p->eligible, p->d_nel, p->ctl, p->counters);
   CKL("k_phase2_copy"); LAUNCHED(1);
   const int var2 = g.dyadic ? 1 : 2;
   for (;;) {
     CKR(run_rounds(p, var2, st));
     stats->sweeps++;
-    k_sweep_start<<<1, 1, 0, st>>>(p->ctl, p->eligible, p->d_nel);
+    k_sweep_start<<<1, 1, 0, st>>>(p->ctl, p->eligible, p->d_nel, p->counters);
     CKL("k_sweep_start"); LAUNCHED(1);
     if (p->timing) CK(cudaEventRecord(p->ev0, st));
     CKR(launch_round_kernels(p, var2, (int)p->n_inband, st, -1));  // sweep: n_el <= in-band
@@ -1275,7 +1307,7 @@ int lrcvt_mg_begin(lrcvt_plan* p, int64_t n_sites, const double* d_site_pos, con
   k_seed_groups<<<grid_for(S, 128), 128, 0, st>>>(g, p->nbm, p->sk_key2, p->sk_val2, p->sk_d, S, ss, d_dist, p->site1, p->bm,
                                                   p->list_a, p->counters, p->zlo, p->zhi);
   CKL("k_seed_groups");
-  k_phase1_start<<<1, 1, 0, st>>>(p->ctl, p->counters, p->list_a, p->list_b, ss, d_dist, p->site1);
+  k_phase1_start<<<1, 1, 0, st>>>(p->ctl, p->counters, p->list_a, p->list_b, ss, d_dist, p->site1, p->loop_min);
   CKL("k_phase1_start");
   CK(cudaMemcpyAsync(p->h_ctl, p->ctl, sizeof(RoundCtl), cudaMemcpyDeviceToHost, st));
   CKR(sync_counters(p, st, C_NCOUNTERS));
@@ -1293,7 +1325,7 @@ int lrcvt_mg_phase2(lrcvt_plan* p, int64_t n_sites, const int32_t* d_site_comp, 
   k_site1_to_state<<<grid_for(p->g.n, 256, 148 * 16), 256, 0, st>>>(p->g, p->site1, p->site_pos, p->mg_ss,
                                                                      p->mg_dist);
   CKL("k_site1_to_state");
-  k_phase2_copy<<<148 * 4, 256, 0, st>>>(p->eligible, p->d_nel, p->ctl);
+  k_phase2_copy<<<148 * 4, 256, 0, st>>>(p->eligible, p->d_nel, p->ctl, p->counters);
   CKL("k_phase2_copy");
   CK(cudaMemcpyAsync(p->h_counters + 7, p->d_nel, sizeof(int), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
@@ -1311,7 +1343,7 @@ int lrcvt_mg_eval(lrcvt_plan* p, int32_t phase, int32_t sweep, int64_t* n_evalua
   cudaStream_t st = (cudaStream_t)stream;
   int n = p->h_ncur;
   if (sweep) {
-    k_sweep_start<<<1, 1, 0, st>>>(p->ctl, p->eligible, p->d_nel);
+    k_sweep_start<<<1, 1, 0, st>>>(p->ctl, p->eligible, p->d_nel, p->counters);
     CKL("k_sweep_start");
     n = (int)p->n_eligible;
   }

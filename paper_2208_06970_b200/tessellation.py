@@ -86,17 +86,28 @@ class DeviceTessellation(Tessellation):
         self.weights = weights
 
     def _get(self, name):
+        """Materialise one output as numpy: (site_of, src) are split on the
+        device (lrcvt_unpack_site_src) and every array is read straight into
+        page-locked host memory from torch's caching host allocator (freed
+        arrays return their pages to the pool), one PCIe pass per array."""
         host = self._host
         if name not in host:
             ss, dist, state = self._dev
+            torch = self._engine.torch
             if name in ("site_of", "src"):
-                a = ss.cpu().numpy()
-                host.setdefault("site_of", np.ascontiguousarray(a[:, 0]))
-                host.setdefault("src", np.ascontiguousarray(a[:, 1]))
-            elif name == "dist":
-                host["dist"] = dist.cpu().numpy()
+                n = ss.shape[0]
+                so = torch.empty(n, dtype=torch.int32, device="cuda")
+                sr = torch.empty(n, dtype=torch.int32, device="cuda")
+                _lib.check(self._engine.L.lrcvt_unpack_site_src(ss.data_ptr(), n, so.data_ptr(), sr.data_ptr(),
+                                                                 _lib.stream_handle(torch)), "lrcvt_unpack_site_src")
+                got = [_to_pinned(torch, so), _to_pinned(torch, sr)]
+                torch.cuda.current_stream().synchronize()
+                host.setdefault("site_of", got[0].numpy())
+                host.setdefault("src", got[1].numpy())
             else:
-                host["state"] = state.cpu().numpy()
+                got = _to_pinned(torch, dist if name == "dist" else state)
+                torch.cuda.current_stream().synchronize()
+                host[name] = got.numpy()
         return host[name]
 
     def _set(self, name, value):
@@ -111,6 +122,14 @@ class DeviceTessellation(Tessellation):
     def device_state(self):
         """(ss, dist, state) device tensors while they are authoritative, else None."""
         return None if self._dirty else self._dev
+
+
+def _to_pinned(torch, t):
+    """Asynchronous device->host copy into a page-locked tensor (the caller
+    synchronises the stream before reading it)."""
+    h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+    h.copy_(t, non_blocking=True)
+    return h
 
 
 def voxel_length(dims, spacing) -> float:

@@ -362,6 +362,134 @@ def dump_lloyd(G, S, T, big: bool):
         print(f"{name}: {time.time() - t0:.1f}s", file=sys.stderr)
 
 
+def c4_aggregates(G, ST, grid, labels, tess, every=64, bins=64):
+    """C4 per-cell aggregation (pipeline.py:187-238) with the reference's own
+    stats.accumulate / merge / histogram1d. The region selection
+    `in_band[region == rid]` is taken from one stable argsort by site instead of
+    S boolean scans (the selected index arrays are identical, so every
+    accumulate call sees the same samples in the same order); at 512^3 the
+    O(S * N_in) scan of aggregate_moments itself would take days.
+    Stored: sha256 of the exact per-region n / min / max arrays, full blobs of
+    every `every`-th region, all component and layer blobs, and 64-bin
+    histograms of f and g per cell on the global in-band [min, max] axes
+    (sha of the full count table + the sampled rows)."""
+    in_band = np.nonzero(labels.component != -1)[0]
+    comp = labels.component[in_band]
+    region = tess.site_of[in_band]
+    order = np.argsort(region, kind="stable")
+    sreg = region[order]
+    nS = len(tess.sites)
+    starts = np.searchsorted(sreg, np.arange(nS), side="left")
+    ends = np.searchsorted(sreg, np.arange(nS), side="right")
+    unassigned = in_band[region == -1]
+    site_comp = tess.site_components()
+    layer_of_comp = {c.id: c.layer for c in labels.component_table}
+    pairs = [("f", "f"), ("f", "g"), ("g", "g")]
+    out = {"every": every, "pairs": pairs, "n_sites": nS}
+    for xn, yn in pairs:
+        fx = grid.fields[xn].astype(np.float64)
+        fy = grid.fields[yn].astype(np.float64)
+        region_aggs = []
+        for rid in range(nS):
+            sel = in_band[order[starts[rid]:ends[rid]]]
+            region_aggs.append(ST.accumulate(np.stack([fx[sel], fy[sel]], axis=1), xn, yn))
+        stray = {}
+        if unassigned.size:
+            uc = labels.component[unassigned]
+            for c in np.unique(uc):
+                sel = unassigned[uc == c]
+                stray[int(c)] = ST.accumulate(np.stack([fx[sel], fy[sel]], axis=1), xn, yn)
+        comp_aggs = {}
+        for info in labels.component_table:
+            agg = ST.MomentAggregate(x_name=xn, y_name=yn)
+            for rid in np.nonzero(site_comp == info.id)[0]:
+                agg = ST.merge(agg, region_aggs[int(rid)])
+            if info.id in stray:
+                agg = ST.merge(agg, stray[info.id])
+            comp_aggs[info.id] = agg
+        layer_aggs = []
+        for li in range(labels.n_layers):
+            agg = ST.MomentAggregate(x_name=xn, y_name=yn)
+            for cid, a in comp_aggs.items():
+                if layer_of_comp[cid] == li:
+                    agg = ST.merge(agg, a)
+            layer_aggs.append(agg)
+        key = f"{xn}{yn}"
+        out[key] = {
+            "n_sha": sha(np.array([a.n for a in region_aggs], np.int64)),
+            "minmax_sha": sha(np.array([[a.min_x, a.max_x, a.min_y, a.max_y] for a in region_aggs], np.float64)),
+            "regions": {str(r): region_aggs[r].to_dict() for r in range(0, nS, every)},
+            "stray": {str(c): a.to_dict() for c, a in stray.items()},
+            "components": {str(c): a.to_dict() for c, a in comp_aggs.items()},
+            "layers": [a.to_dict() for a in layer_aggs],
+        }
+        print(f"  c4 aggregate {key} done", file=sys.stderr, flush=True)
+    hist = {}
+    for nm in ("f", "g"):
+        v = grid.fields[nm].astype(np.float64)
+        lo, hi = float(v[in_band].min()), float(v[in_band].max())
+        rows = np.zeros((nS, bins + 2), np.int64)
+        for rid in range(nS):
+            sel = in_band[order[starts[rid]:ends[rid]]]
+            h = ST.histogram1d(v[sel], bins=bins, lo=lo, hi=hi)
+            rows[rid, :bins] = h.counts
+            rows[rid, bins] = h.underflow
+            rows[rid, bins + 1] = h.overflow
+        hist[nm] = {"lo": lo, "hi": hi, "sha": sha(rows),
+                    "rows": {str(r): rows[r].tolist() for r in range(0, nS, every)}}
+    out["hist"] = hist
+    return out
+
+
+def dump_c4(G, S, T, ST):
+    """C4: 512^3 random-smooth, iso [0.35, 0.5, 0.65, 0.8],
+    alpha 32768, weight 'g'; two Lloyd iterations + the final classify
+    recorded as digests, then the per-cell aggregation of the final state.
+    ~17 GB RSS, tens of minutes in this container."""
+    t0 = time.time()
+    kind, dims, iso = "random-smooth", (512, 512, 512), [0.35, 0.5, 0.65, 0.8]
+    sp = dict(alpha=32768, weight_field="g", seed=0)
+    g = G.synth_field(kind, dims, 0)
+    print(f"c4 synth {time.time() - t0:.0f}s", file=sys.stderr, flush=True)
+    l = G.label_components(G.classify_isobands(g, G.IsobandSpec("f", iso)))
+    print(f"c4 labels {time.time() - t0:.0f}s", file=sys.stderr, flush=True)
+    params = S.SeedingParams(**sp)
+    sites, _ = S.seed_sites(g, l, params)
+    weights = S.voxel_weights(g, params)
+    rec = {"sites": [[list(s.position) for s in sites]], "trace": [], "iter_stats": []}
+    for it in range(2):
+        t1 = time.time()
+        tess = T.voronoi_classify(g, l, sites, weights)
+        t2 = time.time()
+        sites, mean_ds = T.centroidal_update(tess)
+        rec["trace"].append(mean_ds)
+        rec["sites"].append([list(s.position) for s in sites])
+        rec["iter_stats"].append({"site_of": sha(tess.site_of), "dist": sha(tess.dist), "src": sha(tess.src),
+                                  "state": sha(tess.state), "rounds": tess.report["rounds"],
+                                  "sweeps": tess.report["sweeps"], "assigned": tess.report["assigned"],
+                                  "classify_s": t2 - t1, "update_s": time.time() - t2})
+        print(f"c4 iteration {it}: classify {t2 - t1:.0f}s", file=sys.stderr, flush=True)
+        del tess
+    final = T.voronoi_classify(g, l, sites, weights)
+    rec["final"] = {"site_of": sha(final.site_of), "dist": sha(final.dist), "src": sha(final.src),
+                    "state": sha(final.state),
+                    "report": {k: final.report[k] for k in ("rounds", "sweeps", "assigned")}}
+    rec["site_comp"] = [s.component_id for s in sites]
+    rec["labels"] = {"layer": sha(l.layer), "component": sha(l.component), "n_components": l.n_components,
+                     "table": table_json(l)}
+    rec["f_sha"] = sha(g.fields["f"])
+    rec["g_sha"] = sha(g.fields["g"])
+    rec.update(kind=kind, dims=list(dims), iso=iso, params=sp, iters=2)
+    arrays = {"sites_hist": np.array(rec.pop("sites"), dtype=np.float64)}
+    np.savez_compressed(OUT / "lloyd_c4_smooth512.npz", **arrays)
+    (OUT / "lloyd_c4_smooth512.json").write_text(json.dumps(rec))
+    print(f"c4 lloyd done {time.time() - t0:.0f}s", file=sys.stderr, flush=True)
+    agg = c4_aggregates(G, ST, g, l, final)
+    with gzip.open(OUT / "aggregate_c4.json.gz", "wt") as fh:
+        json.dump(agg, fh)
+    print(f"c4 all done {time.time() - t0:.0f}s", file=sys.stderr, flush=True)
+
+
 def dump_blocks(G, S, T, P):
     """Block-mode run_pipeline (pipeline.py:45-160) results for the
     distributed block driver."""
@@ -508,6 +636,8 @@ def main():
         dump_layout(G, S, T, P)
     if "sitegraph" in todo:
         dump_sitegraph(G, S, T)
+    if "c4" in todo:  # only on request (--only c4): tens of minutes, ~17 GB
+        dump_c4(G, S, T, ST)
 
 
 if __name__ == "__main__":

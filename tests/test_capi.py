@@ -101,3 +101,29 @@ def test_new_entry_points_validate_arguments_without_device():
     assert rc == -2 and b"lrcvt_layout_records" in L.lrcvt_last_error()
     rc = L.lrcvt_region_adjacency(4, 4, 4, None, None, 3, 10, None, ctypes.byref(got), None)
     assert rc == -2 and b"lrcvt_region_adjacency" in L.lrcvt_last_error()
+
+
+@pytest.mark.parametrize("n_inband", [0, 1, 2047, 2048, 2049, 5_000_000, (1 << 29) - 1, 1 << 29, (1 << 29) + 1,
+                                      (1 << 30) + 12345, (1 << 31) - 2])
+def test_round_classes_cover_inband_without_overflow(n_inband):
+    """Size classes of the round graph (lrcvt_capi.cu build_round_graph): every
+    class launches between 1 and n_inband voxels (< 2^31, so the int launch
+    arithmetic cannot wrap -- the class cap 2^31 above 2^29 in-band voxels
+    did), the launch sizes grow, and the last class covers the whole in-band
+    set (a sweep or phase-2 start evaluates all of it)."""
+    import ctypes
+
+    from paper_2208_06970_b200 import _lib
+
+    L = _lib.lib()
+    buf = (ctypes.c_int64 * 16)()
+    n = L.lrcvt_round_classes(n_inband, buf, 16)
+    assert 1 <= n <= 12
+    items = [buf[i] for i in range(n)]
+    nin = max(n_inband, 1)
+    assert all(1 <= it <= nin < 2**31 for it in items)
+    assert items == sorted(items)
+    assert items[-1] == nin
+    # the eval launch grid of the largest class fits an int
+    assert (items[-1] + 63) // 64 < 2**31
+    assert L.lrcvt_round_classes(-1, buf, 16) < 0
