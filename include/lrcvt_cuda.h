@@ -187,29 +187,79 @@ int lrcvt_region_adjacency(int64_t nx, int64_t ny, int64_t nz, const int32_t *d_
                            const int32_t *d_component, int64_t n_sites, int64_t max_edges,
                            int64_t *d_edges, int64_t *n_edges, void *stream);
 
-/* Multi-GPU global mode (z-slab partitioned evaluation over replicated
- * state). A rank's plan owns planes [zlo, zhi); the caller
- * drives rounds: begin -> { eval -> all-gather proposals -> commit }* ->
- * phase2 -> { rounds, sweep (eval sweep=1, commit sweep=1) }* -> finish.
- * Proposals are 24-byte records {f64 d; i32 v, site, src, pad} at
- * lrcvt_mg_proposals(plan) after an eval; commit takes the concatenation of
- * all ranks' proposals (any order). Counts are summed by the caller for
- * report rounds/evaluations/commits; results are bit-identical to
- * lrcvt_classify on one domain. */
+/* Multi-GPU global mode: ONE volume in
+ * z-slabs, one plan per rank. A rank owns planes [zlo, zhi); its own slab and
+ * one halo plane on each side are kept current locally, the rare far reads
+ * (phase-2 shortcut nodes, phi chains of the vote) go to the owning rank's
+ * state buffer through peer pointers (same device, CUDA IPC, or NVLink P2P).
+ * The caller drives the rounds and the collectives:
+ *   set_slab, set_peers -> begin -> { eval -> exchange boundary proposals
+ *   (lo -> rank-1, hi -> rank+1) -> commit(halo) -> all-reduce frontier }*
+ *   -> phase2 -> { rounds, sweep (eval/commit with sweep=1) }* -> finish.
+ * Proposals are 24-byte records {f64 d; i32 v, site, src, pad}. Results,
+ * rounds, sweeps and the summed evaluation / commit counters equal
+ * lrcvt_classify on one domain bit for bit. */
 int lrcvt_mg_set_slab(lrcvt_plan *plan, int64_t zlo, int64_t zhi);
+/* plan-owned full-volume (site_of, src) int32[N][2] / dist float64[N]
+ * buffers (allocated on first call; base allocations, IPC-exportable) */
+int lrcvt_mg_state(lrcvt_plan *plan, void **d_ss, void **d_dist);
+/* z_bounds int64[world + 1] (rank r owns [z_bounds[r], z_bounds[r+1]));
+ * peer_ss / peer_dist: HOST arrays of `world` device pointers, valid in this
+ * process, to every rank's state buffers (this rank's own included) */
+int lrcvt_mg_set_peers(lrcvt_plan *plan, int32_t world, const int64_t *z_bounds, void *const *peer_ss,
+                       void *const *peer_dist);
 int lrcvt_mg_begin(lrcvt_plan *plan, int64_t n_sites, const double *d_site_pos,
                    const int32_t *d_site_comp, int32_t *d_site_src, double *d_dist,
                    int64_t *n_frontier, void *stream);
 int lrcvt_mg_phase2(lrcvt_plan *plan, int64_t n_sites, const int32_t *d_site_comp,
                     int64_t *n_frontier, void *stream);
+/* evaluate the own frontier (sweep: the own eligible list); *n_prop =
+ * improved proposals, *n_lo / *n_hi = those on planes zlo / zhi - 1, at
+ * lrcvt_mg_boundary(plan, 0 / 1) for rank - 1 / rank + 1 */
 int lrcvt_mg_eval(lrcvt_plan *plan, int32_t phase, int32_t sweep, int64_t *n_evaluated,
-                  int64_t *n_prop, void *stream);
-void *lrcvt_mg_proposals(lrcvt_plan *plan);
-int lrcvt_mg_copy_proposals(lrcvt_plan *plan, void *d_dst, int64_t n, void *stream);
-int lrcvt_mg_commit(lrcvt_plan *plan, const void *d_props, int64_t n_props, int32_t sweep,
+                  int64_t *n_prop, int64_t *n_lo, int64_t *n_hi, void *stream);
+void *lrcvt_mg_boundary(lrcvt_plan *plan, int32_t side);
+/* commit the own proposals and the n_halo proposals received from the
+ * neighbour ranks; *n_next = the own next frontier */
+int lrcvt_mg_commit(lrcvt_plan *plan, const void *d_halo, int64_t n_halo, int32_t sweep,
                     int64_t *n_next, void *stream);
+/* state bits of the own slab; *assigned = own assigned voxels */
 int lrcvt_mg_finish(lrcvt_plan *plan, const int32_t *d_site_src, uint8_t *d_state,
                     int64_t *assigned, void *stream);
+/* vote over the own slab. Unit weights (exact integers): vote_exact writes
+ * d_acc uint64[4][S] partial sums; all-reduce (sum) them, then
+ * vote_exact_finish -> d_sums float64[4][S]. Any weights (voxel-order
+ * chains): vote_box writes the own per-site boxes int32[6][S] (x0,y0,z0
+ * min; x1,y1,z1 max) -> all-reduce min / max; vote_scan mode 1 (sites whose
+ * box starts in this slab, chains from 0) and mode 2 (box starts earlier,
+ * chains continue from d_init = the running sums after the previous slab)
+ * write d_out float64[4][S]; vote_carry builds the running sums after this
+ * slab for the next rank; the last rank's are the sums. */
+int lrcvt_mg_vote_exact(lrcvt_plan *plan, int64_t n_sites, const int32_t *d_site_src, uint64_t *d_acc,
+                        void *stream);
+int lrcvt_mg_vote_exact_finish(lrcvt_plan *plan, int64_t n_sites, const uint64_t *d_acc, double *d_sums,
+                               void *stream);
+int lrcvt_mg_vote_box(lrcvt_plan *plan, int64_t n_sites, const int32_t *d_site_src, int32_t *d_box,
+                      void *stream);
+int lrcvt_mg_vote_scan(lrcvt_plan *plan, int64_t n_sites, const int32_t *d_site_comp, int32_t weight_mode,
+                       const void *d_weights, int32_t mode, const int32_t *d_box, const double *d_init,
+                       double *d_out, void *stream);
+int lrcvt_mg_vote_carry(lrcvt_plan *plan, int64_t n_sites, const int32_t *d_box, const double *d_res,
+                        const double *d_carry_in, double *d_carry_out, void *stream);
+/* _move_sites on every rank from the identical reduced sums */
+int lrcvt_mg_move(lrcvt_plan *plan, int64_t n_sites, const double *d_site_pos, const int32_t *d_site_comp,
+                  const double *d_sums, double backoff, double *d_new_pos, double *d_disp,
+                  int64_t *empty_regions, void *stream);
+/* CUDA IPC of a base device allocation (64-byte handle) */
+int lrcvt_ipc_export(const void *d_ptr, uint8_t *handle64);
+int lrcvt_ipc_open(const uint8_t *handle64, void **d_ptr);
+int lrcvt_ipc_close(void *d_ptr);
+
+/* Output buffers passed to consecutive lrcvt_classify calls of this plan
+ * are the same and untouched in between (a Lloyd loop over one engine's
+ * buffers), and lrcvt_plan_reuse_eligible holds: the classify then resets
+ * and rewrites only the eligible voxels. */
+int lrcvt_plan_persistent_outputs(lrcvt_plan *plan, int enable);
 
 /* Instrumentation for bench.py: enable CUDA-event timing of every k_eval
  * launch (the dominant kernel) on the plan; read back launches, voxels

@@ -71,14 +71,28 @@ SIGNATURES = {
     "lrcvt_plan_profile": (c_int, [c_void_p, POINTER(c_double)]),
     "lrcvt_round_classes": (c_int32, [c_int64, POINTER(c_int64), c_int32]),
     "lrcvt_mg_set_slab": (c_int, [c_void_p, c_int64, c_int64]),
+    "lrcvt_mg_state": (c_int, [c_void_p, POINTER(c_void_p), POINTER(c_void_p)]),
+    "lrcvt_mg_set_peers": (c_int, [c_void_p, c_int32, c_void_p, c_void_p, c_void_p]),
     "lrcvt_mg_begin": (c_int, [c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_void_p, POINTER(c_int64),
                                c_void_p]),
     "lrcvt_mg_phase2": (c_int, [c_void_p, c_int64, c_void_p, POINTER(c_int64), c_void_p]),
-    "lrcvt_mg_eval": (c_int, [c_void_p, c_int32, c_int32, POINTER(c_int64), POINTER(c_int64), c_void_p]),
-    "lrcvt_mg_proposals": (c_void_p, [c_void_p]),
-    "lrcvt_mg_copy_proposals": (c_int, [c_void_p, c_void_p, c_int64, c_void_p]),
+    "lrcvt_mg_eval": (c_int, [c_void_p, c_int32, c_int32, POINTER(c_int64), POINTER(c_int64), POINTER(c_int64),
+                              POINTER(c_int64), c_void_p]),
+    "lrcvt_mg_boundary": (c_void_p, [c_void_p, c_int32]),
     "lrcvt_mg_commit": (c_int, [c_void_p, c_void_p, c_int64, c_int32, POINTER(c_int64), c_void_p]),
     "lrcvt_mg_finish": (c_int, [c_void_p, c_void_p, c_void_p, POINTER(c_int64), c_void_p]),
+    "lrcvt_mg_vote_exact": (c_int, [c_void_p, c_int64, c_void_p, c_void_p, c_void_p]),
+    "lrcvt_mg_vote_exact_finish": (c_int, [c_void_p, c_int64, c_void_p, c_void_p, c_void_p]),
+    "lrcvt_mg_vote_box": (c_int, [c_void_p, c_int64, c_void_p, c_void_p, c_void_p]),
+    "lrcvt_mg_vote_scan": (c_int, [c_void_p, c_int64, c_void_p, c_int32, c_void_p, c_int32, c_void_p, c_void_p,
+                                   c_void_p, c_void_p]),
+    "lrcvt_mg_vote_carry": (c_int, [c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "lrcvt_mg_move": (c_int, [c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_double, c_void_p, c_void_p,
+                              POINTER(c_int64), c_void_p]),
+    "lrcvt_ipc_export": (c_int, [c_void_p, c_void_p]),
+    "lrcvt_ipc_open": (c_int, [c_void_p, POINTER(c_void_p)]),
+    "lrcvt_ipc_close": (c_int, [c_void_p]),
+    "lrcvt_plan_persistent_outputs": (c_int, [c_void_p, c_int]),
     "lrcvt_isobands": (
         c_int,
         [c_int64, c_void_p, c_void_p, c_int32, c_void_p, c_void_p],

@@ -43,18 +43,19 @@ struct RoundCtl {
   int tile_next;     // dynamic tile scheduler of the eval kernels (reset per round)
   int loop_min;      // the round graph loops while n_cur > loop_min (small frontiers: k_rounds_small)
   long long rounds, evals, commits, rounds_p1;
+  long long rounds_small, small_launches;  // rounds run inside k_rounds_small, and its launches
 };
 
 // Counter slots in the plan's small device array.
-enum { C_NIMP = 0, C_NNEXT = 1, C_BAD = 2, C_ASSIGNED = 3, C_DONE = 4, C_NCOUNTERS = 8 };
+enum { C_NIMP = 0, C_NNEXT = 1, C_BAD = 2, C_ASSIGNED = 3, C_DONE = 4, C_LO = 5, C_HI = 6, C_NCOUNTERS = 8 };
 
-__global__ void k_fill_state(int2* __restrict__ ss, double* __restrict__ dist, int* __restrict__ site1,
-                             int64_t n) {
+// tessellation.py:120-122 fill values of the output arrays (site1, the
+// phase-1 scratch, is reset over the eligible list by k_fill_list)
+__global__ void k_fill_state(int2* __restrict__ ss, double* __restrict__ dist, int64_t n) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (; i < n; i += stride) {
     ss[i] = make_int2(LRCVT_NONE, LRCVT_NONE);
-    site1[i] = LRCVT_NONE;
     dist[i] = __longlong_as_double(0x7ff0000000000000LL);  // +inf
   }
 }
@@ -300,54 +301,6 @@ __device__ __forceinline__ void round_end(RoundCtl* ctl, int* counters, const cu
   }
 }
 
-__global__ void __launch_bounds__(128) k_commit(const Prop* __restrict__ imp,
-                                                int* __restrict__ counters, RoundCtl* __restrict__ ctl,
-                                                Geo g, const uint32_t* __restrict__ nbm,
-                                                uint32_t* __restrict__ bm,
-                                                const cudaGraphConditionalHandle* __restrict__ hs, int n_classes,
-                                                cudaGraphConditionalHandle loop, int end_mode,
-                                                int zlo = 0, int zhi = 1 << 30) {
-  const int n_imp = *(volatile int*)(counters + C_NIMP);
-  int* next = ctl->nxt;
-  int2* __restrict__ ss = ctl->ss;
-  double* __restrict__ dist = ctl->dist;
-  int* __restrict__ site1 = ctl->site1;
-  const int stride = gridDim.x * blockDim.x;
-  for (int base = blockIdx.x * blockDim.x; base < n_imp; base += stride) {  // warp-uniform
-    const int i = base + threadIdx.x;
-    const bool active = i < n_imp;
-    int v = 0;
-    if (active) {
-      const Prop p = imp[i];
-      v = p.v;
-      // explicit global stores (the pointers come from RoundCtl); ss and dist
-      // are rebuilt from site1 once when phase 2 starts (k_site1_to_state),
-      // saving two scattered 8-byte stores per phase-1 commit.
-      // Phase 1 keeps only the compact LOS site: its distance is a pure
-      // function of (voxel, site) and is recomputed where needed.
-      if (site1) {
-        __stcg(site1 + v, p.src == p.v ? p.s : (int)LRCVT_NONE);
-      } else {
-        __stcg(ss + v, make_int2(p.s, p.src));
-        __stcg(dist + v, p.d);
-      }
-    }
-    mark_and_append(g, nbm, active, v, false, bm, next, counters + C_NNEXT, zlo, zhi);
-  }
-  if (end_mode < 0) return;  // sweep / multi-GPU: the host ends the round
-  // the last block to finish ends the round (no separate launch)
-  __shared__ bool last;
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) last = atomicAdd(counters + C_DONE, 1) == (int)gridDim.x - 1;
-  __syncthreads();
-  if (last && threadIdx.x == 0) {
-    __threadfence();
-    counters[C_DONE] = 0;
-    round_end(ctl, counters, hs, n_classes, loop, end_mode);
-  }
-}
-
 __global__ void k_loop_init(const RoundCtl* ctl, cudaGraphConditionalHandle h,
                             const cudaGraphConditionalHandle* hs, int n_classes) {
   set_size_class(ctl->n_cur, hs, n_classes);
@@ -366,6 +319,7 @@ __global__ void k_phase1_start(RoundCtl* ctl, int* counters, int* first, int* se
   ctl->stash = nullptr;
   ctl->n_cur = counters[C_NNEXT];
   ctl->rounds = ctl->evals = ctl->commits = ctl->rounds_p1 = 0;
+  ctl->rounds_small = ctl->small_launches = 0;
   ctl->sweep_imp = 0;
   ctl->tile_next = 0;
   counters[C_NIMP] = 0;
@@ -375,17 +329,39 @@ __global__ void k_phase1_start(RoundCtl* ctl, int* counters, int* first, int* se
 // phase 2 starts from a copy of the eligible list (tessellation.py:166-167)
 // phase-1 states are LOS (src == v): (site_of, src) and dist = |c_v - p_site|
 // (the very dist3 the phase-1 kernels and the seeds compute) from site1
+// Over the eligible list (list != null, *n_list entries: every voxel phase 1
+// can have assigned) or the voxel range [v0, v1) (list == null: the halo
+// planes of a multi-GPU slab).
 __global__ void k_site1_to_state(Geo g, const int* __restrict__ site1, const double4* __restrict__ site_pos,
-                                 int2* __restrict__ ss, double* __restrict__ dist) {
+                                 int2* __restrict__ ss, double* __restrict__ dist, const int* __restrict__ list,
+                                 const int* __restrict__ n_list, int64_t v0, int64_t v1) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < g.n; i += stride) {
-    const int s = __ldcs(site1 + i);
+  const int64_t n = list ? (int64_t)*n_list : v1 - v0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+    const int v = list ? __ldg(list + i) : (int)(v0 + i);
+    const int s = __ldcs(site1 + v);
     if (s < 0) continue;  // still the fill values (-1, -1) / inf
     int x, y, z;
-    coords(g, (int)i, x, y, z);
+    coords(g, v, x, y, z);
     const double4 p = ld_d4(site_pos + s);
-    __stcs(ss + i, make_int2(s, (int)i));
-    __stcs(dist + i, dist3(centre1(x, g.sx), centre1(y, g.sy), centre1(z, g.sz), p.x, p.y, p.z));
+    __stcs(ss + v, make_int2(s, v));
+    __stcs(dist + v, dist3(centre1(x, g.sx), centre1(y, g.sy), centre1(z, g.sz), p.x, p.y, p.z));
+  }
+}
+
+// fill values (-1, -1) / inf / site1 -1 for the voxels of a list (*n_list
+// entries); ss / dist may be null (site1 only)
+__global__ void k_fill_list(const int* __restrict__ list, const int* __restrict__ n_list, int2* __restrict__ ss,
+                            double* __restrict__ dist, int* __restrict__ site1) {
+  const int n = *n_list;
+  const int stride = gridDim.x * blockDim.x;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const int v = __ldg(list + i);
+    if (ss) {
+      ss[v] = make_int2(LRCVT_NONE, LRCVT_NONE);
+      dist[v] = __longlong_as_double(0x7ff0000000000000LL);
+    }
+    site1[v] = LRCVT_NONE;
   }
 }
 
@@ -487,21 +463,25 @@ __global__ void __launch_bounds__(128) k_seed_groups(Geo g, const uint32_t* __re
   mark_and_append(g, nbm, head, v, true, bm, next, counters + C_NNEXT, zlo, zhi);
 }
 
-// tessellation.py:191-194 state bits, plus the `assigned` count.
-__global__ void k_state(const int2* __restrict__ ss, int64_t n, uint8_t* __restrict__ state,
-                        int* __restrict__ counters) {
+// tessellation.py:191-194 state bits, plus the `assigned` count, over the
+// eligible list (list != null, *n_list entries: no other voxel can be
+// assigned; the caller zeroes the rest of `state`) or the range [v0, v1).
+__global__ void k_state(const int2* __restrict__ ss, const int* __restrict__ list, const int* __restrict__ n_list,
+                        int64_t v0, int64_t v1, uint8_t* __restrict__ state, int* __restrict__ counters) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t n = list ? (int64_t)*n_list : v1 - v0;
   int cnt = 0;
   for (; i < n; i += stride) {
-    const int2 a = ss[i];
+    const int v = list ? __ldg(list + i) : (int)(v0 + i);
+    const int2 a = ss[v];
     uint8_t st = 0;
     if (a.x != LRCVT_NONE) {
       st = 2 | 4;
       cnt++;
-      if (a.y == (int)i) st |= 1;
+      if (a.y == v) st |= 1;
     }
-    if (state) state[i] = st;
+    if (state) state[v] = st;
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);

@@ -1,0 +1,394 @@
+// compact.cuh -- the next relaxation frontier, in voxel order.
+//
+// _apply_and_enqueue (_kernels.py:313-333) enqueues the same-component
+// 26-neighbours of every improved voxel, deduplicated by `stamp`. The set is
+// all that matters (each round reads only pre-round state), so the order of
+// the list is ours to choose. k_commit marks the set in the frontier bitmap
+// (1 bit per voxel, flat x-fastest order) and in a coarse bitmap (1 bit per
+// 32 words = 1024 voxels); k_compact then turns the bitmap into the next
+// worklist IN VOXEL ORDER with one single-pass scan (decoupled look-back over
+// tiles of 2048 words), clearing the words it read. A voxel-ordered list puts
+// neighbouring voxels in neighbouring lanes and concurrently running CTAs on
+// neighbouring planes, so the eval kernels' 26-neighbour gathers and ray
+// walks hit L1/L2 instead of re-reading HBM (the proposal-order list of the
+// append scheme scattered them: 122 B of DRAM per evaluation at 512^3
+// against 20 algorithmic).
+#pragma once
+#include "classify.cuh"
+
+namespace lrcvt {
+
+constexpr int CT_THREADS = 256;
+constexpr int CT_WPT = 8;                          // bitmap words per thread
+constexpr int CT_WORDS = CT_THREADS * CT_WPT;      // words per tile (65536 voxels)
+constexpr int CT_CHUNK = 32;                       // words per coarse bit
+constexpr int CT_CWORDS = CT_WORDS / CT_CHUNK / 32;  // coarse words per tile (2)
+
+// persistent compaction state (zeroed once per plan): [0] epoch, [1] dynamic
+// tile counter, [2] finished-CTA counter
+enum { CS_EPOCH = 0, CS_TILE = 1, CS_DONE = 2, CS_N = 4 };
+
+__host__ __device__ inline int64_t compact_tiles(int64_t bm_words) { return (bm_words + CT_WORDS - 1) / CT_WORDS; }
+__host__ __device__ inline int64_t coarse_words(int64_t bm_words) {
+  return compact_tiles(bm_words) * CT_CWORDS;  // whole tiles: no bounds checks on the coarse reads
+}
+
+// Set the frontier bits of v's same-component neighbours (v itself when
+// `self`) -- the marking half of mark_and_append (classify.cuh), plus the
+// coarse bit of every word this thread turned from empty to non-empty.
+__device__ __forceinline__ void mark_bits(const Geo& g, const uint32_t* __restrict__ nbm, bool active, int v,
+                                          uint32_t* __restrict__ bm, uint32_t* __restrict__ cbm, int zlo = 0,
+                                          int zhi = 1 << 30) {
+  if (!active) return;
+  int vz = 0;
+  const bool slab = zlo > 0 || zhi < g.nz;
+  if (slab) {
+    vz = (int)((unsigned)v / (unsigned)g.nxy);
+    if (vz < zlo - 1 || vz > zhi) return;
+  }
+  const unsigned same = __ldg(nbm + v);
+#pragma unroll
+  for (int r = 0; r < 9; r++) {
+    const int dy = r % 3 - 1, dz = r / 3 - 1;
+    if (slab && (vz + dz < zlo || vz + dz >= zhi)) continue;
+    const int j0 = 3 * r;
+    unsigned want = 0;  // bit t <=> dx = t - 1
+#pragma unroll
+    for (int t = 0; t < 3; t++) {
+      const int j = j0 + t;
+      if (j != 13) {
+        const int k = j < 13 ? j : j - 1;
+        if ((same >> k) & 1u) want |= 1u << t;
+      }
+    }
+    if (!want) continue;
+    const int f = __ffs(want) - 1;
+    const unsigned wv = want >> f;
+    const int base = v + (f - 1) + dy * g.nx + dz * g.nxy;
+    const int w0 = base >> 5;
+    const int sh = base & 31;
+    const unsigned lo = wv << sh;
+    const unsigned hi = sh > 29 ? (wv >> (32 - sh)) : 0u;
+    if (lo && (__ldca(bm + w0) & lo) != lo) {
+      const uint32_t old = atomicOr(bm + w0, lo);
+      if (old == 0u) {
+        const int c = w0 >> 5;  // coarse bit = word / 32
+        const uint32_t cb = 1u << (c & 31);
+        if (!(__ldca(cbm + (c >> 5)) & cb)) atomicOr(cbm + (c >> 5), cb);
+      }
+    }
+    if (hi && (__ldca(bm + w0 + 1) & hi) != hi) {
+      const uint32_t old = atomicOr(bm + w0 + 1, hi);
+      if (old == 0u) {
+        const int c = (w0 + 1) >> 5;
+        const uint32_t cb = 1u << (c & 31);
+        if (!(__ldca(cbm + (c >> 5)) & cb)) atomicOr(cbm + (c >> 5), cb);
+      }
+    }
+  }
+}
+
+// _kernels.py:285-334: commit the round's improved proposals and enqueue
+// the same-component neighbours of every improved voxel. Proposals are SPARSE
+// (pf != null): slot i of `imp` belongs to frontier item i and pf[i] says
+// whether it improved -- the eval kernels write them without atomics or
+// block barriers -- or a COMPACT list of n_props records (pf == null; the
+// multi-GPU steps). Enqueue: `compact` = mark the frontier + coarse bitmaps
+// only (k_compact builds the voxel-ordered list and ends the round), else the
+// stamp-deduplicated append of mark_and_append, the last CTA ending the round
+// unless end_mode < 0. Grid-stride (at most one resident wave); the number of
+// committed proposals is added to counters[C_NIMP] once per CTA.
+constexpr int CM_THREADS = 256;
+constexpr int CM_SLOTS = 4 * CM_THREADS;  // sparse slots scanned per CTA step
+
+__device__ __forceinline__ void commit_one(const Prop& p, int2* __restrict__ ss, double* __restrict__ dist,
+                                           int* __restrict__ site1) {
+  // ss and dist are rebuilt from site1 once when phase 2 starts
+  // (k_site1_to_state): phase 1 keeps only the compact LOS site, whose
+  // distance is a pure function of (voxel, site)
+  if (site1) {
+    __stcg(site1 + p.v, p.src == p.v ? p.s : (int)LRCVT_NONE);
+  } else {
+    __stcg(ss + p.v, make_int2(p.s, p.src));
+    __stcg(dist + p.v, p.d);
+  }
+}
+
+__global__ void __launch_bounds__(CM_THREADS) k_commit(const Prop* __restrict__ imp, const uint8_t* __restrict__ pf,
+                                                       int n_props, int* __restrict__ counters,
+                                                       RoundCtl* __restrict__ ctl, Geo g,
+                                                       const uint32_t* __restrict__ nbm, uint32_t* __restrict__ bm,
+                                                       uint32_t* __restrict__ cbm, int compact,
+                                                       const cudaGraphConditionalHandle* __restrict__ hs,
+                                                       int n_classes, cudaGraphConditionalHandle loop, int end_mode,
+                                                       int zlo, int zhi) {
+  __shared__ int s_idx[CM_SLOTS];
+  __shared__ int s_wcnt[CM_THREADS / 32];
+  __shared__ int s_tot;
+  int2* __restrict__ ss = ctl->ss;
+  double* __restrict__ dist = ctl->dist;
+  int* __restrict__ site1 = ctl->site1;
+  int* next = ctl->nxt;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int mine = 0;
+  if (pf) {
+    // sparse slots: each CTA step compacts the improved slots of CM_SLOTS
+    // frontier items into shared memory, then commits them one per thread
+    // (full lanes for the enqueue, one list reservation per CTA step)
+    const int n = *(volatile const int*)&ctl->n_cur;
+    for (int base = blockIdx.x * CM_SLOTS; base < n; base += gridDim.x * CM_SLOTS) {  // block-uniform
+      const int i0 = base + 4 * threadIdx.x;
+      uchar4 f = make_uchar4(0, 0, 0, 0);
+      if (i0 + 3 < n && ((reinterpret_cast<uintptr_t>(pf + i0) & 3) == 0)) {
+        f = *reinterpret_cast<const uchar4*>(pf + i0);
+      } else {
+        if (i0 < n) f.x = pf[i0];
+        if (i0 + 1 < n) f.y = pf[i0 + 1];
+        if (i0 + 2 < n) f.z = pf[i0 + 2];
+        if (i0 + 3 < n) f.w = pf[i0 + 3];
+      }
+      const int c = (f.x != 0) + (f.y != 0) + (f.z != 0) + (f.w != 0);
+      int incl = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      if (lane == 31) s_wcnt[wid] = incl;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        int sum = 0;
+        for (int w = 0; w < CM_THREADS / 32; w++) {
+          const int t = s_wcnt[w];
+          s_wcnt[w] = sum;
+          sum += t;
+        }
+        s_tot = sum;
+      }
+      __syncthreads();
+      int pos = s_wcnt[wid] + incl - c;
+      if (f.x) s_idx[pos++] = i0;
+      if (f.y) s_idx[pos++] = i0 + 1;
+      if (f.z) s_idx[pos++] = i0 + 2;
+      if (f.w) s_idx[pos++] = i0 + 3;
+      __syncthreads();
+      const int tot = s_tot;
+      for (int k0 = 0; k0 < tot; k0 += CM_THREADS) {  // block-uniform
+        const int k = k0 + threadIdx.x;
+        const bool take = k < tot;
+        int v = 0;
+        if (take) {
+          const Prop p = imp[s_idx[k]];
+          v = p.v;
+          mine++;
+          commit_one(p, ss, dist, site1);
+        }
+        if (compact)
+          mark_bits(g, nbm, take, v, bm, cbm, zlo, zhi);
+        else
+          mark_and_append(g, nbm, take, v, false, bm, next, counters + C_NNEXT, zlo, zhi);
+      }
+      __syncthreads();  // s_idx / s_wcnt reused by the next step
+    }
+  } else {
+    const int n = n_props;
+    for (int base = blockIdx.x * blockDim.x; base < n; base += gridDim.x * blockDim.x) {  // block-uniform
+      const int i = base + threadIdx.x;
+      const bool take = i < n;
+      int v = 0;
+      if (take) {
+        const Prop p = imp[i];
+        v = p.v;
+        mine++;
+        commit_one(p, ss, dist, site1);
+      }
+      if (compact)
+        mark_bits(g, nbm, take, v, bm, cbm, zlo, zhi);
+      else
+        mark_and_append(g, nbm, take, v, false, bm, next, counters + C_NNEXT, zlo, zhi);
+    }
+  }
+  // committed count: warp sums, one atomic per CTA
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
+  __shared__ int s_cnt;
+  if (threadIdx.x == 0) s_cnt = 0;
+  __syncthreads();
+  if (lane == 0 && mine) atomicAdd(&s_cnt, mine);
+  __syncthreads();
+  if (threadIdx.x == 0 && s_cnt) atomicAdd(counters + C_NIMP, s_cnt);
+  if (compact || end_mode < 0) return;  // k_compact / the host / k_sweep_end ends the round
+  // the last block to finish ends the round (no separate launch)
+  __shared__ bool last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(counters + C_DONE, 1) == (int)gridDim.x - 1;
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    __threadfence();
+    counters[C_DONE] = 0;
+    round_end(ctl, counters, hs, n_classes, loop, end_mode);
+  }
+}
+
+// multi-GPU eval step: sparse proposal slots -> a compact list (any order)
+__global__ void __launch_bounds__(128) k_gather_props(const Prop* __restrict__ imp, const uint8_t* __restrict__ pf,
+                                                      int n, Prop* __restrict__ out, int* __restrict__ count) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool take = i < n && pf[i];
+  const int slot = block_append(count, take);
+  if (take) out[slot] = imp[i];
+}
+
+// tile status word: epoch << 33 | inclusive << 32 | count
+__device__ __forceinline__ unsigned long long ct_pack(unsigned epoch, bool incl, unsigned cnt) {
+  return ((unsigned long long)epoch << 33) | ((unsigned long long)(incl ? 1u : 0u) << 32) | cnt;
+}
+
+__device__ __forceinline__ unsigned long long ct_load(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void ct_store(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// end_mode: 1 = round end inside the round graph (arms the size class and the
+// WHILE condition), 0 = round end without graph conditionals (host-driven
+// rounds), -1 = only publish the count in counters[C_NNEXT] (sweeps and the
+// multi-GPU steps, whose own kernels swap the lists).
+__global__ void __launch_bounds__(CT_THREADS) k_compact(uint32_t* __restrict__ bm, uint32_t* __restrict__ cbm,
+                                                        int64_t bm_words, unsigned long long* __restrict__ status,
+                                                        int* __restrict__ cs, RoundCtl* __restrict__ ctl,
+                                                        int* __restrict__ counters,
+                                                        const cudaGraphConditionalHandle* __restrict__ hs,
+                                                        int n_classes, cudaGraphConditionalHandle loop, int end_mode) {
+  __shared__ int s_tile;
+  __shared__ unsigned s_epoch;
+  __shared__ int s_warp[CT_THREADS / 32];
+  __shared__ unsigned s_excl;
+  __shared__ bool s_last;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  if (tid == 0) {
+    s_tile = atomicAdd(cs + CS_TILE, 1);  // dynamic ids: a tile only waits on tiles already started
+    s_epoch = (unsigned)*(volatile int*)(cs + CS_EPOCH) + 1u;
+  }
+  __syncthreads();
+  const int tile = s_tile;
+  const unsigned epoch = s_epoch & 0x7fffffffu;
+  const int64_t w0 = (int64_t)tile * CT_WORDS + (int64_t)tid * CT_WPT;
+  // coarse bit of this thread's 8 words: chunk (tid * 8) / 32 of the tile
+  const uint32_t cw = cbm[(int64_t)tile * CT_CWORDS + (tid * CT_WPT / CT_CHUNK) / 32];
+  const bool any = (cw >> ((tid * CT_WPT / CT_CHUNK) & 31)) & 1u;
+  uint32_t w[CT_WPT];
+  int cnt = 0;
+#pragma unroll
+  for (int k = 0; k < CT_WPT; k++) w[k] = 0u;
+  if (any && w0 < bm_words) {
+    if (w0 + CT_WPT <= bm_words) {
+      const uint4 a = *reinterpret_cast<const uint4*>(bm + w0);
+      const uint4 b = *reinterpret_cast<const uint4*>(bm + w0 + 4);
+      w[0] = a.x; w[1] = a.y; w[2] = a.z; w[3] = a.w; w[4] = b.x; w[5] = b.y; w[6] = b.z; w[7] = b.w;
+    } else {
+      for (int k = 0; k < CT_WPT; k++)
+        if (w0 + k < bm_words) w[k] = bm[w0 + k];
+    }
+#pragma unroll
+    for (int k = 0; k < CT_WPT; k++) cnt += __popc(w[k]);
+  }
+  // block exclusive scan of the per-thread counts
+  int incl = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  if (lane == 31) s_warp[wid] = incl;
+  __syncthreads();
+  if (wid == 0) {
+    int x = lane < CT_THREADS / 32 ? s_warp[lane] : 0;
+    int xi = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, xi, o);
+      if (lane >= o) xi += t;
+    }
+    if (lane < CT_THREADS / 32) s_warp[lane] = xi - x;  // exclusive warp offsets
+    const unsigned total = (unsigned)__shfl_sync(0xffffffffu, xi, CT_THREADS / 32 - 1);
+    // publish, then look back over the predecessors (decoupled look-back)
+    unsigned excl = 0;
+    if (tile == 0) {
+      if (lane == 0) ct_store(status, ct_pack(epoch, true, total));
+    } else {
+      if (lane == 0) ct_store(status + tile, ct_pack(epoch, false, total));
+      int j = tile - 1;
+      for (;;) {
+        const int jj = j - lane;
+        unsigned long long st = 0;
+        bool ok = jj < 0;
+        while (true) {
+          if (!ok) {
+            st = ct_load(status + jj);
+            ok = (unsigned)(st >> 33) == epoch;
+          }
+          if (__all_sync(0xffffffffu, ok)) break;
+        }
+        const bool inc = jj >= 0 && ((st >> 32) & 1ull);
+        const unsigned val = jj >= 0 ? (unsigned)st : 0u;
+        const unsigned incm = __ballot_sync(0xffffffffu, inc);
+        const int stop = incm ? __ffs(incm) - 1 : 32;  // first lane (nearest tile) holding an inclusive prefix
+        unsigned part = lane <= stop ? val : 0u;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+        excl += part;
+        if (incm || j - 32 < 0) break;
+        j -= 32;
+      }
+      if (lane == 0) ct_store(status + tile, ct_pack(epoch, true, excl + total));
+    }
+    if (lane == 0) s_excl = excl;
+  }
+  __syncthreads();
+  int pos = (int)s_excl + s_warp[wid] + incl - cnt;
+  int* out = ctl->nxt;
+  if (cnt) {
+#pragma unroll
+    for (int k = 0; k < CT_WPT; k++) {
+      uint32_t m = w[k];
+      const int vb = (int)((w0 + k) << 5);
+      while (m) {
+        const int b = __ffs(m) - 1;
+        m &= m - 1u;
+        out[pos++] = vb + b;
+      }
+    }
+    // consume the words read (the commit of the next round marks afresh)
+    if (w0 + CT_WPT <= bm_words) {
+      *reinterpret_cast<uint4*>(bm + w0) = make_uint4(0u, 0u, 0u, 0u);
+      *reinterpret_cast<uint4*>(bm + w0 + 4) = make_uint4(0u, 0u, 0u, 0u);
+    } else {
+      for (int k = 0; k < CT_WPT; k++)
+        if (w0 + k < bm_words) bm[w0 + k] = 0u;
+    }
+  }
+  __syncthreads();  // every thread has read its coarse word
+  if (tid < CT_CWORDS) cbm[(int64_t)tile * CT_CWORDS + tid] = 0u;
+  // the last CTA publishes the count and ends the round
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) s_last = atomicAdd(cs + CS_DONE, 1) == (int)gridDim.x - 1;
+  __syncthreads();
+  if (s_last && tid == 0) {
+    __threadfence();
+    const unsigned long long st = ct_load(status + (gridDim.x - 1));
+    counters[C_NNEXT] = (int)(unsigned)st;  // inclusive prefix of the last tile = list length
+    cs[CS_TILE] = 0;
+    cs[CS_DONE] = 0;
+    cs[CS_EPOCH] = (int)epoch;
+    __threadfence();
+    if (end_mode >= 0) round_end(ctl, counters, hs, n_classes, loop, end_mode);
+  }
+}
+
+}  // namespace lrcvt

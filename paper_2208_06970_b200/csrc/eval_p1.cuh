@@ -47,8 +47,7 @@ __device__ __forceinline__ void p1_tile(const int* __restrict__ list, int n, con
                                                    const double* __restrict__ dist,
                                                    const double4* __restrict__ site_pos,
                                                    uint32_t* __restrict__ bm,
-                                                   Prop* __restrict__ imp,
-                                                   int* __restrict__ counters) {
+                                                   Prop* __restrict__ imp, uint8_t* __restrict__ pf) {
   __shared__ int s_row[26][BLOCK];  // [k][thread]: conflict-free column per thread
   // per-warp queue of speculated rays (no block-wide barrier needed)
   __shared__ int q_v[BLOCK * P1_SPEC], q_s[BLOCK * P1_SPEC];
@@ -117,7 +116,9 @@ __device__ __forceinline__ void p1_tile(const int* __restrict__ list, int n, con
   }
 #pragma unroll
   for (int j = 0; j < P1_TAB; j++) {
-    if (ts[j] >= 0) {
+    if (ts[j] == orig_s) {  // the voxel's own LOS site: the very dist3 already computed (orig_d)
+      td[j] = orig_d;
+    } else if (ts[j] >= 0) {
       const double4 sp = ld_d4(site_pos + ts[j]);
       td[j] = dist3(px, py, pz, sp.x, sp.y, sp.z);
     }
@@ -225,10 +226,13 @@ __device__ __forceinline__ void p1_tile(const int* __restrict__ list, int n, con
     }
   }
   const bool improved = active && ((best_s != orig_s) || (best_d < __dsub_rn(orig_d, LRCVT_EPS)));
-  Prop pr;
-  pr.d = best_d; pr.v = v; pr.s = best_s; pr.src = best_src; pr.pad = 0;
-  const int slot = block_append(counters + C_NIMP, improved);
-  if (improved) imp[slot] = pr;
+  // sparse proposal: slot i of this frontier item (no atomics, no block barrier)
+  if (improved) {
+    Prop pr;
+    pr.d = best_d; pr.v = v; pr.s = best_s; pr.src = best_src; pr.pad = 0;
+    imp[i] = pr;
+  }
+  if (active) pf[i] = improved ? 1 : 0;
 }
 
 // Grid-stride over 128-voxel tiles of the worklist held in the round control
@@ -239,8 +243,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_eval_p1(RoundCtl* __restrict__ 
                                                    const uint32_t* __restrict__ nbm,
                                                    const double4* __restrict__ site_pos,
                                                    uint32_t* __restrict__ bm,
-                                                   Prop* __restrict__ imp,
-                                                   int* __restrict__ counters) {
+                                                   Prop* __restrict__ imp, uint8_t* __restrict__ pf) {
   const int n = ctl->n_cur;
   const int* list = ctl->cur;
   const int* __restrict__ site1 = ctl->site1;
@@ -249,7 +252,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_eval_p1(RoundCtl* __restrict__ 
   // (exact grid on the host path, size-class grid >= n inside the graph)
   const int base = blockIdx.x * BLOCK;
   if (base >= n) return;
-  p1_tile<BLOCK>(list, n, base + (int)threadIdx.x, g, comp, nbm, site1, dist, site_pos, bm, imp, counters);
+  p1_tile<BLOCK>(list, n, base + (int)threadIdx.x, g, comp, nbm, site1, dist, site_pos, bm, imp, pf);
 }
 
 }  // namespace lrcvt

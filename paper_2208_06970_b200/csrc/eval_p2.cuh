@@ -17,13 +17,16 @@
 //    and resume at the next neighbour -- the reference's decision sequence.
 #pragma once
 #include "classify.cuh"
+#include "mg.cuh"
 
 namespace lrcvt {
 
 constexpr int P2_STAB = 4;  // distinct LOS sites
 constexpr int P2_NTAB = 6;  // distinct shortcut nodes
 
-template <int BLOCK, bool DYADIC>
+// MG: multi-GPU slab mode, the far node reads of shortcut candidates go
+// through the PeerView (mg.cuh)
+template <int BLOCK, bool DYADIC, bool MG>
 __device__ __forceinline__ void p2_tile(const int* __restrict__ list, int n, const int i, const Geo& g,
                                                    const int* __restrict__ comp,
                                                    const uint32_t* __restrict__ nbm,
@@ -31,8 +34,8 @@ __device__ __forceinline__ void p2_tile(const int* __restrict__ list, int n, con
                                                    const double* __restrict__ dist,
                                                    const double4* __restrict__ site_pos,
                                                    uint32_t* __restrict__ bm,
-                                                   Prop* __restrict__ imp,
-                                                   int* __restrict__ counters) {
+                                                   Prop* __restrict__ imp, uint8_t* __restrict__ pf,
+                                                   const PeerView* __restrict__ pv) {
   __shared__ int s_site[26][BLOCK];    // site(w) or -1 (not a candidate source)
   __shared__ int s_node[26][BLOCK];    // -2: w is LOS; -1: no shortcut; else src(w)
   __shared__ double s_dw[26][BLOCK];   // dist[w] + |c_w - p| (path candidate)
@@ -123,9 +126,15 @@ __device__ __forceinline__ void p2_tile(const int* __restrict__ list, int n, con
     best_s = sv.x; best_src = sv.y;
     orig_d = best_d; orig_s = best_s;
   }
+  // a LOS voxel's stored distance is exactly dist3(c_v, site) (every LOS
+  // commit and seed computes it in this operand order), so its own site's
+  // entry needs no recomputation
+  const bool orig_los = active && best_src == v;
 #pragma unroll
   for (int j = 0; j < P2_STAB; j++) {
-    if (ts[j] >= 0) {
+    if (orig_los && ts[j] == orig_s) {
+      td[j] = orig_d;
+    } else if (ts[j] >= 0) {
       const double4 sp = ld_d4(site_pos + ts[j]);
       td[j] = dist3(px, py, pz, sp.x, sp.y, sp.z);
     }
@@ -134,13 +143,13 @@ __device__ __forceinline__ void p2_tile(const int* __restrict__ list, int n, con
   for (int j = 0; j < P2_NTAB; j++) {
     const int u = tu[j];
     if (u >= 0) {
-      const int2 nu = __ldg(ss + u);
+      const int2 nu = ld_ss<MG>(pv, ss, u);
       if (nu.x >= 0 && __ldg(comp + u) == cv) {
         int ux, uy, uz;
         coords(g, u, ux, uy, uz);
         tus[j] = nu.x;
-        tud[j] = __dadd_rn(__ldg(dist + u), dist3(px, py, pz, centre1(ux, g.sx), centre1(uy, g.sy),
-                                          centre1(uz, g.sz)));
+        tud[j] = __dadd_rn(ld_dist<MG>(pv, dist, u), dist3(px, py, pz, centre1(ux, g.sx), centre1(uy, g.sy),
+                                                   centre1(uz, g.sz)));
       }
     }
   }
@@ -178,13 +187,13 @@ __device__ __forceinline__ void p2_tile(const int* __restrict__ list, int n, con
         for (int j = 0; j < P2_NTAB; j++)
           if (tu[j] == u) { su = tus[j]; d = tud[j]; hit = true; }
         if (!hit) {  // more than P2_NTAB distinct nodes (rare)
-          const int2 nu = __ldg(ss + u);
+          const int2 nu = ld_ss<MG>(pv, ss, u);
           if (nu.x >= 0 && __ldg(comp + u) == cv) {
             int ux, uy, uz;
             coords(g, u, ux, uy, uz);
             su = nu.x;
-            d = __dadd_rn(__ldg(dist + u), dist3(px, py, pz, centre1(ux, g.sx), centre1(uy, g.sy),
-                                         centre1(uz, g.sz)));
+            d = __dadd_rn(ld_dist<MG>(pv, dist, u), dist3(px, py, pz, centre1(ux, g.sx), centre1(uy, g.sy),
+                                                  centre1(uz, g.sz)));
           }
         }
         if (su >= 0 && beats(d, su, best_d, best_s)) { rs = su; rd = d; rsrc = u; los = false; break; }
@@ -210,20 +219,23 @@ __device__ __forceinline__ void p2_tile(const int* __restrict__ list, int n, con
     k++;
   }
   const bool improved = active && ((best_s != orig_s) || (best_d < __dsub_rn(orig_d, LRCVT_EPS)));
-  Prop pr;
-  pr.d = best_d; pr.v = v; pr.s = best_s; pr.src = best_src; pr.pad = 0;
-  const int slot = block_append(counters + C_NIMP, improved);
-  if (improved) imp[slot] = pr;
+  // sparse proposal: slot i of this frontier item (no atomics, no block barrier)
+  if (improved) {
+    Prop pr;
+    pr.d = best_d; pr.v = v; pr.s = best_s; pr.src = best_src; pr.pad = 0;
+    imp[i] = pr;
+  }
+  if (active) pf[i] = improved ? 1 : 0;
 }
 
-template <int BLOCK, bool DYADIC>
+template <int BLOCK, bool DYADIC, bool MG = false>
 __global__ void __launch_bounds__(BLOCK, 512 / BLOCK) k_eval_p2(RoundCtl* __restrict__ ctl, Geo g,
                                                                 const int* __restrict__ comp,
                                                                 const uint32_t* __restrict__ nbm,
                                                                 const double4* __restrict__ site_pos,
                                                                 uint32_t* __restrict__ bm,
-                                                                Prop* __restrict__ imp,
-                                                                int* __restrict__ counters) {
+                                                                Prop* __restrict__ imp, uint8_t* __restrict__ pf,
+                                                                const PeerView* __restrict__ pv = nullptr) {
   const int n = ctl->n_cur;
   const int* list = ctl->cur;
   const int2* __restrict__ ss = ctl->ss;
@@ -232,7 +244,7 @@ __global__ void __launch_bounds__(BLOCK, 512 / BLOCK) k_eval_p2(RoundCtl* __rest
   // (exact grid on the host path, size-class grid >= n inside the graph)
   const int base = blockIdx.x * BLOCK;
   if (base >= n) return;
-  p2_tile<BLOCK, DYADIC>(list, n, base + (int)threadIdx.x, g, comp, nbm, ss, dist, site_pos, bm, imp, counters);
+  p2_tile<BLOCK, DYADIC, MG>(list, n, base + (int)threadIdx.x, g, comp, nbm, ss, dist, site_pos, bm, imp, pf, pv);
 }
 
 }  // namespace lrcvt

@@ -25,6 +25,7 @@
 //   replays the exact sequential fold over the gathered candidates.
 #pragma once
 #include "classify.cuh"
+#include "mg.cuh"
 
 namespace lrcvt {
 
@@ -187,12 +188,13 @@ __device__ __forceinline__ T ldst(const T* p) {
 }
 
 // evaluate frontier item i of `list` with the calling warp (all 32 lanes)
-template <bool PHASE2, bool COH>
+template <bool PHASE2, bool COH, bool MG = false>
 __device__ __forceinline__ void ew_voxel(const int* list, const int2* ss, const int* site1, const double* dist,
                                          const int i, const Geo& g, const int* __restrict__ comp,
                                          const uint32_t* __restrict__ nbm, const double4* __restrict__ site_pos,
                                          uint32_t* __restrict__ bm, Prop* __restrict__ imp,
-                                         int* __restrict__ counters, EwStage& st) {
+                                         uint8_t* __restrict__ pf, EwStage& st,
+                                         const PeerView* __restrict__ pv = nullptr) {
   const int lane = threadIdx.x & 31;
   const int v = ldst<COH>(list + i);
   int x, y, z;
@@ -245,12 +247,12 @@ __device__ __forceinline__ void ew_voxel(const int* list, const int2* ss, const 
         ed[1] = dist3(px, py, pz, sp.x, sp.y, sp.z); es[1] = nw.x; esrc[1] = v; et[1] = EW_LOS;
       } else if (PHASE2 && nw.y >= 0) {
         const int u = nw.y;
-        const int2 nu = ldst<COH>(ss + u);
+        const int2 nu = MG ? ld_ss<true>(pv, ss, u) : ldst<COH>(ss + u);
         if (nu.x >= 0 && __ldg(comp + u) == cv) {
           int ux, uy, uz;
           coords(g, u, ux, uy, uz);
-          ed[1] = __dadd_rn(ldst<COH>(dist + u), dist3(px, py, pz, centre1(ux, g.sx), centre1(uy, g.sy),
-                                                   centre1(uz, g.sz)));
+          ed[1] = __dadd_rn(MG ? ld_dist<true>(pv, dist, u) : ldst<COH>(dist + u),
+                            dist3(px, py, pz, centre1(ux, g.sx), centre1(uy, g.sy), centre1(uz, g.sz)));
           es[1] = nu.x; esrc[1] = u; et[1] = EW_SHORT;
         }
       }
@@ -277,27 +279,29 @@ __device__ __forceinline__ void ew_voxel(const int* list, const int2* ss, const 
   }
   if (lane == 0) {
     const bool improved = (best_s != orig_s) || (best_d < __dsub_rn(orig_d, LRCVT_EPS));
-    if (improved) {
+    if (improved) {  // sparse proposal slot i (k_commit reads pf)
       Prop pr;
       pr.d = best_d; pr.v = v; pr.s = best_s; pr.src = best_src; pr.pad = 0;
-      imp[atomicAdd(counters + C_NIMP, 1)] = pr;
+      imp[i] = pr;
     }
+    pf[i] = improved ? 1 : 0;
   }
 }
 
-template <bool PHASE2>
+template <bool PHASE2, bool MG = false>
 __global__ void __launch_bounds__(32 * EW_WARPS) k_eval_warp(RoundCtl* __restrict__ ctl, Geo g,
                                                              const int* __restrict__ comp,
                                                              const uint32_t* __restrict__ nbm,
                                                              const double4* __restrict__ site_pos,
                                                              uint32_t* __restrict__ bm, Prop* __restrict__ imp,
-                                                             int* __restrict__ counters) {
+                                                             uint8_t* __restrict__ pf,
+                                                             const PeerView* __restrict__ pv = nullptr) {
   __shared__ EwStage stage[EW_WARPS];
   const int wid = threadIdx.x >> 5;
   const int i = blockIdx.x * EW_WARPS + wid;
   if (i >= ctl->n_cur) return;  // warp-uniform
-  ew_voxel<PHASE2, false>(ctl->cur, ctl->ss, ctl->site1, ctl->dist, i, g, comp, nbm, site_pos, bm, imp, counters,
-                          stage[wid]);
+  ew_voxel<PHASE2, false, MG>(ctl->cur, ctl->ss, ctl->site1, ctl->dist, i, g, comp, nbm, site_pos, bm, imp, pf,
+                              stage[wid], pv);
 }
 
 }  // namespace lrcvt

@@ -13,6 +13,7 @@
 
 #include "../../include/lrcvt_cuda.h"
 #include "classify.cuh"
+#include "compact.cuh"
 #include "vote.cuh"
 #include "masks.cuh"
 #include "eval_p1.cuh"
@@ -195,13 +196,27 @@ struct lrcvt_plan {
   int* list_a = nullptr;
   int* list_b = nullptr;
   int* eligible = nullptr;
-  Prop* imp = nullptr;
+  Prop* imp = nullptr;      // sparse proposals: slot i <-> frontier item i
+  uint8_t* pf = nullptr;    // pf[i] = 1 iff slot i holds an improved proposal
+  Prop* mg_props = nullptr;  // compact proposal list of a multi-GPU eval step
+  bool compact = false;      // voxel-ordered frontier through k_compact (LRCVT_COMPACT=1)
+  int p1_bs = 128, p2_bs = 64;  // eval CTA sizes (LRCVT_EVAL_BS=p1,p2)
   uint32_t* bm = nullptr;  // frontier bitmap (1 bit per voxel)
   int64_t bm_words = 0;
+  uint32_t* cbm = nullptr;                 // coarse frontier bitmap (1 bit per 32 words), compact.cuh
+  unsigned long long* ct_status = nullptr;  // k_compact tile status (decoupled look-back)
+  int* ct_state = nullptr;                  // k_compact epoch / tile / done counters
+  int ct_tiles = 0;
   uint32_t* nbm = nullptr;  // static same-component neighbour masks
   int* site1 = nullptr;     // phase-1 LOS site per voxel (RoundCtl::site1)
   int2* mg_ss = nullptr;    // (site_of, src) buffer of the multi-GPU classify in flight
   double* mg_dist = nullptr;
+  int2* mg_own_ss = nullptr;      // plan-owned multi-GPU state buffers (lrcvt_mg_state; IPC-exportable)
+  double* mg_own_dist = nullptr;
+  PeerView* d_pv = nullptr;       // multi-GPU peer view (lrcvt_mg_set_peers), null on one domain
+  int mg_world = 1;
+  Prop* mg_lo = nullptr;          // boundary-plane proposals for rank - 1 / rank + 1
+  Prop* mg_hi = nullptr;
   int* counters = nullptr;
   int* h_counters = nullptr;  // pinned
   uint8_t* has_site = nullptr;
@@ -222,6 +237,9 @@ struct lrcvt_plan {
   unsigned long long* vt_pv2 = nullptr;
   int* seg_b = nullptr;
   int* seg_e = nullptr;
+  int2* vt_sp = nullptr;  // (site, phi) per voxel for the bounding-box vote
+  int* vt_box = nullptr;  // [6][S] per-site bounding boxes
+  bool vote_bbox = true;  // LRCVT_VOTE=sort: stable radix sort of (site, (phi, v)) pairs instead
   // cub
   void* cub_tmp = nullptr;
   size_t cub_bytes = 0;
@@ -255,6 +273,11 @@ struct lrcvt_plan {
   int ncl_arg() const { return class_switch ? -n_classes : n_classes; }
   bool eligible_valid = false;
   int64_t eligible_sites = -1;
+  // persistent output buffers (lrcvt_plan_persistent_outputs): the last classify's output pointers
+  bool persist = false;
+  const void* last_ss = nullptr;
+  const void* last_dist = nullptr;
+  const void* last_state = nullptr;
   // optional per-launch timing of the dominant kernel (k_eval)
   bool timing = false;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr;
@@ -323,43 +346,76 @@ int launch_eval_kernel(lrcvt_plan* p, int var, int items, cudaStream_t st) {
   if (items < 1) items = 1;
   if ((items <= p->ew_small && p->warp_eval) || p->warp_eval_all) {
     const int blocks = (int)(((int64_t)items + EW_WARPS - 1) / EW_WARPS);
-    if (var == 0)
+    if (var != 0 && p->d_pv)
+      k_eval_warp<true, true><<<blocks, 32 * EW_WARPS, 0, st>>>(p->ctl, g, p->comp, p->nbm, p->site_pos, p->bm,
+                                                                 p->imp, p->pf, p->d_pv);
+    else if (var == 0)
       k_eval_warp<false><<<blocks, 32 * EW_WARPS, 0, st>>>(p->ctl, g, p->comp, p->nbm, p->site_pos, p->bm, p->imp,
-                                                            p->counters);
+                                                            p->pf);
     else
       k_eval_warp<true><<<blocks, 32 * EW_WARPS, 0, st>>>(p->ctl, g, p->comp, p->nbm, p->site_pos, p->bm, p->imp,
-                                                           p->counters);
+                                                           p->pf);
     CKL("k_eval_warp");
     return 0;
   }
-  const int bs = var == 0 ? 128 : 64;
+  const int bs = var == 0 ? p->p1_bs : p->p2_bs;
   const int blocks = (int)(((int64_t)items + bs - 1) / bs);
-  if (var == 0 && items >= P1_BIG_ROUND)
-    k_eval_p1<128, P1_MIN_BLOCKS_BIG><<<blocks, 128, 0, st>>>(p->ctl, g, p->comp, p->nbm, p->site_pos, p->bm,
-                                                              p->imp, p->counters);
-  else if (var == 0)
-    k_eval_p1<128><<<blocks, 128, 0, st>>>(p->ctl, g, p->comp, p->nbm, p->site_pos, p->bm, p->imp, p->counters);
-  else if (var == 1)
-    k_eval_p2<64, true><<<blocks, 64, 0, st>>>(p->ctl, g, p->comp, p->nbm, p->site_pos, p->bm, p->imp,
-                                               p->counters);
-  else
-    k_eval_p2<64, false><<<blocks, 64, 0, st>>>(p->ctl, g, p->comp, p->nbm, p->site_pos, p->bm, p->imp,
-                                                p->counters);
+  RoundCtl* c = p->ctl;
+  const int* cm = p->comp;
+  const uint32_t* nb = p->nbm;
+  const double4* sp = p->site_pos;
+  const bool big = items >= P1_BIG_ROUND;
+  if (var == 0) {  // CTA size x register budget (see eval_p1.cuh)
+    if (bs == 32 && big)
+      k_eval_p1<32, 32><<<blocks, 32, 0, st>>>(c, g, cm, nb, sp, p->bm, p->imp, p->pf);
+    else if (bs == 32)
+      k_eval_p1<32, 20><<<blocks, 32, 0, st>>>(c, g, cm, nb, sp, p->bm, p->imp, p->pf);
+    else if (big)
+      k_eval_p1<128, P1_MIN_BLOCKS_BIG><<<blocks, 128, 0, st>>>(c, g, cm, nb, sp, p->bm, p->imp, p->pf);
+    else
+      k_eval_p1<128><<<blocks, 128, 0, st>>>(c, g, cm, nb, sp, p->bm, p->imp, p->pf);
+  } else if (p->d_pv) {  // multi-GPU slab: far reads through the peer view
+    if (var == 1)
+      k_eval_p2<64, true, true><<<blocks, 64, 0, st>>>(c, g, cm, nb, sp, p->bm, p->imp, p->pf, p->d_pv);
+    else
+      k_eval_p2<64, false, true><<<blocks, 64, 0, st>>>(c, g, cm, nb, sp, p->bm, p->imp, p->pf, p->d_pv);
+  } else if (bs == 32) {
+    if (var == 1)
+      k_eval_p2<32, true><<<blocks, 32, 0, st>>>(c, g, cm, nb, sp, p->bm, p->imp, p->pf);
+    else
+      k_eval_p2<32, false><<<blocks, 32, 0, st>>>(c, g, cm, nb, sp, p->bm, p->imp, p->pf);
+  } else {
+    if (var == 1)
+      k_eval_p2<64, true><<<blocks, 64, 0, st>>>(c, g, cm, nb, sp, p->bm, p->imp, p->pf);
+    else
+      k_eval_p2<64, false><<<blocks, 64, 0, st>>>(c, g, cm, nb, sp, p->bm, p->imp, p->pf);
+  }
   CKL("k_eval");
   return 0;
 }
-int eval_block_size(int var) { return var == 0 ? 128 : 64; }
 
-// commit + enqueue (+ round end in its last block unless end_mode < 0)
-int launch_commit_kernel(lrcvt_plan* p, int blocks, cudaStream_t st, const cudaGraphConditionalHandle* hs,
-                         cudaGraphConditionalHandle loop, int end_mode) {
+// commit + enqueue of the next frontier (compact.cuh k_commit): the sparse
+// proposals of the round's eval (props == null) or a compact list of n_props
+// records; end_mode as k_commit / k_compact
+int launch_commit_kernel(lrcvt_plan* p, int64_t items, cudaStream_t st, const Prop* props = nullptr,
+                         int64_t n_props = 0, const cudaGraphConditionalHandle* hs = nullptr,
+                         cudaGraphConditionalHandle loop = cudaGraphConditionalHandle{}, int end_mode = -1) {
+  int64_t blocks = props ? (items + CM_THREADS - 1) / CM_THREADS : (items + CM_SLOTS - 1) / CM_SLOTS;
   if (blocks < 1) blocks = 1;
-  // grid-stride: at most one resident wave (the last-block round end costs one
-  // same-address atomic per block)
-  if (blocks > p->commit_blocks) blocks = p->commit_blocks;
-  k_commit<<<blocks, 128, 0, st>>>(p->imp, p->counters, p->ctl, p->g, p->nbm, p->bm, hs, p->ncl_arg(), loop,
-                                   end_mode);
+  if (blocks > p->commit_blocks) blocks = p->commit_blocks;  // grid-stride, one resident wave at most
+  k_commit<<<(int)blocks, CM_THREADS, 0, st>>>(props ? props : p->imp, props ? nullptr : p->pf, (int)n_props, p->counters,
+                                        p->ctl, p->g, p->nbm, p->bm, p->cbm, p->compact ? 1 : 0, hs, p->ncl_arg(),
+                                        loop, end_mode, p->zlo, p->zhi);
   CKL("k_commit");
+  return 0;
+}
+
+// bitmap -> next worklist in voxel order (+ round end, see k_compact)
+int launch_compact_kernel(lrcvt_plan* p, cudaStream_t st, const cudaGraphConditionalHandle* hs,
+                          cudaGraphConditionalHandle loop, int end_mode) {
+  k_compact<<<p->ct_tiles, CT_THREADS, 0, st>>>(p->bm, p->cbm, p->bm_words, p->ct_status, p->ct_state, p->ctl,
+                                                 p->counters, hs, p->ncl_arg(), loop, end_mode);
+  CKL("k_compact");
   return 0;
 }
 
@@ -368,7 +424,8 @@ int launch_commit_kernel(lrcvt_plan* p, int blocks, cudaStream_t st, const cudaG
 int launch_round_kernels(lrcvt_plan* p, int var, int n, cudaStream_t st, int end_mode = 0) {
   CKR(launch_eval_kernel(p, var, n, st));
   if (p->timing) CK(cudaEventRecord(p->ev1, st));
-  CKR(launch_commit_kernel(p, (n + 127) / 128, st, nullptr, cudaGraphConditionalHandle{}, end_mode));
+  CKR(launch_commit_kernel(p, n, st, nullptr, 0, nullptr, cudaGraphConditionalHandle{}, end_mode));
+  if (p->compact) CKR(launch_compact_kernel(p, st, nullptr, cudaGraphConditionalHandle{}, end_mode));
   if (p->timing) CK(cudaEventRecord(p->ev2, st));
   return 0;
 }
@@ -397,9 +454,10 @@ int launch_rounds_small(lrcvt_plan* p, int var, cudaStream_t st, const cudaGraph
   const double4* sp = p->site_pos;
   uint32_t* bm = p->bm;
   Prop* imp = p->imp;
+  uint8_t* pf = p->pf;
   int* counters = p->counters;
   int small = p->ew_small, max_rounds = 1 << 20, ncl = p->ncl_arg();
-  void* args[] = {&ctl, &g, &comp, &nbm, &sp, &bm, &imp, &counters, &small, &max_rounds, &hs, &ncl, &loop,
+  void* args[] = {&ctl, &g, &comp, &nbm, &sp, &bm, &imp, &pf, &counters, &small, &max_rounds, &hs, &ncl, &loop,
                   &in_graph};
   void* fn = var == 0 ? (void*)k_rounds_small<false> : (void*)k_rounds_small<true>;
   if (!in_graph) {
@@ -473,7 +531,6 @@ int build_round_graph(lrcvt_plan* p, int var) {
   // body: SWITCH(class) { case c: eval with cap[c]/BLOCK blocks; commit + round
   // end with cap[c]/128 blocks } (or one IF node per class); the last commit
   // block arms the next round's class and the WHILE condition
-  const int bs = eval_block_size(var);
   cudaGraphNode_t prev = nullptr;
   cudaGraph_t* sw_bodies = nullptr;  // SWITCH: body c runs when the handle holds c
   if (p->class_switch) {
@@ -507,7 +564,8 @@ int build_round_graph(lrcvt_plan* p, int var) {
       rc = launch_rounds_small(p, var, p->cap, d_hs, h, 1);  // all small rounds in one cooperative node
     } else {
       rc = launch_eval_kernel(p, var, (int)cap, p->cap);
-      if (!rc) rc = launch_commit_kernel(p, (int)((cap + 127) / 128), p->cap, d_hs, h, 1);
+      if (!rc) rc = launch_commit_kernel(p, cap, p->cap, nullptr, 0, d_hs, h, 1);
+      if (!rc && p->compact) rc = launch_compact_kernel(p, p->cap, d_hs, h, 1);
     }
     cudaGraph_t captured;
     const cudaError_t ee = cudaStreamEndCapture(p->cap, &captured);
@@ -633,6 +691,15 @@ int lrcvt_plan_create(lrcvt_plan** plan, int64_t nx, int64_t ny, int64_t nz, dou
   }
   if (const char* e = getenv("LRCVT_EW_SMALL")) p->ew_small = atoi(e);
   if (const char* e = getenv("LRCVT_SWITCH")) p->class_switch = e[0] != '0';
+  if (const char* e = getenv("LRCVT_VOTE")) p->vote_bbox = strcmp(e, "sort") != 0;
+  if (const char* e = getenv("LRCVT_COMPACT")) p->compact = e[0] == '1';
+  if (const char* e = getenv("LRCVT_EVAL_BS")) {
+    int a = 0, b = 0;
+    if (sscanf(e, "%d,%d", &a, &b) == 2) {
+      if (a == 32 || a == 128) p->p1_bs = a;
+      if (b == 32 || b == 64) p->p2_bs = b;
+    }
+  }
   // small frontiers: every round inside one cooperative kernel node of the
   // round graph (C1 2D -14%, C3 -1.5%, C2 neutral; LRCVT_COOP=0 off, =1 host-
   // alternated variant, =2 in-graph)
@@ -676,7 +743,13 @@ int lrcvt_plan_create(lrcvt_plan** plan, int64_t nx, int64_t ny, int64_t nz, dou
   rc |= dalloc(&p->list_b, nin);
   rc |= dalloc(&p->eligible, nin);
   rc |= dalloc(&p->imp, nin);
+  rc |= dalloc(&p->pf, nin);
+  rc |= dalloc(&p->mg_props, nin);
   rc |= dalloc(&p->bm, p->bm_words);
+  p->ct_tiles = (int)compact_tiles(p->bm_words);
+  rc |= dalloc(&p->cbm, coarse_words(p->bm_words));
+  rc |= dalloc(&p->ct_status, p->ct_tiles);
+  rc |= dalloc(&p->ct_state, CS_N);
   rc |= dalloc(&p->nbm, n);
   rc |= dalloc(&p->site1, n);
   rc |= dalloc(&p->ctl, 1);
@@ -714,7 +787,10 @@ int lrcvt_plan_create(lrcvt_plan** plan, int64_t nx, int64_t ny, int64_t nz, dou
     };
     if (const int e = build()) { lrcvt_plan_destroy(p); return e; }
   }
-  if (cudaMemsetAsync(p->bm, 0, sizeof(uint32_t) * p->bm_words, st) != cudaSuccess) {
+  if (cudaMemsetAsync(p->bm, 0, sizeof(uint32_t) * p->bm_words, st) != cudaSuccess ||
+      cudaMemsetAsync(p->cbm, 0, sizeof(uint32_t) * coarse_words(p->bm_words), st) != cudaSuccess ||
+      cudaMemsetAsync(p->ct_status, 0, sizeof(unsigned long long) * p->ct_tiles, st) != cudaSuccess ||
+      cudaMemsetAsync(p->ct_state, 0, sizeof(int) * CS_N, st) != cudaSuccess) {
     lrcvt_plan_destroy(p);
     return set_error(LRCVT_E_CUDA, "bitmap clear");
   }
@@ -752,7 +828,7 @@ int lrcvt_plan_create(lrcvt_plan** plan, int64_t nx, int64_t ny, int64_t nz, dou
     p->eval_blocks[1] = (nb > 0 ? nb : 1) * sms;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_eval_p2<64, false>, 64, 0);
     p->eval_blocks[2] = (nb > 0 ? nb : 1) * sms;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_commit, 128, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_commit, CM_THREADS, 0);
     p->commit_blocks = (nb > 0 ? nb : 1) * sms;
     int nb0 = 0, nb1 = 0;  // cooperative kernel: every CTA co-resident
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb0, k_rounds_small<false>, 32 * EW_WARPS, 0);
@@ -782,10 +858,13 @@ int lrcvt_plan_destroy(lrcvt_plan* p) {
     if (gx) cudaGraphExecDestroy(gx);
   if (p->cap) cudaStreamDestroy(p->cap);
   if (p->h_ctl) cudaFreeHost(p->h_ctl);
-  void* bufs[] = {p->counters, p->ctl, p->d_handles, p->d_nel, p->list_a, p->list_b, p->eligible, p->imp, p->bm, p->nbm, p->site1, p->has_site,
+  void* bufs[] = {p->counters, p->ctl, p->d_handles, p->d_nel, p->list_a, p->list_b, p->eligible, p->imp, p->pf,
+                  p->mg_props, p->bm,
+                  p->cbm, p->ct_status, p->ct_state, p->nbm, p->site1, p->has_site,
                   p->site_pos, p->new_pos, p->sk_key, p->sk_key2, p->sk_val, p->sk_val2, p->sk_d,
                   p->acc, p->sums, p->vt_key, p->vt_key2, p->vt_pv, p->vt_pv2,
-                  p->seg_b, p->seg_e, p->cub_tmp};
+                  p->seg_b, p->seg_e, p->vt_sp, p->vt_box, p->mg_own_ss, p->mg_own_dist, p->d_pv,
+                  p->mg_lo, p->mg_hi, p->cub_tmp};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (p->h_counters) cudaFreeHost(p->h_counters);
@@ -827,6 +906,12 @@ int lrcvt_plan_reuse_eligible(lrcvt_plan* p, int enable) {
   return 0;
 }
 
+int lrcvt_plan_persistent_outputs(lrcvt_plan* p, int enable) {
+  if (!p) return set_error(LRCVT_E_ARG, "lrcvt_plan_persistent_outputs");
+  p->persist = enable != 0;
+  return 0;
+}
+
 int lrcvt_plan_profile(const lrcvt_plan* p, double* out6) {
   if (!p || !out6) return set_error(LRCVT_E_ARG, "lrcvt_plan_profile");
   for (int i = 0; i < 6; i++) out6[i] = p->prof[i];
@@ -847,15 +932,36 @@ int lrcvt_classify(lrcvt_plan* p, int64_t n_sites, const double* d_site_pos,
   const int S = (int)n_sites;
   int2* ss = reinterpret_cast<int2*>(d_site_src);
   memset(stats, 0, sizeof *stats);
-  // tessellation.py:120-122
-  k_fill_state<<<grid_for(g.n, 256, 148 * 32), 256, 0, st>>>(ss, d_dist, p->site1, g.n);
-  CKL("k_fill_state"); LAUNCHED(1);
   CK(cudaMemsetAsync(p->counters, 0, sizeof(int) * C_NCOUNTERS, st));
-  if (S == 0) {  // tessellation.py:126-134
+  if (S == 0) {  // tessellation.py:120-134
+    k_fill_state<<<grid_for(g.n, 256, 148 * 32), 256, 0, st>>>(ss, d_dist, g.n);
+    CKL("k_fill_state"); LAUNCHED(1);
     if (d_state) CK(cudaMemsetAsync(d_state, 0, (size_t)g.n, st));
     CK(cudaStreamSynchronize(st));
     return 0;
   }
+  // the eligible list (in-band voxels of components that have sites,
+  // tessellation.py:161-164) up front: no voxel outside it is ever assigned,
+  // so the per-voxel passes below only touch it
+  const bool reuse = p->reuse_eligible && p->eligible_valid && p->eligible_sites == S;
+  // persistent outputs: the caller passes the buffers of its previous classify again, untouched, with the
+  // same eligible set -- every voxel outside the list still holds its fill value / state 0
+  const bool fast = reuse && p->persist && p->last_ss == ss && p->last_dist == d_dist && p->last_state == d_state;
+  if (!reuse) {
+    if (prepare_eligible(p, S, d_site_comp, st)) return LRCVT_E_CUDA;
+    p->eligible_valid = true;
+    p->eligible_sites = S;
+  }
+  const int el_grid = grid_for(p->n_inband, 256, 148 * 16);
+  if (!fast) {  // tessellation.py:120-122
+    k_fill_state<<<grid_for(g.n, 256, 148 * 32), 256, 0, st>>>(ss, d_dist, g.n);
+    CKL("k_fill_state"); LAUNCHED(1);
+  }
+  k_fill_list<<<el_grid, 256, 0, st>>>(p->eligible, p->d_nel, fast ? ss : nullptr, d_dist, p->site1);
+  CKL("k_fill_list"); LAUNCHED(1);
+  p->last_ss = ss;
+  p->last_dist = d_dist;
+  p->last_state = d_state;
   k_pack_sites<<<grid_for(S, 256), 256, 0, st>>>(d_site_pos, S, p->site_pos);
   CKL("k_pack_sites"); LAUNCHED(1);
   // _place_seeds (tessellation.py:136-140)
@@ -876,11 +982,8 @@ int lrcvt_classify(lrcvt_plan* p, int64_t n_sites, const double* d_site_pos,
   CKL("k_phase1_start"); LAUNCHED(1);
   // phase 1 (tessellation.py:152-156)
   CKR(run_rounds(p, 0, st));
-  // phase 2 (tessellation.py:161-189): eligible list, rounds, verification sweeps
-  if (prepare_eligible(p, S, d_site_comp, st)) return LRCVT_E_CUDA;
-  p->eligible_valid = true;
-  p->eligible_sites = S;
-  k_site1_to_state<<<grid_for(g.n, 256, 148 * 16), 256, 0, st>>>(g, p->site1, p->site_pos, ss, d_dist);
+  // phase 2 (tessellation.py:161-189): rounds from the eligible list, verification sweeps
+  k_site1_to_state<<<el_grid, 256, 0, st>>>(g, p->site1, p->site_pos, ss, d_dist, p->eligible, p->d_nel, 0, 0);
   CKL("k_site1_to_state"); LAUNCHED(1);
   k_phase2_copy<<<148 * 4, 256, 0, st>>>(p->eligible, p->d_nel, p->ctl, p->counters);
   CKL("k_phase2_copy"); LAUNCHED(1);
@@ -893,7 +996,7 @@ int lrcvt_classify(lrcvt_plan* p, int64_t n_sites, const double* d_site_pos,
     if (p->timing) CK(cudaEventRecord(p->ev0, st));
     CKR(launch_round_kernels(p, var2, (int)p->n_inband, st, -1));  // sweep: n_el <= in-band
     k_sweep_end<<<1, 1, 0, st>>>(p->ctl, p->counters);
-    CKL("k_sweep_end"); LAUNCHED(3);  // eval, commit, sweep end
+    CKL("k_sweep_end"); LAUNCHED(4);  // eval, commit, compact, sweep end
     CK(cudaMemcpyAsync(p->h_ctl, p->ctl, sizeof(RoundCtl), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     if (p->timing) {
@@ -903,8 +1006,9 @@ int lrcvt_classify(lrcvt_plan* p, int64_t n_sites, const double* d_site_pos,
     }
     if (p->h_ctl->sweep_imp == 0) break;
   }
-  // state bits + assigned (tessellation.py:191-204)
-  k_state<<<grid_for(g.n, 256, 148 * 16), 256, 0, st>>>(ss, g.n, d_state, p->counters);
+  // state bits + assigned (tessellation.py:191-204): state 0 outside the eligible list
+  if (d_state && !fast) CK(cudaMemsetAsync(d_state, 0, (size_t)g.n, st));
+  k_state<<<el_grid, 256, 0, st>>>(ss, p->eligible, p->d_nel, 0, 0, d_state, p->counters);
   CKL("k_state"); LAUNCHED(1);
   CK(cudaMemcpyAsync(p->h_ctl, p->ctl, sizeof(RoundCtl), cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(p->h_counters + 7, p->d_nel, sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -918,7 +1022,9 @@ int lrcvt_classify(lrcvt_plan* p, int64_t n_sites, const double* d_site_pos,
   stats->commits = c.commits;
   stats->assigned = p->h_counters[C_ASSIGNED];
   stats->bad_sites = p->h_counters[C_BAD];
-  LAUNCHED(2 * c.rounds);  // eval, commit (+ fused round end) per relaxation round
+  // eval, commit, compact (+ fused round end) per launched relaxation round; one k_rounds_small
+  // launch covers all its rounds
+  LAUNCHED((p->compact ? 3 : 2) * (c.rounds - c.rounds_small) + c.small_launches);
   if (p->h_counters[C_BAD]) {
     p->eligible_valid = false;
     return p->h_counters[C_BAD];
@@ -956,12 +1062,30 @@ int lrcvt_centroidal_update(lrcvt_plan* p, int64_t n_sites, const double* d_site
   if (exact) {
     CK(cudaMemsetAsync(p->acc, 0, sizeof(unsigned long long) * 4 * S, st));
     if (n_el > 0) {
-      k_vote_exact<<<grid_for(n_el, 256, 148 * 8), 256, 0, st>>>(p->eligible, n_el, g, ss, p->acc, S);
+      k_vote_exact<false><<<grid_for(n_el, 256, 148 * 8), 256, 0, st>>>(p->eligible, n_el, g, ss, p->acc, S, nullptr);
       CKL("k_vote_exact"); LAUNCHED(1);
     }
     k_vote_exact_finish<<<grid_for(S, 256), 256, 0, st>>>(p->acc, S, 0.5 * g.sx, 0.5 * g.sy, 0.5 * g.sz,
                                                           p->sums);
     CKL("k_vote_exact_finish"); LAUNCHED(1);
+  } else if (p->vote_bbox) {
+    // ordered path, sort-free: per-site bounding-box walk (vote.cuh k_vote_prep / k_vote_scan)
+    if (!p->vt_sp) {
+      int rc = dalloc(&p->vt_sp, g.n);
+      rc |= dalloc(&p->vt_box, 6 * p->max_sites);
+      if (rc) return LRCVT_E_NOMEM;
+    }
+    k_box_init<<<grid_for(S, 256), 256, 0, st>>>(p->vt_box, S);
+    CKL("k_box_init"); LAUNCHED(1);
+    if (n_el > 0) {
+      k_vote_prep<false><<<grid_for(n_el, 256, 148 * 8), 256, 0, st>>>(p->eligible, n_el, g, ss, p->vt_sp, p->vt_box,
+                                                                       S, nullptr);
+      CKL("k_vote_prep"); LAUNCHED(1);
+    }
+    k_vote_scan<4><<<grid_for(S, 4), 128, 0, st>>>(p->vt_sp, p->comp, p->vt_box, d_site_comp, S, g,
+                                                    (const double*)d_weights, (const float*)d_weights, weight_mode,
+                                                    0, g.nz, 0, nullptr, p->sums);
+    CKL("k_vote_scan"); LAUNCHED(1);
   } else {
     const int64_t nin = p->n_inband > 0 ? p->n_inband : 1;
     int rc = 0;
@@ -1249,10 +1373,13 @@ int lrcvt_aggregate(int64_t n, int32_t n_fields, const float* const* field_ptrs,
 
 
 // ---------------------------------------------------------------------------
-// Multi-GPU global mode: replicated per-voxel state, each rank
-// evaluates only its z-slab's frontier; the round's proposals are all-gathered
-// by the caller and committed on every rank (which enqueues only own-slab
-// neighbours). The caller drives rounds with these steps.
+// Multi-GPU global mode (mg.cuh): rank r owns planes [zlo, zhi)
+// of one volume; own slab + one halo plane per side are current locally, far
+// reads (shortcut nodes, phi chains) go to the owner through the PeerView.
+// Per relaxation round: eval own frontier -> forward the proposals of the
+// two boundary planes to the neighbour ranks -> commit own proposals + the
+// received halo proposals (enqueue restricted to the own slab) -> global
+// frontier count. The caller drives rounds and collectives (multigpu.py).
 
 __global__ void k_mg_round_end(RoundCtl* ctl, int* counters, int sweep) {
   const int n_next = counters[C_NNEXT];
@@ -1269,11 +1396,81 @@ __global__ void k_mg_round_end(RoundCtl* ctl, int* counters, int sweep) {
   counters[C_NNEXT] = 0;
 }
 
+// the round's improved proposals on the boundary planes: z == zlo -> lo (for
+// rank - 1), z == zhi - 1 -> hi (for rank + 1); all improved counted too
+__global__ void __launch_bounds__(128) k_mg_boundary(const RoundCtl* __restrict__ ctl, const Prop* __restrict__ imp,
+                                                     const uint8_t* __restrict__ pf, int nxy, int zlo, int zhi,
+                                                     int want_lo, int want_hi, Prop* __restrict__ lo,
+                                                     Prop* __restrict__ hi, int* __restrict__ counters) {
+  const int n = ctl->n_cur;
+  const int stride = gridDim.x * blockDim.x;
+  int mine = 0;
+  for (int base = blockIdx.x * blockDim.x; base < n; base += stride) {
+    const int i = base + threadIdx.x;
+    const bool take = i < n && pf[i];
+    int z = -1;
+    Prop pr;
+    if (take) {
+      pr = imp[i];
+      z = (int)((unsigned)pr.v / (unsigned)nxy);
+      mine++;
+    }
+    const bool tl = take && want_lo && z == zlo, th = take && want_hi && z == zhi - 1;
+    const int sl = block_append(counters + C_LO, tl);
+    if (tl) lo[sl] = pr;
+    const int sh = block_append(counters + C_HI, th);
+    if (th) hi[sh] = pr;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
+  if ((threadIdx.x & 31) == 0 && mine) atomicAdd(counters + C_NIMP, mine);
+}
+
+int mg_require(lrcvt_plan* p, const char* what) {
+  if (!p) return set_error(LRCVT_E_ARG, what);
+  return 0;
+}
+
 int lrcvt_mg_set_slab(lrcvt_plan* p, int64_t zlo, int64_t zhi) {
   if (!p || zlo < 0 || zhi <= zlo || zlo >= p->g.nz) return set_error(LRCVT_E_ARG, "lrcvt_mg_set_slab");
   p->zlo = (int)zlo;
   p->zhi = zhi >= p->g.nz ? p->g.nz : (int)zhi;  // kernels filter iff zlo > 0 || zhi < nz
   p->eligible_valid = false;
+  return 0;
+}
+
+int lrcvt_mg_state(lrcvt_plan* p, void** d_ss, void** d_dist) {
+  if (!p || !d_ss || !d_dist) return set_error(LRCVT_E_ARG, "lrcvt_mg_state");
+  if (!p->mg_own_ss) {
+    int rc = dalloc(&p->mg_own_ss, p->g.n);
+    rc |= dalloc(&p->mg_own_dist, p->g.n);
+    if (rc) return LRCVT_E_NOMEM;
+  }
+  *d_ss = p->mg_own_ss;
+  *d_dist = p->mg_own_dist;
+  return 0;
+}
+
+int lrcvt_mg_set_peers(lrcvt_plan* p, int32_t world, const int64_t* z_bounds, void* const* peer_ss,
+                       void* const* peer_dist) {
+  if (!p || world < 1 || world > MG_MAX || !z_bounds || !peer_ss || !peer_dist)
+    return set_error(LRCVT_E_ARG, "lrcvt_mg_set_peers: bad arguments");
+  PeerView pv;
+  memset(&pv, 0, sizeof pv);
+  pv.world = world;
+  pv.nxy = p->g.nxy;
+  for (int r = 0; r <= world; r++) pv.zb[r] = (int)z_bounds[r];
+  for (int r = world + 1; r <= MG_MAX; r++) pv.zb[r] = p->g.nz;
+  for (int r = 0; r < world; r++) {
+    pv.ss[r] = (const int2*)peer_ss[r];
+    pv.dist[r] = (const double*)peer_dist[r];
+    if (z_bounds[r + 1] <= z_bounds[r]) return set_error(LRCVT_E_ARG, "lrcvt_mg_set_peers: empty slab");
+  }
+  pv.lo = p->zlo - 1;
+  pv.hi = p->zhi;
+  if (!p->d_pv) CK(cudaMalloc((void**)&p->d_pv, sizeof(PeerView)));
+  CK(cudaMemcpy(p->d_pv, &pv, sizeof pv, cudaMemcpyHostToDevice));
+  p->mg_world = world;
   return 0;
 }
 
@@ -1289,9 +1486,14 @@ int lrcvt_mg_begin(lrcvt_plan* p, int64_t n_sites, const double* d_site_pos, con
   int2* ss = reinterpret_cast<int2*>(d_site_src);
   p->mg_ss = ss;
   p->mg_dist = d_dist;
-  k_fill_state<<<grid_for(g.n, 256, 148 * 32), 256, 0, st>>>(ss, d_dist, p->site1, g.n);
-  CKL("k_fill_state");
   CK(cudaMemsetAsync(p->counters, 0, sizeof(int) * C_NCOUNTERS, st));
+  // own-slab eligible list (tessellation.py:161-164 restricted to [zlo, zhi))
+  if (prepare_eligible(p, S, d_site_comp, st)) return LRCVT_E_CUDA;
+  p->eligible_valid = true;
+  p->eligible_sites = S;
+  k_fill_state<<<grid_for(g.n, 256, 148 * 32), 256, 0, st>>>(ss, d_dist, g.n);
+  CKL("k_fill_state");
+  CK(cudaMemsetAsync(p->site1, 0xff, sizeof(int) * (size_t)g.n, st));
   k_pack_sites<<<grid_for(S, 256), 256, 0, st>>>(d_site_pos, S, p->site_pos);
   CKL("k_pack_sites");
   k_site_voxel<<<grid_for(S, 256), 256, 0, st>>>(g, p->comp, p->site_pos, d_site_comp, S, p->sk_key, p->sk_val,
@@ -1302,44 +1504,43 @@ int lrcvt_mg_begin(lrcvt_plan* p, int64_t n_sites, const double* d_site_pos, con
     CK(cub::DeviceRadixSort::SortPairs(p->cub_tmp, bytes, p->sk_key, p->sk_key2, p->sk_val, p->sk_val2, S, 0, 32,
                                        st));
   }
-  // every rank places every seed (replicated state); the phase-1 worklist
-  // holds the own slab's part only
+  // every rank places every seed (cheap, S-sized); the phase-1 worklist holds the own slab's part only
   k_seed_groups<<<grid_for(S, 128), 128, 0, st>>>(g, p->nbm, p->sk_key2, p->sk_val2, p->sk_d, S, ss, d_dist, p->site1, p->bm,
                                                   p->list_a, p->counters, p->zlo, p->zhi);
   CKL("k_seed_groups");
-  k_phase1_start<<<1, 1, 0, st>>>(p->ctl, p->counters, p->list_a, p->list_b, ss, d_dist, p->site1, p->loop_min);
+  k_phase1_start<<<1, 1, 0, st>>>(p->ctl, p->counters, p->list_a, p->list_b, ss, d_dist, p->site1, 0);
   CKL("k_phase1_start");
   CK(cudaMemcpyAsync(p->h_ctl, p->ctl, sizeof(RoundCtl), cudaMemcpyDeviceToHost, st));
   CKR(sync_counters(p, st, C_NCOUNTERS));
   if (p->h_counters[C_BAD]) return p->h_counters[C_BAD];
   p->h_ncur = p->h_ctl->n_cur;
   *n_frontier = p->h_ncur;
-  p->eligible_valid = false;
   return 0;
 }
 
 int lrcvt_mg_phase2(lrcvt_plan* p, int64_t n_sites, const int32_t* d_site_comp, int64_t* n_frontier, void* stream) {
-  if (!p || !d_site_comp || !n_frontier) return set_error(LRCVT_E_ARG, "lrcvt_mg_phase2");
+  if (!p || !d_site_comp || !n_frontier || !p->eligible_valid) return set_error(LRCVT_E_ARG, "lrcvt_mg_phase2");
   cudaStream_t st = (cudaStream_t)stream;
-  if (prepare_eligible(p, (int)n_sites, d_site_comp, st)) return LRCVT_E_CUDA;
-  k_site1_to_state<<<grid_for(p->g.n, 256, 148 * 16), 256, 0, st>>>(p->g, p->site1, p->site_pos, p->mg_ss,
-                                                                     p->mg_dist);
+  const Geo& g = p->g;
+  // phase-1 LOS states -> (site, src) / dist on the own slab and its halo planes (site1 is current there)
+  const int64_t z0 = p->zlo > 0 ? p->zlo - 1 : 0, z1 = p->zhi < g.nz ? p->zhi + 1 : g.nz;
+  k_site1_to_state<<<grid_for((z1 - z0) * g.nxy, 256, 148 * 16), 256, 0, st>>>(
+      g, p->site1, p->site_pos, p->mg_ss, p->mg_dist, nullptr, nullptr, z0 * g.nxy, z1 * g.nxy);
   CKL("k_site1_to_state");
   k_phase2_copy<<<148 * 4, 256, 0, st>>>(p->eligible, p->d_nel, p->ctl, p->counters);
   CKL("k_phase2_copy");
   CK(cudaMemcpyAsync(p->h_counters + 7, p->d_nel, sizeof(int), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   p->n_eligible = p->h_counters[7];
-  p->eligible_valid = true;
-  p->eligible_sites = n_sites;
   p->h_ncur = (int)p->n_eligible;
   *n_frontier = p->h_ncur;
   return 0;
 }
 
 int lrcvt_mg_eval(lrcvt_plan* p, int32_t phase, int32_t sweep, int64_t* n_evaluated, int64_t* n_prop,
-                  void* stream) {
-  if (!p || phase < 1 || phase > 2 || !n_prop || !n_evaluated) return set_error(LRCVT_E_ARG, "lrcvt_mg_eval");
+                  int64_t* n_lo, int64_t* n_hi, void* stream) {
+  if (!p || phase < 1 || phase > 2 || !n_prop || !n_evaluated || !n_lo || !n_hi)
+    return set_error(LRCVT_E_ARG, "lrcvt_mg_eval");
   cudaStream_t st = (cudaStream_t)stream;
   int n = p->h_ncur;
   if (sweep) {
@@ -1348,35 +1549,42 @@ int lrcvt_mg_eval(lrcvt_plan* p, int32_t phase, int32_t sweep, int64_t* n_evalua
     n = (int)p->n_eligible;
   }
   CK(cudaMemsetAsync(p->counters, 0, sizeof(int) * 2, st));
+  CK(cudaMemsetAsync(p->counters + C_LO, 0, sizeof(int) * 2, st));
   const int var = phase == 1 ? 0 : (p->g.dyadic ? 1 : 2);
-  if (n > 0) CKR(launch_eval_kernel(p, var, n, st));
-  CKR(sync_counters(p, st, 1));
+  if (n > 0) {
+    CKR(launch_eval_kernel(p, var, n, st));
+    if (!p->mg_lo) {
+      int rc = dalloc(&p->mg_lo, p->g.nxy);
+      rc |= dalloc(&p->mg_hi, p->g.nxy);
+      if (rc) return LRCVT_E_NOMEM;
+    }
+    k_mg_boundary<<<grid_for(n, 128, 148 * 16), 128, 0, st>>>(p->ctl, p->imp, p->pf, p->g.nxy, p->zlo, p->zhi,
+                                                              p->zlo > 0, p->zhi < p->g.nz, p->mg_lo, p->mg_hi,
+                                                              p->counters);
+    CKL("k_mg_boundary");
+  }
+  CKR(sync_counters(p, st, C_HI + 1));
   *n_evaluated = n;
   *n_prop = p->h_counters[C_NIMP];
+  *n_lo = p->h_counters[C_LO];
+  *n_hi = p->h_counters[C_HI];
   return 0;
 }
 
-void* lrcvt_mg_proposals(lrcvt_plan* p) { return p ? (void*)p->imp : nullptr; }
-
-int lrcvt_mg_copy_proposals(lrcvt_plan* p, void* d_dst, int64_t n, void* stream) {
-  if (!p || n < 0 || (n > 0 && !d_dst)) return set_error(LRCVT_E_ARG, "lrcvt_mg_copy_proposals");
-  if (n > 0) CK(cudaMemcpyAsync(d_dst, p->imp, sizeof(Prop) * n, cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
-  return 0;
+void* lrcvt_mg_boundary(lrcvt_plan* p, int32_t side) {
+  if (!p) return nullptr;
+  return side == 0 ? (void*)p->mg_lo : (void*)p->mg_hi;
 }
 
-int lrcvt_mg_commit(lrcvt_plan* p, const void* d_props, int64_t n_props, int32_t sweep, int64_t* n_next,
+int lrcvt_mg_commit(lrcvt_plan* p, const void* d_halo, int64_t n_halo, int32_t sweep, int64_t* n_next,
                     void* stream) {
-  if (!p || n_props < 0 || (n_props > 0 && !d_props) || !n_next) return set_error(LRCVT_E_ARG, "lrcvt_mg_commit");
+  if (!p || n_halo < 0 || (n_halo > 0 && !d_halo) || !n_next) return set_error(LRCVT_E_ARG, "lrcvt_mg_commit");
   cudaStream_t st = (cudaStream_t)stream;
-  int hv[2] = {(int)n_props, 0};
-  CK(cudaMemcpyAsync(p->counters, hv, sizeof(int) * 2, cudaMemcpyHostToDevice, st));
-  if (n_props > 0) {
-    int blocks = (int)((n_props + 127) / 128);
-    if (blocks > p->commit_blocks) blocks = p->commit_blocks;
-    k_commit<<<blocks, 128, 0, st>>>((const Prop*)d_props, p->counters, p->ctl, p->g, p->nbm, p->bm, nullptr,
-                                     p->n_classes, cudaGraphConditionalHandle{}, -1, p->zlo, p->zhi);
-    CKL("k_commit");
-  }
+  CK(cudaMemsetAsync(p->counters, 0, sizeof(int) * 2, st));
+  const int n = sweep ? (int)p->n_eligible : p->h_ncur;
+  if (n > 0) CKR(launch_commit_kernel(p, n, st));  // own sparse proposals
+  if (n_halo > 0) CKR(launch_commit_kernel(p, n_halo, st, (const Prop*)d_halo, n_halo));  // halo planes
+  if (p->compact) CKR(launch_compact_kernel(p, st, nullptr, cudaGraphConditionalHandle{}, -1));
   CKR(sync_counters(p, st, 2));
   const int nn = p->h_counters[C_NNEXT];
   k_mg_round_end<<<1, 1, 0, st>>>(p->ctl, p->counters, sweep);
@@ -1389,12 +1597,143 @@ int lrcvt_mg_commit(lrcvt_plan* p, const void* d_props, int64_t n_props, int32_t
 int lrcvt_mg_finish(lrcvt_plan* p, const int32_t* d_site_src, uint8_t* d_state, int64_t* assigned, void* stream) {
   if (!p || !d_site_src || !assigned) return set_error(LRCVT_E_ARG, "lrcvt_mg_finish");
   cudaStream_t st = (cudaStream_t)stream;
+  const Geo& g = p->g;
   CK(cudaMemsetAsync(p->counters + C_ASSIGNED, 0, sizeof(int), st));
-  k_state<<<grid_for(p->g.n, 256, 148 * 16), 256, 0, st>>>(reinterpret_cast<const int2*>(d_site_src), p->g.n,
-                                                           d_state, p->counters);
+  const int64_t v0 = (int64_t)p->zlo * g.nxy, v1 = (int64_t)(p->zhi < g.nz ? p->zhi : g.nz) * g.nxy;
+  k_state<<<grid_for(v1 - v0, 256, 148 * 16), 256, 0, st>>>(reinterpret_cast<const int2*>(d_site_src), nullptr,
+                                                             nullptr, v0, v1, d_state, p->counters);
   CKL("k_state");
   CKR(sync_counters(p, st, C_ASSIGNED + 1));
   *assigned = p->h_counters[C_ASSIGNED];
+  return 0;
+}
+
+// ---- vote on the own slab (tessellation.py:211-248 partitioned)
+
+int lrcvt_mg_vote_exact(lrcvt_plan* p, int64_t n_sites, const int32_t* d_site_src, uint64_t* d_acc, void* stream) {
+  if (!p || n_sites < 1 || n_sites > p->max_sites || !d_site_src || !d_acc || !p->eligible_valid)
+    return set_error(LRCVT_E_ARG, "lrcvt_mg_vote_exact");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int S = (int)n_sites;
+  CK(cudaMemsetAsync(d_acc, 0, sizeof(uint64_t) * 4 * S, st));
+  const int n_el = (int)p->n_eligible;
+  if (n_el > 0) {
+    const int2* ss = reinterpret_cast<const int2*>(d_site_src);
+    if (p->d_pv)
+      k_vote_exact<true><<<grid_for(n_el, 256, 148 * 8), 256, 0, st>>>(p->eligible, n_el, p->g, ss,
+                                                                       (unsigned long long*)d_acc, S, p->d_pv);
+    else
+      k_vote_exact<false><<<grid_for(n_el, 256, 148 * 8), 256, 0, st>>>(p->eligible, n_el, p->g, ss,
+                                                                        (unsigned long long*)d_acc, S, nullptr);
+    CKL("k_vote_exact");
+  }
+  return 0;
+}
+
+int lrcvt_mg_vote_exact_finish(lrcvt_plan* p, int64_t n_sites, const uint64_t* d_acc, double* d_sums, void* stream) {
+  if (!p || n_sites < 1 || !d_acc || !d_sums) return set_error(LRCVT_E_ARG, "lrcvt_mg_vote_exact_finish");
+  const int S = (int)n_sites;
+  const Geo& g = p->g;
+  k_vote_exact_finish<<<grid_for(S, 256), 256, 0, (cudaStream_t)stream>>>((const unsigned long long*)d_acc, S,
+                                                                          0.5 * g.sx, 0.5 * g.sy, 0.5 * g.sz, d_sums);
+  CKL("k_vote_exact_finish");
+  return 0;
+}
+
+int lrcvt_mg_vote_box(lrcvt_plan* p, int64_t n_sites, const int32_t* d_site_src, int32_t* d_box, void* stream) {
+  if (!p || n_sites < 1 || n_sites > p->max_sites || !d_site_src || !d_box || !p->eligible_valid)
+    return set_error(LRCVT_E_ARG, "lrcvt_mg_vote_box");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int S = (int)n_sites;
+  if (!p->vt_sp) {
+    int rc = dalloc(&p->vt_sp, p->g.n);
+    rc |= dalloc(&p->vt_box, 6 * p->max_sites);
+    if (rc) return LRCVT_E_NOMEM;
+  }
+  k_box_init<<<grid_for(S, 256), 256, 0, st>>>(d_box, S);
+  CKL("k_box_init");
+  const int n_el = (int)p->n_eligible;
+  if (n_el > 0) {
+    const int2* ss = reinterpret_cast<const int2*>(d_site_src);
+    if (p->d_pv)
+      k_vote_prep<true><<<grid_for(n_el, 256, 148 * 8), 256, 0, st>>>(p->eligible, n_el, p->g, ss, p->vt_sp, d_box,
+                                                                      S, p->d_pv);
+    else
+      k_vote_prep<false><<<grid_for(n_el, 256, 148 * 8), 256, 0, st>>>(p->eligible, n_el, p->g, ss, p->vt_sp,
+                                                                       d_box, S, nullptr);
+    CKL("k_vote_prep");
+  }
+  return 0;
+}
+
+int lrcvt_mg_vote_scan(lrcvt_plan* p, int64_t n_sites, const int32_t* d_site_comp, int32_t weight_mode,
+                       const void* d_weights, int32_t mode, const int32_t* d_box, const double* d_init, double* d_out,
+                       void* stream) {
+  if (!p || n_sites < 1 || !d_site_comp || !d_box || !d_out || mode < 0 || mode > 2 || !p->vt_sp ||
+      weight_mode < 0 || weight_mode > 3 || (weight_mode != LRCVT_W_ONES && !d_weights) || (mode == 2 && !d_init))
+    return set_error(LRCVT_E_ARG, "lrcvt_mg_vote_scan");
+  const int S = (int)n_sites;
+  const Geo& g = p->g;
+  k_vote_scan<4><<<grid_for(S, 4), 128, 0, (cudaStream_t)stream>>>(
+      p->vt_sp, p->comp, d_box, d_site_comp, S, g, (const double*)d_weights, (const float*)d_weights, weight_mode,
+      p->zlo, p->zhi < g.nz ? p->zhi : g.nz, mode, d_init, d_out);
+  CKL("k_vote_scan");
+  return 0;
+}
+
+int lrcvt_mg_vote_carry(lrcvt_plan* p, int64_t n_sites, const int32_t* d_box, const double* d_res,
+                        const double* d_carry_in, double* d_carry_out, void* stream) {
+  if (!p || n_sites < 1 || !d_box || !d_res || !d_carry_out) return set_error(LRCVT_E_ARG, "lrcvt_mg_vote_carry");
+  const int S = (int)n_sites;
+  k_vote_carry<<<grid_for(S, 256), 256, 0, (cudaStream_t)stream>>>(d_box, S, p->zlo,
+                                                                   p->zhi < p->g.nz ? p->zhi : p->g.nz, d_res,
+                                                                   d_carry_in, d_carry_out);
+  CKL("k_vote_carry");
+  return 0;
+}
+
+int lrcvt_mg_move(lrcvt_plan* p, int64_t n_sites, const double* d_site_pos, const int32_t* d_site_comp,
+                  const double* d_sums, double backoff, double* d_new_pos, double* d_disp, int64_t* empty_regions,
+                  void* stream) {
+  if (!p || n_sites < 1 || n_sites > p->max_sites || !d_site_pos || !d_site_comp || !d_sums || !d_new_pos ||
+      !d_disp)
+    return set_error(LRCVT_E_ARG, "lrcvt_mg_move");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int S = (int)n_sites;
+  k_pack_sites<<<grid_for(S, 256), 256, 0, st>>>(d_site_pos, S, p->site_pos);
+  CKL("k_pack_sites");
+  CK(cudaMemsetAsync(p->counters + C_BAD, 0, sizeof(int), st));
+  k_move_sites<<<grid_for(S, 128), 128, 0, st>>>(p->g, p->comp, p->site_pos, d_site_comp, d_sums, S, backoff,
+                                                 p->new_pos, d_disp, p->counters + C_BAD);
+  CKL("k_move_sites");
+  k_unpack_sites<<<grid_for(S, 256), 256, 0, st>>>(p->new_pos, S, d_new_pos);
+  CKL("k_unpack_sites");
+  CKR(sync_counters(p, st, C_BAD + 1));
+  if (empty_regions) *empty_regions = p->h_counters[C_BAD];
+  return 0;
+}
+
+// ---- CUDA IPC: another process's (or device's) buffers as peer pointers
+
+int lrcvt_ipc_export(const void* d_ptr, uint8_t* handle64) {
+  if (!d_ptr || !handle64) return set_error(LRCVT_E_ARG, "lrcvt_ipc_export");
+  cudaIpcMemHandle_t h;
+  CK(cudaIpcGetMemHandle(&h, const_cast<void*>(d_ptr)));
+  memcpy(handle64, &h, sizeof h < 64 ? sizeof h : 64);
+  return 0;
+}
+
+int lrcvt_ipc_open(const uint8_t* handle64, void** d_ptr) {
+  if (!handle64 || !d_ptr) return set_error(LRCVT_E_ARG, "lrcvt_ipc_open");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle64, sizeof h < 64 ? sizeof h : 64);
+  CK(cudaIpcOpenMemHandle(d_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return 0;
+}
+
+int lrcvt_ipc_close(void* d_ptr) {
+  if (!d_ptr) return set_error(LRCVT_E_ARG, "lrcvt_ipc_close");
+  CK(cudaIpcCloseMemHandle(d_ptr));
   return 0;
 }
 

@@ -24,6 +24,7 @@ __global__ void __launch_bounds__(32 * EW_WARPS) k_rounds_small(RoundCtl* __rest
                                                                 const uint32_t* __restrict__ nbm,
                                                                 const double4* __restrict__ site_pos,
                                                                 uint32_t* __restrict__ bm, Prop* __restrict__ imp,
+                                                                uint8_t* __restrict__ pf,
                                                                 int* __restrict__ counters, int small,
                                                                 int max_rounds,
                                                                 const cudaGraphConditionalHandle* hs, int n_classes,
@@ -42,27 +43,29 @@ __global__ void __launch_bounds__(32 * EW_WARPS) k_rounds_small(RoundCtl* __rest
     const int* site1 = vctl->site1;
     const double* dist = vctl->dist;
     for (int i = gw; i < n; i += n_warps)
-      ew_voxel<PHASE2, true>(list, ss, site1, dist, i, g, comp, nbm, site_pos, bm, imp, counters, stage[wid]);
+      ew_voxel<PHASE2, true>(list, ss, site1, dist, i, g, comp, nbm, site_pos, bm, imp, pf, stage[wid]);
     grid.sync();
-    // commit (k_commit's body): one thread per proposal, block-uniform trip count
-    const int n_imp = *(volatile int*)(counters + C_NIMP);
+    // commit (k_commit's body over the sparse proposal slots): one thread per
+    // frontier item, block-uniform trip count
     int* next = vctl->nxt;
     int2* wss = vctl->ss;
     double* wdist = vctl->dist;
     int* wsite1 = vctl->site1;
-    for (int base = blockIdx.x * blockDim.x; base < n_imp; base += gridDim.x * blockDim.x) {
+    int mine = 0;
+    for (int base = blockIdx.x * blockDim.x; base < n; base += gridDim.x * blockDim.x) {
       const int i = base + threadIdx.x;
-      const bool active = i < n_imp;
+      const bool active = i < n && __ldcg(pf + i);  // written this round by other SMs
       int v = 0;
       if (active) {
         Prop p;
         {
-          const double pd = __ldcg(&imp[i].d);  // written this round by other SMs
+          const double pd = __ldcg(&imp[i].d);
           const int2 a = __ldcg(reinterpret_cast<const int2*>(&imp[i].v));
           const int2 b = __ldcg(reinterpret_cast<const int2*>(&imp[i].src));
           p.d = pd; p.v = a.x; p.s = a.y; p.src = b.x; p.pad = b.y;
         }
         v = p.v;
+        mine++;
         if (wsite1) {
           __stcg(wsite1 + v, p.src == p.v ? p.s : (int)LRCVT_NONE);
         } else {
@@ -72,11 +75,15 @@ __global__ void __launch_bounds__(32 * EW_WARPS) k_rounds_small(RoundCtl* __rest
       }
       mark_and_append<true>(g, nbm, active, v, false, bm, next, counters + C_NNEXT);
     }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
+    if ((threadIdx.x & 31) == 0 && mine) atomicAdd(counters + C_NIMP, mine);
     grid.sync();
     if (blockIdx.x == 0 && threadIdx.x == 0) {  // round_end with coherent (volatile) accesses
       volatile int* vc = counters;
       const int n_imp_all = vc[C_NIMP], n_next = vc[C_NNEXT];
       vctl->rounds = vctl->rounds + 1;
+      vctl->rounds_small = vctl->rounds_small + 1;
       vctl->evals = vctl->evals + vctl->n_cur;
       vctl->commits = vctl->commits + n_imp_all;
       int* t = vctl->cur;
@@ -92,6 +99,7 @@ __global__ void __launch_bounds__(32 * EW_WARPS) k_rounds_small(RoundCtl* __rest
   }
   // inside the round graph: arm the next size class and the WHILE condition
   // (the frontier is empty, or too large for this kernel)
+  if (blockIdx.x == 0 && threadIdx.x == 0) vctl->small_launches = vctl->small_launches + 1;
   if (in_graph && blockIdx.x == 0 && threadIdx.x == 0) {
     const int n = vctl->n_cur;
     set_size_class(n, hs, n_classes);

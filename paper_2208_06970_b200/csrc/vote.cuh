@@ -11,12 +11,15 @@
 //     the sequential fp64 sum equals the exact integer sum. Kernels reduce
 //     (2x+1) integers with warp match/reduce + 64-bit integer atomics and
 //     scale once: order-independent AND identical to the reference.
-//   * ORDERED path (any weights): a stable radix sort groups (phi(v), v)
-//     pairs by site in voxel order; one warp per site forms the terms
-//     (w, RN(w*ax), RN(w*ay), RN(w*az)) 32 at a time and four lanes add them
-//     in exactly the reference order.
+//   * ORDERED path (any weights): one warp per site walks the site's
+//     bounding box in voxel order and four lanes add the terms
+//     (w, RN(w*ax), RN(w*ay), RN(w*az)) of the region's voxels in exactly
+//     the reference order (k_vote_prep / k_vote_scan below). The earlier
+//     variant -- a stable radix sort of (site, (phi(v), v)) pairs, then
+//     k_vote_sum over the segments -- stays behind LRCVT_VOTE=sort.
 #pragma once
 #include "common.cuh"
+#include "mg.cuh"
 
 namespace lrcvt {
 
@@ -31,10 +34,11 @@ __device__ __forceinline__ int phi_chase(const int2* __restrict__ ss, int v, int
 }
 
 // EXACT path. acc layout: [4][S] u64 = count, sum(2x+1), sum(2y+1), sum(2z+1).
+template <bool MG>
 __global__ void __launch_bounds__(256) k_vote_exact(const int* __restrict__ list, int n, Geo g,
                                                     const int2* __restrict__ ss,
                                                     unsigned long long* __restrict__ acc,
-                                                    int n_sites) {
+                                                    int n_sites, const PeerView* __restrict__ pv) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x; i0 < n; i0 += stride) {
     const int64_t i = i0 + threadIdx.x;
@@ -45,7 +49,7 @@ __global__ void __launch_bounds__(256) k_vote_exact(const int* __restrict__ list
       const int2 a = ss[v];
       s = a.x;
       if (s >= 0) {
-        const int u = phi_chase(ss, v, a);
+        const int u = phi_chase_pv<MG>(pv, ss, v, a);
         int x, y, z;
         coords(g, u, x, y, z);
         cx = 2u * x + 1u; cy = 2u * y + 1u; cz = 2u * z + 1u;
@@ -152,6 +156,172 @@ __global__ void __launch_bounds__(WARPS * 32) k_vote_sum(const unsigned long lon
     q1 = q2; q2 = q3; w1 = w2;
   }
   if (lane < 4) sums[lane * n_sites + s] = acc;
+}
+
+// ---------------------------------------------------------------------------
+// ORDERED path without a sort: every site's voxels, in increasing voxel
+// order, are exactly the voxels of its region met by a row-major walk over
+// the region's bounding box (the box's own flat order is a sub-order of the
+// volume's x-fastest order). Two kernels:
+//   k_vote_prep  over the eligible list (voxel order): phi by chasing src,
+//                (site, phi) stored per voxel, per-site bounding box by warp
+//                match + reduce_min/max and six atomics per site group;
+//   k_vote_scan  one warp per site walks its box in chunks of 32 voxels
+//                (flat box order), picks the voxels of its region, forms their
+//                terms and lanes 0-3 add them in order -- the reference's
+//                exact accumulation order (_kernels.py:519-531).
+// A voxel belongs to region s iff sp[v].x == s and comp[v] == site_comp[s]
+// (entries of voxels outside the current eligible set may be stale; every
+// voxel of region s lies in s's component).
+constexpr int BOX_BIG = 0x3fffffff;
+constexpr int VS_DEPTH = 4;  // chunks in flight per warp in k_vote_scan
+
+template <bool MG>
+__global__ void __launch_bounds__(256) k_vote_prep(const int* __restrict__ list, int n, Geo g,
+                                                   const int2* __restrict__ ss, int2* __restrict__ sp,
+                                                   int* __restrict__ box, int n_sites,
+                                                   const PeerView* __restrict__ pv) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x; i0 < n; i0 += stride) {
+    const int64_t i = i0 + threadIdx.x;
+    int s = -1, x = 0, y = 0, z = 0;
+    if (i < n) {
+      const int v = list[i];
+      const int2 a = ss[v];
+      s = a.x;
+      int u = -1;
+      if (s >= 0) {
+        u = phi_chase_pv<MG>(pv, ss, v, a);
+        coords(g, v, x, y, z);
+      }
+      sp[v] = make_int2(s, u);
+    }
+    const unsigned grp = __match_any_sync(0xffffffffu, s);
+    const int x0 = __reduce_min_sync(grp, x), x1 = __reduce_max_sync(grp, x);
+    const int y0 = __reduce_min_sync(grp, y), y1 = __reduce_max_sync(grp, y);
+    const int z0 = __reduce_min_sync(grp, z), z1 = __reduce_max_sync(grp, z);
+    if (s >= 0 && (threadIdx.x & 31) == __ffs(grp) - 1) {
+      atomicMin(box + s, x0);
+      atomicMin(box + n_sites + s, y0);
+      atomicMin(box + 2 * n_sites + s, z0);
+      atomicMax(box + 3 * n_sites + s, x1);
+      atomicMax(box + 4 * n_sites + s, y1);
+      atomicMax(box + 5 * n_sites + s, z1);
+    }
+  }
+}
+
+__global__ void k_box_init(int* __restrict__ box, int n_sites) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n_sites) return;
+  box[s] = box[n_sites + s] = box[2 * n_sites + s] = BOX_BIG;
+  box[3 * n_sites + s] = box[4 * n_sites + s] = box[5 * n_sites + s] = -1;
+}
+
+// One warp per site; a (WARPS x 32 x 4) shared stage holds a chunk's terms.
+// The walk covers the box rows inside planes [zlo, zhi) (the whole volume on
+// one GPU). mode 0: every site, chains start at 0 (or init[s]); multi-GPU
+// slab steps: mode 1 = only sites whose box starts in this slab (chains
+// start at 0), mode 2 = only sites whose box starts in an earlier slab
+// (chains continue from init[s], the running sums handed over by the
+// previous slab). Sites a mode skips are left untouched in `sums`.
+template <int WARPS>
+__global__ void __launch_bounds__(WARPS * 32) k_vote_scan(const int2* __restrict__ sp, const int* __restrict__ comp,
+                                                          const int* __restrict__ box,
+                                                          const int* __restrict__ site_comp, int n_sites, Geo g,
+                                                          const double* __restrict__ w64,
+                                                          const float* __restrict__ w32, int w_mode, int zlo,
+                                                          int zhi, int mode, const double* __restrict__ init,
+                                                          double* __restrict__ sums) {
+  __shared__ double buf[WARPS][32][4];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int s = blockIdx.x * WARPS + wid;
+  if (s >= n_sites) return;
+  const int x0 = box[s], y0 = box[n_sites + s], bz0 = box[2 * n_sites + s];
+  const int bz1 = box[5 * n_sites + s];
+  if (mode == 1 && !(bz0 >= zlo && bz0 < zhi)) return;
+  if (mode == 2 && !(bz0 < zlo && bz1 >= zlo)) return;
+  const int z0 = bz0 > zlo ? bz0 : zlo;
+  const int z1 = bz1 < zhi - 1 ? bz1 : zhi - 1;
+  const int W = box[3 * n_sites + s] - x0 + 1, H = box[4 * n_sites + s] - y0 + 1, D = z1 - z0 + 1;
+  double acc = (init && mode != 1 && lane < 4) ? init[lane * n_sites + s] : 0.0;
+  if (W > 0 && H > 0 && D > 0) {
+    const int cs = __ldg(site_comp + s);
+    const long long T = (long long)W * H * D;
+    // flat box index k = lane + 32 * chunk -> (dx, dy, dz), advanced by 32 per chunk
+    int dx = lane % W, r = lane / W;
+    int dy = r % H, dz = r / H;
+    long long k = lane;  // flat index of this lane's next voxel to load
+    // VS_DEPTH chunks in flight: (site, phi), component and weight of every
+    // lane's voxel are loaded VS_DEPTH chunks ahead of the ordered adds (the
+    // walk is latency-bound otherwise: one chunk ~ one memory round trip)
+    int2 a[VS_DEPTH];
+    int c[VS_DEPTH];
+    double w[VS_DEPTH];
+    auto load = [&](int j) {
+      a[j] = make_int2(-1, -1);
+      c[j] = -2;
+      w[j] = 0.0;
+      if (k < T) {
+        const int v = (x0 + dx) + g.nx * ((y0 + dy) + g.ny * (z0 + dz));
+        a[j] = __ldg(sp + v);
+        c[j] = __ldg(comp + v);
+        w[j] = vote_weight(v, w64, w32, w_mode);
+      }
+      k += 32;
+      dx += 32;
+      if (dx >= W) {
+        const int q = dx / W;
+        dx -= q * W;
+        dy += q;
+        if (dy >= H) {
+          const int q2 = dy / H;
+          dy -= q2 * H;
+          dz += q2;
+        }
+      }
+    };
+#pragma unroll
+    for (int j = 0; j < VS_DEPTH; j++) load(j);
+    for (long long base = 0; base < T; base += 32 * VS_DEPTH) {
+#pragma unroll
+      for (int j = 0; j < VS_DEPTH; j++) {
+        const bool mine = a[j].x == s && c[j] == cs;
+        const int u = a[j].y;
+        const double wt = w[j];
+        load(j);  // refill this slot VS_DEPTH chunks ahead
+        const unsigned m = __ballot_sync(0xffffffffu, mine);
+        if (m) {
+          if (mine) {
+            const double4 t = vote_term(g, u, wt);
+            const int slot = __popc(m & ((1u << lane) - 1u));
+            buf[wid][slot][0] = t.x; buf[wid][slot][1] = t.y; buf[wid][slot][2] = t.z; buf[wid][slot][3] = t.w;
+          }
+          __syncwarp();
+          const int cnt = __popc(m);
+          if (lane < 4)
+            for (int q = 0; q < cnt; q++) acc = __dadd_rn(acc, buf[wid][q][lane]);
+          __syncwarp();
+        }
+      }
+    }
+  }
+  if (lane < 4) sums[lane * n_sites + s] = acc;
+}
+
+// multi-GPU ordered vote hand-over: the running sums after this slab --
+// this slab's chain results for sites whose box meets it, the incoming
+// running sums (zero on the first slab) for the others
+__global__ void k_vote_carry(const int* __restrict__ box, int n_sites, int zlo, int zhi,
+                             const double* __restrict__ res, const double* __restrict__ carry_in,
+                             double* __restrict__ carry_out) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n_sites) return;
+  const int bz0 = box[2 * n_sites + s], bz1 = box[5 * n_sites + s];
+  const bool meets = bz0 <= zhi - 1 && bz1 >= zlo && bz0 <= bz1;
+#pragma unroll
+  for (int k = 0; k < 4; k++)
+    carry_out[k * n_sites + s] = meets ? res[k * n_sites + s] : (carry_in ? carry_in[k * n_sites + s] : 0.0);
 }
 
 // step 2 (after the stable sort by key): segment starts/ends per site.

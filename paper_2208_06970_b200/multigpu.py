@@ -1,21 +1,35 @@
-"""Multi-GPU global mode: one tessellation over z-slabs of the whole volume,
+"""Multi-GPU global mode: ONE tessellation over z-slabs of the whole volume,
 bit-identical to the single-domain result (north star).
 
-Design: the per-voxel state is REPLICATED on every rank and
-the EVALUATION is partitioned -- rank r evaluates only the frontier voxels of
-its z-slab [zlo_r, zhi_r). After each relaxation round the improved
-proposals (24-byte records) are all-gathered over NVLink and every rank
-commits all of them, enqueueing only the neighbours that fall in its own
-slab. Every evaluation therefore reads exactly the global pre-round state,
-so site_of/dist/src, rounds, sweeps and the E/C counters equal the
-single-domain run; per round the only traffic is the proposal all-gather
-plus two count exchanges. The vote runs redundantly on every rank's
-identical state (no exchange, bit-exact).
+Design (csrc/mg.cuh): rank r OWNS planes [zlo_r, zhi_r).
+Every rank keeps full-size per-voxel buffers, but only its own slab plus one
+halo plane on each side is current locally:
 
-`Collective` hides where the ranks live:
-  * `Emulated` -- all ranks in this process on one GPU (state copies per
-    rank); used by the parity tests, since this environment has one GPU;
-  * `TorchDist` -- one rank per process, torch.distributed (NCCL on GPUs).
+  * evaluation: own frontier only (_eval_voxel, _kernels.py:147-246); the
+    26-neighbourhood lies in slab + halo; the rare far reads -- the state of a
+    shortcut node u = src(w) and the phi chains of the vote -- go to the
+    owning rank's buffer through a peer pointer (NVLink P2P / CUDA IPC);
+  * per round, only the improved proposals on the two boundary planes travel
+    (to rank - 1 and rank + 1), and each rank commits its own proposals plus
+    the received halo ones (_apply_and_enqueue, _kernels.py:285-334, with the
+    enqueue restricted to the own slab); the global frontier size decides
+    the next round (_run_phase, _kernels.py:337-385) and the sweeps
+    (tessellation.py:170-189);
+  * vote (_centroid_targets, _kernels.py:513-532) over the own slab: unit
+    weights give exact integer partial sums, summed by an all-reduce; any
+    other weights keep the reference's voxel-order fp64 chains -- each site's
+    chain runs slab after slab, the running sums handed from rank to rank
+    for the sites that straddle a slab boundary (all other sites in
+    parallel); every rank then moves all sites from identical sums.
+
+Every evaluation reads exactly the global pre-round state, so site_of / dist
+/ src / state, rounds, sweeps and the E / C counters equal the single-domain
+run. `Collective` hides where the ranks live:
+  * `Emulated` -- all ranks in this process on one GPU; the ranks' steps run
+    one after another on one stream (no kernel ever waits on another);
+  * `TorchDist` -- one rank per process, torch.distributed (NCCL on GPUs,
+    gloo with host staging in the CPU-coordinated tests); peer pointers via
+    CUDA IPC handles exchanged at set-up.
 """
 
 from __future__ import annotations
@@ -40,24 +54,68 @@ def slab_bounds(nz: int, world: int) -> list[tuple[int, int]]:
     return out
 
 
+class _DevBuf:
+    """A raw device allocation seen as a torch tensor (zero copy)."""
+
+    def __init__(self, ptr: int, shape, typestr: str):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr, "data": (int(ptr), False),
+                                         "version": 3, "strides": None}
+
+
+def as_tensor(torch, ptr, shape, typestr):
+    return torch.as_tensor(_DevBuf(ptr, shape, typestr), device="cuda")
+
+
 class Emulated:
-    """All ranks live in this process (one GPU): gathers are concatenations."""
+    """All ranks live in this process (one GPU): collectives are host-side
+    list operations over the ranks' tensors."""
 
     def __init__(self, world: int):
         self.world = world
         self.local_ranks = list(range(world))
 
-    def all_counts(self, local: list[int]) -> list[int]:
-        return list(local)
+    def sum_ints(self, per_rank: dict) -> list[int]:
+        vals = list(per_rank.values())
+        return [int(sum(v[i] for v in vals)) for i in range(len(vals[0]))]
 
-    def all_props(self, local: list, torch):
-        return torch.cat(local) if local else torch.empty(0, dtype=torch.uint8, device="cuda")
+    def exchange_halo(self, lo: dict, hi: dict, torch) -> dict:
+        """rank r receives hi of r - 1 and lo of r + 1 (uint8 tensors)."""
+        out = {}
+        for r in self.local_ranks:
+            parts = ([hi[r - 1]] if r > 0 else []) + ([lo[r + 1]] if r + 1 < self.world else [])
+            parts = [p for p in parts if p.numel()]
+            out[r] = torch.cat(parts) if parts else torch.empty(0, dtype=torch.uint8, device="cuda")
+        return out
+
+    def allreduce(self, per_rank: dict, op: str, torch):
+        ts = list(per_rank.values())
+        acc = ts[0].clone()
+        for t in ts[1:]:
+            if op == "sum":
+                acc += t
+            elif op == "min":
+                torch.minimum(acc, t, out=acc)
+            else:
+                torch.maximum(acc, t, out=acc)
+        return acc
+
+    def chain(self, step, shape, torch):
+        """carry = step(r, carry) for r = 0..world-1 in order; returns the last
+        rank's carry (the final running sums), identical on every rank."""
+        carry = None
+        for r in range(self.world):
+            carry = step(r, carry)
+        return carry
+
+    def peer_pointers(self, own: dict):
+        """own: {rank: (ss_ptr, dist_ptr)} -> lists over all ranks."""
+        return [own[r][0] for r in range(self.world)], [own[r][1] for r in range(self.world)]
 
 
 class TorchDist:
     """One rank per process over torch.distributed: NCCL on CUDA tensors for
-    the GPU path; any backend works for the host-side protocol (device="cpu"
-    with gloo in the CPU tests)."""
+    the GPU path; device="cpu" stages every collective through host memory
+    (gloo) -- the CPU-coordinated tests of the protocol."""
 
     def __init__(self, group=None, device: str = "cuda"):
         import torch.distributed as dist
@@ -66,7 +124,15 @@ class TorchDist:
         self.group = group
         self.device = device
         self.world = dist.get_world_size(group)
-        self.local_ranks = [dist.get_rank(group)]
+        self.rank = dist.get_rank(group)
+        self.local_ranks = [self.rank]
+        self._opened = []
+        import torch
+
+        self.home = "cuda" if torch.cuda.is_available() else "cpu"  # where results are handed back
+
+    def _to(self, t):
+        return t.to(self.device) if str(t.device) != self.device else t
 
     def all_counts(self, local: list[int]) -> list[int]:
         import torch
@@ -76,120 +142,319 @@ class TorchDist:
         self.dist.all_gather(out, t, group=self.group)
         return [int(v) for x in out for v in x.tolist()]
 
-    def all_props(self, local: list, torch):
-        """Concatenate every rank's proposal bytes in rank order (padded
-        all_gather: NCCL has no variable-size all-gather)."""
-        counts = self.all_counts([int(local[0].numel())])
-        m = max(counts)
+    def sum_ints(self, per_rank: dict) -> list[int]:
+        import torch
+
+        t = torch.tensor(per_rank[self.rank], dtype=torch.int64, device=self.device)
+        self.dist.all_reduce(t, group=self.group)
+        return [int(v) for v in t.tolist()]
+
+    def _all_bytes(self, local, torch):
+        """all ranks' uint8 tensors (variable sizes) in rank order."""
+        n = self.all_counts([int(local.numel())])
+        m = max(n)
         if m == 0:
-            return torch.empty(0, dtype=torch.uint8, device=self.device)
+            return [local[:0]] * self.world
         pad = torch.zeros(m, dtype=torch.uint8, device=self.device)
-        pad[: local[0].numel()] = local[0]
+        pad[: local.numel()] = self._to(local)
         out = [torch.empty(m, dtype=torch.uint8, device=self.device) for _ in range(self.world)]
         self.dist.all_gather(out, pad, group=self.group)
-        return torch.cat([o[:c] for o, c in zip(out, counts)])
+        return [o[:c] for o, c in zip(out, n)]
+
+    def all_props(self, local: list, torch):
+        """Concatenate every rank's proposal bytes in rank order."""
+        return torch.cat(self._all_bytes(local[0], torch))
+
+    def exchange_halo(self, lo: dict, hi: dict, torch) -> dict:
+        r = self.rank
+        los = self._all_bytes(lo[r], torch)
+        his = self._all_bytes(hi[r], torch)
+        parts = ([his[r - 1]] if r > 0 else []) + ([los[r + 1]] if r + 1 < self.world else [])
+        parts = [p for p in parts if p.numel()]
+        got = torch.cat(parts) if parts else torch.empty(0, dtype=torch.uint8, device=self.device)
+        return {r: got.to(self.home)}
+
+    def allreduce(self, per_rank: dict, op: str, torch):
+        t = self._to(per_rank[self.rank].clone())
+        red = {"sum": self.dist.ReduceOp.SUM, "min": self.dist.ReduceOp.MIN, "max": self.dist.ReduceOp.MAX}[op]
+        self.dist.all_reduce(t, op=red, group=self.group)
+        return t.to(self.home)
+
+    def chain(self, step, shape, torch):
+        r = self.rank
+        carry = None
+        if r > 0:
+            buf = torch.empty(shape, dtype=torch.float64, device=self.device)
+            self.dist.recv(buf, src=r - 1, group=self.group)
+            carry = buf.to(self.home)
+        carry = step(r, carry)
+        if r + 1 < self.world:
+            if self.home == "cuda":
+                torch.cuda.current_stream().synchronize()
+            self.dist.send(self._to(carry), dst=r + 1, group=self.group)
+        final = self._to(carry) if r == self.world - 1 else torch.empty(shape, dtype=torch.float64,
+                                                                      device=self.device)
+        self.dist.broadcast(final, src=self.world - 1, group=self.group)
+        return final.to(self.home)
+
+    def peer_pointers(self, own: dict):
+        """CUDA IPC: export this rank's state buffers, open every other rank's."""
+        import torch
+
+        L = _lib.lib()
+        h = (ctypes.c_uint8 * 128)()
+        base = ctypes.addressof(h)
+        ss, dist = own[self.rank]
+        _lib.check(L.lrcvt_ipc_export(ss, base), "ipc export")
+        _lib.check(L.lrcvt_ipc_export(dist, base + 64), "ipc export")
+        mine = torch.tensor(list(bytes(h)), dtype=torch.uint8, device=self.device)
+        allh = [torch.empty_like(mine) for _ in range(self.world)]
+        self.dist.all_gather(allh, mine, group=self.group)
+        pss, pdist = [], []
+        for q, t in enumerate(allh):
+            if q == self.rank:
+                pss.append(ss)
+                pdist.append(dist)
+                continue
+            raw = (ctypes.c_uint8 * 128)(*t.cpu().tolist())
+            a, b = ctypes.c_void_p(), ctypes.c_void_p()
+            _lib.check(L.lrcvt_ipc_open(ctypes.addressof(raw), ctypes.byref(a)), "ipc open")
+            _lib.check(L.lrcvt_ipc_open(ctypes.addressof(raw) + 64, ctypes.byref(b)), "ipc open")
+            self._opened += [a.value, b.value]
+            pss.append(a.value)
+            pdist.append(b.value)
+        return pss, pdist
+
+    def close(self):
+        L = _lib.lib()
+        for p in self._opened:
+            L.lrcvt_ipc_close(p)
+        self._opened = []
 
 
 class GlobalClassifier:
-    """Slab-partitioned voronoi_classify over a Collective. Each local rank
-    owns an Engine (plan with slab bounds) holding a full replicated copy of
-    the per-voxel state (engine.ss / engine.dist / engine.state)."""
+    """Slab-partitioned voronoi_classify and centroidal update over a
+    Collective. Each local rank owns an Engine (plan with slab bounds and
+    peer view); its plan-owned state buffers are current on the own slab
+    (engine.ss / engine.dist views of them, engine.state its state bits)."""
 
     def __init__(self, dims, spacing, component: np.ndarray, n_components: int, max_sites: int, coll):
-        self.torch = _lib.require_cuda()
+        torch = self.torch = _lib.require_cuda()
         self.L = _lib.lib()
         self.coll = coll
         self.dims = tuple(int(d) for d in dims)
+        self.spacing = tuple(float(s) for s in spacing)
+        self.n = int(np.prod(self.dims))
         self.bounds = slab_bounds(self.dims[2], coll.world)
         self.engines = {}
         comp_dev = None
+        own = {}
         for r in coll.local_ranks:
             eng = Engine(self.dims, spacing, component, n_components, max_sites, comp_dev)
             comp_dev = eng.comp  # replicated labels shared between in-process ranks
             lo, hi = self.bounds[r]
             _lib.check(self.L.lrcvt_mg_set_slab(eng.plan, lo, hi), "lrcvt_mg_set_slab")
+            a, b = ctypes.c_void_p(), ctypes.c_void_p()
+            _lib.check(self.L.lrcvt_mg_state(eng.plan, ctypes.byref(a), ctypes.byref(b)), "lrcvt_mg_state")
+            eng.ss = as_tensor(torch, a.value, (self.n, 2), "<i4")
+            eng.dist = as_tensor(torch, b.value, (self.n,), "<f8")
+            own[r] = (a.value, b.value)
             self.engines[r] = eng
+        self.timing = False  # per-rank device time (CUDA events around every rank's calls)
+        self._ev = {r: [] for r in self.engines}
+        pss, pdist = coll.peer_pointers(own)
+        zb = (ctypes.c_int64 * (coll.world + 1))(*([lo for lo, _ in self.bounds] + [self.dims[2]]))
+        arr_ss = (ctypes.c_void_p * coll.world)(*pss)
+        arr_d = (ctypes.c_void_p * coll.world)(*pdist)
+        for r, eng in self.engines.items():
+            _lib.check(self.L.lrcvt_mg_set_peers(eng.plan, coll.world, zb, arr_ss, arr_d), "lrcvt_mg_set_peers")
+        self._S = 0
 
-    def _props(self, eng, n):
-        t = self.torch.empty(n * PROP_BYTES, dtype=self.torch.uint8, device="cuda")
-        _lib.check(self.L.lrcvt_mg_copy_proposals(eng.plan, t.data_ptr() if n else None, n,
-                                                   _lib.stream_handle(self.torch)), "copy proposals")
-        return t
+    def _st(self):
+        return _lib.stream_handle(self.torch)
+
+    def _t(self, r, fn):
+        """run fn() for rank r, bracketed by CUDA events when timing"""
+        if not self.timing:
+            return fn()
+        torch = self.torch
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        out = fn()
+        b.record()
+        self._ev[r].append((a, b))
+        return out
+
+    def rank_ms(self) -> dict:
+        """device milliseconds spent in each local rank's own kernels since the
+        last call (emulated ranks share one GPU and never overlap)"""
+        self.torch.cuda.synchronize()
+        out = {r: sum(a.elapsed_time(b) for a, b in evs) for r, evs in self._ev.items()}
+        self._ev = {r: [] for r in self.engines}
+        return out
 
     def _round(self, phase: int, sweep: int, stats: dict) -> int:
         """One relaxation round (or sweep) on all ranks; returns the global
-        number of improved proposals."""
-        L, st = self.L, _lib.stream_handle(self.torch)
-        evals, props = [], []
+        number of improved proposals and sets the global frontier size."""
+        L, torch, st = self.L, self.torch, self._st()
+        counts, lo, hi = {}, {}, {}
         for r, eng in self.engines.items():
-            ne, nimp = ctypes.c_int64(), ctypes.c_int64()
-            _lib.check(L.lrcvt_mg_eval(eng.plan, phase, sweep, ctypes.byref(ne), ctypes.byref(nimp), st),
-                       "lrcvt_mg_eval")
-            evals.append(int(ne.value))
-            props.append(self._props(eng, int(nimp.value)))
-        stats["evaluations"] += sum(self.coll.all_counts(evals))
-        allp = self.coll.all_props(props, self.torch)
-        n_all = allp.numel() // PROP_BYTES
-        stats["commits"] += n_all
-        if sweep and n_all == 0:
-            return 0
-        nexts = []
+            ne, npr, nlo, nhi = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+            self._t(r, lambda: _lib.check(L.lrcvt_mg_eval(eng.plan, phase, sweep, ctypes.byref(ne), ctypes.byref(npr),
+                                                          ctypes.byref(nlo), ctypes.byref(nhi), st), "lrcvt_mg_eval"))
+            counts[r] = [int(ne.value), int(npr.value)]
+            lo[r] = self._bytes(L.lrcvt_mg_boundary(eng.plan, 0), int(nlo.value))
+            hi[r] = self._bytes(L.lrcvt_mg_boundary(eng.plan, 1), int(nhi.value))
+        halo = self.coll.exchange_halo(lo, hi, torch)
+        nexts = {}
         for r, eng in self.engines.items():
+            h = halo[r]
             nn = ctypes.c_int64()
-            _lib.check(L.lrcvt_mg_commit(eng.plan, allp.data_ptr() if n_all else None, n_all, sweep,
-                                         ctypes.byref(nn), st), "lrcvt_mg_commit")
-            nexts.append(int(nn.value))
-        self._frontier = nexts
-        return n_all
+            self._t(r, lambda: _lib.check(L.lrcvt_mg_commit(eng.plan, h.data_ptr() if h.numel() else None,
+                                                            h.numel() // PROP_BYTES, sweep, ctypes.byref(nn), st),
+                                          "lrcvt_mg_commit"))
+            nexts[r] = [int(nn.value)] + counts[r]
+        tot = self.coll.sum_ints(nexts)
+        self._frontier = tot[0]
+        stats["evaluations"] += tot[1]
+        stats["commits"] += tot[2]
+        return tot[2]
+
+    def _bytes(self, ptr, n):
+        torch = self.torch
+        if n == 0 or not ptr:
+            return torch.empty(0, dtype=torch.uint8, device="cuda")
+        return as_tensor(torch, ptr, (n * PROP_BYTES,), "|u1").clone()
 
     def _run_rounds(self, phase: int, stats: dict):
-        while sum(self.coll.all_counts(self._frontier)) > 0:
+        while self._frontier > 0:
             stats["rounds"] += 1
             self._round(phase, 0, stats)
 
     def classify(self, site_pos, site_comp) -> dict:
         """site_pos float64[S,3], site_comp int32[S] on the device; returns
         the report counters (rounds, sweeps, assigned, evaluations, commits)."""
-        L, st = self.L, _lib.stream_handle(self.torch)
+        L, st = self.L, self._st()
         S = int(site_pos.shape[0])
+        self._S = S
         stats = {"rounds": 0, "sweeps": 0, "evaluations": 0, "commits": 0}
-        self._frontier = []
+        front, bad = {}, 0
         for r, eng in self.engines.items():
-            eng.reserve(S)
-            _lib.check(L.lrcvt_mg_set_slab(eng.plan, *self.bounds[r]), "lrcvt_mg_set_slab")
+            if S > eng.max_sites:
+                raise ValueError("more sites than the global classifier was sized for")
             nf = ctypes.c_int64()
-            rc = _lib.check(L.lrcvt_mg_begin(eng.plan, S, site_pos.data_ptr(), site_comp.data_ptr(),
-                                             eng.ss.data_ptr(), eng.dist.data_ptr(), ctypes.byref(nf), st),
-                            "lrcvt_mg_begin")
-            if rc > 0:
-                raise ValueError(f"{rc} sites sit outside their recorded component")
-            self._frontier.append(int(nf.value))
+            rc = self._t(r, lambda: _lib.check(L.lrcvt_mg_begin(eng.plan, S, site_pos.data_ptr(),
+                                                                site_comp.data_ptr(), eng.ss.data_ptr(),
+                                                                eng.dist.data_ptr(), ctypes.byref(nf), st),
+                                               "lrcvt_mg_begin"))
+            bad = max(bad, rc)
+            front[r] = [int(nf.value)]
+        if bad > 0:
+            raise ValueError(f"{bad} sites sit outside their recorded component")
+        self._frontier = self.coll.sum_ints(front)[0]
         self._run_rounds(1, stats)  # phase 1 (tessellation.py:151-156)
-        self._frontier = []
+        front = {}
         for r, eng in self.engines.items():
             nf = ctypes.c_int64()
-            _lib.check(L.lrcvt_mg_phase2(eng.plan, S, site_comp.data_ptr(), ctypes.byref(nf), st), "phase2")
-            self._frontier.append(int(nf.value))
+            self._t(r, lambda: _lib.check(L.lrcvt_mg_phase2(eng.plan, S, site_comp.data_ptr(), ctypes.byref(nf),
+                                                            st), "phase2"))
+            front[r] = [int(nf.value)]
+        self._frontier = self.coll.sum_ints(front)[0]
         while True:  # phase 2 + verification sweeps (tessellation.py:170-189)
             self._run_rounds(2, stats)
             stats["sweeps"] += 1
             if self._round(2, 1, stats) == 0:
                 break
+        assigned = {}
         for r, eng in self.engines.items():
             a = ctypes.c_int64()
-            _lib.check(L.lrcvt_mg_finish(eng.plan, eng.ss.data_ptr(), eng.state.data_ptr(), ctypes.byref(a), st),
-                       "lrcvt_mg_finish")
-            stats["assigned"] = int(a.value)
+            self._t(r, lambda: _lib.check(L.lrcvt_mg_finish(eng.plan, eng.ss.data_ptr(), eng.state.data_ptr(),
+                                                            ctypes.byref(a), st), "lrcvt_mg_finish"))
+            assigned[r] = [int(a.value)]
+        stats["assigned"] = self.coll.sum_ints(assigned)[0]
         return stats
+
+    def centroidal(self, site_pos, site_comp, weight_mode: int, weights, backoff: float):
+        """centroidal_update (tessellation.py:211-248) over the slabs; returns
+        (new_pos, disp, empty) -- identical on every rank."""
+        torch, L, st = self.torch, self.L, self._st()
+        S = int(site_pos.shape[0])
+        sx, sy, sz = self.spacing
+        exact = (weight_mode == _lib.W_ONES and all(_pow2(s) for s in self.spacing)
+                 and max(self.dims) <= (1 << 20))
+        if exact:
+            acc = {}
+            for r, eng in self.engines.items():
+                a = torch.empty((4, S), dtype=torch.int64, device="cuda")
+                self._t(r, lambda: _lib.check(L.lrcvt_mg_vote_exact(eng.plan, S, eng.ss.data_ptr(), a.data_ptr(), st),
+                                              "vote"))
+                acc[r] = a
+            red = self.coll.allreduce(acc, "sum", torch)
+            sums = torch.empty((4, S), dtype=torch.float64, device="cuda")
+            eng0 = next(iter(self.engines.values()))
+            _lib.check(L.lrcvt_mg_vote_exact_finish(eng0.plan, S, red.data_ptr(), sums.data_ptr(), st), "finish")
+        else:
+            boxes, res = {}, {}
+            for r, eng in self.engines.items():
+                b = torch.empty((6, S), dtype=torch.int32, device="cuda")
+                self._t(r, lambda: _lib.check(L.lrcvt_mg_vote_box(eng.plan, S, eng.ss.data_ptr(), b.data_ptr(), st),
+                                              "vote box"))
+                boxes[r] = b
+            lo = self.coll.allreduce({r: b[:3].contiguous() for r, b in boxes.items()}, "min", torch)
+            hi = self.coll.allreduce({r: b[3:].contiguous() for r, b in boxes.items()}, "max", torch)
+            box = torch.cat([lo, hi]).contiguous()
+            wp = _lib.ptr(weights)
+            for r, eng in self.engines.items():  # sites whose box starts in the own slab: all ranks at once
+                out = torch.zeros((4, S), dtype=torch.float64, device="cuda")
+                self._t(r, lambda: _lib.check(L.lrcvt_mg_vote_scan(eng.plan, S, site_comp.data_ptr(), weight_mode, wp,
+                                                                   1, box.data_ptr(), None, out.data_ptr(), st),
+                                              "vote scan"))
+                res[r] = out
+
+            def step(r, carry):  # sites continuing from earlier slabs, then the hand-over
+                eng = self.engines[r]
+                if carry is not None:
+                    self._t(r, lambda: _lib.check(L.lrcvt_mg_vote_scan(eng.plan, S, site_comp.data_ptr(), weight_mode,
+                                                                       wp, 2, box.data_ptr(), carry.data_ptr(),
+                                                                       res[r].data_ptr(), st), "vote scan"))
+                out = torch.empty((4, S), dtype=torch.float64, device="cuda")
+                self._t(r, lambda: _lib.check(L.lrcvt_mg_vote_carry(eng.plan, S, box.data_ptr(), res[r].data_ptr(),
+                                                                    carry.data_ptr() if carry is not None else None,
+                                                                    out.data_ptr(), st), "vote carry"))
+                return out
+
+            sums = self.coll.chain(step, (4, S), torch)
+        new_pos = disp = None
+        empty = ctypes.c_int64()
+        for r, eng in self.engines.items():  # every rank moves every site (identical inputs)
+            new_pos = torch.empty((S, 3), dtype=torch.float64, device="cuda")
+            disp = torch.empty(S, dtype=torch.float64, device="cuda")
+            np_, dp_ = new_pos, disp
+            self._t(r, lambda: _lib.check(L.lrcvt_mg_move(eng.plan, S, site_pos.data_ptr(), site_comp.data_ptr(),
+                                                          sums.data_ptr(), float(backoff), np_.data_ptr(),
+                                                          dp_.data_ptr(), ctypes.byref(empty), st), "lrcvt_mg_move"))
+        return new_pos, disp, int(empty.value)
+
+    def own_slab(self, r):
+        """(voxel range, engine) of rank r's own slab."""
+        lo, hi = self.bounds[r]
+        nxy = self.dims[0] * self.dims[1]
+        return lo * nxy, hi * nxy, self.engines[r]
 
     def any_engine(self) -> Engine:
         return next(iter(self.engines.values()))
 
 
+def _pow2(s: float) -> bool:
+    m, _ = math.frexp(s)
+    return s > 0 and m == 0.5
+
+
 def global_lrcvt(grid, labels, seeding, lloyd, coll=None):
-    """lrcvt() (tessellation.py:251-275) in global mode: classification
-    partitioned over the Collective's ranks, vote + move redundantly on each
-    rank's replicated state. Returns (Tessellation, trace) on every rank."""
+    """lrcvt() (tessellation.py:251-275) in global mode: classification and
+    vote partitioned over the Collective's ranks. Returns (Tessellation,
+    trace); the per-voxel arrays are assembled from the local ranks' slabs
+    (every slab when all ranks are local)."""
     from .seeding import Site, seed_sites, voxel_weights
     from .tessellation import Tessellation, lloyd_weight_mode, voxel_length
 
@@ -209,20 +474,25 @@ def global_lrcvt(grid, labels, seeding, lloyd, coll=None):
     trace: list[float] = []
     for _ in range(lloyd.max_updates):
         gc.classify(pos_d, sc_d)
-        new = None
-        for eng in gc.engines.values():  # identical on every rank
-            # the vote covers the whole (replicated) volume: full-range plan
-            _lib.check(gc.L.lrcvt_mg_set_slab(eng.plan, 0, grid.dims[2]), "lrcvt_mg_set_slab")
-            new, disp, _, _ = eng.centroidal(pos_d, sc_d, mode, w_d, 0.5 * vlen)
-        pos_d = new
+        pos_d, disp, _ = gc.centroidal(pos_d, sc_d, mode, w_d, 0.5 * vlen)
         d = disp.cpu().numpy()
         mean_ds = float(d.mean() / vlen) if d.size else 0.0
         trace.append(mean_ds)
         if mean_ds < lloyd.ds_tolerance:
             break
     st = gc.classify(pos_d, sc_d)
-    eng = gc.any_engine()
-    ss = eng.ss.cpu().numpy()
+    n = grid.size
+    site_of = np.full(n, -1, np.int32)
+    src = np.full(n, -1, np.int32)
+    dist = np.full(n, np.inf)
+    state = np.zeros(n, np.uint8)
+    for r in gc.engines:
+        v0, v1, eng = gc.own_slab(r)
+        ss = eng.ss[v0:v1].cpu().numpy()
+        site_of[v0:v1] = ss[:, 0]
+        src[v0:v1] = ss[:, 1]
+        dist[v0:v1] = eng.dist[v0:v1].cpu().numpy()
+        state[v0:v1] = eng.state[v0:v1].cpu().numpy()
     final_pos = pos_d.cpu().numpy()
     final_sites = [Site((float(p[0]), float(p[1]), float(p[2])), int(c)) for p, c in zip(final_pos, sc)]
     has = np.zeros(max(labels.n_components, 1), dtype=bool)
@@ -231,7 +501,6 @@ def global_lrcvt(grid, labels, seeding, lloyd, coll=None):
               "components_without_sites": sorted(int(c.id) for c in labels.component_table if not has[c.id]),
               "assigned": st["assigned"], "seeding": seed_report, "updates": len(trace),
               "evaluations": st["evaluations"], "commits": st["commits"]}
-    tess = Tessellation(grid.dims, grid.spacing, np.ascontiguousarray(ss[:, 0]), eng.dist.cpu().numpy(),
-                        np.ascontiguousarray(ss[:, 1]), eng.state.cpu().numpy(),
+    tess = Tessellation(grid.dims, grid.spacing, site_of, dist, src, state,
                         np.ascontiguousarray(labels.component, dtype=np.int32), final_sites, report, weights)
     return tess, trace

@@ -168,6 +168,7 @@ class Engine:
         self.version = 0  # bumps on every classify; guards host<->device reuse
         self.classify_seq = 0  # bumps on every classify call (the plan's eligible list follows it)
         self.stats = _lib.ClassifyStats()
+        self._out_dirty = True
         self._fin = weakref.finalize(self, Engine._destroy, self.L, self.plan)
 
     @staticmethod
@@ -202,10 +203,18 @@ class Engine:
         self.reserve(S)
         ss, dist, state = out if out is not None else (self.ss, self.dist, self.state)
         self.classify_seq += 1
-        rc = _lib.check(self.L.lrcvt_classify(
-            self.plan, S, _lib.ptr(site_pos), _lib.ptr(site_comp), ss.data_ptr(),
-            dist.data_ptr(), state.data_ptr() if want_state else None,
-            ctypes.byref(self.stats), _lib.stream_handle(self.torch)), "lrcvt_classify")
+        # the engine's own buffers are only ever written by its classifies: the plan may reset just the
+        # eligible voxels when they come back (lrcvt_plan_persistent_outputs)
+        self.L.lrcvt_plan_persistent_outputs(self.plan, 1 if out is None and not self._out_dirty else 0)
+        if out is None:
+            self._out_dirty = False
+        try:
+            rc = _lib.check(self.L.lrcvt_classify(
+                self.plan, S, _lib.ptr(site_pos), _lib.ptr(site_comp), ss.data_ptr(),
+                dist.data_ptr(), state.data_ptr() if want_state else None,
+                ctypes.byref(self.stats), _lib.stream_handle(self.torch)), "lrcvt_classify")
+        finally:
+            self.L.lrcvt_plan_persistent_outputs(self.plan, 0)
         if out is None:
             self.version += 1
         if rc > 0:
@@ -247,6 +256,7 @@ class Engine:
         packed[:, 0] = site_of
         packed[:, 1] = src
         self.ss.copy_(self.torch.from_numpy(packed))
+        self._out_dirty = True  # written outside a classify: the next one resets every voxel
         self.version += 1
 
 

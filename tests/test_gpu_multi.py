@@ -41,12 +41,43 @@ def test_global_classify_matches_single_domain(world, case):
     assert st["assigned"] == ref.report["assigned"]
     assert st["evaluations"] == ref._b200_stats["evaluations"]
     assert st["commits"] == ref._b200_stats["commits"]
-    for r, eng in gc.engines.items():
-        ss = eng.ss.cpu().numpy()
-        assert np.array_equal(ss[:, 0], ref.site_of), r
-        assert np.array_equal(ss[:, 1], ref.src), r
-        assert np.array_equal(eng.dist.cpu().numpy(), ref.dist), r
-        assert np.array_equal(eng.state.cpu().numpy(), ref.state), r
+    for r in gc.engines:  # every rank's own slab
+        v0, v1, eng = gc.own_slab(r)
+        ss = eng.ss[v0:v1].cpu().numpy()
+        assert np.array_equal(ss[:, 0], ref.site_of[v0:v1]), r
+        assert np.array_equal(ss[:, 1], ref.src[v0:v1]), r
+        assert np.array_equal(eng.dist[v0:v1].cpu().numpy(), ref.dist[v0:v1]), r
+        assert np.array_equal(eng.state[v0:v1].cpu().numpy(), ref.state[v0:v1]), r
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+@pytest.mark.parametrize("wf,gamma", [(None, 1.0), ("g", 1.0), ("g", 0.5)])
+def test_global_centroidal_matches_single_domain(world, wf, gamma):
+    """The slab-partitioned vote (integer all-reduce for unit weights, the
+    running-sum hand-over for voxel-order fp64 chains) and the replicated
+    move give the single-domain sums and sites bit for bit."""
+    import torch
+
+    from paper_2208_06970_b200 import SeedingParams, centroidal_update, seed_sites, voronoi_classify, voxel_weights
+    from paper_2208_06970_b200.multigpu import Emulated, GlobalClassifier
+    from paper_2208_06970_b200.tessellation import lloyd_weight_mode, voxel_length
+
+    grid, labels, _, _ = _setup("random-smooth", (36, 40, 44), [0.35, 0.6, 0.8], 40)
+    params = SeedingParams(alpha=70, seed=3, weight_field=wf, gamma=gamma)
+    sites, _ = seed_sites(grid, labels, params)
+    w = voxel_weights(grid, params)
+    ref = voronoi_classify(grid, labels, sites, w)
+    want, want_ds = centroidal_update(ref)
+    pos = torch.from_numpy(ref.site_positions()).cuda()
+    sc = torch.from_numpy(ref.site_components()).cuda()
+    gc = GlobalClassifier(grid.dims, grid.spacing, labels.component, labels.n_components, len(sites),
+                          Emulated(world))
+    gc.classify(pos, sc)
+    mode, w_d = lloyd_weight_mode(torch, grid, params, w)
+    vlen = voxel_length(grid.dims, grid.spacing)
+    new_pos, disp, _ = gc.centroidal(pos, sc, mode, w_d, 0.5 * vlen)
+    assert np.array_equal(new_pos.cpu().numpy(), np.array([s.position for s in want]))
+    assert float(disp.cpu().numpy().mean() / vlen) == want_ds
 
 
 @pytest.mark.parametrize("world", [2, 4])
@@ -90,6 +121,73 @@ def test_global_classify_over_nccl_single_rank():
         eng = gc.any_engine()
         assert np.array_equal(eng.ss.cpu().numpy()[:, 0], ref.site_of)
         assert np.array_equal(eng.dist.cpu().numpy(), ref.dist)
+        assert np.array_equal(eng.state.cpu().numpy(), ref.state)
         assert st["evaluations"] == ref._b200_stats["evaluations"]
     finally:
         dist.destroy_process_group()
+
+
+def _two_proc_worker(rank, world, port, outdir):
+    """One rank per process, both on cuda:0: gloo (host) for the collectives,
+    CUDA IPC mappings of the other rank's state buffers for the far reads."""
+    import os
+    import sys
+    from pathlib import Path
+
+    sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+    import torch
+    import torch.distributed as dist
+
+    from paper_2208_06970_b200 import SeedingParams, centroidal_update, seed_sites, voronoi_classify, voxel_weights
+    from paper_2208_06970_b200.multigpu import GlobalClassifier, TorchDist
+    from paper_2208_06970_b200.tessellation import lloyd_weight_mode, voxel_length
+
+    torch.cuda.set_device(0)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        grid, labels, _, _ = _setup("horseshoe", (48, 44, 40), [0.0, 0.12, 0.3], 50)
+        params = SeedingParams(alpha=60, seed=5, weight_field="g")
+        sites, _ = seed_sites(grid, labels, params)
+        w = voxel_weights(grid, params)
+        ref = voronoi_classify(grid, labels, sites, w)
+        want, _ = centroidal_update(ref)
+        pos = torch.from_numpy(ref.site_positions()).cuda()
+        sc = torch.from_numpy(ref.site_components()).cuda()
+        coll = TorchDist(device="cpu")
+        gc = GlobalClassifier(grid.dims, grid.spacing, labels.component, labels.n_components, len(sites), coll)
+        st = gc.classify(pos, sc)
+        v0, v1, eng = gc.own_slab(rank)
+        ok = (np.array_equal(eng.ss[v0:v1].cpu().numpy()[:, 0], ref.site_of[v0:v1])
+              and np.array_equal(eng.ss[v0:v1].cpu().numpy()[:, 1], ref.src[v0:v1])
+              and np.array_equal(eng.dist[v0:v1].cpu().numpy(), ref.dist[v0:v1])
+              and np.array_equal(eng.state[v0:v1].cpu().numpy(), ref.state[v0:v1])
+              and st["rounds"] == ref.report["rounds"] and st["sweeps"] == ref.report["sweeps"]
+              and st["evaluations"] == ref._b200_stats["evaluations"] and st["assigned"] == ref.report["assigned"])
+        mode, w_d = lloyd_weight_mode(torch, grid, params, w)
+        new_pos, _, _ = gc.centroidal(pos, sc, mode, w_d, 0.5 * voxel_length(grid.dims, grid.spacing))
+        ok = ok and np.array_equal(new_pos.cpu().numpy(), np.array([s.position for s in want]))
+        torch.cuda.synchronize()
+        dist.barrier()
+        coll.close()
+        Path(outdir, f"r{rank}").write_text("ok" if ok else "mismatch")
+    finally:
+        dist.destroy_process_group()
+
+
+def test_global_classify_two_processes_gloo_ipc():
+    """2 processes x 1 shared GPU: the TorchDist protocol (gloo, host-staged)
+    with CUDA-IPC peer reads gives the single-domain result on both slabs."""
+    import os
+    import socket
+    import tempfile
+
+    import torch.multiprocessing as mp
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_two_proc_worker, args=(2, port, d), nprocs=2, join=True)
+        for r in range(2):
+            assert open(os.path.join(d, f"r{r}")).read() == "ok", r

@@ -172,10 +172,13 @@ def test_c5_classify_update_vs_oracle_and_slabs():
     # 2 emulated z-slabs over the same inputs (device-side comparison)
     gc = GlobalClassifier(grid.dims, grid.spacing, labels.component, labels.n_components, S, Emulated(2))
     gst = gc.classify(pos_d, sc_d)
-    for r, e in gc.engines.items():
-        assert torch.equal(e.ss, eng.ss), r
-        assert torch.equal(e.dist, eng.dist), r
-        assert torch.equal(e.state, eng.state), r
+    for r in gc.engines:
+        v0, v1, e = gc.own_slab(r)
+        assert torch.equal(e.ss[v0:v1], eng.ss[v0:v1]), r
+        assert torch.equal(e.dist[v0:v1], eng.dist[v0:v1]), r
+        assert torch.equal(e.state[v0:v1], eng.state[v0:v1]), r
+    g_pos, _, _ = gc.centroidal(pos_d, sc_d, mode, w_d, 0.5 * vlen)
+    assert torch.equal(g_pos, new_pos)
     assert (gst["rounds"], gst["sweeps"], gst["evaluations"], gst["commits"]) == \
         (st["rounds"], st["sweeps"], st["evaluations"], st["commits"])
     del gc

@@ -24,6 +24,24 @@ def test_slab_bounds():
         slab_bounds(3, 4)
 
 
+class _CpuTorch:
+    """torch with "cuda" tensors mapped to the CPU (the protocol test has no GPU)."""
+
+    def __getattr__(self, name):
+        return getattr(torch, name)
+
+    @staticmethod
+    def empty(*a, device=None, **k):
+        return torch.empty(*a, **k)
+
+    @staticmethod
+    def cat(ts):
+        return torch.cat(ts)
+
+
+_CpuTorch = _CpuTorch()
+
+
 def _worker(rank, world, port, outdir):
     import sys
     from pathlib import Path
@@ -46,6 +64,36 @@ def _worker(rank, world, port, outdir):
             want = torch.cat([torch.arange(s * PROP_BYTES, dtype=torch.int64).remainder(251).to(torch.uint8) + r
                               for r, s in enumerate(sizes)])
             assert torch.equal(got, want), sizes
+        # halo exchange: rank r receives hi of r - 1 and lo of r + 1
+        lo = {rank: torch.full((rank * 24,), 10 + rank, dtype=torch.uint8)}
+        hi = {rank: torch.full((24 + rank * 48,), 20 + rank, dtype=torch.uint8)}
+        got = coll.exchange_halo(lo, hi, _CpuTorch)[rank]
+        want = []
+        if rank > 0:
+            want.append(torch.full((24 + (rank - 1) * 48,), 20 + rank - 1, dtype=torch.uint8))
+        if rank + 1 < world:
+            want.append(torch.full(((rank + 1) * 24,), 10 + rank + 1, dtype=torch.uint8))
+        want = torch.cat(want) if want else torch.empty(0, dtype=torch.uint8)
+        assert torch.equal(got.cpu(), want)
+        # all-reduce ops and the rank-ordered carry chain (the ordered vote hand-over)
+        t = torch.tensor([[rank + 1, -rank], [5 * rank, 7]], dtype=torch.int64)
+        assert torch.equal(coll.allreduce({rank: t}, "sum", _CpuTorch).cpu(),
+                           sum(torch.tensor([[r + 1, -r], [5 * r, 7]]) for r in range(world)))
+        assert torch.equal(coll.allreduce({rank: t}, "min", _CpuTorch).cpu(), torch.tensor([[1, -(world - 1)], [0, 7]]))
+        assert torch.equal(coll.allreduce({rank: t}, "max", _CpuTorch).cpu(),
+                           torch.tensor([[world, 0], [5 * (world - 1), 7]]))
+
+        def step(r, carry):
+            # non-associative on purpose: the order of the hand-over matters
+            base = torch.zeros((4, 3), dtype=torch.float64) if carry is None else carry.cpu()
+            return base * 0.5 + (r + 1)
+
+        final = coll.chain(step, (4, 3), _CpuTorch).cpu()
+        want_c = torch.zeros((4, 3), dtype=torch.float64)
+        for r in range(world):
+            want_c = want_c * 0.5 + (r + 1)
+        assert torch.equal(final, want_c)
+        assert coll.sum_ints({rank: [rank, 1]}) == [sum(range(world)), world]
         Path(outdir, f"ok{rank}").write_text("ok")
     finally:
         dist.destroy_process_group()

@@ -24,6 +24,9 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="c4")
     ap.add_argument("--warm", type=int, default=2)
+    ap.add_argument("--host-rounds", action="store_true",
+                    help="host-driven relaxation rounds (plain launches instead of the conditional round graph, "
+                         "whose kernel nodes ncu cannot profile individually)")
     a = ap.parse_args()
     import torch
 
@@ -55,6 +58,8 @@ def main():
     lay = torch.empty(max(labels.n_components, 1), dtype=torch.int32, device="cuda")
     pairs = np.array([[0, 0], [0, 1], [1, 1]], np.int32)
     L.lrcvt_plan_reuse_eligible(eng.plan, 1)
+    if a.host_rounds:
+        _lib.check(L.lrcvt_plan_set_timing(eng.plan, 1), "set_timing")
 
     def once(p):
         _lib.check(L.lrcvt_isobands(n, f.data_ptr(), iso.data_ptr(), iso.numel(), layer.data_ptr(), st), "iso")
