@@ -105,6 +105,12 @@ int lrcvt_segment_hit_t(int64_t nx, int64_t ny, int64_t nz, double sx, double sy
                         const int32_t *d_comp, const double *d_segs, const int32_t *d_want,
                         int64_t n, double *d_t, void *stream);
 
+/* _segment_clear (_kernels.py:128-133) as the eval kernels compute it (the
+ * DDA with the plan's static clearance shortcuts): d_clear[i] = 1 iff
+ * segment i (d_segs float64[n][6]) stays in component d_want[i]. */
+int lrcvt_segment_clear_batch(lrcvt_plan *plan, const double *d_segs, const int32_t *d_want, int64_t n,
+                              uint8_t *d_clear, void *stream);
+
 /* classify_isobands (grid.py:140-163): d_field float32[n], d_iso float64
  * [n_iso] strictly increasing -> d_layer int32[n] (band index or -1). */
 int lrcvt_isobands(int64_t n, const float *d_field, const double *d_iso, int32_t n_iso,

@@ -65,6 +65,7 @@ SIGNATURES = {
         [c_int64, c_int64, c_int64, c_double, c_double, c_double, c_void_p, c_void_p,
          c_void_p, c_int64, c_void_p, c_void_p],
     ),
+    "lrcvt_segment_clear_batch": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_void_p, c_void_p]),
     "lrcvt_plan_set_timing": (c_int, [c_void_p, c_int]),
     "lrcvt_plan_timing": (c_int, [c_void_p, POINTER(c_int64), POINTER(c_int64), POINTER(c_double)]),
     "lrcvt_launch_count": (ctypes.c_ulonglong, []),

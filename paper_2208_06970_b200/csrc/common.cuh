@@ -263,6 +263,76 @@ __device__ __forceinline__ bool ray_clear_near(unsigned nbm_v, double px, double
                                 fabsf((float)(pz - cz)) * isz);
 }
 
+// _segment_clear (_kernels.py:128-133), i.e. segment_hit_box(...) >= 1.0,
+// with the same DDA (same cells, same order, same exact comparisons) and two
+// exact shortcuts from the static clearance clr(c) = min(D(c), 32) in nbm
+// bits 26..31 (D: Chebyshev distance to the nearest foreign or out-of-grid
+// voxel; every cell within Chebyshev radius clr(c) - 1 of c is in c's
+// component):
+//   * a step from a cell with clr >= 2 lands on a 26-neighbour, which is
+//     in-grid and in the component: no bounds test, no comp load;
+//   * from the current cell c, the walk only visits cells within Chebyshev
+//     distance max_a |e_a - c_a| + 1 of c (monotone steps towards the end
+//     cell e, at most one rounded overstep), so clr(c) >= that + 2 (one cell
+//     of extra slack here) proves every remaining cell, e included, in the
+//     component: the reference returns 1.0.
+__device__ __noinline__ bool segment_clear_fast(const int* __restrict__ comp, const uint32_t* __restrict__ nbm,
+                                                const Box g, double ax, double ay, double az, double bx, double by,
+                                                double bz, int want) {
+  int cx = cell_of_box(ax, g.sx, g.ix, g.dyadic, g.nx), cy = cell_of_box(ay, g.sy, g.iy, g.dyadic, g.ny),
+      cz = cell_of_box(az, g.sz, g.iz, g.dyadic, g.nz);
+  const int ex = cell_of_box(bx, g.sx, g.ix, g.dyadic, g.nx), ey = cell_of_box(by, g.sy, g.iy, g.dyadic, g.ny),
+            ez = cell_of_box(bz, g.sz, g.iz, g.dyadic, g.nz);
+  const int sxy = g.nx * g.ny;
+  int idx = cx + g.nx * cy + sxy * cz;
+  if (__ldg(comp + idx) != want) return false;
+  const double dx = __dsub_rn(bx, ax), dy = __dsub_rn(by, ay), dz = __dsub_rn(bz, az);
+  const int stepx = dx > 0 ? 1 : -1, stepy = dy > 0 ? 1 : -1, stepz = dz > 0 ? 1 : -1;
+  const double big = 1e30;
+  double tmaxx, tmaxy, tmaxz, tdx, tdy, tdz;
+  if (dx != 0.0) {
+    const double nxt = dx > 0 ? __dmul_rn((double)(cx + 1), g.sx) : __dmul_rn((double)cx, g.sx);
+    tmaxx = __ddiv_rn(__dsub_rn(nxt, ax), dx);
+    tdx = __ddiv_rn(g.sx, fabs(dx));
+  } else { tmaxx = big; tdx = big; }
+  if (dy != 0.0) {
+    const double nxt = dy > 0 ? __dmul_rn((double)(cy + 1), g.sy) : __dmul_rn((double)cy, g.sy);
+    tmaxy = __ddiv_rn(__dsub_rn(nxt, ay), dy);
+    tdy = __ddiv_rn(g.sy, fabs(dy));
+  } else { tmaxy = big; tdy = big; }
+  if (dz != 0.0) {
+    const double nxt = dz > 0 ? __dmul_rn((double)(cz + 1), g.sz) : __dmul_rn((double)cz, g.sz);
+    tmaxz = __ddiv_rn(__dsub_rn(nxt, az), dz);
+    tdz = __ddiv_rn(g.sz, fabs(dz));
+  } else { tmaxz = big; tdz = big; }
+  const int ix = stepx, iy = stepy * g.nx, iz = stepz * sxy;
+  int clr = (int)(__ldg(nbm + idx) >> NBM_CLR_SHIFT);
+  const int max_steps = abs(ex - cx) + abs(ey - cy) + abs(ez - cz) + 8;
+  for (int i = 0; i < max_steps; i++) {
+    if (cx == ex && cy == ey && cz == ez) return true;
+    const int rem = max(abs(ex - cx), max(abs(ey - cy), abs(ez - cz)));
+    if (clr >= rem + 3) return true;
+    const double t = fmin(tmaxx, fmin(tmaxy, tmaxz));
+    if (t > 1.0) return __ldg(comp + ex + g.nx * ey + sxy * ez) == want;
+    const bool inside = clr >= 2;  // every 26-neighbour in-grid and in the component
+    if (tmaxx == t) {
+      cx += stepx; idx += ix; tmaxx = __dadd_rn(tmaxx, tdx);
+      if (!inside && (unsigned)cx >= (unsigned)g.nx) return false;
+    }
+    if (tmaxy == t) {
+      cy += stepy; idx += iy; tmaxy = __dadd_rn(tmaxy, tdy);
+      if (!inside && (unsigned)cy >= (unsigned)g.ny) return false;
+    }
+    if (tmaxz == t) {
+      cz += stepz; idx += iz; tmaxz = __dadd_rn(tmaxz, tdz);
+      if (!inside && (unsigned)cz >= (unsigned)g.nz) return false;
+    }
+    if (!inside && __ldg(comp + idx) != want) return false;
+    clr = (int)(__ldg(nbm + idx) >> NBM_CLR_SHIFT);
+  }
+  return true;
+}
+
 // Warp-aggregated append of `take` (0/1) items; returns this lane's slot
 // (valid only when take). All 32 lanes must call it.
 // CTA-aggregated append: one atomic per CTA. Every thread of the CTA must

@@ -231,15 +231,6 @@ __global__ void __launch_bounds__(CM_THREADS) k_commit(const Prop* __restrict__ 
   }
 }
 
-// multi-GPU eval step: sparse proposal slots -> a compact list (any order)
-__global__ void __launch_bounds__(128) k_gather_props(const Prop* __restrict__ imp, const uint8_t* __restrict__ pf,
-                                                      int n, Prop* __restrict__ out, int* __restrict__ count) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  const bool take = i < n && pf[i];
-  const int slot = block_append(count, take);
-  if (take) out[slot] = imp[i];
-}
-
 // tile status word: epoch << 33 | inclusive << 32 | count
 __device__ __forceinline__ unsigned long long ct_pack(unsigned epoch, bool incl, unsigned cnt) {
   return ((unsigned long long)epoch << 33) | ((unsigned long long)(incl ? 1u : 0u) << 32) | cnt;

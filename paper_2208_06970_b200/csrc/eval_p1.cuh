@@ -80,19 +80,28 @@ __device__ __forceinline__ void p1_tile(const int* __restrict__ list, int n, con
     nbv = same;
     // ---- A
     // phase 1: site1[w] is site_of[w] when src[w] == w (every phase-1 assignment), else -1
-    int nw[26];
-#pragma unroll
-    for (int k = 0; k < 26; k++) {
-      const int w = v + off_dx(k) + off_dy(k) * g.nx + off_dz(k) * g.nxy;
-      nw[k] = ((same >> k) & 1u) ? __ldg(site1 + w) : -1;
-    }
+    // phase-1 states are LOS (src == v) and their distance is |c_v - p_site|
+    orig_s = __ldg(site1 + v);
     int nt = 0;
+    // two batches of 13 loads in flight (bounds the live registers of the
+    // big-round variant, whose 64-register budget otherwise spills)
 #pragma unroll
-    for (int k = 0; k < 26; k++) {
-      const int s = nw[k];
+    for (int h = 0; h < 2; h++) {
+    int nw[13];
+#pragma unroll
+    for (int q = 0; q < 13; q++) {
+      const int k = 13 * h + q;
+      const int w = v + off_dx(k) + off_dy(k) * g.nx + off_dz(k) * g.nxy;
+      nw[q] = ((same >> k) & 1u) ? __ldg(site1 + w) : -1;
+    }
+#pragma unroll
+    for (int q = 0; q < 13; q++) {
+      const int k = 13 * h + q;
+      const int s = nw[q];
       row[k * BLOCK] = s;
-      // ---- B: distinct-site table
-      bool seen = s < 0;
+      // ---- B: distinct-site table; the voxel's own site is not entered: its
+      // candidate (orig_d, orig_s, v) is the current state itself
+      bool seen = s < 0 || s == orig_s;
 #pragma unroll
       for (int j = 0; j < P1_TAB; j++) seen |= ts[j] == s;
       if (!seen && nt < P1_TAB) {
@@ -104,8 +113,8 @@ __device__ __forceinline__ void p1_tile(const int* __restrict__ list, int n, con
         ovf = true;
       }
     }
-    // phase-1 states are LOS (src == v) and their distance is |c_v - p_site|
-    best_s = __ldg(site1 + v); best_src = v;
+    }
+    best_s = orig_s; best_src = v;
     if (best_s >= 0) {
       const double4 sp = ld_d4(site_pos + best_s);
       best_d = dist3(px, py, pz, sp.x, sp.y, sp.z);
@@ -116,9 +125,7 @@ __device__ __forceinline__ void p1_tile(const int* __restrict__ list, int n, con
   }
 #pragma unroll
   for (int j = 0; j < P1_TAB; j++) {
-    if (ts[j] == orig_s) {  // the voxel's own LOS site: the very dist3 already computed (orig_d)
-      td[j] = orig_d;
-    } else if (ts[j] >= 0) {
+    if (ts[j] >= 0) {
       const double4 sp = ld_d4(site_pos + ts[j]);
       td[j] = dist3(px, py, pz, sp.x, sp.y, sp.z);
     }
@@ -186,7 +193,7 @@ __device__ __forceinline__ void p1_tile(const int* __restrict__ list, int n, con
     const double4 sp = ld_d4(site_pos + qs[j]);
     const double cx = centre1(rx, g.sx), cy = centre1(ry, g.sy), cz = centre1(rz, g.sz);
     qok[j] = ray_clear_near(__ldg(nbm + rv), sp.x, sp.y, sp.z, cx, cy, cz, isx, isy, isz) ||
-                     segment_clear(comp, g, cx, cy, cz, sp.x, sp.y, sp.z, __ldg(comp + rv))
+                     segment_clear_fast(comp, nbm, box_of(g), cx, cy, cz, sp.x, sp.y, sp.z, __ldg(comp + rv))
                  ? 1 : 0;
   }
   __syncwarp();
@@ -206,7 +213,8 @@ __device__ __forceinline__ void p1_tile(const int* __restrict__ list, int n, con
       const int s = row[k * BLOCK];
       if (s < 0) continue;
       double d;
-      if (s == ts[0]) d = td[0];
+      if (s == orig_s) d = orig_d;  // the own site: the very dist3 of the current state
+      else if (s == ts[0]) d = td[0];
       else if (s == ts[1]) d = td[1];
       else if (s == ts[2]) d = td[2];
       else if (s == ts[3]) d = td[3];
@@ -217,7 +225,7 @@ __device__ __forceinline__ void p1_tile(const int* __restrict__ list, int n, con
       if (beats(d, s, best_d, best_s) && s != failed) {
         const double4 sp = ld_d4(site_pos + s);
         if (ray_clear_near(nbv, sp.x, sp.y, sp.z, px, py, pz, isx, isy, isz) ||
-            segment_clear(comp, g, px, py, pz, sp.x, sp.y, sp.z, cv)) {
+            segment_clear_fast(comp, nbm, box_of(g), px, py, pz, sp.x, sp.y, sp.z, cv)) {
           best_d = d; best_s = s; best_src = v;
         } else {
           failed = s;

@@ -55,6 +55,7 @@ __device__ __forceinline__ void p2_tile(const int* __restrict__ list, int n, con
   for (int j = 0; j < P2_NTAB; j++) { tu[j] = -1; tus[j] = -1; tud[j] = 0.0; }
   double best_d = 0.0, orig_d = 0.0;
   int best_s = -1, best_src = -1, orig_s = -1;
+  int own_los = -1;  // the voxel's own site when its state is LOS (src == v)
   bool done = !active;
   if (active) {
     bm[v >> 5] = 0u;  // consume this round's frontier word
@@ -93,6 +94,14 @@ __device__ __forceinline__ void p2_tile(const int* __restrict__ list, int n, con
         s_dw[k][t] = __dadd_rn(dw[q], len);
       }
     }
+    const int2 sv = __ldg(ss + v);
+    best_d = __ldg(dist + v);
+    best_s = sv.x; best_src = sv.y;
+    orig_d = best_d; orig_s = best_s;
+    // a LOS voxel's stored distance is exactly dist3(c_v, site) (every LOS
+    // commit and seed computes it in this operand order): its own site's LOS
+    // candidate is the current state itself and needs no table entry
+    own_los = best_src == v ? orig_s : -1;
     // ---- B: distinct LOS sites and distinct shortcut nodes
     int nts = 0, ntu = 0;
 #pragma unroll
@@ -100,7 +109,7 @@ __device__ __forceinline__ void p2_tile(const int* __restrict__ list, int n, con
       const int s = s_site[k][t];
       const int u = s_node[k][t];
       if (u == -2) {
-        bool seen = false;
+        bool seen = s == own_los;
 #pragma unroll
         for (int j = 0; j < P2_STAB; j++) seen |= ts[j] == s;
         if (!seen && nts < P2_STAB) {
@@ -121,20 +130,10 @@ __device__ __forceinline__ void p2_tile(const int* __restrict__ list, int n, con
         }
       }
     }
-    const int2 sv = __ldg(ss + v);
-    best_d = __ldg(dist + v);
-    best_s = sv.x; best_src = sv.y;
-    orig_d = best_d; orig_s = best_s;
   }
-  // a LOS voxel's stored distance is exactly dist3(c_v, site) (every LOS
-  // commit and seed computes it in this operand order), so its own site's
-  // entry needs no recomputation
-  const bool orig_los = active && best_src == v;
 #pragma unroll
   for (int j = 0; j < P2_STAB; j++) {
-    if (orig_los && ts[j] == orig_s) {
-      td[j] = orig_d;
-    } else if (ts[j] >= 0) {
+    if (ts[j] >= 0) {
       const double4 sp = ld_d4(site_pos + ts[j]);
       td[j] = dist3(px, py, pz, sp.x, sp.y, sp.z);
     }
@@ -170,7 +169,8 @@ __device__ __forceinline__ void p2_tile(const int* __restrict__ list, int n, con
       }
       if (u == -2) {
         double d;
-        if (s == ts[0]) d = td[0];
+        if (s == own_los) d = orig_d;  // the own LOS site: exactly the stored distance
+        else if (s == ts[0]) d = td[0];
         else if (s == ts[1]) d = td[1];
         else if (s == ts[2]) d = td[2];
         else if (s == ts[3]) d = td[3];
@@ -211,7 +211,7 @@ __device__ __forceinline__ void p2_tile(const int* __restrict__ list, int n, con
     }
     if (ray_clear_near(nbv, qx, qy, qz, px, py, pz, (float)(1.0 / g.sx), (float)(1.0 / g.sy),
                        (float)(1.0 / g.sz)) ||
-        segment_clear(comp, g, px, py, pz, qx, qy, qz, cv)) {
+        segment_clear_fast(comp, nbm, box_of(g), px, py, pz, qx, qy, qz, cv)) {
       best_d = rd; best_s = rs; best_src = rsrc;
     } else if (los) {
       failed = rs;

@@ -47,7 +47,8 @@ constexpr int EW_NONE = -1, EW_PATH = 0, EW_LOS = 1, EW_SHORT = 2;
 __device__ __forceinline__ bool ew_strict(const int lane, const double orig_d, const int orig_s,
                                           const int orig_src, const double* ed, const int* es,
                                           const int* esrc, const int* et, const Geo& g, const int* comp,
-                                          const double4* site_pos, unsigned nbv, double px, double py,
+                                          const uint32_t* nbm, const double4* site_pos, unsigned nbv, double px,
+                                          double py,
                                           double pz, int cv, double& best_d, int& best_s, int& best_src) {
   const double inf = __longlong_as_double(0x7ff0000000000000LL);
   double lmin = lane == 0 ? orig_d : inf;
@@ -123,7 +124,7 @@ __device__ __forceinline__ bool ew_strict(const int lane, const double orig_d, c
       }
       ok = (ray_clear_near(nbv, qx, qy, qz, px, py, pz, (float)(1.0 / g.sx), (float)(1.0 / g.sy),
                            (float)(1.0 / g.sz)) ||
-            segment_clear(comp, g, px, py, pz, qx, qy, qz, cv))
+            segment_clear_fast(comp, nbm, box_of(g), px, py, pz, qx, qy, qz, cv))
                ? 1 : 0;
     }
     clear = __shfl_sync(0xffffffffu, ok, holder) != 0;
@@ -136,7 +137,8 @@ __device__ __forceinline__ bool ew_strict(const int lane, const double orig_d, c
 // The reference's sequential fold over the gathered elements (slot order).
 __device__ __forceinline__ void ew_exact(const double (*ed)[2], const int (*es)[2], const int (*esrc)[2],
                                          const int (*et)[2], const Geo& g, const int* comp,
-                                         const double4* site_pos, unsigned nbv, double px, double py,
+                                         const uint32_t* nbm, const double4* site_pos, unsigned nbv, double px,
+                                         double py,
                                          double pz, int cv, double& best_d, int& best_s, int& best_src) {
   int failed = -1;
   const float isx = (float)(1.0 / g.sx), isy = (float)(1.0 / g.sy), isz = (float)(1.0 / g.sz);
@@ -162,7 +164,7 @@ __device__ __forceinline__ void ew_exact(const double (*ed)[2], const int (*es)[
         qx = centre1(ux, g.sx); qy = centre1(uy, g.sy); qz = centre1(uz, g.sz);
       }
       if (ray_clear_near(nbv, qx, qy, qz, px, py, pz, isx, isy, isz) ||
-          segment_clear(comp, g, px, py, pz, qx, qy, qz, cv)) {
+          segment_clear_fast(comp, nbm, box_of(g), px, py, pz, qx, qy, qz, cv)) {
         best_d = d; best_s = s; best_src = esrc[k][e];
       } else if (t == EW_LOS) {
         failed = s;
@@ -260,7 +262,7 @@ __device__ __forceinline__ void ew_voxel(const int* list, const int2* ss, const 
   }
   double best_d = orig_d;
   int best_s = orig_s, best_src = orig_src;
-  const bool decided = ew_strict(lane, orig_d, orig_s, orig_src, ed, es, esrc, et, g, comp, site_pos, nbv, px,
+  const bool decided = ew_strict(lane, orig_d, orig_s, orig_src, ed, es, esrc, et, g, comp, nbm, site_pos, nbv, px,
                                  py, pz, cv, best_d, best_s, best_src);
   if (!decided) {
     if (lane < 26) {
@@ -273,7 +275,7 @@ __device__ __forceinline__ void ew_voxel(const int* list, const int2* ss, const 
     __syncwarp();
     if (lane == 0) {
       best_d = orig_d; best_s = orig_s; best_src = orig_src;
-      ew_exact(st.d, st.s, st.src, st.t, g, comp, site_pos, nbv, px, py, pz, cv, best_d, best_s, best_src);
+      ew_exact(st.d, st.s, st.src, st.t, g, comp, nbm, site_pos, nbv, px, py, pz, cv, best_d, best_s, best_src);
     }
     __syncwarp();  // st is reused by this warp's next item
   }

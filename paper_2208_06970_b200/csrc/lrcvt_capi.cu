@@ -148,6 +148,15 @@ __global__ void k_segment_batch(Geo g, const int* __restrict__ comp, const doubl
   t[i] = segment_hit_t(comp, g, s[0], s[1], s[2], s[3], s[4], s[5], want[i]);
 }
 
+__global__ void k_segment_clear_batch(Geo g, const int* __restrict__ comp, const uint32_t* __restrict__ nbm,
+                                      const double* __restrict__ segs, const int* __restrict__ want, int64_t n,
+                                      uint8_t* __restrict__ out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double* s = segs + 6 * i;
+  out[i] = segment_clear_fast(comp, nbm, box_of(g), s[0], s[1], s[2], s[3], s[4], s[5], want[i]) ? 1 : 0;
+}
+
 Geo make_geo(int64_t nx, int64_t ny, int64_t nz, double sx, double sy, double sz) {
   Geo g;
   memset(&g, 0, sizeof g);
@@ -198,7 +207,6 @@ struct lrcvt_plan {
   int* eligible = nullptr;
   Prop* imp = nullptr;      // sparse proposals: slot i <-> frontier item i
   uint8_t* pf = nullptr;    // pf[i] = 1 iff slot i holds an improved proposal
-  Prop* mg_props = nullptr;  // compact proposal list of a multi-GPU eval step
   bool compact = false;      // voxel-ordered frontier through k_compact (LRCVT_COMPACT=1)
   int p1_bs = 128, p2_bs = 64;  // eval CTA sizes (LRCVT_EVAL_BS=p1,p2)
   uint32_t* bm = nullptr;  // frontier bitmap (1 bit per voxel)
@@ -238,6 +246,7 @@ struct lrcvt_plan {
   int* seg_b = nullptr;
   int* seg_e = nullptr;
   int2* vt_sp = nullptr;  // (site, phi) per voxel for the bounding-box vote
+  bool sp_stale = true;   // vt_sp must be reset to -1 before the next k_vote_prep
   int* vt_box = nullptr;  // [6][S] per-site bounding boxes
   bool vote_bbox = true;  // LRCVT_VOTE=sort: stable radix sort of (site, (phi, v)) pairs instead
   // cub
@@ -334,6 +343,7 @@ int prepare_eligible(lrcvt_plan* p, int n_sites, const int* site_comp, cudaStrea
   cub::CountingInputIterator<int> it(z0 * p->g.nxy);
   size_t bytes = p->cub_bytes;
   CK(cub::DeviceSelect::If(p->cub_tmp, bytes, it, p->eligible, p->d_nel, (z1 - z0) * p->g.nxy, pred, st));
+  p->sp_stale = true;  // the bounding-box vote's (site, phi) entries of the previous set are now stale
   return 0;
 }
 
@@ -744,7 +754,6 @@ int lrcvt_plan_create(lrcvt_plan** plan, int64_t nx, int64_t ny, int64_t nz, dou
   rc |= dalloc(&p->eligible, nin);
   rc |= dalloc(&p->imp, nin);
   rc |= dalloc(&p->pf, nin);
-  rc |= dalloc(&p->mg_props, nin);
   rc |= dalloc(&p->bm, p->bm_words);
   p->ct_tiles = (int)compact_tiles(p->bm_words);
   rc |= dalloc(&p->cbm, coarse_words(p->bm_words));
@@ -859,7 +868,7 @@ int lrcvt_plan_destroy(lrcvt_plan* p) {
   if (p->cap) cudaStreamDestroy(p->cap);
   if (p->h_ctl) cudaFreeHost(p->h_ctl);
   void* bufs[] = {p->counters, p->ctl, p->d_handles, p->d_nel, p->list_a, p->list_b, p->eligible, p->imp, p->pf,
-                  p->mg_props, p->bm,
+                  p->bm,
                   p->cbm, p->ct_status, p->ct_state, p->nbm, p->site1, p->has_site,
                   p->site_pos, p->new_pos, p->sk_key, p->sk_key2, p->sk_val, p->sk_val2, p->sk_d,
                   p->acc, p->sums, p->vt_key, p->vt_key2, p->vt_pv, p->vt_pv2,
@@ -1075,6 +1084,10 @@ int lrcvt_centroidal_update(lrcvt_plan* p, int64_t n_sites, const double* d_site
       rc |= dalloc(&p->vt_box, 6 * p->max_sites);
       if (rc) return LRCVT_E_NOMEM;
     }
+    if (p->sp_stale) {
+      CK(cudaMemsetAsync(p->vt_sp, 0xff, sizeof(int2) * (size_t)g.n, st));
+      p->sp_stale = false;
+    }
     k_box_init<<<grid_for(S, 256), 256, 0, st>>>(p->vt_box, S);
     CKL("k_box_init"); LAUNCHED(1);
     if (n_el > 0) {
@@ -1147,6 +1160,17 @@ int lrcvt_segment_hit_t(int64_t nx, int64_t ny, int64_t nz, double sx, double sy
   return 0;
 }
 
+
+int lrcvt_segment_clear_batch(lrcvt_plan* p, const double* d_segs, const int32_t* d_want, int64_t n,
+                              uint8_t* d_clear, void* stream) {
+  if (!p || n < 0 || (n > 0 && (!d_segs || !d_want || !d_clear)))
+    return set_error(LRCVT_E_ARG, "lrcvt_segment_clear_batch: bad arguments");
+  if (n == 0) return 0;
+  k_segment_clear_batch<<<grid_for(n, 128), 128, 0, (cudaStream_t)stream>>>(p->g, p->comp, p->nbm, d_segs, d_want,
+                                                                           n, d_clear);
+  CKL("k_segment_clear_batch"); LAUNCHED(1);
+  return 0;
+}
 
 int lrcvt_isobands(int64_t n, const float* d_field, const double* d_iso, int32_t n_iso, int32_t* d_layer,
                    void* stream) {
@@ -1649,6 +1673,10 @@ int lrcvt_mg_vote_box(lrcvt_plan* p, int64_t n_sites, const int32_t* d_site_src,
     int rc = dalloc(&p->vt_sp, p->g.n);
     rc |= dalloc(&p->vt_box, 6 * p->max_sites);
     if (rc) return LRCVT_E_NOMEM;
+  }
+  if (p->sp_stale) {
+    CK(cudaMemsetAsync(p->vt_sp, 0xff, sizeof(int2) * (size_t)p->g.n, st));
+    p->sp_stale = false;
   }
   k_box_init<<<grid_for(S, 256), 256, 0, st>>>(d_box, S);
   CKL("k_box_init");

@@ -170,9 +170,9 @@ __global__ void __launch_bounds__(WARPS * 32) k_vote_sum(const unsigned long lon
 //                (flat box order), picks the voxels of its region, forms their
 //                terms and lanes 0-3 add them in order -- the reference's
 //                exact accumulation order (_kernels.py:519-531).
-// A voxel belongs to region s iff sp[v].x == s and comp[v] == site_comp[s]
-// (entries of voxels outside the current eligible set may be stale; every
-// voxel of region s lies in s's component).
+// A voxel belongs to region s iff sp[v].x == s: sp is reset to -1 whenever
+// the eligible set is rebuilt, and k_vote_prep writes every eligible voxel,
+// so no stale entry survives.
 constexpr int BOX_BIG = 0x3fffffff;
 constexpr int VS_DEPTH = 4;  // chunks in flight per warp in k_vote_scan
 
@@ -246,7 +246,6 @@ __global__ void __launch_bounds__(WARPS * 32) k_vote_scan(const int2* __restrict
   const int W = box[3 * n_sites + s] - x0 + 1, H = box[4 * n_sites + s] - y0 + 1, D = z1 - z0 + 1;
   double acc = (init && mode != 1 && lane < 4) ? init[lane * n_sites + s] : 0.0;
   if (W > 0 && H > 0 && D > 0) {
-    const int cs = __ldg(site_comp + s);
     const long long T = (long long)W * H * D;
     // flat box index k = lane + 32 * chunk -> (dx, dy, dz), advanced by 32 per chunk
     int dx = lane % W, r = lane / W;
@@ -256,16 +255,13 @@ __global__ void __launch_bounds__(WARPS * 32) k_vote_scan(const int2* __restrict
     // lane's voxel are loaded VS_DEPTH chunks ahead of the ordered adds (the
     // walk is latency-bound otherwise: one chunk ~ one memory round trip)
     int2 a[VS_DEPTH];
-    int c[VS_DEPTH];
     double w[VS_DEPTH];
     auto load = [&](int j) {
       a[j] = make_int2(-1, -1);
-      c[j] = -2;
       w[j] = 0.0;
       if (k < T) {
         const int v = (x0 + dx) + g.nx * ((y0 + dy) + g.ny * (z0 + dz));
         a[j] = __ldg(sp + v);
-        c[j] = __ldg(comp + v);
         w[j] = vote_weight(v, w64, w32, w_mode);
       }
       k += 32;
@@ -286,7 +282,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_vote_scan(const int2* __restrict
     for (long long base = 0; base < T; base += 32 * VS_DEPTH) {
 #pragma unroll
       for (int j = 0; j < VS_DEPTH; j++) {
-        const bool mine = a[j].x == s && c[j] == cs;
+        const bool mine = a[j].x == s;
         const int u = a[j].y;
         const double wt = w[j];
         load(j);  // refill this slot VS_DEPTH chunks ahead

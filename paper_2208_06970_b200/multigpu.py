@@ -250,7 +250,7 @@ class GlobalClassifier:
         comp_dev = None
         own = {}
         for r in coll.local_ranks:
-            eng = Engine(self.dims, spacing, component, n_components, max_sites, comp_dev)
+            eng = Engine(self.dims, spacing, component, n_components, max_sites, comp_dev, alloc_state=False)
             comp_dev = eng.comp  # replicated labels shared between in-process ranks
             lo, hi = self.bounds[r]
             _lib.check(self.L.lrcvt_mg_set_slab(eng.plan, lo, hi), "lrcvt_mg_set_slab")

@@ -149,7 +149,7 @@ class Engine:
     packed (site_of, src) int32[N][2], dist float64[N] and state uint8[N]."""
 
     def __init__(self, dims, spacing, component: np.ndarray, n_components: int, max_sites: int,
-                 comp_dev=None):
+                 comp_dev=None, alloc_state: bool = True):
         torch = _lib.require_cuda()
         self.torch = torch
         self.L = _lib.lib()
@@ -162,8 +162,9 @@ class Engine:
         self.max_sites = 0
         self.plan = ctypes.c_void_p()
         self._make_plan(max(int(max_sites), 1))
-        self.ss = torch.empty((self.n, 2), dtype=torch.int32, device="cuda")
-        self.dist = torch.empty(self.n, dtype=torch.float64, device="cuda")
+        # alloc_state=False: the caller supplies ss / dist (multi-GPU slabs use plan-owned buffers)
+        self.ss = torch.empty((self.n, 2), dtype=torch.int32, device="cuda") if alloc_state else None
+        self.dist = torch.empty(self.n, dtype=torch.float64, device="cuda") if alloc_state else None
         self.state = torch.empty(self.n, dtype=torch.uint8, device="cuda")
         self.version = 0  # bumps on every classify; guards host<->device reuse
         self.classify_seq = 0  # bumps on every classify call (the plan's eligible list follows it)

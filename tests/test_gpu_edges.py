@@ -152,3 +152,51 @@ def test_labyrinth_thin_walls_and_thick_chambers(spacing, oracle_mod):
                 break
         sites.append(Site(((x + rng.random()) * sx, (y + rng.random()) * sy, (z + rng.random()) * sz), 0))
     _check(grid, labels, sites, oracle_mod)
+
+
+@pytest.mark.parametrize("kind,dims,iso,spacing", [
+    ("random-smooth", (48, 40, 36), [0.35, 0.5, 0.65, 0.8], (1.0, 1.0, 1.0)),
+    ("horseshoe", (40, 40, 32), [0.0, 0.12, 0.3], (1.0, 0.5, 2.0)),
+    ("spiral", (64, 64, 1), [0.3, 0.55, 0.8], (1.0, 1.0, 1.0)),
+])
+def test_clearance_dda_equals_reference_dda(kind, dims, iso, spacing):
+    """The eval kernels' ray test (segment_clear_fast: the reference DDA plus
+    the static-clearance shortcuts) agrees with the plain DDA
+    (_segment_hit_t >= 1, itself pinned to the reference's ray golden) on
+    random segments between in-band points, long and short."""
+    import torch
+
+    from paper_2208_06970_b200 import IsobandSpec, classify_isobands, label_components, synth_field
+    from paper_2208_06970_b200 import _lib
+    from paper_2208_06970_b200.grid import VoxelGrid
+    from paper_2208_06970_b200.tessellation import engine_for, segment_hit_t_batch
+
+    g0 = synth_field(kind, dims, 1)
+    grid = VoxelGrid(dims, spacing, g0.fields)
+    labels = label_components(classify_isobands(grid, IsobandSpec("f", iso)))
+    eng = engine_for(labels, spacing, 1)
+    rng = np.random.default_rng(4)
+    inb = np.flatnonzero(labels.component >= 0)
+    n = 60000
+    nx, ny, nz = dims
+    v = rng.choice(inb, n)
+    a = np.stack([v % nx + rng.random(n), (v // nx) % ny + rng.random(n), v // (nx * ny) + rng.random(n)], 1)
+    span = np.where(rng.random(n) < 0.5, 4.0, 40.0)[:, None]
+    b = a + (rng.random((n, 3)) - 0.5) * 2 * span
+    if nz == 1:
+        a[:, 2] = 0.5
+        b[:, 2] = 0.5
+    a *= spacing
+    b *= spacing
+    segs = np.ascontiguousarray(np.concatenate([a, b], 1))
+    want = labels.component[v].astype(np.int32)
+    t = segment_hit_t_batch(labels, segs, want, spacing)
+    L = _lib.lib()
+    segs_d = torch.from_numpy(segs).cuda()
+    want_d = torch.from_numpy(want).cuda()
+    out = torch.empty(n, dtype=torch.uint8, device="cuda")
+    _lib.check(L.lrcvt_segment_clear_batch(eng.plan, segs_d.data_ptr(), want_d.data_ptr(), n, out.data_ptr(),
+                                           _lib.stream_handle(torch)), "clear batch")
+    fast = out.cpu().numpy().astype(bool)
+    assert np.array_equal(fast, t >= 1.0)
+    assert 0.05 < fast.mean() < 0.95  # both outcomes well represented
