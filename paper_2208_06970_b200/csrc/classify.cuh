@@ -148,7 +148,8 @@ __device__ __forceinline__ void mark_and_append(const Geo& g, const uint32_t* __
                                                 bool active, int v, bool self,
                                                 uint32_t* __restrict__ bm,
                                                 int* __restrict__ next, int* counter,
-                                                int zlo = 0, int zhi = 1 << 30) {
+                                                int zlo = 0, int zhi = 1 << 30,
+                                                uint32_t* __restrict__ cbm = nullptr) {
   // COH: inside the persistent small-round kernel the precheck must not see a
   // stale L1 copy of a word cleared since (it would skip a needed enqueue)
   // The 27-cube around v is 9 x-rows of 3 voxels (dx = -1, 0, +1); a row's
@@ -197,6 +198,7 @@ __device__ __forceinline__ void mark_and_append(const Geo& g, const uint32_t* __
         if ((cur & lo) != lo) {
           const uint32_t old = atomicOr(bm + w0, lo);
           got |= ((~old) & lo) >> sh;
+          if (cbm && old == 0u) atomicOr(cbm + (w0 >> 10), 1u << ((w0 >> 5) & 31));  // coarse bit (compact.cuh)
         }
       }
       if (hi) {
@@ -204,6 +206,7 @@ __device__ __forceinline__ void mark_and_append(const Geo& g, const uint32_t* __
         if ((cur & hi) != hi) {
           const uint32_t old = atomicOr(bm + w0 + 1, hi);
           got |= ((~old) & hi) << (32 - sh);
+          if (cbm && old == 0u) atomicOr(cbm + ((w0 + 1) >> 10), 1u << (((w0 + 1) >> 5) & 31));
         }
       }
       got <<= f;

@@ -24,6 +24,8 @@ struct Geo {
   double inv_nx, inv_nxy;  // for exact division via fp64 reciprocal + fixup
   int dyadic;              // spacing values are powers of two (exact centre diffs)
   double len_cls[8];       // |offset| in world units by class (exact when dyadic)
+  float isx, isy, isz;     // 1 / spacing in float (clearance tests only)
+  double ix, iy, iz;       // 1 / spacing (exact reciprocals of powers of two when dyadic)
   int off_d[26];           // flat index delta of offset k
 };
 
@@ -174,7 +176,7 @@ struct Box {
   int dyadic;
 };
 __device__ __forceinline__ Box box_of(const Geo& g) {
-  return Box{g.nx, g.ny, g.nz, g.sx, g.sy, g.sz, 1.0 / g.sx, 1.0 / g.sy, 1.0 / g.sz, g.dyadic};
+  return Box{g.nx, g.ny, g.nz, g.sx, g.sy, g.sz, g.ix, g.iy, g.iz, g.dyadic};
 }
 
 __device__ __forceinline__ int cell_of_box(double a, double s, double inv, int dyadic, int n) {

@@ -1,18 +1,19 @@
-// compact.cuh -- the next relaxation frontier, in voxel order.
+// compact.cuh -- commit + enqueue of a relaxation round, and the optional
+// voxel-order rebuild of large frontiers.
 //
 // _apply_and_enqueue (_kernels.py:313-333) enqueues the same-component
 // 26-neighbours of every improved voxel, deduplicated by `stamp`. The set is
 // all that matters (each round reads only pre-round state), so the order of
-// the list is ours to choose. k_commit marks the set in the frontier bitmap
-// (1 bit per voxel, flat x-fastest order) and in a coarse bitmap (1 bit per
-// 32 words = 1024 voxels); k_compact then turns the bitmap into the next
-// worklist IN VOXEL ORDER with one single-pass scan (decoupled look-back over
-// tiles of 2048 words), clearing the words it read. A voxel-ordered list puts
-// neighbouring voxels in neighbouring lanes and concurrently running CTAs on
-// neighbouring planes, so the eval kernels' 26-neighbour gathers and ray
-// walks hit L1/L2 instead of re-reading HBM (the proposal-order list of the
-// append scheme scattered them: 122 B of DRAM per evaluation at 512^3
-// against 20 algorithmic).
+// the list is ours to choose. k_commit commits the round's proposals and
+// appends the newly marked neighbours (frontier bitmap dedup,
+// mark_and_append); with LRCVT_COMPACT=1 it also marks a coarse bitmap (1 bit
+// per 32 words = 1024 voxels) and k_reorder rewrites every frontier of at
+// least REORDER_MIN voxels IN VOXEL ORDER from the bitmap: one single-pass
+// scan over the marked chunks (decoupled look-back over tiles of 2048 words),
+// warp-cooperative coalesced output. A voxel-ordered list puts neighbouring
+// voxels in neighbouring lanes, so the eval kernels' 26-neighbour gathers
+// and ray walks hit L1/L2 more often (measured at 512^3: ~50 instead of ~150
+// bytes of DRAM per evaluation).
 #pragma once
 #include "classify.cuh"
 
@@ -33,71 +34,6 @@ __host__ __device__ inline int64_t coarse_words(int64_t bm_words) {
   return compact_tiles(bm_words) * CT_CWORDS;  // whole tiles: no bounds checks on the coarse reads
 }
 
-// Set the frontier bits of v's same-component neighbours (v itself when
-// `self`) -- the marking half of mark_and_append (classify.cuh), plus the
-// coarse bit of every word this thread turned from empty to non-empty.
-__device__ __forceinline__ void mark_bits(const Geo& g, const uint32_t* __restrict__ nbm, bool active, int v,
-                                          uint32_t* __restrict__ bm, uint32_t* __restrict__ cbm, int zlo = 0,
-                                          int zhi = 1 << 30) {
-  if (!active) return;
-  int vz = 0;
-  const bool slab = zlo > 0 || zhi < g.nz;
-  if (slab) {
-    vz = (int)((unsigned)v / (unsigned)g.nxy);
-    if (vz < zlo - 1 || vz > zhi) return;
-  }
-  const unsigned same = __ldg(nbm + v);
-#pragma unroll
-  for (int r = 0; r < 9; r++) {
-    const int dy = r % 3 - 1, dz = r / 3 - 1;
-    if (slab && (vz + dz < zlo || vz + dz >= zhi)) continue;
-    const int j0 = 3 * r;
-    unsigned want = 0;  // bit t <=> dx = t - 1
-#pragma unroll
-    for (int t = 0; t < 3; t++) {
-      const int j = j0 + t;
-      if (j != 13) {
-        const int k = j < 13 ? j : j - 1;
-        if ((same >> k) & 1u) want |= 1u << t;
-      }
-    }
-    if (!want) continue;
-    const int f = __ffs(want) - 1;
-    const unsigned wv = want >> f;
-    const int base = v + (f - 1) + dy * g.nx + dz * g.nxy;
-    const int w0 = base >> 5;
-    const int sh = base & 31;
-    const unsigned lo = wv << sh;
-    const unsigned hi = sh > 29 ? (wv >> (32 - sh)) : 0u;
-    if (lo && (__ldca(bm + w0) & lo) != lo) {
-      const uint32_t old = atomicOr(bm + w0, lo);
-      if (old == 0u) {
-        const int c = w0 >> 5;  // coarse bit = word / 32
-        const uint32_t cb = 1u << (c & 31);
-        if (!(__ldca(cbm + (c >> 5)) & cb)) atomicOr(cbm + (c >> 5), cb);
-      }
-    }
-    if (hi && (__ldca(bm + w0 + 1) & hi) != hi) {
-      const uint32_t old = atomicOr(bm + w0 + 1, hi);
-      if (old == 0u) {
-        const int c = (w0 + 1) >> 5;
-        const uint32_t cb = 1u << (c & 31);
-        if (!(__ldca(cbm + (c >> 5)) & cb)) atomicOr(cbm + (c >> 5), cb);
-      }
-    }
-  }
-}
-
-// _kernels.py:285-334: commit the round's improved proposals and enqueue
-// the same-component neighbours of every improved voxel. Proposals are SPARSE
-// (pf != null): slot i of `imp` belongs to frontier item i and pf[i] says
-// whether it improved -- the eval kernels write them without atomics or
-// block barriers -- or a COMPACT list of n_props records (pf == null; the
-// multi-GPU steps). Enqueue: `compact` = mark the frontier + coarse bitmaps
-// only (k_compact builds the voxel-ordered list and ends the round), else the
-// stamp-deduplicated append of mark_and_append, the last CTA ending the round
-// unless end_mode < 0. Grid-stride (at most one resident wave); the number of
-// committed proposals is added to counters[C_NIMP] once per CTA.
 constexpr int CM_THREADS = 256;
 constexpr int CM_SLOTS = 4 * CM_THREADS;  // sparse slots scanned per CTA step
 
@@ -118,7 +54,7 @@ __global__ void __launch_bounds__(CM_THREADS) k_commit(const Prop* __restrict__ 
                                                        int n_props, int* __restrict__ counters,
                                                        RoundCtl* __restrict__ ctl, Geo g,
                                                        const uint32_t* __restrict__ nbm, uint32_t* __restrict__ bm,
-                                                       uint32_t* __restrict__ cbm, int compact,
+                                                       uint32_t* __restrict__ cbm,
                                                        const cudaGraphConditionalHandle* __restrict__ hs,
                                                        int n_classes, cudaGraphConditionalHandle loop, int end_mode,
                                                        int zlo, int zhi) {
@@ -183,10 +119,7 @@ __global__ void __launch_bounds__(CM_THREADS) k_commit(const Prop* __restrict__ 
           mine++;
           commit_one(p, ss, dist, site1);
         }
-        if (compact)
-          mark_bits(g, nbm, take, v, bm, cbm, zlo, zhi);
-        else
-          mark_and_append(g, nbm, take, v, false, bm, next, counters + C_NNEXT, zlo, zhi);
+        mark_and_append(g, nbm, take, v, false, bm, next, counters + C_NNEXT, zlo, zhi, cbm);
       }
       __syncthreads();  // s_idx / s_wcnt reused by the next step
     }
@@ -202,10 +135,7 @@ __global__ void __launch_bounds__(CM_THREADS) k_commit(const Prop* __restrict__ 
         mine++;
         commit_one(p, ss, dist, site1);
       }
-      if (compact)
-        mark_bits(g, nbm, take, v, bm, cbm, zlo, zhi);
-      else
-        mark_and_append(g, nbm, take, v, false, bm, next, counters + C_NNEXT, zlo, zhi);
+      mark_and_append(g, nbm, take, v, false, bm, next, counters + C_NNEXT, zlo, zhi, cbm);
     }
   }
   // committed count: warp sums, one atomic per CTA
@@ -217,7 +147,7 @@ __global__ void __launch_bounds__(CM_THREADS) k_commit(const Prop* __restrict__ 
   if (lane == 0 && mine) atomicAdd(&s_cnt, mine);
   __syncthreads();
   if (threadIdx.x == 0 && s_cnt) atomicAdd(counters + C_NIMP, s_cnt);
-  if (compact || end_mode < 0) return;  // k_compact / the host / k_sweep_end ends the round
+  if (end_mode < 0) return;  // the host / k_sweep_end ends the round
   // the last block to finish ends the round (no separate launch)
   __shared__ bool last;
   __threadfence();
@@ -245,16 +175,18 @@ __device__ __forceinline__ void ct_store(unsigned long long* p, unsigned long lo
   asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-// end_mode: 1 = round end inside the round graph (arms the size class and the
-// WHILE condition), 0 = round end without graph conditionals (host-driven
-// rounds), -1 = only publish the count in counters[C_NNEXT] (sweeps and the
-// multi-GPU steps, whose own kernels swap the lists).
-__global__ void __launch_bounds__(CT_THREADS) k_compact(uint32_t* __restrict__ bm, uint32_t* __restrict__ cbm,
+constexpr int REORDER_MIN = 1 << 20;  // frontiers below this keep the append order
+
+// Rewrites the frontier ctl->cur (n = ctl->n_cur voxels, after the round end)
+// in voxel order from the frontier bitmap, clearing the words and coarse bits
+// it reads. Frontiers under REORDER_MIN return at once (their bits are
+// cleared by the next eval as usual). Tile = 2048 words = 8 warps x 8 passes
+// of 32 words (one coarse chunk per pass, skipped when its coarse bit is 0).
+__global__ void __launch_bounds__(CT_THREADS) k_reorder(uint32_t* __restrict__ bm, uint32_t* __restrict__ cbm,
                                                         int64_t bm_words, unsigned long long* __restrict__ status,
-                                                        int* __restrict__ cs, RoundCtl* __restrict__ ctl,
-                                                        int* __restrict__ counters,
-                                                        const cudaGraphConditionalHandle* __restrict__ hs,
-                                                        int n_classes, cudaGraphConditionalHandle loop, int end_mode) {
+                                                        int* __restrict__ cs, RoundCtl* __restrict__ ctl) {
+  const int n = *(volatile const int*)&ctl->n_cur;
+  if (n < REORDER_MIN) return;
   __shared__ int s_tile;
   __shared__ unsigned s_epoch;
   __shared__ int s_warp[CT_THREADS / 32];
@@ -268,37 +200,23 @@ __global__ void __launch_bounds__(CT_THREADS) k_compact(uint32_t* __restrict__ b
   __syncthreads();
   const int tile = s_tile;
   const unsigned epoch = s_epoch & 0x7fffffffu;
-  const int64_t w0 = (int64_t)tile * CT_WORDS + (int64_t)tid * CT_WPT;
-  // coarse bit of this thread's 8 words: chunk (tid * 8) / 32 of the tile
-  const uint32_t cw = cbm[(int64_t)tile * CT_CWORDS + (tid * CT_WPT / CT_CHUNK) / 32];
-  const bool any = (cw >> ((tid * CT_WPT / CT_CHUNK) & 31)) & 1u;
-  uint32_t w[CT_WPT];
-  int cnt = 0;
+  const int64_t wbase = (int64_t)tile * CT_WORDS + (int64_t)wid * 256;  // this warp's 256 words
+  const uint32_t cw = cbm[(int64_t)tile * CT_CWORDS + (wid >> 2)];   // its 8 coarse bits: (wid * 8 + k) & 31
+  uint32_t wk[CT_WPT];
+  int tot = 0;
 #pragma unroll
-  for (int k = 0; k < CT_WPT; k++) w[k] = 0u;
-  if (any && w0 < bm_words) {
-    if (w0 + CT_WPT <= bm_words) {
-      const uint4 a = *reinterpret_cast<const uint4*>(bm + w0);
-      const uint4 b = *reinterpret_cast<const uint4*>(bm + w0 + 4);
-      w[0] = a.x; w[1] = a.y; w[2] = a.z; w[3] = a.w; w[4] = b.x; w[5] = b.y; w[6] = b.z; w[7] = b.w;
-    } else {
-      for (int k = 0; k < CT_WPT; k++)
-        if (w0 + k < bm_words) w[k] = bm[w0 + k];
-    }
-#pragma unroll
-    for (int k = 0; k < CT_WPT; k++) cnt += __popc(w[k]);
+  for (int k = 0; k < CT_WPT; k++) {
+    const int64_t w = wbase + 32 * k + lane;
+    const bool on = (cw >> ((wid * 8 + k) & 31)) & 1u;
+    wk[k] = (on && w < bm_words) ? bm[w] : 0u;
+    tot += __popc(wk[k]);
   }
-  // block exclusive scan of the per-thread counts
-  int incl = cnt;
 #pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int t = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += t;
-  }
-  if (lane == 31) s_warp[wid] = incl;
+  for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+  if (lane == 0) s_warp[wid] = tot;
   __syncthreads();
   if (wid == 0) {
-    int x = lane < CT_THREADS / 32 ? s_warp[lane] : 0;
+    const int x = lane < CT_THREADS / 32 ? s_warp[lane] : 0;
     int xi = x;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -341,44 +259,52 @@ __global__ void __launch_bounds__(CT_THREADS) k_compact(uint32_t* __restrict__ b
     if (lane == 0) s_excl = excl;
   }
   __syncthreads();
-  int pos = (int)s_excl + s_warp[wid] + incl - cnt;
-  int* out = ctl->nxt;
-  if (cnt) {
+  // warp-cooperative expansion: output slot o of a pass goes to lane o % 32,
+  // which finds its word by a binary search over the pass's inclusive counts
+  int* out = ctl->cur;
+  int off = (int)s_excl + s_warp[wid];
 #pragma unroll
-    for (int k = 0; k < CT_WPT; k++) {
-      uint32_t m = w[k];
-      const int vb = (int)((w0 + k) << 5);
-      while (m) {
-        const int b = __ffs(m) - 1;
-        m &= m - 1u;
-        out[pos++] = vb + b;
+  for (int k = 0; k < CT_WPT; k++) {
+    const int c = __popc(wk[k]);
+    int incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    const int T = __shfl_sync(0xffffffffu, incl, 31);
+    for (int j = 0; j < T; j += 32) {  // warp-uniform
+      const int o = j + lane;
+      int L = 0;
+#pragma unroll
+      for (int st = 16; st > 0; st >>= 1) {
+        const int probe = __shfl_sync(0xffffffffu, incl, L + st - 1);
+        if (probe <= o) L += st;
+      }
+      L = L > 31 ? 31 : L;
+      const int inclL = __shfl_sync(0xffffffffu, incl, L);
+      const int cL = __shfl_sync(0xffffffffu, c, L);
+      const uint32_t wL = __shfl_sync(0xffffffffu, wk[k], L);
+      if (o < T) {
+        const int rank = o - (inclL - cL);
+        const int bit = (int)__fns(wL, 0, rank + 1);
+        out[off + o] = (int)(((wbase + 32 * k + L) << 5) + bit);
       }
     }
-    // consume the words read (the commit of the next round marks afresh)
-    if (w0 + CT_WPT <= bm_words) {
-      *reinterpret_cast<uint4*>(bm + w0) = make_uint4(0u, 0u, 0u, 0u);
-      *reinterpret_cast<uint4*>(bm + w0 + 4) = make_uint4(0u, 0u, 0u, 0u);
-    } else {
-      for (int k = 0; k < CT_WPT; k++)
-        if (w0 + k < bm_words) bm[w0 + k] = 0u;
-    }
+    off += T;
+    if (wk[k]) bm[wbase + 32 * k + lane] = 0u;  // consumed
   }
-  __syncthreads();  // every thread has read its coarse word
+  __syncthreads();  // every warp has read its coarse word
   if (tid < CT_CWORDS) cbm[(int64_t)tile * CT_CWORDS + tid] = 0u;
-  // the last CTA publishes the count and ends the round
   __threadfence();
   __syncthreads();
   if (tid == 0) s_last = atomicAdd(cs + CS_DONE, 1) == (int)gridDim.x - 1;
   __syncthreads();
   if (s_last && tid == 0) {
-    __threadfence();
-    const unsigned long long st = ct_load(status + (gridDim.x - 1));
-    counters[C_NNEXT] = (int)(unsigned)st;  // inclusive prefix of the last tile = list length
     cs[CS_TILE] = 0;
     cs[CS_DONE] = 0;
     cs[CS_EPOCH] = (int)epoch;
     __threadfence();
-    if (end_mode >= 0) round_end(ctl, counters, hs, n_classes, loop, end_mode);
   }
 }
 

@@ -82,7 +82,6 @@ __device__ __forceinline__ void p1_tile(const int* __restrict__ list, int n, con
     // phase 1: site1[w] is site_of[w] when src[w] == w (every phase-1 assignment), else -1
     // phase-1 states are LOS (src == v) and their distance is |c_v - p_site|
     orig_s = __ldg(site1 + v);
-    int nt = 0;
     // two batches of 13 loads in flight (bounds the live registers of the
     // big-round variant, whose 64-register budget otherwise spills)
 #pragma unroll
@@ -104,14 +103,12 @@ __device__ __forceinline__ void p1_tile(const int* __restrict__ list, int n, con
       bool seen = s < 0 || s == orig_s;
 #pragma unroll
       for (int j = 0; j < P1_TAB; j++) seen |= ts[j] == s;
-      if (!seen && nt < P1_TAB) {
+      // branch-free insert at the front (the table is a set); a fifth site overflows
+      const bool ins = !seen;
+      ovf |= ins && ts[P1_TAB - 1] >= 0;
 #pragma unroll
-        for (int j = 0; j < P1_TAB; j++)
-          if (j == nt) ts[j] = s;
-        nt++;
-      } else if (!seen) {
-        ovf = true;
-      }
+      for (int j = P1_TAB - 1; j > 0; j--) ts[j] = ins ? ts[j - 1] : ts[j];
+      ts[0] = ins ? s : ts[0];
     }
     }
     best_s = orig_s; best_src = v;
@@ -142,7 +139,12 @@ __device__ __forceinline__ void p1_tile(const int* __restrict__ list, int n, con
   // lane takes the exact non-speculative fold below.
   bool strict = false;
   int jwin = -1;
-  if (active && !ovf) {
+  // no-improvement certificate (see eval_p2.cuh): no table site beats the
+  // current state -> the fold never replaces it; decided without rays
+  bool cert = active && !ovf;
+#pragma unroll
+  for (int j = 0; j < P1_TAB; j++) cert = cert && !(ts[j] >= 0 && beats(td[j], ts[j], orig_d, orig_s));
+  if (active && !ovf && !cert) {
     strict = true;
 #pragma unroll
     for (int a = 0; a <= P1_TAB; a++) {
@@ -166,7 +168,7 @@ __device__ __forceinline__ void p1_tile(const int* __restrict__ list, int n, con
     }
   }
   __syncwarp();  // q_n initialised
-  const float isx = (float)(1.0 / g.sx), isy = (float)(1.0 / g.sy), isz = (float)(1.0 / g.sz);
+  const float isx = g.isx, isy = g.isy, isz = g.isz;
   int win_slot = -1;   // queue slot of the strict winner's ray (-1: none or proven clear)
   int win_s = -1;
   double win_d = 0.0;
@@ -199,7 +201,9 @@ __device__ __forceinline__ void p1_tile(const int* __restrict__ list, int n, con
   __syncwarp();
   // ---- E: strict lanes take their winner (or fall back to the exact fold)
   int kres = 26;  // start of the exact sequential fold (26: not needed)
-  if (active && strict) {
+  if (cert) {
+    // the current state stands
+  } else if (active && strict) {
     if (jwin >= 0 && (win_slot < 0 || qok[win_slot])) {
       best_d = win_d; best_s = win_s; best_src = v;
     } else if (jwin >= 0) {

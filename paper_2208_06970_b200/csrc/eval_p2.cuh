@@ -57,6 +57,13 @@ __device__ __forceinline__ void p2_tile(const int* __restrict__ list, int n, con
   int best_s = -1, best_src = -1, orig_s = -1;
   int own_los = -1;  // the voxel's own site when its state is LOS (src == v)
   bool done = !active;
+  // No-improvement certificate: when no candidate beats the CURRENT state,
+  // the reference's fold never replaces it (each step compares against the
+  // running best, which stays the current state), so the voxel proposes
+  // nothing -- whatever the rays would say. Every candidate distance is
+  // known exactly before the fold (path rows, LOS-site and node tables); a
+  // candidate outside a full table voids the certificate.
+  bool cert = active;
   if (active) {
     bm[v >> 5] = 0u;  // consume this round's frontier word
     coords(g, v, x, y, z);
@@ -64,6 +71,12 @@ __device__ __forceinline__ void p2_tile(const int* __restrict__ list, int n, con
     px = centre1(x, g.sx); py = centre1(y, g.sy); pz = centre1(z, g.sz);
     const unsigned same = __ldg(nbm + v);
     nbv = same;
+    {
+      const int2 sv = __ldg(ss + v);
+      best_d = __ldg(dist + v);
+      best_s = sv.x; best_src = sv.y;
+      orig_d = best_d; orig_s = best_s;
+    }
     // ---- A: gather (two batches of 13 to bound register pressure)
 #pragma unroll
     for (int h = 0; h < 2; h++) {
@@ -91,44 +104,38 @@ __device__ __forceinline__ void p2_tile(const int* __restrict__ list, int n, con
           len = dist3(px, py, pz, centre1(x + off_dx(k), g.sx), centre1(y + off_dy(k), g.sy),
                       centre1(z + off_dz(k), g.sz));
         }
-        s_dw[k][t] = __dadd_rn(dw[q], len);
+        const double dpath = __dadd_rn(dw[q], len);
+        s_dw[k][t] = dpath;
+        cert = cert && !(cand && beats(dpath, nw[q].x, orig_d, orig_s));
       }
     }
-    const int2 sv = __ldg(ss + v);
-    best_d = __ldg(dist + v);
-    best_s = sv.x; best_src = sv.y;
-    orig_d = best_d; orig_s = best_s;
     // a LOS voxel's stored distance is exactly dist3(c_v, site) (every LOS
     // commit and seed computes it in this operand order): its own site's LOS
     // candidate is the current state itself and needs no table entry
     own_los = best_src == v ? orig_s : -1;
     // ---- B: distinct LOS sites and distinct shortcut nodes
-    int nts = 0, ntu = 0;
 #pragma unroll
     for (int k = 0; k < 26; k++) {
       const int s = s_site[k][t];
       const int u = s_node[k][t];
-      if (u == -2) {
-        bool seen = s == own_los;
+      // branch-free set inserts (at the front; entries beyond the table size
+      // are looked up on the fly by the fold)
+      bool seen = u != -2 || s == own_los;
 #pragma unroll
-        for (int j = 0; j < P2_STAB; j++) seen |= ts[j] == s;
-        if (!seen && nts < P2_STAB) {
+      for (int j = 0; j < P2_STAB; j++) seen |= ts[j] == s;
+      const bool ins = !seen && ts[P2_STAB - 1] < 0;
+      cert = cert && (seen || ins);  // a LOS site the full table drops is not certified
 #pragma unroll
-          for (int j = 0; j < P2_STAB; j++)
-            if (j == nts) ts[j] = s;
-          nts++;
-        }
-      } else if (u >= 0) {
-        bool seen = false;
+      for (int j = P2_STAB - 1; j > 0; j--) ts[j] = ins ? ts[j - 1] : ts[j];
+      ts[0] = ins ? s : ts[0];
+      bool useen = u < 0;
 #pragma unroll
-        for (int j = 0; j < P2_NTAB; j++) seen |= tu[j] == u;
-        if (!seen && ntu < P2_NTAB) {
+      for (int j = 0; j < P2_NTAB; j++) useen |= tu[j] == u;
+      const bool uins = !useen && tu[P2_NTAB - 1] < 0;
+      cert = cert && (useen || uins);
 #pragma unroll
-          for (int j = 0; j < P2_NTAB; j++)
-            if (j == ntu) tu[j] = u;
-          ntu++;
-        }
-      }
+      for (int j = P2_NTAB - 1; j > 0; j--) tu[j] = uins ? tu[j - 1] : tu[j];
+      tu[0] = uins ? u : tu[0];
     }
   }
 #pragma unroll
@@ -152,6 +159,11 @@ __device__ __forceinline__ void p2_tile(const int* __restrict__ list, int n, con
       }
     }
   }
+#pragma unroll
+  for (int j = 0; j < P2_STAB; j++) cert = cert && !(ts[j] >= 0 && beats(td[j], ts[j], orig_d, orig_s));
+#pragma unroll
+  for (int j = 0; j < P2_NTAB; j++) cert = cert && !(tus[j] >= 0 && beats(tud[j], tus[j], orig_d, orig_s));
+  if (cert) done = true;  // the current state stands: no fold, no rays
   // ---- C: fold
   int failed = -1;
   int k = 0;
@@ -209,8 +221,7 @@ __device__ __forceinline__ void p2_tile(const int* __restrict__ list, int n, con
       coords(g, rsrc, ux, uy, uz);
       qx = centre1(ux, g.sx); qy = centre1(uy, g.sy); qz = centre1(uz, g.sz);
     }
-    if (ray_clear_near(nbv, qx, qy, qz, px, py, pz, (float)(1.0 / g.sx), (float)(1.0 / g.sy),
-                       (float)(1.0 / g.sz)) ||
+    if (ray_clear_near(nbv, qx, qy, qz, px, py, pz, g.isx, g.isy, g.isz) ||
         segment_clear_fast(comp, nbm, box_of(g), px, py, pz, qx, qy, qz, cv)) {
       best_d = rd; best_s = rs; best_src = rsrc;
     } else if (los) {

@@ -141,7 +141,7 @@ __device__ __forceinline__ void ew_exact(const double (*ed)[2], const int (*es)[
                                          double py,
                                          double pz, int cv, double& best_d, int& best_s, int& best_src) {
   int failed = -1;
-  const float isx = (float)(1.0 / g.sx), isy = (float)(1.0 / g.sy), isz = (float)(1.0 / g.sz);
+  const float isx = g.isx, isy = g.isy, isz = g.isz;
   for (int k = 0; k < 26; k++) {
     for (int e = 0; e < 2; e++) {
       const int t = et[k][e];

@@ -167,6 +167,12 @@ Geo make_geo(int64_t nx, int64_t ny, int64_t nz, double sx, double sy, double sz
   g.inv_nx = 1.0 / (double)nx;
   g.inv_nxy = 1.0 / (double)(nx * ny);
   g.dyadic = is_pow2(sx) && is_pow2(sy) && is_pow2(sz);
+  g.ix = 1.0 / sx;
+  g.iy = 1.0 / sy;
+  g.iz = 1.0 / sz;
+  g.isx = (float)(1.0 / sx);
+  g.isy = (float)(1.0 / sy);
+  g.isz = (float)(1.0 / sz);
   for (int k = 0; k < 26; k++) {
     int dx, dy, dz;
     offset_of(k, dx, dy, dz);
@@ -207,13 +213,13 @@ struct lrcvt_plan {
   int* eligible = nullptr;
   Prop* imp = nullptr;      // sparse proposals: slot i <-> frontier item i
   uint8_t* pf = nullptr;    // pf[i] = 1 iff slot i holds an improved proposal
-  bool compact = false;      // voxel-ordered frontier through k_compact (LRCVT_COMPACT=1)
+  bool compact = false;      // large frontiers rewritten in voxel order by k_reorder (LRCVT_COMPACT=1)
   int p1_bs = 128, p2_bs = 64;  // eval CTA sizes (LRCVT_EVAL_BS=p1,p2)
   uint32_t* bm = nullptr;  // frontier bitmap (1 bit per voxel)
   int64_t bm_words = 0;
   uint32_t* cbm = nullptr;                 // coarse frontier bitmap (1 bit per 32 words), compact.cuh
-  unsigned long long* ct_status = nullptr;  // k_compact tile status (decoupled look-back)
-  int* ct_state = nullptr;                  // k_compact epoch / tile / done counters
+  unsigned long long* ct_status = nullptr;  // k_reorder tile status (decoupled look-back)
+  int* ct_state = nullptr;                  // k_reorder epoch / tile / done counters
   int ct_tiles = 0;
   uint32_t* nbm = nullptr;  // static same-component neighbour masks
   int* site1 = nullptr;     // phase-1 LOS site per voxel (RoundCtl::site1)
@@ -406,7 +412,7 @@ int launch_eval_kernel(lrcvt_plan* p, int var, int items, cudaStream_t st) {
 
 // commit + enqueue of the next frontier (compact.cuh k_commit): the sparse
 // proposals of the round's eval (props == null) or a compact list of n_props
-// records; end_mode as k_commit / k_compact
+// records; end_mode as k_commit
 int launch_commit_kernel(lrcvt_plan* p, int64_t items, cudaStream_t st, const Prop* props = nullptr,
                          int64_t n_props = 0, const cudaGraphConditionalHandle* hs = nullptr,
                          cudaGraphConditionalHandle loop = cudaGraphConditionalHandle{}, int end_mode = -1) {
@@ -414,18 +420,17 @@ int launch_commit_kernel(lrcvt_plan* p, int64_t items, cudaStream_t st, const Pr
   if (blocks < 1) blocks = 1;
   if (blocks > p->commit_blocks) blocks = p->commit_blocks;  // grid-stride, one resident wave at most
   k_commit<<<(int)blocks, CM_THREADS, 0, st>>>(props ? props : p->imp, props ? nullptr : p->pf, (int)n_props, p->counters,
-                                        p->ctl, p->g, p->nbm, p->bm, p->cbm, p->compact ? 1 : 0, hs, p->ncl_arg(),
+                                        p->ctl, p->g, p->nbm, p->bm, p->compact ? p->cbm : nullptr, hs, p->ncl_arg(),
                                         loop, end_mode, p->zlo, p->zhi);
   CKL("k_commit");
   return 0;
 }
 
-// bitmap -> next worklist in voxel order (+ round end, see k_compact)
-int launch_compact_kernel(lrcvt_plan* p, cudaStream_t st, const cudaGraphConditionalHandle* hs,
-                          cudaGraphConditionalHandle loop, int end_mode) {
-  k_compact<<<p->ct_tiles, CT_THREADS, 0, st>>>(p->bm, p->cbm, p->bm_words, p->ct_status, p->ct_state, p->ctl,
-                                                 p->counters, hs, p->ncl_arg(), loop, end_mode);
-  CKL("k_compact");
+// the next frontier rewritten in voxel order when large (k_reorder; after the round end)
+int launch_reorder_kernel(lrcvt_plan* p, cudaStream_t st) {
+  if (!p->compact) return 0;
+  k_reorder<<<p->ct_tiles, CT_THREADS, 0, st>>>(p->bm, p->cbm, p->bm_words, p->ct_status, p->ct_state, p->ctl);
+  CKL("k_reorder");
   return 0;
 }
 
@@ -435,7 +440,7 @@ int launch_round_kernels(lrcvt_plan* p, int var, int n, cudaStream_t st, int end
   CKR(launch_eval_kernel(p, var, n, st));
   if (p->timing) CK(cudaEventRecord(p->ev1, st));
   CKR(launch_commit_kernel(p, n, st, nullptr, 0, nullptr, cudaGraphConditionalHandle{}, end_mode));
-  if (p->compact) CKR(launch_compact_kernel(p, st, nullptr, cudaGraphConditionalHandle{}, end_mode));
+  if (end_mode >= 0) CKR(launch_reorder_kernel(p, st));  // sweeps: after k_sweep_end
   if (p->timing) CK(cudaEventRecord(p->ev2, st));
   return 0;
 }
@@ -575,7 +580,7 @@ int build_round_graph(lrcvt_plan* p, int var) {
     } else {
       rc = launch_eval_kernel(p, var, (int)cap, p->cap);
       if (!rc) rc = launch_commit_kernel(p, cap, p->cap, nullptr, 0, d_hs, h, 1);
-      if (!rc && p->compact) rc = launch_compact_kernel(p, p->cap, d_hs, h, 1);
+      if (!rc) rc = launch_reorder_kernel(p, p->cap);
     }
     cudaGraph_t captured;
     const cudaError_t ee = cudaStreamEndCapture(p->cap, &captured);
@@ -1005,7 +1010,8 @@ int lrcvt_classify(lrcvt_plan* p, int64_t n_sites, const double* d_site_pos,
     if (p->timing) CK(cudaEventRecord(p->ev0, st));
     CKR(launch_round_kernels(p, var2, (int)p->n_inband, st, -1));  // sweep: n_el <= in-band
     k_sweep_end<<<1, 1, 0, st>>>(p->ctl, p->counters);
-    CKL("k_sweep_end"); LAUNCHED(4);  // eval, commit, compact, sweep end
+    CKL("k_sweep_end"); LAUNCHED(3);  // eval, commit, sweep end
+    CKR(launch_reorder_kernel(p, st));
     CK(cudaMemcpyAsync(p->h_ctl, p->ctl, sizeof(RoundCtl), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     if (p->timing) {
@@ -1033,7 +1039,7 @@ int lrcvt_classify(lrcvt_plan* p, int64_t n_sites, const double* d_site_pos,
   stats->bad_sites = p->h_counters[C_BAD];
   // eval, commit, compact (+ fused round end) per launched relaxation round; one k_rounds_small
   // launch covers all its rounds
-  LAUNCHED((p->compact ? 3 : 2) * (c.rounds - c.rounds_small) + c.small_launches);
+  LAUNCHED((p->compact ? 3 : 2) * (c.rounds - c.rounds_small) + c.small_launches);  // + k_reorder when on
   if (p->h_counters[C_BAD]) {
     p->eligible_valid = false;
     return p->h_counters[C_BAD];
@@ -1608,7 +1614,6 @@ int lrcvt_mg_commit(lrcvt_plan* p, const void* d_halo, int64_t n_halo, int32_t s
   const int n = sweep ? (int)p->n_eligible : p->h_ncur;
   if (n > 0) CKR(launch_commit_kernel(p, n, st));  // own sparse proposals
   if (n_halo > 0) CKR(launch_commit_kernel(p, n_halo, st, (const Prop*)d_halo, n_halo));  // halo planes
-  if (p->compact) CKR(launch_compact_kernel(p, st, nullptr, cudaGraphConditionalHandle{}, -1));
   CKR(sync_counters(p, st, 2));
   const int nn = p->h_counters[C_NNEXT];
   k_mg_round_end<<<1, 1, 0, st>>>(p->ctl, p->counters, sweep);

@@ -103,6 +103,24 @@ __global__ void __launch_bounds__(256) k_vote_pairs(const int* __restrict__ list
   }
 }
 
+// acc + t[0] + t[1] + ... + t[cnt-1] left to right (the reference's
+// sequential accumulation), t[q] = col[4 * q]: the staged terms are loaded
+// 16 at a time ahead of the dependent adds, so the chain runs at add latency
+// instead of shared-memory load latency per term.
+__device__ __forceinline__ double ordered_add(double acc, const double* col, int cnt) {
+#pragma unroll
+  for (int h = 0; h < 32; h += 16) {
+    if (h >= cnt) break;
+    double t[16];
+#pragma unroll
+    for (int q = 0; q < 16; q++) t[q] = col[4 * (h + q)];
+#pragma unroll
+    for (int q = 0; q < 16; q++)
+      if (h + q < cnt) acc = __dadd_rn(acc, t[q]);
+  }
+  return acc;
+}
+
 // weight m_v**gamma of voxel v (seeding.py:68 for the modes the device forms)
 __device__ __forceinline__ double vote_weight(int v, const double* __restrict__ w64, const float* __restrict__ w32,
                                               int w_mode) {
@@ -150,7 +168,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_vote_sum(const unsigned long lon
     __syncwarp();
     const int cnt = min(32, e - j0);
     if (lane < 4) {
-      for (int k = 0; k < cnt; k++) acc = __dadd_rn(acc, buf[wid][k][lane]);
+      acc = ordered_add(acc, &buf[wid][0][lane], cnt);
     }
     __syncwarp();
     q1 = q2; q2 = q3; w1 = w2;
@@ -296,7 +314,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_vote_scan(const int2* __restrict
           __syncwarp();
           const int cnt = __popc(m);
           if (lane < 4)
-            for (int q = 0; q < cnt; q++) acc = __dadd_rn(acc, buf[wid][q][lane]);
+            acc = ordered_add(acc, &buf[wid][0][lane], cnt);
           __syncwarp();
         }
       }
