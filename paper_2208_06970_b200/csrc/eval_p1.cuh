@@ -139,12 +139,7 @@ __device__ __forceinline__ void p1_tile(const int* __restrict__ list, int n, con
   // lane takes the exact non-speculative fold below.
   bool strict = false;
   int jwin = -1;
-  // no-improvement certificate (see eval_p2.cuh): no table site beats the
-  // current state -> the fold never replaces it; decided without rays
-  bool cert = active && !ovf;
-#pragma unroll
-  for (int j = 0; j < P1_TAB; j++) cert = cert && !(ts[j] >= 0 && beats(td[j], ts[j], orig_d, orig_s));
-  if (active && !ovf && !cert) {
+  if (active && !ovf) {
     strict = true;
 #pragma unroll
     for (int a = 0; a <= P1_TAB; a++) {
@@ -201,9 +196,7 @@ __device__ __forceinline__ void p1_tile(const int* __restrict__ list, int n, con
   __syncwarp();
   // ---- E: strict lanes take their winner (or fall back to the exact fold)
   int kres = 26;  // start of the exact sequential fold (26: not needed)
-  if (cert) {
-    // the current state stands
-  } else if (active && strict) {
+  if (active && strict) {
     if (jwin >= 0 && (win_slot < 0 || qok[win_slot])) {
       best_d = win_d; best_s = win_s; best_src = v;
     } else if (jwin >= 0) {
