@@ -215,6 +215,7 @@ struct lrcvt_plan {
   uint8_t* pf = nullptr;    // pf[i] = 1 iff slot i holds an improved proposal
   bool compact = false;      // large frontiers rewritten in voxel order by k_reorder (LRCVT_COMPACT=1)
   int p1_bs = 128, p2_bs = 64;  // eval CTA sizes (LRCVT_EVAL_BS=p1,p2)
+  int p1_big_minb = P1_MIN_BLOCKS_BIG;  // register budget of the big-round phase-1 eval (LRCVT_P1_MINB=6|7|8)
   uint32_t* bm = nullptr;  // frontier bitmap (1 bit per voxel)
   int64_t bm_words = 0;
   uint32_t* cbm = nullptr;                 // coarse frontier bitmap (1 bit per 32 words), compact.cuh
@@ -386,6 +387,10 @@ int launch_eval_kernel(lrcvt_plan* p, int var, int items, cudaStream_t st) {
       k_eval_p1<32, 32><<<blocks, 32, 0, st>>>(c, g, cm, nb, sp, p->bm, p->imp, p->pf);
     else if (bs == 32)
       k_eval_p1<32, 20><<<blocks, 32, 0, st>>>(c, g, cm, nb, sp, p->bm, p->imp, p->pf);
+    else if (big && p->p1_big_minb == 6)
+      k_eval_p1<128, 6><<<blocks, 128, 0, st>>>(c, g, cm, nb, sp, p->bm, p->imp, p->pf);
+    else if (big && p->p1_big_minb == 7)
+      k_eval_p1<128, 7><<<blocks, 128, 0, st>>>(c, g, cm, nb, sp, p->bm, p->imp, p->pf);
     else if (big)
       k_eval_p1<128, P1_MIN_BLOCKS_BIG><<<blocks, 128, 0, st>>>(c, g, cm, nb, sp, p->bm, p->imp, p->pf);
     else
@@ -708,6 +713,7 @@ int lrcvt_plan_create(lrcvt_plan** plan, int64_t nx, int64_t ny, int64_t nz, dou
   if (const char* e = getenv("LRCVT_SWITCH")) p->class_switch = e[0] != '0';
   if (const char* e = getenv("LRCVT_VOTE")) p->vote_bbox = strcmp(e, "sort") != 0;
   if (const char* e = getenv("LRCVT_COMPACT")) p->compact = e[0] == '1';
+  if (const char* e = getenv("LRCVT_P1_MINB")) p->p1_big_minb = atoi(e);
   if (const char* e = getenv("LRCVT_EVAL_BS")) {
     int a = 0, b = 0;
     if (sscanf(e, "%d,%d", &a, &b) == 2) {
