@@ -140,9 +140,15 @@ __global__ void k_mark_site_comps(const int* __restrict__ site_comp, int n_sites
 // Mark same-component neighbours of v (and v itself when `self`) in the
 // frontier bitmap; newly set bits are appended to `next`. Reproduces the
 // stamp-deduplicated enqueue of _kernels.py:313-333 (self=false) and
-// _kernels.py:425-454 (self=true). All 32 lanes must call it.
-// Three unrolled stages keep every load/atomic of a stage independent (26
-// requests in flight per thread instead of 26 dependent round trips).
+// _kernels.py:425-454 (self=true). All threads of the CTA must call it.
+// The 27-cube around v is 9 x-rows of 3 voxels (dx = -1, 0, +1); a row's
+// three bits sit in one bitmap word (two when they straddle a word). Four
+// unrolled stages keep the requests of a stage independent: the 9 rows'
+// masks, their precheck loads (a cached word that already holds the bits
+// skips the atomic; a stale copy only under-reports set bits), the atomics,
+// then the newly set bits. newmask uses the 27-cube index
+// j = (dz+1)*9 + (dy+1)*3 + (dx+1). With cbm, the word turned non-empty
+// also marks its coarse bit (compact.cuh).
 template <bool COH = false>
 __device__ __forceinline__ void mark_and_append(const Geo& g, const uint32_t* __restrict__ nbm,
                                                 bool active, int v, bool self,
@@ -150,32 +156,25 @@ __device__ __forceinline__ void mark_and_append(const Geo& g, const uint32_t* __
                                                 int* __restrict__ next, int* counter,
                                                 int zlo = 0, int zhi = 1 << 30,
                                                 uint32_t* __restrict__ cbm = nullptr) {
-  // COH: inside the persistent small-round kernel the precheck must not see a
-  // stale L1 copy of a word cleared since (it would skip a needed enqueue)
-  // The 27-cube around v is 9 x-rows of 3 voxels (dx = -1, 0, +1); a row's
-  // three bits sit in one bitmap word (two when they straddle a word), so
-  // each row costs one cached precheck load and at most one atomicOr with a
-  // 3-bit mask. A stale cached word can only under-report set bits (bits are
-  // only set during a round), which merely sends that row to the atomic.
-  // newmask uses the 27-cube index j = (dz+1)*9 + (dy+1)*3 + (dx+1).
   unsigned newmask = 0;
+  const bool slab = zlo > 0 || zhi < g.nz;
   int vz = 0;
-  if (active && (zlo > 0 || zhi < g.nz)) {  // slab mode: only rows inside [zlo, zhi)
+  if (active && slab) {  // slab mode: only rows inside [zlo, zhi)
     vz = (int)((unsigned)v / (unsigned)g.nxy);
     if (vz < zlo - 1 || vz > zhi) active = false;
   }
   if (active) {
     const unsigned same = __ldg(nbm + v);
+    int w0[9];
+    unsigned lo[9], hi[9], shv[9];
+    // stage 1: per row, the wanted bits of words w0 / w0 + 1
 #pragma unroll
     for (int r = 0; r < 9; r++) {
       const int dy = r % 3 - 1, dz = r / 3 - 1;
-      if ((zlo > 0 || zhi < g.nz) && (vz + dz < zlo || vz + dz >= zhi)) continue;
-      // k of (dx=-1,dy,dz): j = 3r (+0), k = j < 13 ? j : j - 1
-      const int j0 = 3 * r;
       unsigned want = 0;  // bit t <=> dx = t - 1
 #pragma unroll
       for (int t = 0; t < 3; t++) {
-        const int j = j0 + t;
+        const int j = 3 * r + t;
         if (j == 13) {
           if (self) want |= 1u << t;
         } else {
@@ -183,34 +182,44 @@ __device__ __forceinline__ void mark_and_append(const Geo& g, const uint32_t* __
           if ((same >> k) & 1u) want |= 1u << t;
         }
       }
-      if (!want) continue;
-      // anchor the window at the first wanted voxel (always inside the grid)
-      const int f = __ffs(want) - 1;
+      if (slab && (vz + dz < zlo || vz + dz >= zhi)) want = 0;
+      // anchor the window at the row's dx = -1 position (v - 1 may lie in the
+      // previous row / word; the shifted mask never addresses a voxel outside
+      // `want`, which only holds in-grid neighbours)
+      const int base = v - 1 + dy * g.nx + dz * g.nxy;
+      const int f = want ? __ffs(want) - 1 : 0;
+      const int b0 = base + f;
       const unsigned wv = want >> f;
-      const int base = v + (f - 1) + dy * g.nx + dz * g.nxy;
-      const int w0 = base >> 5;
-      const int sh = base & 31;
-      const unsigned lo = wv << sh;                           // bits in word w0
-      const unsigned hi = sh > 29 ? (wv >> (32 - sh)) : 0u;   // spill into w0 + 1
-      unsigned got = 0;  // newly set by this thread, in `wv` coordinates
-      if (lo) {
-        const uint32_t cur = COH ? __ldcg(bm + w0) : __ldca(bm + w0);
-        if ((cur & lo) != lo) {
-          const uint32_t old = atomicOr(bm + w0, lo);
-          got |= ((~old) & lo) >> sh;
-          if (cbm && old == 0u) atomicOr(cbm + (w0 >> 10), 1u << ((w0 >> 5) & 31));  // coarse bit (compact.cuh)
-        }
+      w0[r] = b0 >> 5;
+      const int sh = b0 & 31;
+      shv[r] = (unsigned)sh | ((unsigned)f << 8);
+      lo[r] = wv << sh;
+      hi[r] = sh > 29 ? (wv >> (32 - sh)) : 0u;
+    }
+    // stage 2: precheck loads
+    unsigned clo[9], chi[9];
+#pragma unroll
+    for (int r = 0; r < 9; r++) {
+      clo[r] = lo[r] ? (COH ? __ldcg(bm + w0[r]) : __ldca(bm + w0[r])) : 0u;
+      chi[r] = hi[r] ? (COH ? __ldcg(bm + w0[r] + 1) : __ldca(bm + w0[r] + 1)) : 0u;
+    }
+    // stage 3: atomics where bits are missing
+#pragma unroll
+    for (int r = 0; r < 9; r++) {
+      clo[r] = (lo[r] && (clo[r] & lo[r]) != lo[r]) ? atomicOr(bm + w0[r], lo[r]) : ~0u;
+      chi[r] = (hi[r] && (chi[r] & hi[r]) != hi[r]) ? atomicOr(bm + w0[r] + 1, hi[r]) : ~0u;
+    }
+    // stage 4: newly set bits (and coarse marks)
+#pragma unroll
+    for (int r = 0; r < 9; r++) {
+      const int sh = (int)(shv[r] & 0xff), f = (int)(shv[r] >> 8);
+      unsigned got = ((~clo[r]) & lo[r]) >> sh;
+      got |= sh > 29 ? (((~chi[r]) & hi[r]) << (32 - sh)) : 0u;
+      newmask |= (got << f) << (3 * r);
+      if (cbm) {
+        if (lo[r] && clo[r] == 0u) atomicOr(cbm + (w0[r] >> 10), 1u << ((w0[r] >> 5) & 31));
+        if (hi[r] && chi[r] == 0u) atomicOr(cbm + ((w0[r] + 1) >> 10), 1u << (((w0[r] + 1) >> 5) & 31));
       }
-      if (hi) {
-        const uint32_t cur = COH ? __ldcg(bm + w0 + 1) : __ldca(bm + w0 + 1);
-        if ((cur & hi) != hi) {
-          const uint32_t old = atomicOr(bm + w0 + 1, hi);
-          got |= ((~old) & hi) << (32 - sh);
-          if (cbm && old == 0u) atomicOr(cbm + ((w0 + 1) >> 10), 1u << (((w0 + 1) >> 5) & 31));
-        }
-      }
-      got <<= f;
-      newmask |= got << j0;
     }
   }
   const int cnt = __popc(newmask);
@@ -241,11 +250,12 @@ __device__ __forceinline__ void mark_and_append(const Geo& g, const uint32_t* __
   __syncthreads();
   int pos = s_cbase + s_wbase[wid] + incl - cnt;
   __syncthreads();  // the next call may overwrite s_wbase / s_cbase
-  while (newmask) {
-    const int j = __ffs(newmask) - 1;
-    newmask &= newmask - 1;
-    const int dx = j % 3 - 1, dy = (j / 3) % 3 - 1, dz = j / 9 - 1;
-    next[pos++] = v + dx + dy * g.nx + dz * g.nxy;
+  if (newmask) {
+    // unrolled over the 27-cube: compile-time (dx, dy, dz) per bit
+#pragma unroll
+    for (int j = 0; j < 27; j++) {
+      if ((newmask >> j) & 1u) next[pos++] = v + (j % 3 - 1) + (j / 3 % 3 - 1) * g.nx + (j / 9 - 1) * g.nxy;
+    }
   }
 }
 

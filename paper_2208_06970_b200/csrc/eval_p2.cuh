@@ -24,6 +24,13 @@ namespace lrcvt {
 constexpr int P2_STAB = 4;  // distinct LOS sites
 constexpr int P2_NTAB = 6;  // distinct shortcut nodes
 
+// |c_w - c_v| for neighbour k: exact by offset class when the spacing is dyadic
+template <bool DYADIC>
+__device__ __forceinline__ double p2_len(const Geo& g, int k, int x, int y, int z, double px, double py, double pz) {
+  if (DYADIC) return len_of(g, off_cls(k));
+  return dist3(px, py, pz, centre1(x + off_dx(k), g.sx), centre1(y + off_dy(k), g.sy), centre1(z + off_dz(k), g.sz));
+}
+
 // MG: multi-GPU slab mode, the far node reads of shortcut candidates go
 // through the PeerView (mg.cuh)
 template <int BLOCK, bool DYADIC, bool MG>
@@ -36,12 +43,8 @@ __device__ __forceinline__ void p2_tile(const int* __restrict__ list, int n, con
                                                    uint32_t* __restrict__ bm,
                                                    Prop* __restrict__ imp, uint8_t* __restrict__ pf,
                                                    const PeerView* __restrict__ pv) {
-  __shared__ int s_site[26][BLOCK];    // site(w) or -1 (not a candidate source)
-  __shared__ int s_node[26][BLOCK];    // -2: w is LOS; -1: no shortcut; else src(w)
-  __shared__ double s_dw[26][BLOCK];   // dist[w] + |c_w - p| (path candidate)
   const bool active = i < n;
   const int v = active ? __ldg(list + i) : 0;
-  const int t = threadIdx.x;
   int x = 0, y = 0, z = 0, cv = -3;
   unsigned nbv = 0;  // this voxel's nbm word (neighbour bits + clearance)
   double px = 0, py = 0, pz = 0;
@@ -76,6 +79,10 @@ __device__ __forceinline__ void p2_tile(const int* __restrict__ list, int n, con
       best_d = __ldg(dist + v);
       best_s = sv.x; best_src = sv.y;
       orig_d = best_d; orig_s = best_s;
+      // a LOS voxel's stored distance is exactly dist3(c_v, site) (every LOS
+      // commit and seed computes it in this operand order): its own site's LOS
+      // candidate is the current state itself and needs no table entry
+      own_los = best_src == v ? orig_s : -1;
     }
     // ---- A: gather (two batches of 13 to bound register pressure)
 #pragma unroll
@@ -95,47 +102,30 @@ __device__ __forceinline__ void p2_tile(const int* __restrict__ list, int n, con
         const int k = 13 * h + q;
         const int w = v + off_dx(k) + off_dy(k) * g.nx + off_dz(k) * g.nxy;
         const bool cand = nw[q].x >= 0;
-        s_site[k][t] = cand ? nw[q].x : -1;
-        s_node[k][t] = !cand ? -1 : (nw[q].y == w ? -2 : (nw[q].y >= 0 ? nw[q].y : -1));
-        double len;
-        if (DYADIC) {
-          len = len_of(g, off_cls(k));
-        } else {
-          len = dist3(px, py, pz, centre1(x + off_dx(k), g.sx), centre1(y + off_dy(k), g.sy),
-                      centre1(z + off_dz(k), g.sz));
-        }
-        const double dpath = __dadd_rn(dw[q], len);
-        s_dw[k][t] = dpath;
-        cert = cert && !(cand && beats(dpath, nw[q].x, orig_d, orig_s));
+        const int s = cand ? nw[q].x : -1;
+        const int u = !cand ? -1 : (nw[q].y == w ? -2 : (nw[q].y >= 0 ? nw[q].y : -1));
+        const double dpath = __dadd_rn(dw[q], p2_len<DYADIC>(g, k, x, y, z, px, py, pz));
+        cert = cert && !(cand && beats(dpath, s, orig_d, orig_s));
+        // ---- B: distinct LOS sites and distinct shortcut nodes, branch-free set
+        // inserts (at the front; entries beyond the table size are looked up on
+        // the fly by the fold, and void the certificate)
+        bool seen = u != -2 || s == own_los;
+#pragma unroll
+        for (int j = 0; j < P2_STAB; j++) seen |= ts[j] == s;
+        const bool ins = !seen && ts[P2_STAB - 1] < 0;
+        cert = cert && (seen || ins);
+#pragma unroll
+        for (int j = P2_STAB - 1; j > 0; j--) ts[j] = ins ? ts[j - 1] : ts[j];
+        ts[0] = ins ? s : ts[0];
+        bool useen = u < 0;
+#pragma unroll
+        for (int j = 0; j < P2_NTAB; j++) useen |= tu[j] == u;
+        const bool uins = !useen && tu[P2_NTAB - 1] < 0;
+        cert = cert && (useen || uins);
+#pragma unroll
+        for (int j = P2_NTAB - 1; j > 0; j--) tu[j] = uins ? tu[j - 1] : tu[j];
+        tu[0] = uins ? u : tu[0];
       }
-    }
-    // a LOS voxel's stored distance is exactly dist3(c_v, site) (every LOS
-    // commit and seed computes it in this operand order): its own site's LOS
-    // candidate is the current state itself and needs no table entry
-    own_los = best_src == v ? orig_s : -1;
-    // ---- B: distinct LOS sites and distinct shortcut nodes
-#pragma unroll
-    for (int k = 0; k < 26; k++) {
-      const int s = s_site[k][t];
-      const int u = s_node[k][t];
-      // branch-free set inserts (at the front; entries beyond the table size
-      // are looked up on the fly by the fold)
-      bool seen = u != -2 || s == own_los;
-#pragma unroll
-      for (int j = 0; j < P2_STAB; j++) seen |= ts[j] == s;
-      const bool ins = !seen && ts[P2_STAB - 1] < 0;
-      cert = cert && (seen || ins);  // a LOS site the full table drops is not certified
-#pragma unroll
-      for (int j = P2_STAB - 1; j > 0; j--) ts[j] = ins ? ts[j - 1] : ts[j];
-      ts[0] = ins ? s : ts[0];
-      bool useen = u < 0;
-#pragma unroll
-      for (int j = 0; j < P2_NTAB; j++) useen |= tu[j] == u;
-      const bool uins = !useen && tu[P2_NTAB - 1] < 0;
-      cert = cert && (useen || uins);
-#pragma unroll
-      for (int j = P2_NTAB - 1; j > 0; j--) tu[j] = uins ? tu[j - 1] : tu[j];
-      tu[0] = uins ? u : tu[0];
     }
   }
 #pragma unroll
@@ -172,12 +162,18 @@ __device__ __forceinline__ void p2_tile(const int* __restrict__ list, int n, con
     double rd = 0.0;
     bool los = false;
     for (; k < 26; k++) {
-      const int s = s_site[k][t];
+      // the fold runs only where the certificate failed: re-read the neighbour
+      // (an L1 hit: this thread gathered it above) instead of keeping rows
+      if (!((nbv >> k) & 1u)) continue;
+      const char4 o = c_off[k];
+      const int w = nbr_index(v, o, g.nx, g.nxy);
+      const int2 nw = __ldg(ss + w);
+      const int s = nw.x;
       if (s < 0) continue;
-      const int u = s_node[k][t];
-      const double dpath = s_dw[k][t];
+      const int u = nw.y == w ? -2 : (nw.y >= 0 ? nw.y : -1);
+      const double dpath = __dadd_rn(__ldg(dist + w), p2_len<DYADIC>(g, k, x, y, z, px, py, pz));
       if (beats(dpath, s, best_d, best_s)) {
-        best_d = dpath; best_s = s; best_src = nbr_index(v, c_off[k], g.nx, g.nxy);
+        best_d = dpath; best_s = s; best_src = w;
       }
       if (u == -2) {
         double d;
@@ -239,8 +235,8 @@ __device__ __forceinline__ void p2_tile(const int* __restrict__ list, int n, con
   if (active) pf[i] = improved ? 1 : 0;
 }
 
-template <int BLOCK, bool DYADIC, bool MG = false>
-__global__ void __launch_bounds__(BLOCK, 512 / BLOCK) k_eval_p2(RoundCtl* __restrict__ ctl, Geo g,
+template <int BLOCK, bool DYADIC, bool MG = false, int MINB = 512 / BLOCK>
+__global__ void __launch_bounds__(BLOCK, MINB) k_eval_p2(RoundCtl* __restrict__ ctl, Geo g,
                                                                 const int* __restrict__ comp,
                                                                 const uint32_t* __restrict__ nbm,
                                                                 const double4* __restrict__ site_pos,

@@ -216,6 +216,7 @@ struct lrcvt_plan {
   bool compact = false;      // large frontiers rewritten in voxel order by k_reorder (LRCVT_COMPACT=1)
   int p1_bs = 128, p2_bs = 64;  // eval CTA sizes (LRCVT_EVAL_BS=p1,p2)
   int p1_big_minb = P1_MIN_BLOCKS_BIG;  // register budget of the big-round phase-1 eval (LRCVT_P1_MINB=6|7|8)
+  int p2_minb = 12;                     // CTAs per SM the phase-2 eval is compiled for (LRCVT_P2_MINB=8|12|16)
   uint32_t* bm = nullptr;  // frontier bitmap (1 bit per voxel)
   int64_t bm_words = 0;
   uint32_t* cbm = nullptr;                 // coarse frontier bitmap (1 bit per 32 words), compact.cuh
@@ -405,6 +406,16 @@ int launch_eval_kernel(lrcvt_plan* p, int var, int items, cudaStream_t st) {
       k_eval_p2<32, true><<<blocks, 32, 0, st>>>(c, g, cm, nb, sp, p->bm, p->imp, p->pf);
     else
       k_eval_p2<32, false><<<blocks, 32, 0, st>>>(c, g, cm, nb, sp, p->bm, p->imp, p->pf);
+  } else if (p->p2_minb == 12) {  // register budget of the phase-2 eval (LRCVT_P2_MINB)
+    if (var == 1)
+      k_eval_p2<64, true, false, 12><<<blocks, 64, 0, st>>>(c, g, cm, nb, sp, p->bm, p->imp, p->pf);
+    else
+      k_eval_p2<64, false, false, 12><<<blocks, 64, 0, st>>>(c, g, cm, nb, sp, p->bm, p->imp, p->pf);
+  } else if (p->p2_minb == 16) {
+    if (var == 1)
+      k_eval_p2<64, true, false, 16><<<blocks, 64, 0, st>>>(c, g, cm, nb, sp, p->bm, p->imp, p->pf);
+    else
+      k_eval_p2<64, false, false, 16><<<blocks, 64, 0, st>>>(c, g, cm, nb, sp, p->bm, p->imp, p->pf);
   } else {
     if (var == 1)
       k_eval_p2<64, true><<<blocks, 64, 0, st>>>(c, g, cm, nb, sp, p->bm, p->imp, p->pf);
@@ -714,6 +725,7 @@ int lrcvt_plan_create(lrcvt_plan** plan, int64_t nx, int64_t ny, int64_t nz, dou
   if (const char* e = getenv("LRCVT_VOTE")) p->vote_bbox = strcmp(e, "sort") != 0;
   if (const char* e = getenv("LRCVT_COMPACT")) p->compact = e[0] == '1';
   if (const char* e = getenv("LRCVT_P1_MINB")) p->p1_big_minb = atoi(e);
+  if (const char* e = getenv("LRCVT_P2_MINB")) p->p2_minb = atoi(e);
   if (const char* e = getenv("LRCVT_EVAL_BS")) {
     int a = 0, b = 0;
     if (sscanf(e, "%d,%d", &a, &b) == 2) {

@@ -265,13 +265,14 @@ __global__ void __launch_bounds__(WARPS * 32) k_vote_scan(const int2* __restrict
   double acc = (init && mode != 1 && lane < 4) ? init[lane * n_sites + s] : 0.0;
   if (W > 0 && H > 0 && D > 0) {
     const long long T = (long long)W * H * D;
-    // flat box index k = lane + 32 * chunk -> (dx, dy, dz), advanced by 32 per chunk
+    // flat box index k = lane + 32 * chunk -> (dx, dy, dz); 32 = qa * W + qb,
+    // so a chunk advance is dx += qb, dy += qa plus at most one x carry
+    const int qa = 32 / W, qb = 32 - qa * W;
     int dx = lane % W, r = lane / W;
     int dy = r % H, dz = r / H;
     long long k = lane;  // flat index of this lane's next voxel to load
-    // VS_DEPTH chunks in flight: (site, phi), component and weight of every
-    // lane's voxel are loaded VS_DEPTH chunks ahead of the ordered adds (the
-    // walk is latency-bound otherwise: one chunk ~ one memory round trip)
+    // VS_DEPTH chunks in flight: (site, phi) and weight of every lane's voxel
+    // are loaded VS_DEPTH chunks ahead of the ordered adds
     int2 a[VS_DEPTH];
     double w[VS_DEPTH];
     auto load = [&](int j) {
@@ -283,17 +284,10 @@ __global__ void __launch_bounds__(WARPS * 32) k_vote_scan(const int2* __restrict
         w[j] = vote_weight(v, w64, w32, w_mode);
       }
       k += 32;
-      dx += 32;
-      if (dx >= W) {
-        const int q = dx / W;
-        dx -= q * W;
-        dy += q;
-        if (dy >= H) {
-          const int q2 = dy / H;
-          dy -= q2 * H;
-          dz += q2;
-        }
-      }
+      dx += qb;
+      dy += qa;
+      if (dx >= W) { dx -= W; dy++; }
+      while (dy >= H) { dy -= H; dz++; }
     };
 #pragma unroll
     for (int j = 0; j < VS_DEPTH; j++) load(j);

@@ -1,0 +1,13 @@
+#!/bin/bash
+# p2 without shared-memory rows (fold re-reads), register budgets, row-packed vote walk
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_edges.py tests/test_gpu_classify.py tests/test_gpu_multi.py tests/test_gpu_warp_eval.py tests/test_gpu_parity_big.py -k "not c5" -q -x -p no:cacheprovider > gpurun_out/g9_quick.log 2>&1; echo "quick rc=$?"; tail -2 gpurun_out/g9_quick.log
+LRCVT_P2_MINB=12 timeout 900 python -m pytest tests/test_gpu_classify.py -q -x -p no:cacheprovider > gpurun_out/g9_q12.log 2>&1; echo "p2 minb 12 rc=$?"; tail -1 gpurun_out/g9_q12.log
+rm -f gpurun_out/g9_ab.txt
+for rep in 1 2; do
+ for cfg in "LRCVT_P2_MINB=8" "LRCVT_P2_MINB=12" "LRCVT_P2_MINB=16" "LRCVT_VOTE=sort"; do
+  env $cfg timeout 900 python bench.py --steps 10 --warmup 3 --no-passes --no-e2e --no-cpu-baseline > gpurun_out/g9_ab.log 2>&1
+  echo "[$cfg] $(grep '^{' gpurun_out/g9_ab.log | python -c 'import json,sys; d=json.loads(sys.stdin.read()); r=d["roofline"]; print("ms/step %.2f" % d["ms_per_step"], {k: round(v,2) for k,v in r["breakdown_ms_per_step"].items()})')" >> gpurun_out/g9_ab.txt
+ done
+done
+cat gpurun_out/g9_ab.txt
