@@ -137,18 +137,29 @@ __global__ void k_mark_site_comps(const int* __restrict__ site_comp, int n_sites
   if (c >= 0 && c < n_slots) has_site[c] = 1;
 }
 
+// the 27-cube j = (dz+1)*9 + (dy+1)*3 + (dx+1) as (dx, dy, dz)
+__constant__ char4 c_cube[27] = {
+#define LRCVT_CUBE(j) {(signed char)((j) % 3 - 1), (signed char)((j) / 3 % 3 - 1), (signed char)((j) / 9 - 1), 0}
+    LRCVT_CUBE(0),  LRCVT_CUBE(1),  LRCVT_CUBE(2),  LRCVT_CUBE(3),  LRCVT_CUBE(4),  LRCVT_CUBE(5),  LRCVT_CUBE(6),
+    LRCVT_CUBE(7),  LRCVT_CUBE(8),  LRCVT_CUBE(9),  LRCVT_CUBE(10), LRCVT_CUBE(11), LRCVT_CUBE(12), LRCVT_CUBE(13),
+    LRCVT_CUBE(14), LRCVT_CUBE(15), LRCVT_CUBE(16), LRCVT_CUBE(17), LRCVT_CUBE(18), LRCVT_CUBE(19), LRCVT_CUBE(20),
+    LRCVT_CUBE(21), LRCVT_CUBE(22), LRCVT_CUBE(23), LRCVT_CUBE(24), LRCVT_CUBE(25), LRCVT_CUBE(26)
+#undef LRCVT_CUBE
+};
+
 // Mark same-component neighbours of v (and v itself when `self`) in the
 // frontier bitmap; newly set bits are appended to `next`. Reproduces the
 // stamp-deduplicated enqueue of _kernels.py:313-333 (self=false) and
 // _kernels.py:425-454 (self=true). All threads of the CTA must call it.
 // The 27-cube around v is 9 x-rows of 3 voxels (dx = -1, 0, +1); a row's
-// three bits sit in one bitmap word (two when they straddle a word). Four
-// unrolled stages keep the requests of a stage independent: the 9 rows'
-// masks, their precheck loads (a cached word that already holds the bits
-// skips the atomic; a stale copy only under-reports set bits), the atomics,
-// then the newly set bits. newmask uses the 27-cube index
+// three bits sit in one bitmap word (two when they straddle a word), so
+// each row costs one cached precheck load and at most one atomicOr with a
+// 3-bit mask (a stale cached word only under-reports set bits, which merely
+// sends that row to the atomic). newmask uses the 27-cube index
 // j = (dz+1)*9 + (dy+1)*3 + (dx+1). With cbm, the word turned non-empty
-// also marks its coarse bit (compact.cuh).
+// also marks its coarse bit (compact.cuh). (Staging all 9 rows' loads, then
+// all atomics, measured 45% slower: more registers, fewer warps, and the
+// prechecks no longer see the bits the earlier rows' atomics set.)
 template <bool COH = false>
 __device__ __forceinline__ void mark_and_append(const Geo& g, const uint32_t* __restrict__ nbm,
                                                 bool active, int v, bool self,
@@ -165,16 +176,15 @@ __device__ __forceinline__ void mark_and_append(const Geo& g, const uint32_t* __
   }
   if (active) {
     const unsigned same = __ldg(nbm + v);
-    int w0[9];
-    unsigned lo[9], hi[9], shv[9];
-    // stage 1: per row, the wanted bits of words w0 / w0 + 1
 #pragma unroll
     for (int r = 0; r < 9; r++) {
       const int dy = r % 3 - 1, dz = r / 3 - 1;
+      if (slab && (vz + dz < zlo || vz + dz >= zhi)) continue;
+      const int j0 = 3 * r;
       unsigned want = 0;  // bit t <=> dx = t - 1
 #pragma unroll
       for (int t = 0; t < 3; t++) {
-        const int j = 3 * r + t;
+        const int j = j0 + t;
         if (j == 13) {
           if (self) want |= 1u << t;
         } else {
@@ -182,44 +192,34 @@ __device__ __forceinline__ void mark_and_append(const Geo& g, const uint32_t* __
           if ((same >> k) & 1u) want |= 1u << t;
         }
       }
-      if (slab && (vz + dz < zlo || vz + dz >= zhi)) want = 0;
-      // anchor the window at the row's dx = -1 position (v - 1 may lie in the
-      // previous row / word; the shifted mask never addresses a voxel outside
-      // `want`, which only holds in-grid neighbours)
-      const int base = v - 1 + dy * g.nx + dz * g.nxy;
-      const int f = want ? __ffs(want) - 1 : 0;
-      const int b0 = base + f;
+      if (!want) continue;
+      // anchor the window at the first wanted voxel (always inside the grid)
+      const int f = __ffs(want) - 1;
       const unsigned wv = want >> f;
-      w0[r] = b0 >> 5;
-      const int sh = b0 & 31;
-      shv[r] = (unsigned)sh | ((unsigned)f << 8);
-      lo[r] = wv << sh;
-      hi[r] = sh > 29 ? (wv >> (32 - sh)) : 0u;
-    }
-    // stage 2: precheck loads
-    unsigned clo[9], chi[9];
-#pragma unroll
-    for (int r = 0; r < 9; r++) {
-      clo[r] = lo[r] ? (COH ? __ldcg(bm + w0[r]) : __ldca(bm + w0[r])) : 0u;
-      chi[r] = hi[r] ? (COH ? __ldcg(bm + w0[r] + 1) : __ldca(bm + w0[r] + 1)) : 0u;
-    }
-    // stage 3: atomics where bits are missing
-#pragma unroll
-    for (int r = 0; r < 9; r++) {
-      clo[r] = (lo[r] && (clo[r] & lo[r]) != lo[r]) ? atomicOr(bm + w0[r], lo[r]) : ~0u;
-      chi[r] = (hi[r] && (chi[r] & hi[r]) != hi[r]) ? atomicOr(bm + w0[r] + 1, hi[r]) : ~0u;
-    }
-    // stage 4: newly set bits (and coarse marks)
-#pragma unroll
-    for (int r = 0; r < 9; r++) {
-      const int sh = (int)(shv[r] & 0xff), f = (int)(shv[r] >> 8);
-      unsigned got = ((~clo[r]) & lo[r]) >> sh;
-      got |= sh > 29 ? (((~chi[r]) & hi[r]) << (32 - sh)) : 0u;
-      newmask |= (got << f) << (3 * r);
-      if (cbm) {
-        if (lo[r] && clo[r] == 0u) atomicOr(cbm + (w0[r] >> 10), 1u << ((w0[r] >> 5) & 31));
-        if (hi[r] && chi[r] == 0u) atomicOr(cbm + ((w0[r] + 1) >> 10), 1u << (((w0[r] + 1) >> 5) & 31));
+      const int base = v + (f - 1) + dy * g.nx + dz * g.nxy;
+      const int w0 = base >> 5;
+      const int sh = base & 31;
+      const unsigned lo = wv << sh;                           // bits in word w0
+      const unsigned hi = sh > 29 ? (wv >> (32 - sh)) : 0u;   // spill into w0 + 1
+      unsigned got = 0;  // newly set by this thread, in `wv` coordinates
+      if (lo) {
+        const uint32_t cur = COH ? __ldcg(bm + w0) : __ldca(bm + w0);
+        if ((cur & lo) != lo) {
+          const uint32_t old = atomicOr(bm + w0, lo);
+          got |= ((~old) & lo) >> sh;
+          if (cbm && old == 0u) atomicOr(cbm + (w0 >> 10), 1u << ((w0 >> 5) & 31));  // coarse bit (compact.cuh)
+        }
       }
+      if (hi) {
+        const uint32_t cur = COH ? __ldcg(bm + w0 + 1) : __ldca(bm + w0 + 1);
+        if ((cur & hi) != hi) {
+          const uint32_t old = atomicOr(bm + w0 + 1, hi);
+          got |= ((~old) & hi) << (32 - sh);
+          if (cbm && old == 0u) atomicOr(cbm + ((w0 + 1) >> 10), 1u << (((w0 + 1) >> 5) & 31));
+        }
+      }
+      got <<= f;
+      newmask |= got << j0;
     }
   }
   const int cnt = __popc(newmask);
@@ -250,12 +250,11 @@ __device__ __forceinline__ void mark_and_append(const Geo& g, const uint32_t* __
   __syncthreads();
   int pos = s_cbase + s_wbase[wid] + incl - cnt;
   __syncthreads();  // the next call may overwrite s_wbase / s_cbase
-  if (newmask) {
-    // unrolled over the 27-cube: compile-time (dx, dy, dz) per bit
-#pragma unroll
-    for (int j = 0; j < 27; j++) {
-      if ((newmask >> j) & 1u) next[pos++] = v + (j % 3 - 1) + (j / 3 % 3 - 1) * g.nx + (j / 9 - 1) * g.nxy;
-    }
+  while (newmask) {  // typically 0-3 new neighbours: decode each set bit through a constant table
+    const int j = __ffs(newmask) - 1;
+    newmask &= newmask - 1;
+    const char4 o = c_cube[j];
+    next[pos++] = v + o.x + o.y * g.nx + o.z * g.nxy;
   }
 }
 

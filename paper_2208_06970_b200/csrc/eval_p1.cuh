@@ -48,7 +48,6 @@ __device__ __forceinline__ void p1_tile(const int* __restrict__ list, int n, con
                                                    const double4* __restrict__ site_pos,
                                                    uint32_t* __restrict__ bm,
                                                    Prop* __restrict__ imp, uint8_t* __restrict__ pf) {
-  __shared__ int s_row[26][BLOCK];  // [k][thread]: conflict-free column per thread
   // per-warp queue of speculated rays (no block-wide barrier needed)
   __shared__ int q_v[BLOCK * P1_SPEC], q_s[BLOCK * P1_SPEC];
   __shared__ unsigned char q_ok[BLOCK * P1_SPEC];
@@ -60,7 +59,6 @@ __device__ __forceinline__ void p1_tile(const int* __restrict__ list, int n, con
   if (lane == 0) q_n[wid] = 0;
   const bool active = i < n;
   const int v = active ? __ldg(list + i) : 0;
-  int* row = &s_row[0][threadIdx.x];
   int x = 0, y = 0, z = 0, cv = -3;
   unsigned nbv = 0;  // this voxel's nbm word (neighbour bits + clearance)
   bool ovf = false;  // more distinct neighbour sites than the table holds
@@ -97,7 +95,6 @@ __device__ __forceinline__ void p1_tile(const int* __restrict__ list, int n, con
     for (int q = 0; q < 13; q++) {
       const int k = 13 * h + q;
       const int s = nw[q];
-      row[k * BLOCK] = s;
       // ---- B: distinct-site table; the voxel's own site is not entered: its
       // candidate (orig_d, orig_s, v) is the current state itself
       bool seen = s < 0 || s == orig_s;
@@ -207,7 +204,9 @@ __device__ __forceinline__ void p1_tile(const int* __restrict__ list, int n, con
   }
   if (active) {
     for (int k = kres; k < 26; k++) {
-      const int s = row[k * BLOCK];
+      // the exact fold is rare: re-read the neighbour's site (an L1 hit) instead of keeping rows
+      if (!((nbv >> k) & 1u)) continue;
+      const int s = __ldg(site1 + v + off_dx(k) + off_dy(k) * g.nx + off_dz(k) * g.nxy);
       if (s < 0) continue;
       double d;
       if (s == orig_s) d = orig_d;  // the own site: the very dist3 of the current state
