@@ -1,0 +1,30 @@
+#!/bin/bash
+# Round-2 records: full GPU suite, bench lines (C4 default with both arms; C1-C3, C5), emulated
+# global mode, and the ncu evidence for every kernel at C4 (launch list + full captures).
+mkdir -p gpurun_out/rec
+R=gpurun_out/rec
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,driver_version --format=csv > $R/smi.txt 2>&1
+timeout 2400 python -m pytest tests -m gpu -q -p no:cacheprovider --durations=12 > $R/pytest.log 2>&1; echo "pytest rc=$?"; tail -16 $R/pytest.log
+timeout 1500 python bench.py > $R/bench_c4.log 2>&1; echo "bench c4 rc=$?"; grep '^{' $R/bench_c4.log | tail -1 > $R/bench_c4.json
+timeout 1500 python bench.py --impl reference > $R/ref_c4.log 2>&1; echo "ref c4 rc=$?"; grep '^{' $R/ref_c4.log | tail -1 > $R/ref_c4.json
+for c in c1 c2 c3; do
+  timeout 900 python bench.py --config $c > $R/bench_$c.log 2>&1; echo "bench $c rc=$?"; grep '^{' $R/bench_$c.log | tail -1 > $R/bench_$c.json
+done
+timeout 1500 python bench.py --config c5 --steps 5 --warmup 3 --no-passes > $R/bench_c5.log 2>&1; echo "bench c5 rc=$?"; grep '^{' $R/bench_c5.log | tail -1 > $R/bench_c5.json
+timeout 1500 python bench.py --mode global --emulate-ranks 8 --steps 5 --warmup 3 > $R/global8_c4.log 2>&1; echo "global8 c4 rc=$?"; grep '^{' $R/global8_c4.log | tail -1 > $R/global8_c4.json
+timeout 1500 python bench.py --mode global --emulate-ranks 4 --steps 5 --warmup 3 > $R/global4_c4.log 2>&1; echo "global4 c4 rc=$?"; grep '^{' $R/global4_c4.log | tail -1 > $R/global4_c4.json
+timeout 1500 python bench.py --mode global --emulate-ranks 2 --steps 5 --warmup 3 > $R/global2_c4.log 2>&1; echo "global2 c4 rc=$?"; grep '^{' $R/global2_c4.log | tail -1 > $R/global2_c4.json
+# ncu evidence at C4: every launch of one pass (graph rounds replaced by host rounds, whose kernel nodes ncu can profile)
+timeout 600 python tools/profile_kernels.py --config c4 --host-rounds > $R/prof_plain.log 2>&1 && \
+timeout 900 ncu --nvtx --nvtx-include "profile/" --metrics gpu__time_duration.sum --clock-control none --csv \
+   --log-file $R/c4_launches.csv python tools/profile_kernels.py --config c4 --host-rounds > $R/ncu_launch.log 2>&1; echo "ncu launches rc=$?"
+timeout 1500 ncu --nvtx --nvtx-include "profile/" --set full --clock-control none --import-source on \
+   -k regex:"k_isobands|k_ccl_|k_agg_|k_vote|k_move_sites|k_fill|k_state|k_site1_to_state|k_seed_groups|k_phase2_copy" \
+   -o $R/c4_other python tools/profile_kernels.py --config c4 --host-rounds > $R/ncu_other.log 2>&1; echo "ncu other rc=$?"
+timeout 1500 ncu --nvtx --nvtx-include "profile/" --set full --clock-control none --import-source on \
+   -k regex:"k_eval_p1|k_commit" -s 6 -c 6 \
+   -o $R/c4_p1 python tools/profile_kernels.py --config c4 --host-rounds > $R/ncu_p1.log 2>&1; echo "ncu p1 rc=$?"
+timeout 1500 ncu --nvtx --nvtx-include "profile/" --set full --clock-control none --import-source on \
+   -k regex:"k_eval_p2" -c 4 \
+   -o $R/c4_p2 python tools/profile_kernels.py --config c4 --host-rounds > $R/ncu_p2.log 2>&1; echo "ncu p2 rc=$?"
+ls -la $R
