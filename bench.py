@@ -462,7 +462,7 @@ def run_global(args, cfg, world, rank, local):
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
-    gc.timing = emulate
+    gc.set_timing(emulate)
     gc.rank_ms()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(int(os.environ.get("LRCVT_BENCH_DEVICE", local))) as clk:
@@ -491,8 +491,9 @@ def run_global(args, cfg, world, rank, local):
                 "slowest_rank_ms_per_step": slow,
                 "projected_value": grid.size / (slow / 1e3),
                 "note": "all slab ranks on ONE GPU one after another; each rank's own kernels timed with CUDA "
-                        "events (collectives are host list operations here, so NVLink transfer time is not "
-                        "included); `value` above is the serial sum over ranks"}
+                        "events (the host round trips of the per-round count reads excluded; collectives are host "
+                        "list operations here, so NVLink transfer time is not included); `value` above is the "
+                        "serial sum over ranks"}
         print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()

@@ -256,6 +256,10 @@ int lrcvt_mg_vote_carry(lrcvt_plan *plan, int64_t n_sites, const int32_t *d_box,
 int lrcvt_mg_move(lrcvt_plan *plan, int64_t n_sites, const double *d_site_pos, const int32_t *d_site_comp,
                   const double *d_sums, double backoff, double *d_new_pos, double *d_disp,
                   int64_t *empty_regions, void *stream);
+/* device milliseconds of this plan's synchronising mg steps (begin, phase2,
+ * eval, commit, finish, move) since the last call: CUDA events around their
+ * kernels, the host round trip of each step excluded. enable = 0 stops. */
+int lrcvt_mg_timing(lrcvt_plan *plan, int32_t enable, double *ms);
 /* CUDA IPC of a base device allocation (64-byte handle) */
 int lrcvt_ipc_export(const void *d_ptr, uint8_t *handle64);
 int lrcvt_ipc_open(const uint8_t *handle64, void **d_ptr);

@@ -90,6 +90,7 @@ SIGNATURES = {
     "lrcvt_mg_vote_carry": (c_int, [c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "lrcvt_mg_move": (c_int, [c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_double, c_void_p, c_void_p,
                               POINTER(c_int64), c_void_p]),
+    "lrcvt_mg_timing": (c_int, [c_void_p, c_int32, POINTER(c_double)]),
     "lrcvt_ipc_export": (c_int, [c_void_p, c_void_p]),
     "lrcvt_ipc_open": (c_int, [c_void_p, POINTER(c_void_p)]),
     "lrcvt_ipc_close": (c_int, [c_void_p]),

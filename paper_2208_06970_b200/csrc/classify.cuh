@@ -35,6 +35,8 @@ struct RoundCtl {
   int* cur;          // this round's worklist
   int* nxt;          // next round's worklist (written by k_commit)
   int* stash;        // the list buffer parked during a verification sweep
+  int* ro;           // a read-only list (the eligible list) while it serves as `cur`
+  int* spare;        // the free list buffer that replaces `ro` when the round ends
   int2* ss;          // per-voxel (site_of, src) of the classify in flight
   double* dist;      // per-voxel distance
   int* site1;        // phase 1 only: per-voxel LOS site (site if src == self, else -1); null in phase 2
@@ -302,7 +304,7 @@ __device__ __forceinline__ void round_end(RoundCtl* ctl, int* counters, const cu
   ctl->commits += n_imp;
   int* t = ctl->cur;
   ctl->cur = ctl->nxt;
-  ctl->nxt = t;
+  ctl->nxt = t == ctl->ro ? ctl->spare : t;  // the eligible list is never written
   ctl->n_cur = n_next;
   ctl->tile_next = 0;
   counters[C_NIMP] = 0;
@@ -329,6 +331,8 @@ __global__ void k_phase1_start(RoundCtl* ctl, int* counters, int* first, int* se
   ctl->cur = first;
   ctl->nxt = second;
   ctl->stash = nullptr;
+  ctl->ro = nullptr;
+  ctl->spare = nullptr;
   ctl->n_cur = counters[C_NNEXT];
   ctl->rounds = ctl->evals = ctl->commits = ctl->rounds_p1 = 0;
   ctl->rounds_small = ctl->small_launches = 0;
@@ -352,7 +356,11 @@ __global__ void k_site1_to_state(Geo g, const int* __restrict__ site1, const dou
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
     const int v = list ? __ldg(list + i) : (int)(v0 + i);
     const int s = __ldcs(site1 + v);
-    if (s < 0) continue;  // still the fill values (-1, -1) / inf
+    if (s < 0) {  // unassigned: the fill values (phase 1 never touches ss / dist)
+      __stcs(ss + v, make_int2(LRCVT_NONE, LRCVT_NONE));
+      __stcs(dist + v, __longlong_as_double(0x7ff0000000000000LL));
+      continue;
+    }
     int x, y, z;
     coords(g, v, x, y, z);
     const double4 p = ld_d4(site_pos + s);
@@ -377,18 +385,19 @@ __global__ void k_fill_list(const int* __restrict__ list, const int* __restrict_
   }
 }
 
-__global__ void k_phase2_copy(const int* __restrict__ eligible, const int* __restrict__ n_el,
+// the first phase-2 round evaluates the eligible list in place (read-only:
+// the round end hands the parked list buffer to the next commit instead)
+__global__ void k_phase2_copy(int* __restrict__ eligible, const int* __restrict__ n_el,
                               RoundCtl* ctl, const int* __restrict__ counters) {
   // bad sites (tessellation.py:139-140 raises before any relaxation): no work
   const int n = counters[C_BAD] ? 0 : *n_el;
-  int* dst = ctl->cur;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) dst[i] = eligible[i];
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    ctl->rounds_p1 = ctl->rounds;
-    ctl->site1 = nullptr;  // phase 2 commits non-LOS states; its kernels read ss
-    ctl->n_cur = n;
-    ctl->tile_next = 0;
-  }
+  ctl->spare = ctl->cur;
+  ctl->cur = eligible;
+  ctl->ro = eligible;
+  ctl->rounds_p1 = ctl->rounds;
+  ctl->site1 = nullptr;  // phase 2 commits non-LOS states; its kernels read ss
+  ctl->n_cur = n;
+  ctl->tile_next = 0;
 }
 
 // verification sweep over the eligible list (tessellation.py:177-189): the

@@ -26,6 +26,7 @@ struct Geo {
   double len_cls[8];       // |offset| in world units by class (exact when dyadic)
   float isx, isy, isz;     // 1 / spacing in float (clearance tests only)
   double ix, iy, iz;       // 1 / spacing (exact reciprocals of powers of two when dyadic)
+  int pack10;              // every axis <= 1024: coordinates pack into 10-bit fields
   int off_d[26];           // flat index delta of offset k
 };
 

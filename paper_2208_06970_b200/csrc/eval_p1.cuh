@@ -69,17 +69,20 @@ __device__ __forceinline__ void p1_tile(const int* __restrict__ list, int n, con
   for (int j = 0; j < P1_TAB; j++) { ts[j] = -1; td[j] = 0.0; }
   double best_d = 0.0, orig_d = 0.0;
   int best_s = -1, best_src = -1, orig_s = -1;
+  unsigned same = 0;  // inactive lanes gather nothing (the warp stays converged for the votes below)
   if (active) {
     bm[v >> 5] = 0u;  // consume this round's frontier word
     coords(g, v, x, y, z);
     cv = __ldg(comp + v);
     px = centre1(x, g.sx); py = centre1(y, g.sy); pz = centre1(z, g.sz);
-    const unsigned same = __ldg(nbm + v);
+    same = __ldg(nbm + v);
     nbv = same;
-    // ---- A
-    // phase 1: site1[w] is site_of[w] when src[w] == w (every phase-1 assignment), else -1
     // phase-1 states are LOS (src == v) and their distance is |c_v - p_site|
     orig_s = __ldg(site1 + v);
+  }
+  {
+    // ---- A
+    // phase 1: site1[w] is site_of[w] when src[w] == w (every phase-1 assignment), else -1
     // two batches of 13 loads in flight (bounds the live registers of the
     // big-round variant, whose 64-register budget otherwise spills)
 #pragma unroll
@@ -100,14 +103,19 @@ __device__ __forceinline__ void p1_tile(const int* __restrict__ list, int n, con
       bool seen = s < 0 || s == orig_s;
 #pragma unroll
       for (int j = 0; j < P1_TAB; j++) seen |= ts[j] == s;
-      // branch-free insert at the front (the table is a set); a fifth site overflows
+      // branch-free insert at the front (the table is a set); a fifth site
+      // overflows; the shift runs only when some lane of the warp inserts
       const bool ins = !seen;
       ovf |= ins && ts[P1_TAB - 1] >= 0;
+      if (__any_sync(0xffffffffu, ins)) {
 #pragma unroll
-      for (int j = P1_TAB - 1; j > 0; j--) ts[j] = ins ? ts[j - 1] : ts[j];
-      ts[0] = ins ? s : ts[0];
+        for (int j = P1_TAB - 1; j > 0; j--) ts[j] = ins ? ts[j - 1] : ts[j];
+        ts[0] = ins ? s : ts[0];
+      }
     }
     }
+  }
+  if (active) {
     best_s = orig_s; best_src = v;
     if (best_s >= 0) {
       const double4 sp = ld_d4(site_pos + best_s);

@@ -167,6 +167,7 @@ Geo make_geo(int64_t nx, int64_t ny, int64_t nz, double sx, double sy, double sz
   g.inv_nx = 1.0 / (double)nx;
   g.inv_nxy = 1.0 / (double)(nx * ny);
   g.dyadic = is_pow2(sx) && is_pow2(sy) && is_pow2(sz);
+  g.pack10 = nx <= 1024 && ny <= 1024 && nz <= 1024;
   g.ix = 1.0 / sx;
   g.iy = 1.0 / sy;
   g.iz = 1.0 / sz;
@@ -233,6 +234,9 @@ struct lrcvt_plan {
   int mg_world = 1;
   Prop* mg_lo = nullptr;          // boundary-plane proposals for rank - 1 / rank + 1
   Prop* mg_hi = nullptr;
+  bool mg_timing = false;         // device time of the syncing mg steps (lrcvt_mg_timing)
+  cudaEvent_t mg_ev[2] = {nullptr, nullptr};
+  double mg_ms = 0.0;
   int* counters = nullptr;
   int* h_counters = nullptr;  // pinned
   uint8_t* has_site = nullptr;
@@ -331,7 +335,7 @@ int note_eval(lrcvt_plan* p, int64_t items, bool phase2, int64_t n_imp) {
 }
 
 int sync_counters(lrcvt_plan* p, cudaStream_t st, int n = C_NCOUNTERS) {
-  CK(cudaMemcpyAsync(p->h_counters, p->counters, sizeof(int) * n, cudaMemcpyDeviceToHost, st));
+  if (n > 0) CK(cudaMemcpyAsync(p->h_counters, p->counters, sizeof(int) * n, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   return 0;
 }
@@ -903,6 +907,8 @@ int lrcvt_plan_destroy(lrcvt_plan* p) {
   if (p->ev0) cudaEventDestroy(p->ev0);
   if (p->ev1) cudaEventDestroy(p->ev1);
   if (p->ev2) cudaEventDestroy(p->ev2);
+  for (cudaEvent_t e : p->mg_ev)
+    if (e) cudaEventDestroy(e);
   delete p;
   return 0;
 }
@@ -989,7 +995,9 @@ int lrcvt_classify(lrcvt_plan* p, int64_t n_sites, const double* d_site_pos,
     k_fill_state<<<grid_for(g.n, 256, 148 * 32), 256, 0, st>>>(ss, d_dist, g.n);
     CKL("k_fill_state"); LAUNCHED(1);
   }
-  k_fill_list<<<el_grid, 256, 0, st>>>(p->eligible, p->d_nel, fast ? ss : nullptr, d_dist, p->site1);
+  // site1 only: every eligible voxel's (site_of, src) / dist is written by k_site1_to_state when phase 2
+  // starts (phase 1 reads and writes site1 alone; the seeds' ss / dist entries are rewritten identically)
+  k_fill_list<<<el_grid, 256, 0, st>>>(p->eligible, p->d_nel, nullptr, d_dist, p->site1);
   CKL("k_fill_list"); LAUNCHED(1);
   p->last_ss = ss;
   p->last_dist = d_dist;
@@ -1017,7 +1025,7 @@ int lrcvt_classify(lrcvt_plan* p, int64_t n_sites, const double* d_site_pos,
   // phase 2 (tessellation.py:161-189): rounds from the eligible list, verification sweeps
   k_site1_to_state<<<el_grid, 256, 0, st>>>(g, p->site1, p->site_pos, ss, d_dist, p->eligible, p->d_nel, 0, 0);
   CKL("k_site1_to_state"); LAUNCHED(1);
-  k_phase2_copy<<<148 * 4, 256, 0, st>>>(p->eligible, p->d_nel, p->ctl, p->counters);
+  k_phase2_copy<<<1, 1, 0, st>>>(p->eligible, p->d_nel, p->ctl, p->counters);
   CKL("k_phase2_copy"); LAUNCHED(1);
   const int var2 = g.dyadic ? 1 : 2;
   for (;;) {
@@ -1437,7 +1445,7 @@ __global__ void k_mg_round_end(RoundCtl* ctl, int* counters, int sweep) {
   } else {
     int* t = ctl->cur;
     ctl->cur = ctl->nxt;
-    ctl->nxt = t;
+    ctl->nxt = t == ctl->ro ? ctl->spare : t;
   }
   ctl->n_cur = n_next;
   counters[C_NIMP] = 0;
@@ -1474,8 +1482,19 @@ __global__ void __launch_bounds__(128) k_mg_boundary(const RoundCtl* __restrict_
   if ((threadIdx.x & 31) == 0 && mine) atomicAdd(counters + C_NIMP, mine);
 }
 
-int mg_require(lrcvt_plan* p, const char* what) {
-  if (!p) return set_error(LRCVT_E_ARG, what);
+// device time of an mg step that ends in a host synchronisation: events
+// around its kernels (the host round trip of the sync is not counted)
+void mg_t0(lrcvt_plan* p, cudaStream_t st) {
+  if (p->mg_timing) cudaEventRecord(p->mg_ev[0], st);
+}
+int mg_sync(lrcvt_plan* p, cudaStream_t st, int n) {
+  if (p->mg_timing) CK(cudaEventRecord(p->mg_ev[1], st));
+  CKR(sync_counters(p, st, n));
+  if (p->mg_timing) {
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, p->mg_ev[0], p->mg_ev[1]));
+    p->mg_ms += ms;
+  }
   return 0;
 }
 
@@ -1534,6 +1553,7 @@ int lrcvt_mg_begin(lrcvt_plan* p, int64_t n_sites, const double* d_site_pos, con
   int2* ss = reinterpret_cast<int2*>(d_site_src);
   p->mg_ss = ss;
   p->mg_dist = d_dist;
+  mg_t0(p, st);
   CK(cudaMemsetAsync(p->counters, 0, sizeof(int) * C_NCOUNTERS, st));
   // own-slab eligible list (tessellation.py:161-164 restricted to [zlo, zhi))
   if (prepare_eligible(p, S, d_site_comp, st)) return LRCVT_E_CUDA;
@@ -1559,7 +1579,7 @@ int lrcvt_mg_begin(lrcvt_plan* p, int64_t n_sites, const double* d_site_pos, con
   k_phase1_start<<<1, 1, 0, st>>>(p->ctl, p->counters, p->list_a, p->list_b, ss, d_dist, p->site1, 0);
   CKL("k_phase1_start");
   CK(cudaMemcpyAsync(p->h_ctl, p->ctl, sizeof(RoundCtl), cudaMemcpyDeviceToHost, st));
-  CKR(sync_counters(p, st, C_NCOUNTERS));
+  CKR(mg_sync(p, st, C_NCOUNTERS));
   if (p->h_counters[C_BAD]) return p->h_counters[C_BAD];
   p->h_ncur = p->h_ctl->n_cur;
   *n_frontier = p->h_ncur;
@@ -1571,14 +1591,15 @@ int lrcvt_mg_phase2(lrcvt_plan* p, int64_t n_sites, const int32_t* d_site_comp, 
   cudaStream_t st = (cudaStream_t)stream;
   const Geo& g = p->g;
   // phase-1 LOS states -> (site, src) / dist on the own slab and its halo planes (site1 is current there)
+  mg_t0(p, st);
   const int64_t z0 = p->zlo > 0 ? p->zlo - 1 : 0, z1 = p->zhi < g.nz ? p->zhi + 1 : g.nz;
   k_site1_to_state<<<grid_for((z1 - z0) * g.nxy, 256, 148 * 16), 256, 0, st>>>(
       g, p->site1, p->site_pos, p->mg_ss, p->mg_dist, nullptr, nullptr, z0 * g.nxy, z1 * g.nxy);
   CKL("k_site1_to_state");
-  k_phase2_copy<<<148 * 4, 256, 0, st>>>(p->eligible, p->d_nel, p->ctl, p->counters);
+  k_phase2_copy<<<1, 1, 0, st>>>(p->eligible, p->d_nel, p->ctl, p->counters);
   CKL("k_phase2_copy");
   CK(cudaMemcpyAsync(p->h_counters + 7, p->d_nel, sizeof(int), cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
+  CKR(mg_sync(p, st, 1));
   p->n_eligible = p->h_counters[7];
   p->h_ncur = (int)p->n_eligible;
   *n_frontier = p->h_ncur;
@@ -1591,6 +1612,7 @@ int lrcvt_mg_eval(lrcvt_plan* p, int32_t phase, int32_t sweep, int64_t* n_evalua
     return set_error(LRCVT_E_ARG, "lrcvt_mg_eval");
   cudaStream_t st = (cudaStream_t)stream;
   int n = p->h_ncur;
+  mg_t0(p, st);
   if (sweep) {
     k_sweep_start<<<1, 1, 0, st>>>(p->ctl, p->eligible, p->d_nel, p->counters);
     CKL("k_sweep_start");
@@ -1611,7 +1633,7 @@ int lrcvt_mg_eval(lrcvt_plan* p, int32_t phase, int32_t sweep, int64_t* n_evalua
                                                               p->counters);
     CKL("k_mg_boundary");
   }
-  CKR(sync_counters(p, st, C_HI + 1));
+  CKR(mg_sync(p, st, C_HI + 1));
   *n_evaluated = n;
   *n_prop = p->h_counters[C_NIMP];
   *n_lo = p->h_counters[C_LO];
@@ -1628,14 +1650,16 @@ int lrcvt_mg_commit(lrcvt_plan* p, const void* d_halo, int64_t n_halo, int32_t s
                     void* stream) {
   if (!p || n_halo < 0 || (n_halo > 0 && !d_halo) || !n_next) return set_error(LRCVT_E_ARG, "lrcvt_mg_commit");
   cudaStream_t st = (cudaStream_t)stream;
+  mg_t0(p, st);
   CK(cudaMemsetAsync(p->counters, 0, sizeof(int) * 2, st));
   const int n = sweep ? (int)p->n_eligible : p->h_ncur;
   if (n > 0) CKR(launch_commit_kernel(p, n, st));  // own sparse proposals
   if (n_halo > 0) CKR(launch_commit_kernel(p, n_halo, st, (const Prop*)d_halo, n_halo));  // halo planes
-  CKR(sync_counters(p, st, 2));
-  const int nn = p->h_counters[C_NNEXT];
+  // the host copy of the counters is taken before the round end resets them
+  CK(cudaMemcpyAsync(p->h_counters, p->counters, sizeof(int) * 2, cudaMemcpyDeviceToHost, st));
   k_mg_round_end<<<1, 1, 0, st>>>(p->ctl, p->counters, sweep);
-  CKL("k_mg_round_end");
+  CKR(mg_sync(p, st, 0));
+  const int nn = p->h_counters[C_NNEXT];
   p->h_ncur = nn;
   *n_next = nn;
   return 0;
@@ -1645,12 +1669,13 @@ int lrcvt_mg_finish(lrcvt_plan* p, const int32_t* d_site_src, uint8_t* d_state, 
   if (!p || !d_site_src || !assigned) return set_error(LRCVT_E_ARG, "lrcvt_mg_finish");
   cudaStream_t st = (cudaStream_t)stream;
   const Geo& g = p->g;
+  mg_t0(p, st);
   CK(cudaMemsetAsync(p->counters + C_ASSIGNED, 0, sizeof(int), st));
   const int64_t v0 = (int64_t)p->zlo * g.nxy, v1 = (int64_t)(p->zhi < g.nz ? p->zhi : g.nz) * g.nxy;
   k_state<<<grid_for(v1 - v0, 256, 148 * 16), 256, 0, st>>>(reinterpret_cast<const int2*>(d_site_src), nullptr,
                                                              nullptr, v0, v1, d_state, p->counters);
   CKL("k_state");
-  CKR(sync_counters(p, st, C_ASSIGNED + 1));
+  CKR(mg_sync(p, st, C_ASSIGNED + 1));
   *assigned = p->h_counters[C_ASSIGNED];
   return 0;
 }
@@ -1751,6 +1776,7 @@ int lrcvt_mg_move(lrcvt_plan* p, int64_t n_sites, const double* d_site_pos, cons
     return set_error(LRCVT_E_ARG, "lrcvt_mg_move");
   cudaStream_t st = (cudaStream_t)stream;
   const int S = (int)n_sites;
+  mg_t0(p, st);
   k_pack_sites<<<grid_for(S, 256), 256, 0, st>>>(d_site_pos, S, p->site_pos);
   CKL("k_pack_sites");
   CK(cudaMemsetAsync(p->counters + C_BAD, 0, sizeof(int), st));
@@ -1759,8 +1785,20 @@ int lrcvt_mg_move(lrcvt_plan* p, int64_t n_sites, const double* d_site_pos, cons
   CKL("k_move_sites");
   k_unpack_sites<<<grid_for(S, 256), 256, 0, st>>>(p->new_pos, S, d_new_pos);
   CKL("k_unpack_sites");
-  CKR(sync_counters(p, st, C_BAD + 1));
+  CKR(mg_sync(p, st, C_BAD + 1));
   if (empty_regions) *empty_regions = p->h_counters[C_BAD];
+  return 0;
+}
+
+int lrcvt_mg_timing(lrcvt_plan* p, int32_t enable, double* ms) {
+  if (!p) return set_error(LRCVT_E_ARG, "lrcvt_mg_timing");
+  if (ms) *ms = p->mg_ms;
+  p->mg_ms = 0.0;
+  if (enable && !p->mg_ev[0]) {
+    CK(cudaEventCreate(&p->mg_ev[0]));
+    CK(cudaEventCreate(&p->mg_ev[1]));
+  }
+  p->mg_timing = enable != 0;
   return 0;
 }
 

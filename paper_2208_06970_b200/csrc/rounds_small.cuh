@@ -88,7 +88,7 @@ __global__ void __launch_bounds__(32 * EW_WARPS) k_rounds_small(RoundCtl* __rest
       vctl->commits = vctl->commits + n_imp_all;
       int* t = vctl->cur;
       vctl->cur = vctl->nxt;
-      vctl->nxt = t;
+      vctl->nxt = t == vctl->ro ? vctl->spare : t;
       vctl->n_cur = n_next;
       vctl->tile_next = 0;
       vc[C_NIMP] = 0;

@@ -139,6 +139,18 @@ __device__ __forceinline__ double4 vote_term(const Geo& g, int u, double w) {
                       __dmul_rn(w, centre1(z, g.sz)));
 }
 
+// (x, y, z) of voxel u packed 10 bits each (Geo::pack10: every axis <= 1024)
+__device__ __forceinline__ int phi_pack(const Geo& g, int u) {
+  int x, y, z;
+  coords(g, u, x, y, z);
+  return x | (y << 10) | (z << 20);
+}
+__device__ __forceinline__ double4 vote_term_packed(const Geo& g, int p, double w) {
+  const int x = p & 1023, y = (p >> 10) & 1023, z = p >> 20;
+  return make_double4(w, __dmul_rn(w, centre1(x, g.sx)), __dmul_rn(w, centre1(y, g.sy)),
+                      __dmul_rn(w, centre1(z, g.sz)));
+}
+
 // ordered path, step 3: one warp per site. A three-stage software pipeline
 // per lane -- (phi, v) pairs two batches ahead, the weight one batch ahead,
 // the term for the batch being summed -- keeps loads off the critical path;
@@ -212,7 +224,9 @@ __global__ void __launch_bounds__(256) k_vote_prep(const int* __restrict__ list,
         u = phi_chase_pv<MG>(pv, ss, v, a);
         coords(g, v, x, y, z);
       }
-      sp[v] = make_int2(s, u);
+      // phi as packed coordinates when every axis fits 10 bits (saves the
+      // scan a flat-index decode per term), else the flat index
+      sp[v] = make_int2(s, u >= 0 && g.pack10 ? phi_pack(g, u) : u);
     }
     const unsigned grp = __match_any_sync(0xffffffffu, s);
     const int x0 = __reduce_min_sync(grp, x), x1 = __reduce_max_sync(grp, x);
@@ -301,7 +315,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_vote_scan(const int2* __restrict
         const unsigned m = __ballot_sync(0xffffffffu, mine);
         if (m) {
           if (mine) {
-            const double4 t = vote_term(g, u, wt);
+            const double4 t = g.pack10 ? vote_term_packed(g, u, wt) : vote_term(g, u, wt);
             const int slot = __popc(m & ((1u << lane) - 1u));
             buf[wid][slot][0] = t.x; buf[wid][slot][1] = t.y; buf[wid][slot][2] = t.z; buf[wid][slot][3] = t.w;
           }

@@ -273,9 +273,17 @@ class GlobalClassifier:
     def _st(self):
         return _lib.stream_handle(self.torch)
 
-    def _t(self, r, fn):
-        """run fn() for rank r, bracketed by CUDA events when timing"""
-        if not self.timing:
+    def set_timing(self, on: bool):
+        """per-rank device time: CUDA events around each rank's non-synchronising calls here, and the
+        library's own events around the kernels of its synchronising steps (lrcvt_mg_timing: a host
+        round trip inside a step is not device work)"""
+        self.timing = on
+        for eng in self.engines.values():
+            _lib.check(self.L.lrcvt_mg_timing(eng.plan, 1 if on else 0, None), "lrcvt_mg_timing")
+
+    def _t(self, r, fn, synced=False):
+        """run fn() for rank r, bracketed by CUDA events when timing (synced steps are timed by the library)"""
+        if not self.timing or synced:
             return fn()
         torch = self.torch
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -291,6 +299,10 @@ class GlobalClassifier:
         self.torch.cuda.synchronize()
         out = {r: sum(a.elapsed_time(b) for a, b in evs) for r, evs in self._ev.items()}
         self._ev = {r: [] for r in self.engines}
+        for r, eng in self.engines.items():
+            ms = ctypes.c_double()
+            _lib.check(self.L.lrcvt_mg_timing(eng.plan, 1 if self.timing else 0, ctypes.byref(ms)), "mg timing")
+            out[r] += ms.value
         return out
 
     def _round(self, phase: int, sweep: int, stats: dict) -> int:
@@ -301,7 +313,7 @@ class GlobalClassifier:
         for r, eng in self.engines.items():
             ne, npr, nlo, nhi = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
             self._t(r, lambda: _lib.check(L.lrcvt_mg_eval(eng.plan, phase, sweep, ctypes.byref(ne), ctypes.byref(npr),
-                                                          ctypes.byref(nlo), ctypes.byref(nhi), st), "lrcvt_mg_eval"))
+                                                          ctypes.byref(nlo), ctypes.byref(nhi), st), "lrcvt_mg_eval"), synced=True)
             counts[r] = [int(ne.value), int(npr.value)]
             lo[r] = self._bytes(L.lrcvt_mg_boundary(eng.plan, 0), int(nlo.value))
             hi[r] = self._bytes(L.lrcvt_mg_boundary(eng.plan, 1), int(nhi.value))
@@ -312,7 +324,7 @@ class GlobalClassifier:
             nn = ctypes.c_int64()
             self._t(r, lambda: _lib.check(L.lrcvt_mg_commit(eng.plan, h.data_ptr() if h.numel() else None,
                                                             h.numel() // PROP_BYTES, sweep, ctypes.byref(nn), st),
-                                          "lrcvt_mg_commit"))
+                                          "lrcvt_mg_commit"), synced=True)
             nexts[r] = [int(nn.value)] + counts[r]
         tot = self.coll.sum_ints(nexts)
         self._frontier = tot[0]
@@ -346,7 +358,7 @@ class GlobalClassifier:
             rc = self._t(r, lambda: _lib.check(L.lrcvt_mg_begin(eng.plan, S, site_pos.data_ptr(),
                                                                 site_comp.data_ptr(), eng.ss.data_ptr(),
                                                                 eng.dist.data_ptr(), ctypes.byref(nf), st),
-                                               "lrcvt_mg_begin"))
+                                               "lrcvt_mg_begin"), synced=True)
             bad = max(bad, rc)
             front[r] = [int(nf.value)]
         if bad > 0:
@@ -357,7 +369,7 @@ class GlobalClassifier:
         for r, eng in self.engines.items():
             nf = ctypes.c_int64()
             self._t(r, lambda: _lib.check(L.lrcvt_mg_phase2(eng.plan, S, site_comp.data_ptr(), ctypes.byref(nf),
-                                                            st), "phase2"))
+                                                            st), "phase2"), synced=True)
             front[r] = [int(nf.value)]
         self._frontier = self.coll.sum_ints(front)[0]
         while True:  # phase 2 + verification sweeps (tessellation.py:170-189)
@@ -369,7 +381,7 @@ class GlobalClassifier:
         for r, eng in self.engines.items():
             a = ctypes.c_int64()
             self._t(r, lambda: _lib.check(L.lrcvt_mg_finish(eng.plan, eng.ss.data_ptr(), eng.state.data_ptr(),
-                                                            ctypes.byref(a), st), "lrcvt_mg_finish"))
+                                                            ctypes.byref(a), st), "lrcvt_mg_finish"), synced=True)
             assigned[r] = [int(a.value)]
         stats["assigned"] = self.coll.sum_ints(assigned)[0]
         return stats
@@ -432,7 +444,7 @@ class GlobalClassifier:
             np_, dp_ = new_pos, disp
             self._t(r, lambda: _lib.check(L.lrcvt_mg_move(eng.plan, S, site_pos.data_ptr(), site_comp.data_ptr(),
                                                           sums.data_ptr(), float(backoff), np_.data_ptr(),
-                                                          dp_.data_ptr(), ctypes.byref(empty), st), "lrcvt_mg_move"))
+                                                          dp_.data_ptr(), ctypes.byref(empty), st), "lrcvt_mg_move"), synced=True)
         return new_pos, disp, int(empty.value)
 
     def own_slab(self, r):
