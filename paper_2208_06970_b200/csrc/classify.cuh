@@ -159,9 +159,11 @@ __constant__ char4 c_cube[27] = {
 // 3-bit mask (a stale cached word only under-reports set bits, which merely
 // sends that row to the atomic). newmask uses the 27-cube index
 // j = (dz+1)*9 + (dy+1)*3 + (dx+1). With cbm, the word turned non-empty
-// also marks its coarse bit (compact.cuh). (Staging all 9 rows' loads, then
-// all atomics, measured 45% slower: more registers, fewer warps, and the
-// prechecks no longer see the bits the earlier rows' atomics set.)
+// also marks its coarse bit (compact.cuh). Measured alternatives, both
+// slower at 512^3: staging all 9 rows' loads, then all atomics (+45%: more
+// registers, and the prechecks no longer see the bits the earlier rows'
+// atomics set); grouping the lanes that want the same word (match_any) and
+// setting each group's OR with one atomic (6x: match_any per row dominates).
 template <bool COH = false>
 __device__ __forceinline__ void mark_and_append(const Geo& g, const uint32_t* __restrict__ nbm,
                                                 bool active, int v, bool self,

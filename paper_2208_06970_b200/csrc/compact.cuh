@@ -50,10 +50,7 @@ __device__ __forceinline__ void commit_one(const Prop& p, int2* __restrict__ ss,
   }
 }
 
-#ifndef CM_MINB
-#define CM_MINB 8  // CTAs per SM the commit's register budget is sized for
-#endif
-__global__ void __launch_bounds__(CM_THREADS, CM_MINB) k_commit(const Prop* __restrict__ imp, const uint8_t* __restrict__ pf,
+__global__ void __launch_bounds__(CM_THREADS, 8) k_commit(const Prop* __restrict__ imp, const uint8_t* __restrict__ pf,
                                                        int n_props, int* __restrict__ counters,
                                                        RoundCtl* __restrict__ ctl, Geo g,
                                                        const uint32_t* __restrict__ nbm, uint32_t* __restrict__ bm,

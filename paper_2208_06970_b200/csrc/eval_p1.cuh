@@ -103,15 +103,12 @@ __device__ __forceinline__ void p1_tile(const int* __restrict__ list, int n, con
       bool seen = s < 0 || s == orig_s;
 #pragma unroll
       for (int j = 0; j < P1_TAB; j++) seen |= ts[j] == s;
-      // branch-free insert at the front (the table is a set); a fifth site
-      // overflows; the shift runs only when some lane of the warp inserts
+      // branch-free insert at the front (the table is a set); a fifth site overflows
       const bool ins = !seen;
       ovf |= ins && ts[P1_TAB - 1] >= 0;
-      if (__any_sync(0xffffffffu, ins)) {
 #pragma unroll
-        for (int j = P1_TAB - 1; j > 0; j--) ts[j] = ins ? ts[j - 1] : ts[j];
-        ts[0] = ins ? s : ts[0];
-      }
+      for (int j = P1_TAB - 1; j > 0; j--) ts[j] = ins ? ts[j - 1] : ts[j];
+      ts[0] = ins ? s : ts[0];
     }
     }
   }

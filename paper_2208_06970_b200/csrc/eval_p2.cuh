@@ -112,31 +112,22 @@ __device__ __forceinline__ void p2_tile(const int* __restrict__ list, int n, con
         // ---- B: distinct LOS sites and distinct shortcut nodes, branch-free set
         // inserts (at the front; entries beyond the table size are looked up on
         // the fly by the fold, and void the certificate)
-        // (inserts are rare once neighbours share sites and nodes: the shifts
-        // run only when some lane of the warp inserts -- a warp-uniform branch)
         bool seen = u != -2 || s == own_los;
 #pragma unroll
         for (int j = 0; j < P2_STAB; j++) seen |= ts[j] == s;
         const bool ins = !seen && ts[P2_STAB - 1] < 0;
         cert = cert && (seen || ins);
-        if (__any_sync(0xffffffffu, ins)) {
 #pragma unroll
-          for (int j = P2_STAB - 1; j > 0; j--) ts[j] = ins ? ts[j - 1] : ts[j];
-          ts[0] = ins ? s : ts[0];
-        }
+        for (int j = P2_STAB - 1; j > 0; j--) ts[j] = ins ? ts[j - 1] : ts[j];
+        ts[0] = ins ? s : ts[0];
         bool useen = u < 0;
-        const bool any_u = __any_sync(0xffffffffu, !useen);
-        if (any_u) {
 #pragma unroll
-          for (int j = 0; j < P2_NTAB; j++) useen |= tu[j] == u;
-        }
+        for (int j = 0; j < P2_NTAB; j++) useen |= tu[j] == u;
         const bool uins = !useen && tu[P2_NTAB - 1] < 0;
         cert = cert && (useen || uins);
-        if (__any_sync(0xffffffffu, uins)) {
 #pragma unroll
-          for (int j = P2_NTAB - 1; j > 0; j--) tu[j] = uins ? tu[j - 1] : tu[j];
-          tu[0] = uins ? u : tu[0];
-        }
+        for (int j = P2_NTAB - 1; j > 0; j--) tu[j] = uins ? tu[j - 1] : tu[j];
+        tu[0] = uins ? u : tu[0];
       }
     }
   }

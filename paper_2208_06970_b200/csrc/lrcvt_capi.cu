@@ -440,8 +440,8 @@ int launch_commit_kernel(lrcvt_plan* p, int64_t items, cudaStream_t st, const Pr
   if (blocks < 1) blocks = 1;
   if (blocks > p->commit_blocks) blocks = p->commit_blocks;  // grid-stride, one resident wave at most
   k_commit<<<(int)blocks, CM_THREADS, 0, st>>>(props ? props : p->imp, props ? nullptr : p->pf, (int)n_props, p->counters,
-                                        p->ctl, p->g, p->nbm, p->bm, p->compact ? p->cbm : nullptr, hs, p->ncl_arg(),
-                                        loop, end_mode, p->zlo, p->zhi);
+                                         p->ctl, p->g, p->nbm, p->bm, p->compact ? p->cbm : nullptr, hs,
+                                         p->ncl_arg(), loop, end_mode, p->zlo, p->zhi);
   CKL("k_commit");
   return 0;
 }

@@ -27,4 +27,15 @@ timeout 1500 ncu --nvtx --nvtx-include "profile/" --set full --clock-control non
 timeout 1500 ncu --nvtx --nvtx-include "profile/" --set full --clock-control none --import-source on \
    -k regex:"k_eval_p2" -c 4 \
    -o $R/c4_p2 python tools/profile_kernels.py --config c4 --host-rounds > $R/ncu_p2.log 2>&1; echo "ncu p2 rc=$?"
-ls -la $R
+# summaries on the box (the .ncu-rep files are too large to bring back)
+python tools/ncu_kernel_table.py $R/c4_other.ncu-rep $R/c4_ncu_other_kernels.json "C4 512^3 one pass of every non-eval kernel (tools/profile_kernels.py --host-rounds), ncu --set full --clock-control none, cold cache per replay" > $R/c4_ncu_other_kernels.txt 2>&1
+python tools/ncu_kernel_table.py $R/c4_p1.ncu-rep $R/c4_ncu_p1_commit.json "C4 phase-1 eval and commit launches (6 after skipping 6), ncu --set full" > $R/c4_ncu_p1_commit.txt 2>&1
+python tools/ncu_kernel_table.py $R/c4_p2.ncu-rep $R/c4_ncu_p2.json "C4 phase-2 eval launches (first 4), ncu --set full" > $R/c4_ncu_p2.txt 2>&1
+python tools/ncu_src_breakdown.py $R/c4_p1.ncu-rep k_eval_p1 40 > $R/c4_src_p1.txt 2>&1
+python tools/ncu_src_breakdown.py $R/c4_p1.ncu-rep k_commit 30 > $R/c4_src_commit.txt 2>&1
+python tools/ncu_src_breakdown.py $R/c4_p2.ncu-rep k_eval_p2 40 > $R/c4_src_p2.txt 2>&1
+python tools/ncu_src_breakdown.py $R/c4_other.ncu-rep k_vote_scan 30 > $R/c4_src_vote_scan.txt 2>&1
+cp $R/c4_p1.ncu-rep /tmp/ && python tools/eval_roof.py /tmp/c4_p1.ncu-rep c4 "phase-1 eval launches" > $R/eval_roof_p1.txt 2>&1; cp profiles/ncu_c4_k_eval.json $R/ncu_c4_k_eval_p1.json
+python tools/eval_roof.py $R/c4_p2.ncu-rep c4 "phase-2 eval launches" > $R/eval_roof_p2.txt 2>&1; cp profiles/ncu_c4_k_eval.json $R/ncu_c4_k_eval_p2.json
+rm -f $R/*.ncu-rep
+ls -la $R; du -sh gpurun_out
