@@ -54,6 +54,25 @@ def slab_bounds(nz: int, world: int) -> list[tuple[int, int]]:
     return out
 
 
+def balanced_slab_bounds(component: np.ndarray, dims, world: int) -> list[tuple[int, int]]:
+    """z-slabs holding about equal numbers of in-band voxels (the work of a
+    rank follows its in-band voxels, not its planes); every slab keeps at
+    least one plane. Any bounds give the same results bit for bit."""
+    nx, ny, nz = (int(d) for d in dims)
+    if world > nz:
+        raise ValueError(f"cannot split {nz} planes into {world} non-empty slabs")
+    per = np.count_nonzero(np.asarray(component).reshape(nz, ny * nx) >= 0, axis=1).astype(np.float64)
+    cum = np.concatenate([[0.0], np.cumsum(per)])
+    total = cum[-1]
+    cuts = [0]
+    for r in range(1, world):
+        z = int(np.searchsorted(cum, total * r / world, side="left"))
+        z = min(max(z, cuts[-1] + 1), nz - (world - r))
+        cuts.append(z)
+    cuts.append(nz)
+    return [(cuts[r], cuts[r + 1]) for r in range(world)]
+
+
 class _DevBuf:
     """A raw device allocation seen as a torch tensor (zero copy)."""
 
@@ -245,7 +264,7 @@ class GlobalClassifier:
         self.dims = tuple(int(d) for d in dims)
         self.spacing = tuple(float(s) for s in spacing)
         self.n = int(np.prod(self.dims))
-        self.bounds = slab_bounds(self.dims[2], coll.world)
+        self.bounds = balanced_slab_bounds(component, self.dims, coll.world)
         self.engines = {}
         comp_dev = None
         own = {}

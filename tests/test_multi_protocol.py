@@ -106,3 +106,17 @@ def test_collective_protocol_gloo_world2():
     with tempfile.TemporaryDirectory() as d:
         mp.spawn(_worker, args=(2, port, d), nprocs=2, join=True)
         assert os.path.exists(os.path.join(d, "ok0")) and os.path.exists(os.path.join(d, "ok1"))
+
+
+def test_balanced_slab_bounds():
+    from paper_2208_06970_b200.multigpu import balanced_slab_bounds
+
+    nx, ny, nz = 4, 3, 40
+    comp = -np.ones((nz, ny, nx), np.int32)
+    comp[30:] = 0  # all in-band voxels in the top 10 planes
+    b = balanced_slab_bounds(comp.ravel(), (nx, ny, nz), 4)
+    assert b[0][0] == 0 and b[-1][1] == nz and all(lo < hi for lo, hi in b)
+    assert all(b[i][1] == b[i + 1][0] for i in range(3))
+    counts = [int(np.count_nonzero(comp[lo:hi] >= 0)) for lo, hi in b]
+    assert max(counts) - min(counts) <= ny * nx * 2  # balanced to within a couple of planes
+    assert balanced_slab_bounds(np.zeros(nx * ny * nz, np.int32), (nx, ny, nz), 40) == [(z, z + 1) for z in range(40)]
