@@ -452,11 +452,14 @@ def run_global(args, cfg, world, rank, local):
     vlen = voxel_length(grid.dims, grid.spacing)
     inband = int(gc.any_engine().inband)
 
+    last = {}
+
     def step(p):
-        gc.classify(p, sc_d)
+        last.update(gc.classify(p, sc_d))
         p2, _, _ = gc.centroidal(p, sc_d, mode, w_d, 0.5 * vlen)
         return p2
 
+    gc.reuse_sites(True)  # Lloyd loop: site components fixed
     for _ in range(args.warmup):
         pos_d = step(pos_d)
     if world > 1:
@@ -472,7 +475,8 @@ def run_global(args, cfg, world, rank, local):
         t1.record()
         torch.cuda.synchronize()
     ms = t0.elapsed_time(t1)
-    per_rank = gc.rank_ms() if emulate else None
+    per_cat = gc.rank_ms(breakdown=True) if emulate else None
+    per_rank = {r: sum(c.values()) for r, c in per_cat.items()} if emulate else None
     if world > 1:
         t = torch.tensor([ms], dtype=torch.float64, device="cuda")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
@@ -483,12 +487,15 @@ def run_global(args, cfg, world, rank, local):
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "mode": "global", "slabs": coll.world,
-            "config": bench_config(cfg, grid.size, S, inband), "clocks": clk.summary()}
+            "config": bench_config(cfg, grid.size, S, inband), "clocks": clk.summary(),
+            "counters": {k: last[k] for k in ("rounds", "sweeps", "evaluations", "commits") if k in last}}
         if emulate:
             slow = max(per_rank.values()) / args.steps
             line["emulated_ranks"] = {
                 "ranks": coll.world, "rank_ms_per_step": {str(r): v / args.steps for r, v in per_rank.items()},
                 "slowest_rank_ms_per_step": slow,
+                "slowest_rank_breakdown_ms_per_step": {
+                    k: v / args.steps for k, v in per_cat[max(per_rank, key=per_rank.get)].items()},
                 "projected_value": grid.size / (slow / 1e3),
                 "note": "all slab ranks on ONE GPU one after another; each rank's own kernels timed with CUDA "
                         "events (the host round trips of the per-round count reads excluded; collectives are host "

@@ -219,16 +219,18 @@ int lrcvt_mg_begin(lrcvt_plan *plan, int64_t n_sites, const double *d_site_pos,
                    int64_t *n_frontier, void *stream);
 int lrcvt_mg_phase2(lrcvt_plan *plan, int64_t n_sites, const int32_t *d_site_comp,
                     int64_t *n_frontier, void *stream);
-/* evaluate the own frontier (sweep: the own eligible list); *n_prop =
- * improved proposals, *n_lo / *n_hi = those on planes zlo / zhi - 1, at
- * lrcvt_mg_boundary(plan, 0 / 1) for rank - 1 / rank + 1 */
+/* evaluate the own frontier (sweep: the own eligible list); *n_lo / *n_hi
+ * = the improved proposals on planes zlo / zhi - 1, at
+ * lrcvt_mg_boundary(plan, 0 / 1) for rank - 1 / rank + 1 (the eval kernels
+ * write them there as they go) */
 int lrcvt_mg_eval(lrcvt_plan *plan, int32_t phase, int32_t sweep, int64_t *n_evaluated,
-                  int64_t *n_prop, int64_t *n_lo, int64_t *n_hi, void *stream);
+                  int64_t *n_lo, int64_t *n_hi, void *stream);
 void *lrcvt_mg_boundary(lrcvt_plan *plan, int32_t side);
 /* commit the own proposals and the n_halo proposals received from the
- * neighbour ranks; *n_next = the own next frontier */
+ * neighbour ranks (one launch, which also ends the round); *n_next = the own
+ * next frontier, *n_committed = own proposals committed (= improved) */
 int lrcvt_mg_commit(lrcvt_plan *plan, const void *d_halo, int64_t n_halo, int32_t sweep,
-                    int64_t *n_next, void *stream);
+                    int64_t *n_next, int64_t *n_committed, void *stream);
 /* state bits of the own slab; *assigned = own assigned voxels */
 int lrcvt_mg_finish(lrcvt_plan *plan, const int32_t *d_site_src, uint8_t *d_state,
                     int64_t *assigned, void *stream);

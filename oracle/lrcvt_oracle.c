@@ -349,7 +349,12 @@ int64_t orc_classify(int64_t nx, int64_t ny, int64_t nz, double sx, double sy,
   int64_t rounds1 = run_phase(&c, 0, n_wl, &rnd);
 
   /* phase 2: tessellation.py:161-189 */
-  for (int64_t s = 0; s < n_sites; s++) has_site[site_comp[s]] = 1;
+  /* comps_with_sites[site_comp] = True: numpy wraps a negative id (a site
+   * recorded in component -1 marks the last component) */
+  for (int64_t s = 0; s < n_sites; s++) {
+    int64_t cs = site_comp[s] < 0 ? site_comp[s] + ncs : site_comp[s];
+    if (cs >= 0 && cs < ncs) has_site[cs] = 1;
+  }
   int64_t n_el = 0;
   for (int64_t v = 0; v < n; v++)
     if (comp[v] != NONE && has_site[comp[v]]) eligible[n_el++] = v;

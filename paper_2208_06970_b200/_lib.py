@@ -78,9 +78,9 @@ SIGNATURES = {
                                c_void_p]),
     "lrcvt_mg_phase2": (c_int, [c_void_p, c_int64, c_void_p, POINTER(c_int64), c_void_p]),
     "lrcvt_mg_eval": (c_int, [c_void_p, c_int32, c_int32, POINTER(c_int64), POINTER(c_int64), POINTER(c_int64),
-                              POINTER(c_int64), c_void_p]),
+                              c_void_p]),
     "lrcvt_mg_boundary": (c_void_p, [c_void_p, c_int32]),
-    "lrcvt_mg_commit": (c_int, [c_void_p, c_void_p, c_int64, c_int32, POINTER(c_int64), c_void_p]),
+    "lrcvt_mg_commit": (c_int, [c_void_p, c_void_p, c_int64, c_int32, POINTER(c_int64), POINTER(c_int64), c_void_p]),
     "lrcvt_mg_finish": (c_int, [c_void_p, c_void_p, c_void_p, POINTER(c_int64), c_void_p]),
     "lrcvt_mg_vote_exact": (c_int, [c_void_p, c_int64, c_void_p, c_void_p, c_void_p]),
     "lrcvt_mg_vote_exact_finish": (c_int, [c_void_p, c_int64, c_void_p, c_void_p, c_void_p]),

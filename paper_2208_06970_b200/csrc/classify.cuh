@@ -31,6 +31,17 @@ struct Prop {
 // Device-resident round control: the worklist pointers and size live in HBM
 // so relaxation rounds can run back to back without the host (CUDA-graph
 // conditional WHILE loop, or the host loop when per-launch timing is on).
+// multi-GPU slab ranks: the eval kernels copy every improved proposal on a
+// boundary plane (z == zlo for rank - 1, z == zhi - 1 for rank + 1) into
+// the outgoing halo lists as they write it (lo == nullptr: one domain)
+struct BoundaryOut {
+  Prop* lo;
+  Prop* hi;
+  int* counters;  // C_LO / C_HI: list sizes
+  int zlo, zhi;   // -1 / INT_MAX when there is no neighbour on that side
+  int nxy;
+};
+
 struct RoundCtl {
   int* cur;          // this round's worklist
   int* nxt;          // next round's worklist (written by k_commit)
@@ -46,10 +57,23 @@ struct RoundCtl {
   int loop_min;      // the round graph loops while n_cur > loop_min (small frontiers: k_rounds_small)
   long long rounds, evals, commits, rounds_p1;
   long long rounds_small, small_launches;  // rounds run inside k_rounds_small, and its launches
+  BoundaryOut bo;    // multi-GPU halo output of the eval kernels
 };
 
 // Counter slots in the plan's small device array.
-enum { C_NIMP = 0, C_NNEXT = 1, C_BAD = 2, C_ASSIGNED = 3, C_DONE = 4, C_LO = 5, C_HI = 6, C_NCOUNTERS = 8 };
+enum {
+  C_NIMP = 0, C_NNEXT = 1, C_BAD = 2, C_ASSIGNED = 3, C_DONE = 4, C_LO = 5, C_HI = 6, C_COLL = 7, C_NPROP = 8,
+  C_NCOUNTERS = 10
+};
+constexpr int H_NEL = 9;  // host-side slot of the pinned counter copy for the eligible count
+
+__device__ __forceinline__ void emit_boundary(const BoundaryOut* bo, const Prop& pr) {
+  if (!bo || !bo->lo) return;
+  const int z = (int)((unsigned)pr.v / (unsigned)bo->nxy);
+  if (z == bo->zlo) bo->lo[atomicAdd(bo->counters + C_LO, 1)] = pr;
+  if (z == bo->zhi - 1) bo->hi[atomicAdd(bo->counters + C_HI, 1)] = pr;
+}
+constexpr int SEED_NONE = 0x7fffffff;  // k_site_voxel: the site places no seed here
 
 // tessellation.py:120-122 fill values of the output arrays (site1, the
 // phase-1 scratch, is reset over the eligible list by k_fill_list)
@@ -317,6 +341,30 @@ __device__ __forceinline__ void round_end(RoundCtl* ctl, int* counters, const cu
   }
 }
 
+// multi-GPU round end (host-driven rounds): swap the worklists, reset every
+// per-round counter for the next eval (which therefore needs no memset) and
+// hand the next frontier size and the own commit count straight to the
+// host's pinned counter copy
+constexpr int END_MG = 3, END_MG_SWEEP = 4;  // k_commit end modes
+__device__ __forceinline__ void mg_round_end(RoundCtl* ctl, int* counters, bool sweep, volatile int* h_out) {
+  const int n_next = counters[C_NNEXT];
+  h_out[C_NNEXT] = n_next;
+  h_out[C_NIMP] = counters[C_NIMP];
+  if (sweep) {
+    ctl->cur = ctl->nxt;
+    ctl->nxt = ctl->stash;
+  } else {
+    int* t = ctl->cur;
+    ctl->cur = ctl->nxt;
+    ctl->nxt = t == ctl->ro ? ctl->spare : t;
+  }
+  ctl->n_cur = n_next;
+  counters[C_NIMP] = 0;
+  counters[C_NNEXT] = 0;
+  counters[C_LO] = 0;
+  counters[C_HI] = 0;
+}
+
 __global__ void k_loop_init(const RoundCtl* ctl, cudaGraphConditionalHandle h,
                             const cudaGraphConditionalHandle* hs, int n_classes) {
   set_size_class(ctl->n_cur, hs, n_classes);
@@ -424,66 +472,121 @@ __global__ void k_sweep_end(RoundCtl* ctl, int* counters) {
   counters[C_NNEXT] = 0;
 }
 
-// _kernels.py:399-422, site part: seed voxel, distance, validity.
+// _kernels.py:399-422, site part: seed voxel, distance, validity, and the
+// smallest site id per seed voxel (atomicMin on site1, which holds -1 =
+// 0xffffffff on every eligible voxel here). A site recorded in component -1
+// on an out-of-band voxel counts as bad here (the reference
+// would seed the out-of-band region itself). Sites outside [zlo-1, zhi] (a
+// multi-GPU slab and its halo planes) are still validated but place nothing.
 __global__ void k_site_voxel(Geo g, const int* __restrict__ comp, const double4* __restrict__ site_pos,
                              const int* __restrict__ site_comp, int n_sites,
-                             int* __restrict__ key, int* __restrict__ val,
-                             double* __restrict__ sd, int* __restrict__ counters) {
+                             int* __restrict__ key, double* __restrict__ sd, int* __restrict__ site1,
+                             int* __restrict__ counters, int zlo = 0, int zhi = 1 << 30) {
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= n_sites) return;
   const double4 p = site_pos[s];
   const int x = cell_of(p.x, g.sx, g.nx), y = cell_of(p.y, g.sy, g.ny), z = cell_of(p.z, g.sz, g.nz);
   const int v = x + g.nx * (y + g.ny * z);
-  val[s] = s;
-  if (comp[v] != site_comp[s]) {
+  if (comp[v] != site_comp[s] || comp[v] < 0) {
     atomicAdd(counters + C_BAD, 1);
-    key[s] = 0x7fffffff;
-    sd[s] = 0.0;
+    key[s] = SEED_NONE;
+    return;
+  }
+  if (z < zlo - 1 || z > zhi) {
+    key[s] = SEED_NONE;
     return;
   }
   key[s] = v;
   sd[s] = dist3(centre1(x, g.sx), centre1(y, g.sy), centre1(z, g.sz), p.x, p.y, p.z);
+  atomicMin(reinterpret_cast<unsigned*>(site1) + v, (unsigned)s);
 }
 
 // _kernels.py:399-422 contested-voxel rule + _kernels.py:425-454 initial
-// worklist. Sites are sorted by (voxel, id) (stable radix sort), so each
-// group head folds its group in increasing site id exactly like the serial
-// reference loop, then enqueues the seed voxel and its same-component
-// neighbours.
+// worklist, without sorting the sites: the smallest site id of each seed
+// voxel (k_site_voxel) places its seed and enqueues the voxel and its
+// same-component neighbours; every other site of an occupied voxel goes to
+// the collision list, whose groups k_seed_collisions folds afterwards in
+// increasing site id exactly like the serial reference loop. The enqueued
+// set does not depend on which site wins a voxel.
 __global__ void __launch_bounds__(128) k_seed_groups(Geo g, const uint32_t* __restrict__ nbm,
                                                      const int* __restrict__ key,
-                                                     const int* __restrict__ val,
                                                      const double* __restrict__ sd_by_site,
                                                      int n_sites, int2* __restrict__ ss,
-                                                     double* __restrict__ dist, int* __restrict__ site1,
+                                                     double* __restrict__ dist, const int* __restrict__ site1,
                                                      uint32_t* __restrict__ bm,
                                                      int* __restrict__ next,
+                                                     unsigned long long* __restrict__ coll,
                                                      int* __restrict__ counters,
                                                      int zlo = 0, int zhi = 1 << 30) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
   // a bad site (k_site_voxel, the previous launch) aborts the classify before
   // any relaxation as the reference's ValueError does: no seeds, no frontier
   if (*(volatile int*)(counters + C_BAD)) return;
   bool head = false;
   int v = 0;
-  if (i < n_sites) {
-    v = key[i];
-    head = v != 0x7fffffff && (i == 0 || key[i - 1] != v);
-  }
-  if (head) {
-    int cur_s = val[i];
-    double cur_d = sd_by_site[cur_s];
-    for (int j = i + 1; j < n_sites && key[j] == v; j++) {
-      const int s = val[j];
-      const double d = sd_by_site[s];
-      if (beats(d, s, cur_d, cur_s)) { cur_s = s; cur_d = d; }
+  if (s < n_sites) {
+    v = key[s];
+    if (v != SEED_NONE) {
+      head = __ldg(site1 + v) == s;
+      if (head) {
+        ss[v] = make_int2(s, v);
+        dist[v] = sd_by_site[s];
+      } else {
+        coll[atomicAdd(counters + C_COLL, 1)] = ((unsigned long long)(unsigned)v << 32) | (unsigned)s;
+      }
     }
-    ss[v] = make_int2(cur_s, v);
-    site1[v] = cur_s;
-    dist[v] = cur_d;
   }
   if (blockIdx.x * blockDim.x >= n_sites) return;
   mark_and_append(g, nbm, head, v, true, bm, next, counters + C_NNEXT, zlo, zhi);
+}
+
+// Voxels holding more than one site (rare: the collision list of
+// k_seed_groups, every site but the smallest id of its voxel). One CTA sorts
+// the (voxel, site) keys with a bitonic network in place (the buffer holds a
+// power of two >= the site count) and each group's first entry folds the
+// group after its smallest site, in increasing site id (_kernels.py:405-422).
+constexpr int SEED_COLL_THREADS = 1024;
+__global__ void __launch_bounds__(SEED_COLL_THREADS) k_seed_collisions(
+    unsigned long long* __restrict__ coll, const double* __restrict__ sd_by_site, int2* __restrict__ ss,
+    double* __restrict__ dist, int* __restrict__ site1, const int* __restrict__ counters) {
+  const int n = *(volatile const int*)(counters + C_COLL);
+  if (n == 0 || *(volatile const int*)(counters + C_BAD)) return;
+  int P = 1;
+  while (P < n) P <<= 1;
+  for (int i = n + threadIdx.x; i < P; i += blockDim.x) coll[i] = ~0ull;
+  __syncthreads();
+  for (int k = 2; k <= P; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < P; i += blockDim.x) {
+        const int l = i ^ j;
+        if (l > i) {
+          const unsigned long long a = coll[i], b = coll[l];
+          if (((i & k) == 0) == (a > b)) {
+            coll[i] = b;
+            coll[l] = a;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const unsigned v = (unsigned)(coll[i] >> 32);
+    if (i > 0 && (unsigned)(coll[i - 1] >> 32) == v) continue;
+    const int first = site1[v];
+    int cur_s = first;
+    double cur_d = sd_by_site[first];
+    for (int j = i; j < n && (unsigned)(coll[j] >> 32) == v; j++) {
+      const int s = (int)(unsigned)coll[j];
+      const double d = sd_by_site[s];
+      if (beats(d, s, cur_d, cur_s)) { cur_s = s; cur_d = d; }
+    }
+    if (cur_s != first) {
+      ss[v] = make_int2(cur_s, (int)v);
+      site1[v] = cur_s;
+      dist[v] = cur_d;
+    }
+  }
 }
 
 // tessellation.py:191-194 state bits, plus the `assigned` count, over the

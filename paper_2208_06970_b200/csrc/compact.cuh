@@ -57,7 +57,9 @@ __global__ void __launch_bounds__(CM_THREADS, 8) k_commit(const Prop* __restrict
                                                        uint32_t* __restrict__ cbm,
                                                        const cudaGraphConditionalHandle* __restrict__ hs,
                                                        int n_classes, cudaGraphConditionalHandle loop, int end_mode,
-                                                       int zlo, int zhi) {
+                                                       int zlo, int zhi, const Prop* __restrict__ halo = nullptr,
+                                                       int n_halo = 0, int own_blocks = 1 << 30,
+                                                       volatile int* h_out = nullptr) {
   __shared__ int s_idx[CM_SLOTS];
   __shared__ int s_wcnt[CM_THREADS / 32];
   __shared__ int s_tot;
@@ -67,12 +69,17 @@ __global__ void __launch_bounds__(CM_THREADS, 8) k_commit(const Prop* __restrict
   int* next = ctl->nxt;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   int mine = 0;
-  if (pf) {
+  // blocks [0, own_blocks): the round's own proposals; the rest (multi-GPU
+  // slabs): the halo-plane proposals received from the neighbour ranks
+  const bool own = (int)blockIdx.x < own_blocks;
+  const int bid = own ? (int)blockIdx.x : (int)blockIdx.x - own_blocks;
+  const int nb = own ? min(own_blocks, (int)gridDim.x) : (int)gridDim.x - own_blocks;
+  if (own && pf) {
     // sparse slots: each CTA step compacts the improved slots of CM_SLOTS
     // frontier items into shared memory, then commits them one per thread
     // (full lanes for the enqueue, one list reservation per CTA step)
     const int n = *(volatile const int*)&ctl->n_cur;
-    for (int base = blockIdx.x * CM_SLOTS; base < n; base += gridDim.x * CM_SLOTS) {  // block-uniform
+    for (int base = bid * CM_SLOTS; base < n; base += nb * CM_SLOTS) {  // block-uniform
       const int i0 = base + 4 * threadIdx.x;
       uchar4 f = make_uchar4(0, 0, 0, 0);
       if (i0 + 3 < n && ((reinterpret_cast<uintptr_t>(pf + i0) & 3) == 0)) {
@@ -124,13 +131,14 @@ __global__ void __launch_bounds__(CM_THREADS, 8) k_commit(const Prop* __restrict
       __syncthreads();  // s_idx / s_wcnt reused by the next step
     }
   } else {
-    const int n = n_props;
-    for (int base = blockIdx.x * blockDim.x; base < n; base += gridDim.x * blockDim.x) {  // block-uniform
+    const Prop* __restrict__ list = own ? imp : halo;
+    const int n = own ? n_props : n_halo;
+    for (int base = bid * blockDim.x; base < n; base += nb * blockDim.x) {  // block-uniform
       const int i = base + threadIdx.x;
       const bool take = i < n;
       int v = 0;
       if (take) {
-        const Prop p = imp[i];
+        const Prop p = list[i];
         v = p.v;
         mine++;
         commit_one(p, ss, dist, site1);
@@ -138,7 +146,8 @@ __global__ void __launch_bounds__(CM_THREADS, 8) k_commit(const Prop* __restrict
       mark_and_append(g, nbm, take, v, false, bm, next, counters + C_NNEXT, zlo, zhi, cbm);
     }
   }
-  // committed count: warp sums, one atomic per CTA
+  // committed count (own proposals: the halo blocks' are the neighbours'): warp sums, one atomic per CTA
+  if (!own) mine = 0;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
   __shared__ int s_cnt;
@@ -157,7 +166,10 @@ __global__ void __launch_bounds__(CM_THREADS, 8) k_commit(const Prop* __restrict
   if (last && threadIdx.x == 0) {
     __threadfence();
     counters[C_DONE] = 0;
-    round_end(ctl, counters, hs, n_classes, loop, end_mode);
+    if (end_mode >= END_MG)
+      mg_round_end(ctl, counters, end_mode == END_MG_SWEEP, h_out);
+    else
+      round_end(ctl, counters, hs, n_classes, loop, end_mode);
   }
 }
 

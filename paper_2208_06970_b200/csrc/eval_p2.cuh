@@ -42,7 +42,8 @@ __device__ __forceinline__ void p2_tile(const int* __restrict__ list, int n, con
                                                    const double4* __restrict__ site_pos,
                                                    uint32_t* __restrict__ bm,
                                                    Prop* __restrict__ imp, uint8_t* __restrict__ pf,
-                                                   const PeerView* __restrict__ pv) {
+                                                   const PeerView* __restrict__ pv,
+                                                   const BoundaryOut* bo = nullptr) {
   const bool active = i < n;
   const int v = active ? __ldg(list + i) : 0;
   int x = 0, y = 0, z = 0, cv = -3;
@@ -234,6 +235,7 @@ __device__ __forceinline__ void p2_tile(const int* __restrict__ list, int n, con
     Prop pr;
     pr.d = best_d; pr.v = v; pr.s = best_s; pr.src = best_src; pr.pad = 0;
     imp[i] = pr;
+    if (MG) emit_boundary(bo, pr);
   }
   if (active) pf[i] = improved ? 1 : 0;
 }
@@ -254,7 +256,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_eval_p2(RoundCtl* __restrict__ 
   // (exact grid on the host path, size-class grid >= n inside the graph)
   const int base = blockIdx.x * BLOCK;
   if (base >= n) return;
-  p2_tile<BLOCK, DYADIC, MG>(list, n, base + (int)threadIdx.x, g, comp, nbm, ss, dist, site_pos, bm, imp, pf, pv);
+  p2_tile<BLOCK, DYADIC, MG>(list, n, base + (int)threadIdx.x, g, comp, nbm, ss, dist, site_pos, bm, imp, pf, pv, &ctl->bo);
 }
 
 }  // namespace lrcvt

@@ -196,7 +196,8 @@ __device__ __forceinline__ void ew_voxel(const int* list, const int2* ss, const 
                                          const uint32_t* __restrict__ nbm, const double4* __restrict__ site_pos,
                                          uint32_t* __restrict__ bm, Prop* __restrict__ imp,
                                          uint8_t* __restrict__ pf, EwStage& st,
-                                         const PeerView* __restrict__ pv = nullptr) {
+                                         const PeerView* __restrict__ pv = nullptr,
+                                         const BoundaryOut* bo = nullptr) {
   const int lane = threadIdx.x & 31;
   const int v = ldst<COH>(list + i);
   int x, y, z;
@@ -285,6 +286,7 @@ __device__ __forceinline__ void ew_voxel(const int* list, const int2* ss, const 
       Prop pr;
       pr.d = best_d; pr.v = v; pr.s = best_s; pr.src = best_src; pr.pad = 0;
       imp[i] = pr;
+      emit_boundary(bo, pr);
     }
     pf[i] = improved ? 1 : 0;
   }
@@ -303,7 +305,7 @@ __global__ void __launch_bounds__(32 * EW_WARPS) k_eval_warp(RoundCtl* __restric
   const int i = blockIdx.x * EW_WARPS + wid;
   if (i >= ctl->n_cur) return;  // warp-uniform
   ew_voxel<PHASE2, false, MG>(ctl->cur, ctl->ss, ctl->site1, ctl->dist, i, g, comp, nbm, site_pos, bm, imp, pf,
-                              stage[wid], pv);
+                              stage[wid], pv, &ctl->bo);
 }
 
 }  // namespace lrcvt

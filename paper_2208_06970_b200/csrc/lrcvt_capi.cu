@@ -239,14 +239,13 @@ struct lrcvt_plan {
   double mg_ms = 0.0;
   int* counters = nullptr;
   int* h_counters = nullptr;  // pinned
+  int* h_counters_dev = nullptr;  // its device-side address (kernels write the host copy directly)
   uint8_t* has_site = nullptr;
   // sites
   double4* site_pos = nullptr;
   double4* new_pos = nullptr;
   int* sk_key = nullptr;
-  int* sk_key2 = nullptr;
-  int* sk_val = nullptr;
-  int* sk_val2 = nullptr;
+  unsigned long long* sk_coll = nullptr;  // seed collision list: a power of two >= max_sites entries
   double* sk_d = nullptr;
   // vote
   unsigned long long* acc = nullptr;
@@ -260,6 +259,8 @@ struct lrcvt_plan {
   int2* vt_sp = nullptr;  // (site, phi) per voxel for the bounding-box vote
   bool sp_stale = true;   // vt_sp must be reset to -1 before the next k_vote_prep
   int* vt_box = nullptr;  // [6][S] per-site bounding boxes
+  int* vt_order = nullptr;  // [S] sites by box volume, largest first (k_vote_scan's schedule)
+  int* vt_hist = nullptr;   // [2][VO_BUCKETS] bucket counts / cursors
   bool vote_bbox = true;  // LRCVT_VOTE=sort: stable radix sort of (site, (phi, v)) pairs instead
   // cub
   void* cub_tmp = nullptr;
@@ -753,7 +754,9 @@ int lrcvt_plan_create(lrcvt_plan** plan, int64_t nx, int64_t ny, int64_t nz, dou
   const int64_t n = p->g.n;
   int rc = 0;
   rc |= dalloc(&p->counters, C_NCOUNTERS);
-  if (cudaMallocHost((void**)&p->h_counters, sizeof(int) * C_NCOUNTERS) != cudaSuccess) rc = LRCVT_E_NOMEM;
+  if (cudaMallocHost((void**)&p->h_counters, sizeof(int) * C_NCOUNTERS) != cudaSuccess ||
+      cudaHostGetDevicePointer((void**)&p->h_counters_dev, p->h_counters, 0) != cudaSuccess)
+    rc = LRCVT_E_NOMEM;
   if (rc) { lrcvt_plan_destroy(p); return set_error(LRCVT_E_NOMEM, "plan counters"); }
   // count in-band voxels
   {
@@ -789,15 +792,18 @@ int lrcvt_plan_create(lrcvt_plan** plan, int64_t nx, int64_t ny, int64_t nz, dou
   rc |= dalloc(&p->nbm, n);
   rc |= dalloc(&p->site1, n);
   rc |= dalloc(&p->ctl, 1);
+  if (!rc && cudaMemsetAsync(p->ctl, 0, sizeof(RoundCtl), st) != cudaSuccess) rc = LRCVT_E_CUDA;  // bo.lo = null
   rc |= dalloc(&p->d_handles, 3 * MAX_CLASSES);
   rc |= dalloc(&p->d_nel, 1);
   rc |= dalloc(&p->has_site, n_components > 0 ? n_components : 1);
   rc |= dalloc(&p->site_pos, S);
   rc |= dalloc(&p->new_pos, S);
   rc |= dalloc(&p->sk_key, S);
-  rc |= dalloc(&p->sk_key2, S);
-  rc |= dalloc(&p->sk_val, S);
-  rc |= dalloc(&p->sk_val2, S);
+  {
+    int64_t pc = 1;
+    while (pc < S) pc <<= 1;
+    rc |= dalloc(&p->sk_coll, pc);
+  }
   rc |= dalloc(&p->sk_d, S);
   rc |= dalloc(&p->acc, 4 * S);
   rc |= dalloc(&p->sums, 4 * S);
@@ -836,9 +842,6 @@ int lrcvt_plan_create(lrcvt_plan** plan, int64_t nx, int64_t ny, int64_t nz, dou
     EligiblePred pred{p->comp, p->has_site};
     cub::CountingInputIterator<int> it(0);
     cub::DeviceSelect::If(nullptr, b, it, p->eligible, p->counters, (int)n, pred, st);
-    need = b > need ? b : need;
-    b = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, b, p->sk_key, p->sk_key2, p->sk_val, p->sk_val2, (int)S, 0, 32, st);
     need = b > need ? b : need;
     b = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, b, p->list_a, p->list_b, p->list_a, p->list_b, (int)nin, 0, 32, st);
@@ -897,9 +900,9 @@ int lrcvt_plan_destroy(lrcvt_plan* p) {
   void* bufs[] = {p->counters, p->ctl, p->d_handles, p->d_nel, p->list_a, p->list_b, p->eligible, p->imp, p->pf,
                   p->bm,
                   p->cbm, p->ct_status, p->ct_state, p->nbm, p->site1, p->has_site,
-                  p->site_pos, p->new_pos, p->sk_key, p->sk_key2, p->sk_val, p->sk_val2, p->sk_d,
+                  p->site_pos, p->new_pos, p->sk_key, p->sk_coll, p->sk_d,
                   p->acc, p->sums, p->vt_key, p->vt_key2, p->vt_pv, p->vt_pv2,
-                  p->seg_b, p->seg_e, p->vt_sp, p->vt_box, p->mg_own_ss, p->mg_own_dist, p->d_pv,
+                  p->seg_b, p->seg_e, p->vt_sp, p->vt_box, p->vt_order, p->vt_hist, p->mg_own_ss, p->mg_own_dist, p->d_pv,
                   p->mg_lo, p->mg_hi, p->cub_tmp};
   for (void* b : bufs)
     if (b) cudaFree(b);
@@ -1005,19 +1008,16 @@ int lrcvt_classify(lrcvt_plan* p, int64_t n_sites, const double* d_site_pos,
   k_pack_sites<<<grid_for(S, 256), 256, 0, st>>>(d_site_pos, S, p->site_pos);
   CKL("k_pack_sites"); LAUNCHED(1);
   // _place_seeds (tessellation.py:136-140)
-  k_site_voxel<<<grid_for(S, 256), 256, 0, st>>>(g, p->comp, p->site_pos, d_site_comp, S, p->sk_key,
-                                                 p->sk_val, p->sk_d, p->counters);
+  k_site_voxel<<<grid_for(S, 256), 256, 0, st>>>(g, p->comp, p->site_pos, d_site_comp, S, p->sk_key, p->sk_d,
+                                                 p->site1, p->counters);
   CKL("k_site_voxel"); LAUNCHED(1);
-  {
-    size_t bytes = p->cub_bytes;
-    CK(cub::DeviceRadixSort::SortPairs(p->cub_tmp, bytes, p->sk_key, p->sk_key2, p->sk_val,
-                                       p->sk_val2, S, 0, 32, st));
-  }
-  // groups -> seeds, then the phase-1 worklist (tessellation.py:151); sites
-  // outside their component (key INT_MAX) are skipped and reported at the end
-  k_seed_groups<<<grid_for(S, 128), 128, 0, st>>>(g, p->nbm, p->sk_key2, p->sk_val2, p->sk_d, S, ss,
-                                                  d_dist, p->site1, p->bm, p->list_a, p->counters);  // marks bm (round-1 frontier)
+  // seeds, then the phase-1 worklist (tessellation.py:151); sites outside
+  // their component are skipped and reported at the end
+  k_seed_groups<<<grid_for(S, 128), 128, 0, st>>>(g, p->nbm, p->sk_key, p->sk_d, S, ss, d_dist, p->site1, p->bm,
+                                                  p->list_a, p->sk_coll, p->counters);  // marks bm (round-1 frontier)
   CKL("k_seed_groups"); LAUNCHED(1);
+  k_seed_collisions<<<1, SEED_COLL_THREADS, 0, st>>>(p->sk_coll, p->sk_d, ss, d_dist, p->site1, p->counters);
+  CKL("k_seed_collisions"); LAUNCHED(1);
   k_phase1_start<<<1, 1, 0, st>>>(p->ctl, p->counters, p->list_a, p->list_b, ss, d_dist, p->site1, p->loop_min);
   CKL("k_phase1_start"); LAUNCHED(1);
   // phase 1 (tessellation.py:152-156)
@@ -1041,9 +1041,9 @@ int lrcvt_classify(lrcvt_plan* p, int64_t n_sites, const double* d_site_pos,
     CK(cudaMemcpyAsync(p->h_ctl, p->ctl, sizeof(RoundCtl), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     if (p->timing) {
-      CK(cudaMemcpyAsync(p->h_counters + 7, p->d_nel, sizeof(int), cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(p->h_counters + H_NEL, p->d_nel, sizeof(int), cudaMemcpyDeviceToHost, st));
       CK(cudaStreamSynchronize(st));
-      CKR(note_eval(p, p->h_counters[7], true, p->h_ctl->sweep_imp));
+      CKR(note_eval(p, p->h_counters[H_NEL], true, p->h_ctl->sweep_imp));
     }
     if (p->h_ctl->sweep_imp == 0) break;
   }
@@ -1052,10 +1052,10 @@ int lrcvt_classify(lrcvt_plan* p, int64_t n_sites, const double* d_site_pos,
   k_state<<<el_grid, 256, 0, st>>>(ss, p->eligible, p->d_nel, 0, 0, d_state, p->counters);
   CKL("k_state"); LAUNCHED(1);
   CK(cudaMemcpyAsync(p->h_ctl, p->ctl, sizeof(RoundCtl), cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(p->h_counters + 7, p->d_nel, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(p->h_counters + H_NEL, p->d_nel, sizeof(int), cudaMemcpyDeviceToHost, st));
   CKR(sync_counters(p, st, C_ASSIGNED + 1));
   const RoundCtl& c = *p->h_ctl;
-  p->n_eligible = p->h_counters[7];
+  p->n_eligible = p->h_counters[H_NEL];
   stats->eligible = p->n_eligible;
   stats->rounds = c.rounds;
   stats->phase1_rounds = c.rounds_p1;
@@ -1070,6 +1070,35 @@ int lrcvt_classify(lrcvt_plan* p, int64_t n_sites, const double* d_site_pos,
     p->eligible_valid = false;
     return p->h_counters[C_BAD];
   }
+  return 0;
+}
+
+// the bounding-box vote's per-voxel (site, phi) entries, reset
+// whenever the eligible set was rebuilt since the last vote (sp_stale)
+static int vote_buffers(lrcvt_plan* p, cudaStream_t st) {
+  const size_t n = (size_t)p->g.n;
+  if (!p->vt_sp) {
+    int rc = dalloc(&p->vt_sp, n);
+    rc |= dalloc(&p->vt_box, 6 * p->max_sites);
+    rc |= dalloc(&p->vt_order, p->max_sites);
+    rc |= dalloc(&p->vt_hist, 2 * VO_BUCKETS);
+    if (rc) return LRCVT_E_NOMEM;
+  }
+  if (p->sp_stale) {
+    CK(cudaMemsetAsync(p->vt_sp, 0xff, sizeof(int2) * n, st));
+    p->sp_stale = false;
+  }
+  return 0;
+}
+
+// k_vote_scan's site order from the boxes: largest first (vote.cuh)
+static int vote_order(lrcvt_plan* p, const int* d_box, int S, cudaStream_t st) {
+  CK(cudaMemsetAsync(p->vt_hist, 0, sizeof(int) * 2 * VO_BUCKETS, st));
+  k_vote_order_hist<<<grid_for(S, 256), 256, 0, st>>>(d_box, S, p->vt_hist);
+  CKL("k_vote_order_hist"); LAUNCHED(1);
+  k_vote_order_scatter<<<grid_for(S, 256), 256, 0, st>>>(d_box, S, p->vt_hist, p->vt_hist + VO_BUCKETS,
+                                                          p->vt_order);
+  CKL("k_vote_order_scatter"); LAUNCHED(1);
   return 0;
 }
 
@@ -1091,9 +1120,9 @@ int lrcvt_centroidal_update(lrcvt_plan* p, int64_t n_sites, const double* d_site
   CKL("k_pack_sites"); LAUNCHED(1);
   if (!(p->reuse_eligible && p->eligible_valid && p->eligible_sites == S)) {
     if (prepare_eligible(p, S, d_site_comp, st)) return LRCVT_E_CUDA;
-    CK(cudaMemcpyAsync(p->h_counters + 7, p->d_nel, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(p->h_counters + H_NEL, p->d_nel, sizeof(int), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    p->n_eligible = p->h_counters[7];
+    p->n_eligible = p->h_counters[H_NEL];
     p->eligible_valid = true;
     p->eligible_sites = S;
   }
@@ -1111,15 +1140,7 @@ int lrcvt_centroidal_update(lrcvt_plan* p, int64_t n_sites, const double* d_site
     CKL("k_vote_exact_finish"); LAUNCHED(1);
   } else if (p->vote_bbox) {
     // ordered path, sort-free: per-site bounding-box walk (vote.cuh k_vote_prep / k_vote_scan)
-    if (!p->vt_sp) {
-      int rc = dalloc(&p->vt_sp, g.n);
-      rc |= dalloc(&p->vt_box, 6 * p->max_sites);
-      if (rc) return LRCVT_E_NOMEM;
-    }
-    if (p->sp_stale) {
-      CK(cudaMemsetAsync(p->vt_sp, 0xff, sizeof(int2) * (size_t)g.n, st));
-      p->sp_stale = false;
-    }
+    CKR(vote_buffers(p, st));
     k_box_init<<<grid_for(S, 256), 256, 0, st>>>(p->vt_box, S);
     CKL("k_box_init"); LAUNCHED(1);
     if (n_el > 0) {
@@ -1127,9 +1148,10 @@ int lrcvt_centroidal_update(lrcvt_plan* p, int64_t n_sites, const double* d_site
                                                                        S, nullptr);
       CKL("k_vote_prep"); LAUNCHED(1);
     }
-    k_vote_scan<4><<<grid_for(S, 4), 128, 0, st>>>(p->vt_sp, p->comp, p->vt_box, d_site_comp, S, g,
-                                                    (const double*)d_weights, (const float*)d_weights, weight_mode,
-                                                    0, g.nz, 0, nullptr, p->sums);
+    CKR(vote_order(p, p->vt_box, S, st));
+    k_vote_scan<4><<<grid_for(S, 4), 128, 0, st>>>(
+        p->vt_sp, p->vt_box, p->vt_order, d_site_comp, S, g, (const double*)d_weights, (const float*)d_weights,
+        weight_mode, 0, g.nz, 0, nullptr, p->sums);
     CKL("k_vote_scan"); LAUNCHED(1);
   } else {
     const int64_t nin = p->n_inband > 0 ? p->n_inband : 1;
@@ -1437,49 +1459,9 @@ int lrcvt_aggregate(int64_t n, int32_t n_fields, const float* const* field_ptrs,
 // received halo proposals (enqueue restricted to the own slab) -> global
 // frontier count. The caller drives rounds and collectives (multigpu.py).
 
-__global__ void k_mg_round_end(RoundCtl* ctl, int* counters, int sweep) {
-  const int n_next = counters[C_NNEXT];
-  if (sweep) {
-    ctl->cur = ctl->nxt;
-    ctl->nxt = ctl->stash;
-  } else {
-    int* t = ctl->cur;
-    ctl->cur = ctl->nxt;
-    ctl->nxt = t == ctl->ro ? ctl->spare : t;
-  }
-  ctl->n_cur = n_next;
-  counters[C_NIMP] = 0;
-  counters[C_NNEXT] = 0;
-}
-
-// the round's improved proposals on the boundary planes: z == zlo -> lo (for
-// rank - 1), z == zhi - 1 -> hi (for rank + 1); all improved counted too
-__global__ void __launch_bounds__(128) k_mg_boundary(const RoundCtl* __restrict__ ctl, const Prop* __restrict__ imp,
-                                                     const uint8_t* __restrict__ pf, int nxy, int zlo, int zhi,
-                                                     int want_lo, int want_hi, Prop* __restrict__ lo,
-                                                     Prop* __restrict__ hi, int* __restrict__ counters) {
-  const int n = ctl->n_cur;
-  const int stride = gridDim.x * blockDim.x;
-  int mine = 0;
-  for (int base = blockIdx.x * blockDim.x; base < n; base += stride) {
-    const int i = base + threadIdx.x;
-    const bool take = i < n && pf[i];
-    int z = -1;
-    Prop pr;
-    if (take) {
-      pr = imp[i];
-      z = (int)((unsigned)pr.v / (unsigned)nxy);
-      mine++;
-    }
-    const bool tl = take && want_lo && z == zlo, th = take && want_hi && z == zhi - 1;
-    const int sl = block_append(counters + C_LO, tl);
-    if (tl) lo[sl] = pr;
-    const int sh = block_append(counters + C_HI, th);
-    if (th) hi[sh] = pr;
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
-  if ((threadIdx.x & 31) == 0 && mine) atomicAdd(counters + C_NIMP, mine);
+// a round with nothing to commit ends here (classify.cuh mg_round_end)
+__global__ void k_mg_round_end(RoundCtl* ctl, int* counters, int sweep, volatile int* h_out) {
+  mg_round_end(ctl, counters, sweep != 0, h_out);
 }
 
 // device time of an mg step that ends in a host synchronisation: events
@@ -1495,6 +1477,17 @@ int mg_sync(lrcvt_plan* p, cudaStream_t st, int n) {
     CK(cudaEventElapsedTime(&ms, p->mg_ev[0], p->mg_ev[1]));
     p->mg_ms += ms;
   }
+  return 0;
+}
+
+// the same for a step that does not synchronise (timing mode only waits for its end event)
+int mg_t1(lrcvt_plan* p, cudaStream_t st) {
+  if (!p->mg_timing) return 0;
+  CK(cudaEventRecord(p->mg_ev[1], st));
+  CK(cudaEventSynchronize(p->mg_ev[1]));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, p->mg_ev[0], p->mg_ev[1]));
+  p->mg_ms += ms;
   return 0;
 }
 
@@ -1553,29 +1546,51 @@ int lrcvt_mg_begin(lrcvt_plan* p, int64_t n_sites, const double* d_site_pos, con
   int2* ss = reinterpret_cast<int2*>(d_site_src);
   p->mg_ss = ss;
   p->mg_dist = d_dist;
+  if (!p->mg_lo) {
+    int rc = dalloc(&p->mg_lo, g.nxy);
+    rc |= dalloc(&p->mg_hi, g.nxy);
+    if (rc) return LRCVT_E_NOMEM;
+  }
   mg_t0(p, st);
+  {  // the eval kernels' halo output (classify.cuh BoundaryOut): planes zlo / zhi - 1 when a neighbour exists
+    BoundaryOut bo;
+    bo.lo = p->mg_lo;
+    bo.hi = p->mg_hi;
+    bo.counters = p->counters;
+    bo.zlo = p->zlo > 0 ? p->zlo : -1;
+    bo.zhi = p->zhi < g.nz ? p->zhi : INT_MAX;
+    bo.nxy = (int)g.nxy;
+    CK(cudaMemcpyAsync(&p->ctl->bo, &bo, sizeof bo, cudaMemcpyHostToDevice, st));
+  }
   CK(cudaMemsetAsync(p->counters, 0, sizeof(int) * C_NCOUNTERS, st));
-  // own-slab eligible list (tessellation.py:161-164 restricted to [zlo, zhi))
-  if (prepare_eligible(p, S, d_site_comp, st)) return LRCVT_E_CUDA;
-  p->eligible_valid = true;
-  p->eligible_sites = S;
-  k_fill_state<<<grid_for(g.n, 256, 148 * 32), 256, 0, st>>>(ss, d_dist, g.n);
-  CKL("k_fill_state");
-  CK(cudaMemsetAsync(p->site1, 0xff, sizeof(int) * (size_t)g.n, st));
+  // own-slab eligible list (tessellation.py:161-164 restricted to [zlo, zhi)); kept across a Lloyd loop
+  // whose site components do not change (lrcvt_plan_reuse_eligible)
+  if (!(p->reuse_eligible && p->eligible_valid && p->eligible_sites == S)) {
+    if (prepare_eligible(p, S, d_site_comp, st)) return LRCVT_E_CUDA;
+    p->eligible_valid = true;
+    p->eligible_sites = S;
+  }
+  // the rank's kernels read its own ss / dist / site1 only on the slab and its halo planes [z0, z1)
+  // (mg.cuh: everything else through the owner's buffers)
+  {
+    const int64_t z0 = p->zlo > 0 ? p->zlo - 1 : 0, z1 = p->zhi < g.nz ? p->zhi + 1 : g.nz;
+    const int64_t v0 = z0 * g.nxy, nv = (z1 - z0) * g.nxy;
+    k_fill_state<<<grid_for(nv, 256, 148 * 32), 256, 0, st>>>(ss + v0, d_dist + v0, nv);
+    CKL("k_fill_state");
+    CK(cudaMemsetAsync(p->site1 + v0, 0xff, sizeof(int) * (size_t)nv, st));
+  }
   k_pack_sites<<<grid_for(S, 256), 256, 0, st>>>(d_site_pos, S, p->site_pos);
   CKL("k_pack_sites");
-  k_site_voxel<<<grid_for(S, 256), 256, 0, st>>>(g, p->comp, p->site_pos, d_site_comp, S, p->sk_key, p->sk_val,
-                                                 p->sk_d, p->counters);
+  // every rank validates every site and places the seeds on its slab and halo planes; the phase-1
+  // worklist holds the own slab's part only
+  k_site_voxel<<<grid_for(S, 256), 256, 0, st>>>(g, p->comp, p->site_pos, d_site_comp, S, p->sk_key, p->sk_d,
+                                                 p->site1, p->counters, p->zlo, p->zhi);
   CKL("k_site_voxel");
-  {
-    size_t bytes = p->cub_bytes;
-    CK(cub::DeviceRadixSort::SortPairs(p->cub_tmp, bytes, p->sk_key, p->sk_key2, p->sk_val, p->sk_val2, S, 0, 32,
-                                       st));
-  }
-  // every rank places every seed (cheap, S-sized); the phase-1 worklist holds the own slab's part only
-  k_seed_groups<<<grid_for(S, 128), 128, 0, st>>>(g, p->nbm, p->sk_key2, p->sk_val2, p->sk_d, S, ss, d_dist, p->site1, p->bm,
-                                                  p->list_a, p->counters, p->zlo, p->zhi);
+  k_seed_groups<<<grid_for(S, 128), 128, 0, st>>>(g, p->nbm, p->sk_key, p->sk_d, S, ss, d_dist, p->site1, p->bm,
+                                                  p->list_a, p->sk_coll, p->counters, p->zlo, p->zhi);
   CKL("k_seed_groups");
+  k_seed_collisions<<<1, SEED_COLL_THREADS, 0, st>>>(p->sk_coll, p->sk_d, ss, d_dist, p->site1, p->counters);
+  CKL("k_seed_collisions");
   k_phase1_start<<<1, 1, 0, st>>>(p->ctl, p->counters, p->list_a, p->list_b, ss, d_dist, p->site1, 0);
   CKL("k_phase1_start");
   CK(cudaMemcpyAsync(p->h_ctl, p->ctl, sizeof(RoundCtl), cudaMemcpyDeviceToHost, st));
@@ -1598,17 +1613,17 @@ int lrcvt_mg_phase2(lrcvt_plan* p, int64_t n_sites, const int32_t* d_site_comp, 
   CKL("k_site1_to_state");
   k_phase2_copy<<<1, 1, 0, st>>>(p->eligible, p->d_nel, p->ctl, p->counters);
   CKL("k_phase2_copy");
-  CK(cudaMemcpyAsync(p->h_counters + 7, p->d_nel, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(p->h_counters + H_NEL, p->d_nel, sizeof(int), cudaMemcpyDeviceToHost, st));
   CKR(mg_sync(p, st, 1));
-  p->n_eligible = p->h_counters[7];
+  p->n_eligible = p->h_counters[H_NEL];
   p->h_ncur = (int)p->n_eligible;
   *n_frontier = p->h_ncur;
   return 0;
 }
 
-int lrcvt_mg_eval(lrcvt_plan* p, int32_t phase, int32_t sweep, int64_t* n_evaluated, int64_t* n_prop,
-                  int64_t* n_lo, int64_t* n_hi, void* stream) {
-  if (!p || phase < 1 || phase > 2 || !n_prop || !n_evaluated || !n_lo || !n_hi)
+int lrcvt_mg_eval(lrcvt_plan* p, int32_t phase, int32_t sweep, int64_t* n_evaluated, int64_t* n_lo,
+                  int64_t* n_hi, void* stream) {
+  if (!p || phase < 1 || phase > 2 || !n_evaluated || !n_lo || !n_hi || !p->mg_lo)
     return set_error(LRCVT_E_ARG, "lrcvt_mg_eval");
   cudaStream_t st = (cudaStream_t)stream;
   int n = p->h_ncur;
@@ -1618,24 +1633,11 @@ int lrcvt_mg_eval(lrcvt_plan* p, int32_t phase, int32_t sweep, int64_t* n_evalua
     CKL("k_sweep_start");
     n = (int)p->n_eligible;
   }
-  CK(cudaMemsetAsync(p->counters, 0, sizeof(int) * 2, st));
-  CK(cudaMemsetAsync(p->counters + C_LO, 0, sizeof(int) * 2, st));
+  // the per-round counters are zero here: reset by the last round end / begin / phase-2 start
   const int var = phase == 1 ? 0 : (p->g.dyadic ? 1 : 2);
-  if (n > 0) {
-    CKR(launch_eval_kernel(p, var, n, st));
-    if (!p->mg_lo) {
-      int rc = dalloc(&p->mg_lo, p->g.nxy);
-      rc |= dalloc(&p->mg_hi, p->g.nxy);
-      if (rc) return LRCVT_E_NOMEM;
-    }
-    k_mg_boundary<<<grid_for(n, 128, 148 * 16), 128, 0, st>>>(p->ctl, p->imp, p->pf, p->g.nxy, p->zlo, p->zhi,
-                                                              p->zlo > 0, p->zhi < p->g.nz, p->mg_lo, p->mg_hi,
-                                                              p->counters);
-    CKL("k_mg_boundary");
-  }
+  if (n > 0) CKR(launch_eval_kernel(p, var, n, st));  // + the boundary-plane proposals (ctl->bo)
   CKR(mg_sync(p, st, C_HI + 1));
   *n_evaluated = n;
-  *n_prop = p->h_counters[C_NIMP];
   *n_lo = p->h_counters[C_LO];
   *n_hi = p->h_counters[C_HI];
   return 0;
@@ -1647,21 +1649,32 @@ void* lrcvt_mg_boundary(lrcvt_plan* p, int32_t side) {
 }
 
 int lrcvt_mg_commit(lrcvt_plan* p, const void* d_halo, int64_t n_halo, int32_t sweep, int64_t* n_next,
-                    void* stream) {
-  if (!p || n_halo < 0 || (n_halo > 0 && !d_halo) || !n_next) return set_error(LRCVT_E_ARG, "lrcvt_mg_commit");
+                    int64_t* n_committed, void* stream) {
+  if (!p || n_halo < 0 || (n_halo > 0 && !d_halo) || !n_next || !n_committed)
+    return set_error(LRCVT_E_ARG, "lrcvt_mg_commit");
   cudaStream_t st = (cudaStream_t)stream;
   mg_t0(p, st);
-  CK(cudaMemsetAsync(p->counters, 0, sizeof(int) * 2, st));
+  // one launch: the own sparse proposals, then the received halo-plane proposals
   const int n = sweep ? (int)p->n_eligible : p->h_ncur;
-  if (n > 0) CKR(launch_commit_kernel(p, n, st));  // own sparse proposals
-  if (n_halo > 0) CKR(launch_commit_kernel(p, n_halo, st, (const Prop*)d_halo, n_halo));  // halo planes
-  // the host copy of the counters is taken before the round end resets them
-  CK(cudaMemcpyAsync(p->h_counters, p->counters, sizeof(int) * 2, cudaMemcpyDeviceToHost, st));
-  k_mg_round_end<<<1, 1, 0, st>>>(p->ctl, p->counters, sweep);
+  int64_t own_blocks = n > 0 ? (n + CM_SLOTS - 1) / CM_SLOTS : 0;
+  int64_t halo_blocks = n_halo > 0 ? (n_halo + CM_THREADS - 1) / CM_THREADS : 0;
+  if (own_blocks > p->commit_blocks) own_blocks = p->commit_blocks;
+  if (halo_blocks > p->commit_blocks) halo_blocks = p->commit_blocks;
+  if (own_blocks + halo_blocks > 0) {  // its last block ends the round (classify.cuh mg_round_end)
+    k_commit<<<(int)(own_blocks + halo_blocks), CM_THREADS, 0, st>>>(
+        p->imp, p->pf, 0, p->counters, p->ctl, p->g, p->nbm, p->bm, p->compact ? p->cbm : nullptr, nullptr,
+        p->ncl_arg(), cudaGraphConditionalHandle{}, sweep ? END_MG_SWEEP : END_MG, p->zlo, p->zhi,
+        (const Prop*)d_halo, (int)n_halo, (int)own_blocks, p->h_counters_dev);
+    CKL("k_commit");
+  } else {
+    k_mg_round_end<<<1, 1, 0, st>>>(p->ctl, p->counters, sweep, p->h_counters_dev);
+    CKL("k_mg_round_end");
+  }
   CKR(mg_sync(p, st, 0));
   const int nn = p->h_counters[C_NNEXT];
   p->h_ncur = nn;
   *n_next = nn;
+  *n_committed = p->h_counters[C_NIMP];
   return 0;
 }
 
@@ -1687,6 +1700,7 @@ int lrcvt_mg_vote_exact(lrcvt_plan* p, int64_t n_sites, const int32_t* d_site_sr
     return set_error(LRCVT_E_ARG, "lrcvt_mg_vote_exact");
   cudaStream_t st = (cudaStream_t)stream;
   const int S = (int)n_sites;
+  mg_t0(p, st);
   CK(cudaMemsetAsync(d_acc, 0, sizeof(uint64_t) * 4 * S, st));
   const int n_el = (int)p->n_eligible;
   if (n_el > 0) {
@@ -1699,17 +1713,18 @@ int lrcvt_mg_vote_exact(lrcvt_plan* p, int64_t n_sites, const int32_t* d_site_sr
                                                                         (unsigned long long*)d_acc, S, nullptr);
     CKL("k_vote_exact");
   }
-  return 0;
+  return mg_t1(p, st);
 }
 
 int lrcvt_mg_vote_exact_finish(lrcvt_plan* p, int64_t n_sites, const uint64_t* d_acc, double* d_sums, void* stream) {
   if (!p || n_sites < 1 || !d_acc || !d_sums) return set_error(LRCVT_E_ARG, "lrcvt_mg_vote_exact_finish");
   const int S = (int)n_sites;
   const Geo& g = p->g;
+  mg_t0(p, (cudaStream_t)stream);
   k_vote_exact_finish<<<grid_for(S, 256), 256, 0, (cudaStream_t)stream>>>((const unsigned long long*)d_acc, S,
                                                                           0.5 * g.sx, 0.5 * g.sy, 0.5 * g.sz, d_sums);
   CKL("k_vote_exact_finish");
-  return 0;
+  return mg_t1(p, (cudaStream_t)stream);
 }
 
 int lrcvt_mg_vote_box(lrcvt_plan* p, int64_t n_sites, const int32_t* d_site_src, int32_t* d_box, void* stream) {
@@ -1717,15 +1732,8 @@ int lrcvt_mg_vote_box(lrcvt_plan* p, int64_t n_sites, const int32_t* d_site_src,
     return set_error(LRCVT_E_ARG, "lrcvt_mg_vote_box");
   cudaStream_t st = (cudaStream_t)stream;
   const int S = (int)n_sites;
-  if (!p->vt_sp) {
-    int rc = dalloc(&p->vt_sp, p->g.n);
-    rc |= dalloc(&p->vt_box, 6 * p->max_sites);
-    if (rc) return LRCVT_E_NOMEM;
-  }
-  if (p->sp_stale) {
-    CK(cudaMemsetAsync(p->vt_sp, 0xff, sizeof(int2) * (size_t)p->g.n, st));
-    p->sp_stale = false;
-  }
+  mg_t0(p, st);
+  CKR(vote_buffers(p, st));
   k_box_init<<<grid_for(S, 256), 256, 0, st>>>(d_box, S);
   CKL("k_box_init");
   const int n_el = (int)p->n_eligible;
@@ -1739,7 +1747,7 @@ int lrcvt_mg_vote_box(lrcvt_plan* p, int64_t n_sites, const int32_t* d_site_src,
                                                                        d_box, S, nullptr);
     CKL("k_vote_prep");
   }
-  return 0;
+  return mg_t1(p, st);
 }
 
 int lrcvt_mg_vote_scan(lrcvt_plan* p, int64_t n_sites, const int32_t* d_site_comp, int32_t weight_mode,
@@ -1750,22 +1758,25 @@ int lrcvt_mg_vote_scan(lrcvt_plan* p, int64_t n_sites, const int32_t* d_site_com
     return set_error(LRCVT_E_ARG, "lrcvt_mg_vote_scan");
   const int S = (int)n_sites;
   const Geo& g = p->g;
+  mg_t0(p, (cudaStream_t)stream);
+  CKR(vote_order(p, d_box, S, (cudaStream_t)stream));
   k_vote_scan<4><<<grid_for(S, 4), 128, 0, (cudaStream_t)stream>>>(
-      p->vt_sp, p->comp, d_box, d_site_comp, S, g, (const double*)d_weights, (const float*)d_weights, weight_mode,
+      p->vt_sp, d_box, p->vt_order, d_site_comp, S, g, (const double*)d_weights, (const float*)d_weights, weight_mode,
       p->zlo, p->zhi < g.nz ? p->zhi : g.nz, mode, d_init, d_out);
   CKL("k_vote_scan");
-  return 0;
+  return mg_t1(p, (cudaStream_t)stream);
 }
 
 int lrcvt_mg_vote_carry(lrcvt_plan* p, int64_t n_sites, const int32_t* d_box, const double* d_res,
                         const double* d_carry_in, double* d_carry_out, void* stream) {
   if (!p || n_sites < 1 || !d_box || !d_res || !d_carry_out) return set_error(LRCVT_E_ARG, "lrcvt_mg_vote_carry");
   const int S = (int)n_sites;
+  mg_t0(p, (cudaStream_t)stream);
   k_vote_carry<<<grid_for(S, 256), 256, 0, (cudaStream_t)stream>>>(d_box, S, p->zlo,
                                                                    p->zhi < p->g.nz ? p->zhi : p->g.nz, d_res,
                                                                    d_carry_in, d_carry_out);
   CKL("k_vote_carry");
-  return 0;
+  return mg_t1(p, (cudaStream_t)stream);
 }
 
 int lrcvt_mg_move(lrcvt_plan* p, int64_t n_sites, const double* d_site_pos, const int32_t* d_site_comp,

@@ -204,7 +204,8 @@ __global__ void __launch_bounds__(WARPS * 32) k_vote_sum(const unsigned long lon
 // the eligible set is rebuilt, and k_vote_prep writes every eligible voxel,
 // so no stale entry survives.
 constexpr int BOX_BIG = 0x3fffffff;
-constexpr int VS_DEPTH = 4;  // chunks in flight per warp in k_vote_scan
+constexpr int VS_DEPTH = 4;  // chunks of (site, phi) / weight loads in flight per warp in k_vote_scan
+
 
 template <bool MG>
 __global__ void __launch_bounds__(256) k_vote_prep(const int* __restrict__ list, int n, Geo g,
@@ -243,6 +244,51 @@ __global__ void __launch_bounds__(256) k_vote_prep(const int* __restrict__ list,
   }
 }
 
+// Largest boxes first: k_vote_scan runs one warp per site and the walk time
+// follows the box volume (a few 100k-voxel boxes among 3.8k-voxel medians at
+// C4), so in site order the last waves ran a handful of long warps on an
+// otherwise idle GPU (SM active 54 % of the elapsed cycles). Sites are
+// bucketed by floor(log2(box volume)) and the scan takes them bucket by
+// bucket, biggest first (order within a bucket is free: every site's chain
+// is independent).
+constexpr int VO_BUCKETS = 64;
+__device__ __forceinline__ int vote_bucket(const int* __restrict__ box, int n_sites, int s) {
+  const long long w = box[3 * n_sites + s] - box[s] + 1, h = box[4 * n_sites + s] - box[n_sites + s] + 1,
+                  d = box[5 * n_sites + s] - box[2 * n_sites + s] + 1;
+  if (w <= 0 || h <= 0 || d <= 0) return 0;
+  return 63 - __clzll((unsigned long long)(w * h * d));
+}
+
+// hist[VO_BUCKETS] (zeroed by the caller) += sites per bucket
+__global__ void k_vote_order_hist(const int* __restrict__ box, int n_sites, int* __restrict__ hist) {
+  __shared__ int sh[VO_BUCKETS];
+  for (int b = threadIdx.x; b < VO_BUCKETS; b += blockDim.x) sh[b] = 0;
+  __syncthreads();
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s < n_sites) atomicAdd(&sh[vote_bucket(box, n_sites, s)], 1);
+  __syncthreads();
+  for (int b = threadIdx.x; b < VO_BUCKETS; b += blockDim.x)
+    if (sh[b]) atomicAdd(hist + b, sh[b]);
+}
+
+// order[] = site ids, largest bucket first; cursor[VO_BUCKETS] zeroed by the caller
+__global__ void k_vote_order_scatter(const int* __restrict__ box, int n_sites, const int* __restrict__ hist,
+                                     int* __restrict__ cursor, int* __restrict__ order) {
+  __shared__ int base[VO_BUCKETS];
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int b = VO_BUCKETS - 1; b >= 0; b--) {
+      base[b] = acc;
+      acc += hist[b];
+    }
+  }
+  __syncthreads();
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n_sites) return;
+  const int b = vote_bucket(box, n_sites, s);
+  order[base[b] + atomicAdd(cursor + b, 1)] = s;
+}
+
 __global__ void k_box_init(int* __restrict__ box, int n_sites) {
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= n_sites) return;
@@ -257,18 +303,49 @@ __global__ void k_box_init(int* __restrict__ box, int n_sites) {
 // start at 0), mode 2 = only sites whose box starts in an earlier slab
 // (chains continue from init[s], the running sums handed over by the
 // previous slab). Sites a mode skips are left untouched in `sums`.
+// acc + t[0] + ... + t[cnt-1] left to right over a chunk's staged terms
+// (row = one chain, 32 slots, slots >= cnt hold +0.0): groups of 8 loaded
+// ahead of their dependent adds, no per-term predicate. Adding the +0.0 pads
+// is exact -- acc starts at +0.0 and so can never become -0.0 -- so the chain
+// equals the reference's sequential sum (_kernels.py:528-531).
+constexpr int VS_ROW = 34;  // doubles per staged row (16-byte aligned, staggered banks)
+__device__ __forceinline__ double ordered_add_padded(double acc, const double* row, int cnt) {
+  for (int h = 0; h < cnt; h += 8) {
+    const double2 a = *reinterpret_cast<const double2*>(row + h);
+    const double2 b = *reinterpret_cast<const double2*>(row + h + 2);
+    const double2 c = *reinterpret_cast<const double2*>(row + h + 4);
+    const double2 d = *reinterpret_cast<const double2*>(row + h + 6);
+    acc = __dadd_rn(acc, a.x); acc = __dadd_rn(acc, a.y);
+    acc = __dadd_rn(acc, b.x); acc = __dadd_rn(acc, b.y);
+    acc = __dadd_rn(acc, c.x); acc = __dadd_rn(acc, c.y);
+    acc = __dadd_rn(acc, d.x); acc = __dadd_rn(acc, d.y);
+  }
+  return acc;
+}
+
+// One warp per site (order[]: largest boxes first); a (WARPS x 4 x VS_ROW) shared stage holds a chunk's
+// terms. The walk covers the box rows inside planes [zlo, zhi) (the whole
+// volume on one GPU). mode 0: every site, chains start at 0 (or init[s]);
+// multi-GPU slab steps: mode 1 = only sites whose box starts in this slab
+// (chains start at 0), mode 2 = only sites whose box starts in an earlier
+// slab (chains continue from init[s], the running sums handed over by the
+// previous slab). Sites a mode skips are left untouched in `sums`.
+// (A variant that read a 2-byte site tag per box voxel first and the 8-byte
+// entry only on a tag match moved more DRAM sectors, not fewer: 4.0 vs 3.7
+// GB per C4 launch, same time.)
 template <int WARPS>
-__global__ void __launch_bounds__(WARPS * 32) k_vote_scan(const int2* __restrict__ sp, const int* __restrict__ comp,
+__global__ void __launch_bounds__(WARPS * 32) k_vote_scan(const int2* __restrict__ sp,
                                                           const int* __restrict__ box,
+                                                          const int* __restrict__ order,
                                                           const int* __restrict__ site_comp, int n_sites, Geo g,
                                                           const double* __restrict__ w64,
                                                           const float* __restrict__ w32, int w_mode, int zlo,
                                                           int zhi, int mode, const double* __restrict__ init,
                                                           double* __restrict__ sums) {
-  __shared__ double buf[WARPS][32][4];
+  __shared__ __align__(16) double buf[WARPS][4][VS_ROW];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int s = blockIdx.x * WARPS + wid;
-  if (s >= n_sites) return;
+  if ((int)blockIdx.x * WARPS + wid >= n_sites) return;
+  const int s = order[blockIdx.x * WARPS + wid];
   const int x0 = box[s], y0 = box[n_sites + s], bz0 = box[2 * n_sites + s];
   const int bz1 = box[5 * n_sites + s];
   if (mode == 1 && !(bz0 >= zlo && bz0 < zhi)) return;
@@ -285,44 +362,67 @@ __global__ void __launch_bounds__(WARPS * 32) k_vote_scan(const int2* __restrict
     int dx = lane % W, r = lane / W;
     int dy = r % H, dz = r / H;
     long long k = lane;  // flat index of this lane's next voxel to load
-    // VS_DEPTH chunks in flight: (site, phi) and weight of every lane's voxel
-    // are loaded VS_DEPTH chunks ahead of the ordered adds
-    int2 a[VS_DEPTH];
-    double w[VS_DEPTH];
-    auto load = [&](int j) {
-      a[j] = make_int2(-1, -1);
-      w[j] = 0.0;
-      if (k < T) {
-        const int v = (x0 + dx) + g.nx * ((y0 + dy) + g.ny * (z0 + dz));
-        a[j] = __ldg(sp + v);
-        w[j] = vote_weight(v, w64, w32, w_mode);
-      }
+    // two-stage pipeline: stage 1 (DA chunks ahead) = the (site, phi) entry
+    // of every lane's voxel; stage 2 (VS_DEPTH chunks ahead, once stage 1
+    // arrived) = the raw weight of the voxels of this site only
+    constexpr int DA = 2 * VS_DEPTH;
+    int vi[DA];
+    int2 s1[DA];
+    int2 pa[VS_DEPTH];
+    double wd[VS_DEPTH];
+    float wf[VS_DEPTH];
+    auto next_voxel = [&]() {
+      int v = -1;
+      if (k < T) v = (x0 + dx) + g.nx * ((y0 + dy) + g.ny * (z0 + dz));
       k += 32;
       dx += qb;
       dy += qa;
       if (dx >= W) { dx -= W; dy++; }
       while (dy >= H) { dy -= H; dz++; }
+      return v;
+    };
+    auto load1 = [&](int j) {
+      vi[j] = next_voxel();
+      s1[j] = vi[j] >= 0 ? __ldg(sp + vi[j]) : make_int2(-1, -1);
+    };
+    auto load2 = [&](int j, int jp) {
+      pa[jp] = s1[j];
+      if (pa[jp].x == s) {  // raw weight: converted only when the term is formed
+        if (w_mode == 1) wd[jp] = __ldg(w64 + vi[j]);
+        else if (w_mode >= 2) wf[jp] = __ldg(w32 + vi[j]);
+      }
     };
 #pragma unroll
-    for (int j = 0; j < VS_DEPTH; j++) load(j);
-    for (long long base = 0; base < T; base += 32 * VS_DEPTH) {
+    for (int j = 0; j < DA; j++) load1(j);
 #pragma unroll
-      for (int j = 0; j < VS_DEPTH; j++) {
-        const bool mine = a[j].x == s;
-        const int u = a[j].y;
-        const double wt = w[j];
-        load(j);  // refill this slot VS_DEPTH chunks ahead
+    for (int j = 0; j < VS_DEPTH; j++) load2(j, j);
+    double* row = &buf[wid][lane & 3][0];
+    for (long long base = 0; base < T; base += 32 * DA) {
+#pragma unroll
+      for (int j = 0; j < DA; j++) {
+        const int jp = j % VS_DEPTH;
+        const int2 e = pa[jp];
+        const bool mine = e.x == s;
+        double wt = 0.0;
+        if (mine)
+          wt = w_mode == 0 ? 1.0
+               : w_mode == 1 ? wd[jp]
+               : w_mode == 2 ? (double)wf[jp]
+                             : __dmul_rn((double)wf[jp], (double)wf[jp]);  // m**1.0 / m**2.0
+        load2((j + VS_DEPTH) % DA, jp);  // chunk + VS_DEPTH, whose stage 1 was issued VS_DEPTH chunks ago
+        load1(j);                        // chunk + DA into the slot this chunk's stage 1 left
         const unsigned m = __ballot_sync(0xffffffffu, mine);
         if (m) {
-          if (mine) {
-            const double4 t = g.pack10 ? vote_term_packed(g, u, wt) : vote_term(g, u, wt);
-            const int slot = __popc(m & ((1u << lane) - 1u));
-            buf[wid][slot][0] = t.x; buf[wid][slot][1] = t.y; buf[wid][slot][2] = t.z; buf[wid][slot][3] = t.w;
-          }
-          __syncwarp();
           const int cnt = __popc(m);
-          if (lane < 4)
-            acc = ordered_add(acc, &buf[wid][0][lane], cnt);
+          // matching lanes take slots [0, cnt) in voxel order, the others
+          // write the +0.0 pads after them
+          const int below = __popc(m & ((1u << lane) - 1u));
+          const int slot = mine ? below : cnt + (lane - below);
+          double4 t = make_double4(0.0, 0.0, 0.0, 0.0);
+          if (mine) t = g.pack10 ? vote_term_packed(g, e.y, wt) : vote_term(g, e.y, wt);
+          buf[wid][0][slot] = t.x; buf[wid][1][slot] = t.y; buf[wid][2][slot] = t.z; buf[wid][3][slot] = t.w;
+          __syncwarp();
+          if (lane < 4) acc = ordered_add_padded(acc, row, cnt);
           __syncwarp();
         }
       }

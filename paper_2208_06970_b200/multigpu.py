@@ -281,6 +281,7 @@ class GlobalClassifier:
             self.engines[r] = eng
         self.timing = False  # per-rank device time (CUDA events around every rank's calls)
         self._ev = {r: [] for r in self.engines}
+        self._lib_ms = {r: {} for r in self.engines}
         pss, pdist = coll.peer_pointers(own)
         zb = (ctypes.c_int64 * (coll.world + 1))(*([lo for lo, _ in self.bounds] + [self.dims[2]]))
         arr_ss = (ctypes.c_void_p * coll.world)(*pss)
@@ -288,6 +289,12 @@ class GlobalClassifier:
         for r, eng in self.engines.items():
             _lib.check(self.L.lrcvt_mg_set_peers(eng.plan, coll.world, zb, arr_ss, arr_d), "lrcvt_mg_set_peers")
         self._S = 0
+
+    def reuse_sites(self, on: bool):
+        """keep each rank's eligible list across classifies (a Lloyd loop: the
+        site components do not change between iterations)"""
+        for eng in self.engines.values():
+            _lib.check(self.L.lrcvt_plan_reuse_eligible(eng.plan, 1 if on else 0), "reuse_eligible")
 
     def _st(self):
         return _lib.stream_handle(self.torch)
@@ -300,29 +307,41 @@ class GlobalClassifier:
         for eng in self.engines.values():
             _lib.check(self.L.lrcvt_mg_timing(eng.plan, 1 if on else 0, None), "lrcvt_mg_timing")
 
-    def _t(self, r, fn, synced=False):
-        """run fn() for rank r, bracketed by CUDA events when timing (synced steps are timed by the library)"""
-        if not self.timing or synced:
+    def _t(self, r, fn, synced=False, cat="other"):
+        """run fn() for rank r, bracketed by CUDA events when timing (synced
+        steps are timed by the library); the time is booked under cat"""
+        if not self.timing:
             return fn()
+        if synced:
+            out = fn()
+            ms = ctypes.c_double()
+            _lib.check(self.L.lrcvt_mg_timing(self.engines[r].plan, 1, ctypes.byref(ms)), "mg timing")
+            self._lib_ms[r][cat] = self._lib_ms[r].get(cat, 0.0) + ms.value
+            return out
         torch = self.torch
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
         out = fn()
         b.record()
-        self._ev[r].append((a, b))
+        self._ev[r].append((cat, a, b))
         return out
 
-    def rank_ms(self) -> dict:
+    def rank_ms(self, breakdown: bool = False) -> dict:
         """device milliseconds spent in each local rank's own kernels since the
-        last call (emulated ranks share one GPU and never overlap)"""
+        last call (emulated ranks share one GPU and never overlap); with
+        breakdown, {rank: {step category: ms}}"""
         self.torch.cuda.synchronize()
-        out = {r: sum(a.elapsed_time(b) for a, b in evs) for r, evs in self._ev.items()}
+        cats = {r: dict(self._lib_ms[r]) for r in self.engines}
+        for r, evs in self._ev.items():
+            for cat, a, b in evs:
+                cats[r][cat] = cats[r].get(cat, 0.0) + a.elapsed_time(b)
         self._ev = {r: [] for r in self.engines}
+        self._lib_ms = {r: {} for r in self.engines}
         for r, eng in self.engines.items():
             ms = ctypes.c_double()
             _lib.check(self.L.lrcvt_mg_timing(eng.plan, 1 if self.timing else 0, ctypes.byref(ms)), "mg timing")
-            out[r] += ms.value
-        return out
+            cats[r]["other"] = cats[r].get("other", 0.0) + ms.value
+        return cats if breakdown else {r: sum(c.values()) for r, c in cats.items()}
 
     def _round(self, phase: int, sweep: int, stats: dict) -> int:
         """One relaxation round (or sweep) on all ranks; returns the global
@@ -330,21 +349,23 @@ class GlobalClassifier:
         L, torch, st = self.L, self.torch, self._st()
         counts, lo, hi = {}, {}, {}
         for r, eng in self.engines.items():
-            ne, npr, nlo, nhi = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
-            self._t(r, lambda: _lib.check(L.lrcvt_mg_eval(eng.plan, phase, sweep, ctypes.byref(ne), ctypes.byref(npr),
-                                                          ctypes.byref(nlo), ctypes.byref(nhi), st), "lrcvt_mg_eval"), synced=True)
-            counts[r] = [int(ne.value), int(npr.value)]
+            ne, nlo, nhi = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+            self._t(r, lambda: _lib.check(L.lrcvt_mg_eval(eng.plan, phase, sweep, ctypes.byref(ne), ctypes.byref(nlo),
+                                                          ctypes.byref(nhi), st), "lrcvt_mg_eval"), synced=True,
+                    cat=f"eval_p{phase}")
+            counts[r] = int(ne.value)
             lo[r] = self._bytes(L.lrcvt_mg_boundary(eng.plan, 0), int(nlo.value))
             hi[r] = self._bytes(L.lrcvt_mg_boundary(eng.plan, 1), int(nhi.value))
         halo = self.coll.exchange_halo(lo, hi, torch)
         nexts = {}
         for r, eng in self.engines.items():
             h = halo[r]
-            nn = ctypes.c_int64()
+            nn, nc = ctypes.c_int64(), ctypes.c_int64()
             self._t(r, lambda: _lib.check(L.lrcvt_mg_commit(eng.plan, h.data_ptr() if h.numel() else None,
-                                                            h.numel() // PROP_BYTES, sweep, ctypes.byref(nn), st),
-                                          "lrcvt_mg_commit"), synced=True)
-            nexts[r] = [int(nn.value)] + counts[r]
+                                                            h.numel() // PROP_BYTES, sweep, ctypes.byref(nn),
+                                                            ctypes.byref(nc), st),
+                                          "lrcvt_mg_commit"), synced=True, cat="commit")
+            nexts[r] = [int(nn.value), counts[r], int(nc.value)]
         tot = self.coll.sum_ints(nexts)
         self._frontier = tot[0]
         stats["evaluations"] += tot[1]
@@ -377,7 +398,7 @@ class GlobalClassifier:
             rc = self._t(r, lambda: _lib.check(L.lrcvt_mg_begin(eng.plan, S, site_pos.data_ptr(),
                                                                 site_comp.data_ptr(), eng.ss.data_ptr(),
                                                                 eng.dist.data_ptr(), ctypes.byref(nf), st),
-                                               "lrcvt_mg_begin"), synced=True)
+                                               "lrcvt_mg_begin"), synced=True, cat="begin")
             bad = max(bad, rc)
             front[r] = [int(nf.value)]
         if bad > 0:
@@ -388,7 +409,7 @@ class GlobalClassifier:
         for r, eng in self.engines.items():
             nf = ctypes.c_int64()
             self._t(r, lambda: _lib.check(L.lrcvt_mg_phase2(eng.plan, S, site_comp.data_ptr(), ctypes.byref(nf),
-                                                            st), "phase2"), synced=True)
+                                                            st), "phase2"), synced=True, cat="phase2")
             front[r] = [int(nf.value)]
         self._frontier = self.coll.sum_ints(front)[0]
         while True:  # phase 2 + verification sweeps (tessellation.py:170-189)
@@ -400,7 +421,8 @@ class GlobalClassifier:
         for r, eng in self.engines.items():
             a = ctypes.c_int64()
             self._t(r, lambda: _lib.check(L.lrcvt_mg_finish(eng.plan, eng.ss.data_ptr(), eng.state.data_ptr(),
-                                                            ctypes.byref(a), st), "lrcvt_mg_finish"), synced=True)
+                                                            ctypes.byref(a), st), "lrcvt_mg_finish"), synced=True,
+                    cat="finish")
             assigned[r] = [int(a.value)]
         stats["assigned"] = self.coll.sum_ints(assigned)[0]
         return stats
@@ -418,7 +440,7 @@ class GlobalClassifier:
             for r, eng in self.engines.items():
                 a = torch.empty((4, S), dtype=torch.int64, device="cuda")
                 self._t(r, lambda: _lib.check(L.lrcvt_mg_vote_exact(eng.plan, S, eng.ss.data_ptr(), a.data_ptr(), st),
-                                              "vote"))
+                                              "vote"), synced=True, cat="vote")
                 acc[r] = a
             red = self.coll.allreduce(acc, "sum", torch)
             sums = torch.empty((4, S), dtype=torch.float64, device="cuda")
@@ -429,7 +451,7 @@ class GlobalClassifier:
             for r, eng in self.engines.items():
                 b = torch.empty((6, S), dtype=torch.int32, device="cuda")
                 self._t(r, lambda: _lib.check(L.lrcvt_mg_vote_box(eng.plan, S, eng.ss.data_ptr(), b.data_ptr(), st),
-                                              "vote box"))
+                                              "vote box"), synced=True, cat="vote")
                 boxes[r] = b
             lo = self.coll.allreduce({r: b[:3].contiguous() for r, b in boxes.items()}, "min", torch)
             hi = self.coll.allreduce({r: b[3:].contiguous() for r, b in boxes.items()}, "max", torch)
@@ -439,7 +461,7 @@ class GlobalClassifier:
                 out = torch.zeros((4, S), dtype=torch.float64, device="cuda")
                 self._t(r, lambda: _lib.check(L.lrcvt_mg_vote_scan(eng.plan, S, site_comp.data_ptr(), weight_mode, wp,
                                                                    1, box.data_ptr(), None, out.data_ptr(), st),
-                                              "vote scan"))
+                                              "vote scan"), synced=True, cat="vote")
                 res[r] = out
 
             def step(r, carry):  # sites continuing from earlier slabs, then the hand-over
@@ -447,11 +469,11 @@ class GlobalClassifier:
                 if carry is not None:
                     self._t(r, lambda: _lib.check(L.lrcvt_mg_vote_scan(eng.plan, S, site_comp.data_ptr(), weight_mode,
                                                                        wp, 2, box.data_ptr(), carry.data_ptr(),
-                                                                       res[r].data_ptr(), st), "vote scan"))
+                                                                       res[r].data_ptr(), st), "vote scan"), synced=True, cat="vote")
                 out = torch.empty((4, S), dtype=torch.float64, device="cuda")
                 self._t(r, lambda: _lib.check(L.lrcvt_mg_vote_carry(eng.plan, S, box.data_ptr(), res[r].data_ptr(),
                                                                     carry.data_ptr() if carry is not None else None,
-                                                                    out.data_ptr(), st), "vote carry"))
+                                                                    out.data_ptr(), st), "vote carry"), synced=True, cat="vote")
                 return out
 
             sums = self.coll.chain(step, (4, S), torch)
@@ -463,7 +485,8 @@ class GlobalClassifier:
             np_, dp_ = new_pos, disp
             self._t(r, lambda: _lib.check(L.lrcvt_mg_move(eng.plan, S, site_pos.data_ptr(), site_comp.data_ptr(),
                                                           sums.data_ptr(), float(backoff), np_.data_ptr(),
-                                                          dp_.data_ptr(), ctypes.byref(empty), st), "lrcvt_mg_move"), synced=True)
+                                                          dp_.data_ptr(), ctypes.byref(empty), st), "lrcvt_mg_move"), synced=True,
+                          cat="move")
         return new_pos, disp, int(empty.value)
 
     def own_slab(self, r):
@@ -503,15 +526,19 @@ def global_lrcvt(grid, labels, seeding, lloyd, coll=None):
     mode, w_d = lloyd_weight_mode(torch, grid, seeding, weights)
     vlen = voxel_length(grid.dims, grid.spacing)
     trace: list[float] = []
-    for _ in range(lloyd.max_updates):
-        gc.classify(pos_d, sc_d)
-        pos_d, disp, _ = gc.centroidal(pos_d, sc_d, mode, w_d, 0.5 * vlen)
-        d = disp.cpu().numpy()
-        mean_ds = float(d.mean() / vlen) if d.size else 0.0
-        trace.append(mean_ds)
-        if mean_ds < lloyd.ds_tolerance:
-            break
-    st = gc.classify(pos_d, sc_d)
+    gc.reuse_sites(True)  # site components fixed for the whole loop
+    try:
+        for _ in range(lloyd.max_updates):
+            gc.classify(pos_d, sc_d)
+            pos_d, disp, _ = gc.centroidal(pos_d, sc_d, mode, w_d, 0.5 * vlen)
+            d = disp.cpu().numpy()
+            mean_ds = float(d.mean() / vlen) if d.size else 0.0
+            trace.append(mean_ds)
+            if mean_ds < lloyd.ds_tolerance:
+                break
+        st = gc.classify(pos_d, sc_d)
+    finally:
+        gc.reuse_sites(False)
     n = grid.size
     site_of = np.full(n, -1, np.int32)
     src = np.full(n, -1, np.int32)

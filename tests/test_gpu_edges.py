@@ -68,6 +68,29 @@ def test_contested_seed_voxels_and_empty_regions(oracle_mod):
     assert tess.report["empty_regions"] >= 1
 
 
+def test_large_seed_collision_groups(oracle_mod):
+    """2600 sites in three voxels (exact duplicates and jittered positions:
+    distance ties inside EPS): the sort-free seed placement folds each group
+    in increasing site id over a multi-pass bitonic sort of the collisions."""
+    from paper_2208_06970_b200 import Site, VoxelGrid
+
+    dims = (16, 16, 4)
+    grid = VoxelGrid(dims, (1, 1, 1), {})
+    comp = np.zeros(int(np.prod(dims)), np.int32)
+    rng = np.random.default_rng(7)
+    cells = [(3, 3, 1), (9, 4, 0), (12, 12, 2)]
+    sites = []
+    for i in range(2600):
+        c = cells[i % 3]
+        if i % 5 == 0:
+            p = (c[0] + 0.5, c[1] + 0.5, c[2] + 0.5)
+        else:
+            p = (c[0] + rng.random(), c[1] + rng.random(), c[2] + rng.random())
+        sites.append(Site(p, 0))
+    tess = _check(grid, _labels(comp, dims), sites, oracle_mod)
+    assert tess.report["empty_regions"] >= 2597
+
+
 def test_components_without_sites_and_many_components(oracle_mod):
     from paper_2208_06970_b200 import (IsobandSpec, Site, VoxelGrid, classify_isobands, label_components)
 
