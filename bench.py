@@ -467,6 +467,7 @@ def run_global(args, cfg, world, rank, local):
     torch.cuda.synchronize()
     gc.set_timing(emulate)
     gc.rank_ms()
+    gc.calls = {r: {} for r in gc.engines}
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(int(os.environ.get("LRCVT_BENCH_DEVICE", local))) as clk:
         t0.record()
@@ -496,6 +497,8 @@ def run_global(args, cfg, world, rank, local):
                 "slowest_rank_ms_per_step": slow,
                 "slowest_rank_breakdown_ms_per_step": {
                     k: v / args.steps for k, v in per_cat[max(per_rank, key=per_rank.get)].items()},
+                "slowest_rank_calls_per_step": {
+                    k: v / args.steps for k, v in gc.calls[max(per_rank, key=per_rank.get)].items()},
                 "projected_value": grid.size / (slow / 1e3),
                 "note": "all slab ranks on ONE GPU one after another; each rank's own kernels timed with CUDA "
                         "events (the host round trips of the per-round count reads excluded; collectives are host "

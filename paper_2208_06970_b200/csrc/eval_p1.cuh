@@ -47,7 +47,8 @@ __device__ __forceinline__ void p1_tile(const int* __restrict__ list, int n, con
                                                    const double* __restrict__ dist,
                                                    const double4* __restrict__ site_pos,
                                                    uint32_t* __restrict__ bm,
-                                                   Prop* __restrict__ imp, uint8_t* __restrict__ pf) {
+                                                   Prop* __restrict__ imp, uint8_t* __restrict__ pf,
+                                                   const BoundaryOut* bo = nullptr) {
   // per-warp queue of speculated rays (no block-wide barrier needed)
   __shared__ int q_v[BLOCK * P1_SPEC], q_s[BLOCK * P1_SPEC];
   __shared__ unsigned char q_ok[BLOCK * P1_SPEC];
@@ -99,6 +100,8 @@ __device__ __forceinline__ void p1_tile(const int* __restrict__ list, int n, con
       const int k = 13 * h + q;
       const int s = nw[q];
       // ---- B: distinct-site table; the voxel's own site is not entered: its
+      // (skipping a batch's inserts when no lane of the warp sees a foreign
+      // site, and whole warps without candidates, measured 4.5 % slower at C4)
       // candidate (orig_d, orig_s, v) is the current state itself
       bool seen = s < 0 || s == orig_s;
 #pragma unroll
@@ -240,6 +243,7 @@ __device__ __forceinline__ void p1_tile(const int* __restrict__ list, int n, con
     Prop pr;
     pr.d = best_d; pr.v = v; pr.s = best_s; pr.src = best_src; pr.pad = 0;
     imp[i] = pr;
+    emit_boundary(bo, pr);
   }
   if (active) pf[i] = improved ? 1 : 0;
 }
@@ -261,7 +265,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_eval_p1(RoundCtl* __restrict__ 
   // (exact grid on the host path, size-class grid >= n inside the graph)
   const int base = blockIdx.x * BLOCK;
   if (base >= n) return;
-  p1_tile<BLOCK>(list, n, base + (int)threadIdx.x, g, comp, nbm, site1, dist, site_pos, bm, imp, pf);
+  p1_tile<BLOCK>(list, n, base + (int)threadIdx.x, g, comp, nbm, site1, dist, site_pos, bm, imp, pf, &ctl->bo);
 }
 
 }  // namespace lrcvt

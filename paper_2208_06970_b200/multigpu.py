@@ -257,14 +257,16 @@ class GlobalClassifier:
     peer view); its plan-owned state buffers are current on the own slab
     (engine.ss / engine.dist views of them, engine.state its state bits)."""
 
-    def __init__(self, dims, spacing, component: np.ndarray, n_components: int, max_sites: int, coll):
+    def __init__(self, dims, spacing, component: np.ndarray, n_components: int, max_sites: int, coll,
+                 bounds=None):
         torch = self.torch = _lib.require_cuda()
         self.L = _lib.lib()
         self.coll = coll
         self.dims = tuple(int(d) for d in dims)
         self.spacing = tuple(float(s) for s in spacing)
         self.n = int(np.prod(self.dims))
-        self.bounds = balanced_slab_bounds(component, self.dims, coll.world)
+        # z-slabs with about equal in-band voxel counts unless given ([(zlo, zhi)] per rank)
+        self.bounds = list(bounds) if bounds is not None else balanced_slab_bounds(component, self.dims, coll.world)
         self.engines = {}
         comp_dev = None
         own = {}
@@ -282,6 +284,7 @@ class GlobalClassifier:
         self.timing = False  # per-rank device time (CUDA events around every rank's calls)
         self._ev = {r: [] for r in self.engines}
         self._lib_ms = {r: {} for r in self.engines}
+        self.calls = {r: {} for r in self.engines}  # timed calls per category (timing mode)
         pss, pdist = coll.peer_pointers(own)
         zb = (ctypes.c_int64 * (coll.world + 1))(*([lo for lo, _ in self.bounds] + [self.dims[2]]))
         arr_ss = (ctypes.c_void_p * coll.world)(*pss)
@@ -316,7 +319,10 @@ class GlobalClassifier:
             out = fn()
             ms = ctypes.c_double()
             _lib.check(self.L.lrcvt_mg_timing(self.engines[r].plan, 1, ctypes.byref(ms)), "mg timing")
+            if callable(cat):
+                cat = cat()
             self._lib_ms[r][cat] = self._lib_ms[r].get(cat, 0.0) + ms.value
+            self.calls[r][cat] = self.calls[r].get(cat, 0) + 1
             return out
         torch = self.torch
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -352,7 +358,7 @@ class GlobalClassifier:
             ne, nlo, nhi = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
             self._t(r, lambda: _lib.check(L.lrcvt_mg_eval(eng.plan, phase, sweep, ctypes.byref(ne), ctypes.byref(nlo),
                                                           ctypes.byref(nhi), st), "lrcvt_mg_eval"), synced=True,
-                    cat=f"eval_p{phase}")
+                    cat=lambda: f"eval_p{phase}_" + _size_class(ne.value))
             counts[r] = int(ne.value)
             lo[r] = self._bytes(L.lrcvt_mg_boundary(eng.plan, 0), int(nlo.value))
             hi[r] = self._bytes(L.lrcvt_mg_boundary(eng.plan, 1), int(nhi.value))
@@ -451,7 +457,7 @@ class GlobalClassifier:
             for r, eng in self.engines.items():
                 b = torch.empty((6, S), dtype=torch.int32, device="cuda")
                 self._t(r, lambda: _lib.check(L.lrcvt_mg_vote_box(eng.plan, S, eng.ss.data_ptr(), b.data_ptr(), st),
-                                              "vote box"), synced=True, cat="vote")
+                                              "vote box"), synced=True, cat="vote_box")
                 boxes[r] = b
             lo = self.coll.allreduce({r: b[:3].contiguous() for r, b in boxes.items()}, "min", torch)
             hi = self.coll.allreduce({r: b[3:].contiguous() for r, b in boxes.items()}, "max", torch)
@@ -461,7 +467,7 @@ class GlobalClassifier:
                 out = torch.zeros((4, S), dtype=torch.float64, device="cuda")
                 self._t(r, lambda: _lib.check(L.lrcvt_mg_vote_scan(eng.plan, S, site_comp.data_ptr(), weight_mode, wp,
                                                                    1, box.data_ptr(), None, out.data_ptr(), st),
-                                              "vote scan"), synced=True, cat="vote")
+                                              "vote scan"), synced=True, cat="vote_scan1")
                 res[r] = out
 
             def step(r, carry):  # sites continuing from earlier slabs, then the hand-over
@@ -469,11 +475,11 @@ class GlobalClassifier:
                 if carry is not None:
                     self._t(r, lambda: _lib.check(L.lrcvt_mg_vote_scan(eng.plan, S, site_comp.data_ptr(), weight_mode,
                                                                        wp, 2, box.data_ptr(), carry.data_ptr(),
-                                                                       res[r].data_ptr(), st), "vote scan"), synced=True, cat="vote")
+                                                                       res[r].data_ptr(), st), "vote scan"), synced=True, cat="vote_scan2")
                 out = torch.empty((4, S), dtype=torch.float64, device="cuda")
                 self._t(r, lambda: _lib.check(L.lrcvt_mg_vote_carry(eng.plan, S, box.data_ptr(), res[r].data_ptr(),
                                                                     carry.data_ptr() if carry is not None else None,
-                                                                    out.data_ptr(), st), "vote carry"), synced=True, cat="vote")
+                                                                    out.data_ptr(), st), "vote carry"), synced=True, cat="vote_carry")
                 return out
 
             sums = self.coll.chain(step, (4, S), torch)
@@ -497,6 +503,11 @@ class GlobalClassifier:
 
     def any_engine(self) -> Engine:
         return next(iter(self.engines.values()))
+
+
+def _size_class(n: int) -> str:
+    """timing category of a round by its per-rank frontier size"""
+    return "small" if n <= 2048 else ("mid" if n <= 65536 else "big")
 
 
 def _pow2(s: float) -> bool:

@@ -191,3 +191,47 @@ def test_global_classify_two_processes_gloo_ipc():
         mp.spawn(_two_proc_worker, args=(2, port, d), nprocs=2, join=True)
         for r in range(2):
             assert open(os.path.join(d, f"r{r}")).read() == "ok", r
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_global_lloyd_large_frontiers_matches_single_domain(world):
+    """Frontiers of tens of thousands of voxels per slab (the thread-per-voxel
+    eval kernels, not only the warp-per-voxel ones), balanced slabs, the
+    eligible list kept across two Lloyd iterations: arrays, counters and the
+    moved sites equal the single-domain engine's."""
+    import torch
+
+    from paper_2208_06970_b200 import SeedingParams, seed_sites, voxel_weights
+    from paper_2208_06970_b200.multigpu import Emulated, GlobalClassifier
+    from paper_2208_06970_b200.tessellation import engine_for, lloyd_weight_mode, voxel_length
+
+    grid, labels, _, _ = _setup("random-smooth", (96, 88, 80), [0.35, 0.5, 0.65], 40)
+    params = SeedingParams(alpha=600, seed=7, weight_field="g", gamma=1.0)
+    sites, _ = seed_sites(grid, labels, params)
+    w = voxel_weights(grid, params)
+    S = len(sites)
+    pos = torch.from_numpy(np.array([s.position for s in sites])).cuda()
+    sc = torch.from_numpy(np.array([s.component_id for s in sites], np.int32)).cuda()
+    mode, w_d = lloyd_weight_mode(torch, grid, params, w)
+    backoff = 0.5 * voxel_length(grid.dims, grid.spacing)
+    eng = engine_for(labels, grid.spacing, S)
+    eng.L.lrcvt_plan_reuse_eligible(eng.plan, 1)
+    gc = GlobalClassifier(grid.dims, grid.spacing, labels.component, labels.n_components, S, Emulated(world))
+    gc.reuse_sites(True)
+    p1, p2 = pos.clone(), pos.clone()
+    try:
+        for _ in range(2):
+            st1 = eng.classify(p1, sc, want_state=True)
+            st2 = gc.classify(p2, sc)
+            assert st1["evaluations"] > 2048 * world * 10
+            for k in ("rounds", "sweeps", "evaluations", "commits", "assigned"):
+                assert st1[k] == st2[k], k
+            for r in gc.engines:
+                v0, v1, e = gc.own_slab(r)
+                for name in ("ss", "dist", "state"):
+                    assert torch.equal(getattr(eng, name)[v0:v1], getattr(e, name)[v0:v1]), (r, name)
+            p1, _, _, _ = eng.centroidal(p1, sc, mode, w_d, backoff)
+            p2, _, _ = gc.centroidal(p2, sc, mode, w_d, backoff)
+            assert torch.equal(p1, p2)
+    finally:
+        eng.L.lrcvt_plan_reuse_eligible(eng.plan, 0)
