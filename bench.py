@@ -462,6 +462,17 @@ def run_global(args, cfg, world, rank, local):
     gc.reuse_sites(True)  # Lloyd loop: site components fixed
     for _ in range(args.warmup):
         pos_d = step(pos_d)
+    bounds0 = list(gc.bounds)
+    if not args.no_rebalance:
+        # slab bounds from measured per-rank device time: one calibration iteration (not timed), re-cut,
+        # one more warm-up iteration on the new bounds
+        gc.set_timing(True)
+        gc.rank_ms()
+        pos_d = step(pos_d)
+        cost = gc.rank_ms()
+        gc.set_timing(False)
+        gc.rebalance(cost)
+        pos_d = step(pos_d)
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
@@ -489,7 +500,8 @@ def run_global(args, cfg, world, rank, local):
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "mode": "global", "slabs": coll.world,
             "config": bench_config(cfg, grid.size, S, inband), "clocks": clk.summary(),
-            "counters": {k: last[k] for k in ("rounds", "sweeps", "evaluations", "commits") if k in last}}
+            "counters": {k: last[k] for k in ("rounds", "sweeps", "evaluations", "commits") if k in last},
+            "slabs_z": [list(b) for b in gc.bounds], "slabs_z_inband_balanced": [list(b) for b in bounds0]}
         if emulate:
             slow = max(per_rank.values()) / args.steps
             line["emulated_ranks"] = {
@@ -578,6 +590,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-passes", action="store_true")
+    ap.add_argument("--no-rebalance", action="store_true",
+                    help="--mode global: keep the in-band-balanced slab bounds (no calibration iteration)")
     ap.add_argument("--emulate-ranks", type=int, default=1,
                     help="--mode global on one process: run this many z-slab ranks on the one GPU")
     ap.add_argument("--mode", default=None, choices=["blocks", "global"],

@@ -258,9 +258,19 @@ struct lrcvt_plan {
   int* seg_e = nullptr;
   int2* vt_sp = nullptr;  // (site, phi) per voxel for the bounding-box vote
   bool sp_stale = true;   // vt_sp must be reset to -1 before the next k_vote_prep
+  bool vote_deep = false;  // k_vote_add with 8 entry / 4 weight batches in flight (LRCVT_VOTE_DEEP=1)
   int* vt_box = nullptr;  // [6][S] per-site bounding boxes
-  int* vt_order = nullptr;  // [S] sites by box volume, largest first (k_vote_scan's schedule)
+  int* vt_order = nullptr;  // [S] sites by box volume, largest first (k_vote_add's schedule)
   int* vt_hist = nullptr;   // [2][VO_BUCKETS] bucket counts / cursors
+  // the walk / sum split of the ordered chains (vote.cuh k_vote_nseg .. k_vote_add)
+  int* vt_nseg = nullptr;    // [S] walk segments per site
+  int* vt_seg0 = nullptr;    // [S] first segment of each site
+  int* vt_tot = nullptr;     // [2] segments, entries
+  int* h_vt = nullptr;       // pinned copy of the segment total
+  int vt_seg_cap = 0;        // segments vt_cnt / vt_off hold
+  int* vt_cnt = nullptr;     // [segments] entries per segment
+  int* vt_off = nullptr;     // [segments] first entry of each segment
+  int2* vt_ent = nullptr;    // [in-band] (phi, v) per site in voxel order
   bool vote_bbox = true;  // LRCVT_VOTE=sort: stable radix sort of (site, (phi, v)) pairs instead
   // cub
   void* cub_tmp = nullptr;
@@ -728,6 +738,7 @@ int lrcvt_plan_create(lrcvt_plan** plan, int64_t nx, int64_t ny, int64_t nz, dou
   if (const char* e = getenv("LRCVT_EW_SMALL")) p->ew_small = atoi(e);
   if (const char* e = getenv("LRCVT_SWITCH")) p->class_switch = e[0] != '0';
   if (const char* e = getenv("LRCVT_VOTE")) p->vote_bbox = strcmp(e, "sort") != 0;
+  if (const char* e = getenv("LRCVT_VOTE_DEEP")) p->vote_deep = e[0] == '1';
   if (const char* e = getenv("LRCVT_COMPACT")) p->compact = e[0] == '1';
   if (const char* e = getenv("LRCVT_P1_MINB")) p->p1_big_minb = atoi(e);
   if (const char* e = getenv("LRCVT_P2_MINB")) p->p2_minb = atoi(e);
@@ -902,11 +913,13 @@ int lrcvt_plan_destroy(lrcvt_plan* p) {
                   p->cbm, p->ct_status, p->ct_state, p->nbm, p->site1, p->has_site,
                   p->site_pos, p->new_pos, p->sk_key, p->sk_coll, p->sk_d,
                   p->acc, p->sums, p->vt_key, p->vt_key2, p->vt_pv, p->vt_pv2,
-                  p->seg_b, p->seg_e, p->vt_sp, p->vt_box, p->vt_order, p->vt_hist, p->mg_own_ss, p->mg_own_dist, p->d_pv,
+                  p->seg_b, p->seg_e, p->vt_sp, p->vt_box, p->vt_order, p->vt_hist, p->vt_nseg, p->vt_seg0, p->vt_tot,
+                  p->vt_cnt, p->vt_off, p->vt_ent, p->mg_own_ss, p->mg_own_dist, p->d_pv,
                   p->mg_lo, p->mg_hi, p->cub_tmp};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (p->h_counters) cudaFreeHost(p->h_counters);
+  if (p->h_vt) cudaFreeHost(p->h_vt);
   if (p->ev0) cudaEventDestroy(p->ev0);
   if (p->ev1) cudaEventDestroy(p->ev1);
   if (p->ev2) cudaEventDestroy(p->ev2);
@@ -1082,6 +1095,11 @@ static int vote_buffers(lrcvt_plan* p, cudaStream_t st) {
     rc |= dalloc(&p->vt_box, 6 * p->max_sites);
     rc |= dalloc(&p->vt_order, p->max_sites);
     rc |= dalloc(&p->vt_hist, 2 * VO_BUCKETS);
+    rc |= dalloc(&p->vt_nseg, p->max_sites);
+    rc |= dalloc(&p->vt_seg0, p->max_sites);
+    rc |= dalloc(&p->vt_tot, 2);
+    rc |= dalloc(&p->vt_ent, p->n_inband > 0 ? p->n_inband : 1);
+    if (!rc && cudaMallocHost((void**)&p->h_vt, sizeof(int) * 2) != cudaSuccess) rc = LRCVT_E_NOMEM;
     if (rc) return LRCVT_E_NOMEM;
   }
   if (p->sp_stale) {
@@ -1091,7 +1109,7 @@ static int vote_buffers(lrcvt_plan* p, cudaStream_t st) {
   return 0;
 }
 
-// k_vote_scan's site order from the boxes: largest first (vote.cuh)
+// k_vote_add's site order from the boxes: largest first (vote.cuh)
 static int vote_order(lrcvt_plan* p, const int* d_box, int S, cudaStream_t st) {
   CK(cudaMemsetAsync(p->vt_hist, 0, sizeof(int) * 2 * VO_BUCKETS, st));
   k_vote_order_hist<<<grid_for(S, 256), 256, 0, st>>>(d_box, S, p->vt_hist);
@@ -1099,6 +1117,49 @@ static int vote_order(lrcvt_plan* p, const int* d_box, int S, cudaStream_t st) {
   k_vote_order_scatter<<<grid_for(S, 256), 256, 0, st>>>(d_box, S, p->vt_hist, p->vt_hist + VO_BUCKETS,
                                                           p->vt_order);
   CKL("k_vote_order_scatter"); LAUNCHED(1);
+  return 0;
+}
+
+// the ordered chains of every site over planes [zlo, zhi) (mode / init as
+// vote.cuh describes): walk segments counted, compacted into per-site entry
+// runs in voxel order, then summed one warp per site, largest boxes first
+static int vote_chains(lrcvt_plan* p, const int* d_box, int S, int w_mode, const void* d_weights, int zlo, int zhi,
+                       int mode, const double* d_init, double* d_out, cudaStream_t st) {
+  const Geo& g = p->g;
+  CKR(vote_order(p, d_box, S, st));
+  k_vote_nseg<<<grid_for(S, 256), 256, 0, st>>>(d_box, S, zlo, zhi, mode, p->vt_nseg);
+  CKL("k_vote_nseg"); LAUNCHED(1);
+  k_scan_excl<<<1, SCAN_THREADS, 0, st>>>(p->vt_nseg, S, p->vt_seg0, p->vt_tot);
+  CKL("k_scan_excl"); LAUNCHED(1);
+  CK(cudaMemcpyAsync(p->h_vt, p->vt_tot, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));  // the segment count sizes the next launches' arrays
+  const int n_seg = p->h_vt[0];
+  if (n_seg > p->vt_seg_cap) {
+    cudaFree(p->vt_cnt);
+    cudaFree(p->vt_off);
+    p->vt_cnt = p->vt_off = nullptr;
+    p->vt_seg_cap = n_seg + n_seg / 4 + 1024;
+    if (dalloc(&p->vt_cnt, p->vt_seg_cap) || dalloc(&p->vt_off, p->vt_seg_cap)) {
+      p->vt_seg_cap = 0;
+      return LRCVT_E_NOMEM;
+    }
+  }
+  if (n_seg > 0) {
+    k_vote_walk<false><<<148 * 8, 128, 0, st>>>(p->vt_sp, d_box, S, g, zlo, zhi, mode, p->vt_seg0, p->vt_tot,
+                                                 p->vt_cnt, nullptr, nullptr);
+    CKL("k_vote_walk<count>"); LAUNCHED(1);
+    k_scan_excl<<<1, SCAN_THREADS, 0, st>>>(p->vt_cnt, n_seg, p->vt_off, p->vt_tot + 1);
+    CKL("k_scan_excl"); LAUNCHED(1);
+    k_vote_walk<true><<<148 * 8, 128, 0, st>>>(p->vt_sp, d_box, S, g, zlo, zhi, mode, p->vt_seg0, p->vt_tot,
+                                                nullptr, p->vt_off, p->vt_ent);
+    CKL("k_vote_walk<write>"); LAUNCHED(1);
+  } else {
+    CK(cudaMemsetAsync(p->vt_tot + 1, 0, sizeof(int), st));
+  }
+  (p->vote_deep ? k_vote_add<4, 8, 4> : k_vote_add<4>)<<<grid_for(S, 4), 128, 0, st>>>(
+      p->vt_order, S, g, (const double*)d_weights, (const float*)d_weights, w_mode, mode, d_init, p->vt_seg0,
+      p->vt_nseg, p->vt_off, p->vt_tot + 1, p->vt_tot, p->vt_ent, d_out);
+  CKL("k_vote_add"); LAUNCHED(1);
   return 0;
 }
 
@@ -1139,7 +1200,7 @@ int lrcvt_centroidal_update(lrcvt_plan* p, int64_t n_sites, const double* d_site
                                                           p->sums);
     CKL("k_vote_exact_finish"); LAUNCHED(1);
   } else if (p->vote_bbox) {
-    // ordered path, sort-free: per-site bounding-box walk (vote.cuh k_vote_prep / k_vote_scan)
+    // ordered path, sort-free: per-site bounding-box walk (vote.cuh k_vote_prep, k_vote_nseg .. k_vote_add)
     CKR(vote_buffers(p, st));
     k_box_init<<<grid_for(S, 256), 256, 0, st>>>(p->vt_box, S);
     CKL("k_box_init"); LAUNCHED(1);
@@ -1148,11 +1209,7 @@ int lrcvt_centroidal_update(lrcvt_plan* p, int64_t n_sites, const double* d_site
                                                                        S, nullptr);
       CKL("k_vote_prep"); LAUNCHED(1);
     }
-    CKR(vote_order(p, p->vt_box, S, st));
-    k_vote_scan<4><<<grid_for(S, 4), 128, 0, st>>>(
-        p->vt_sp, p->vt_box, p->vt_order, d_site_comp, S, g, (const double*)d_weights, (const float*)d_weights,
-        weight_mode, 0, g.nz, 0, nullptr, p->sums);
-    CKL("k_vote_scan"); LAUNCHED(1);
+    CKR(vote_chains(p, p->vt_box, S, weight_mode, d_weights, 0, (int)g.nz, 0, nullptr, p->sums, st));
   } else {
     const int64_t nin = p->n_inband > 0 ? p->n_inband : 1;
     int rc = 0;
@@ -1759,11 +1816,8 @@ int lrcvt_mg_vote_scan(lrcvt_plan* p, int64_t n_sites, const int32_t* d_site_com
   const int S = (int)n_sites;
   const Geo& g = p->g;
   mg_t0(p, (cudaStream_t)stream);
-  CKR(vote_order(p, d_box, S, (cudaStream_t)stream));
-  k_vote_scan<4><<<grid_for(S, 4), 128, 0, (cudaStream_t)stream>>>(
-      p->vt_sp, d_box, p->vt_order, d_site_comp, S, g, (const double*)d_weights, (const float*)d_weights, weight_mode,
-      p->zlo, p->zhi < g.nz ? p->zhi : g.nz, mode, d_init, d_out);
-  CKL("k_vote_scan");
+  CKR(vote_chains(p, d_box, S, weight_mode, d_weights, p->zlo, p->zhi < g.nz ? p->zhi : (int)g.nz, mode, d_init,
+                  d_out, (cudaStream_t)stream));
   return mg_t1(p, (cudaStream_t)stream);
 }
 

@@ -11,10 +11,10 @@
 //     the sequential fp64 sum equals the exact integer sum. Kernels reduce
 //     (2x+1) integers with warp match/reduce + 64-bit integer atomics and
 //     scale once: order-independent AND identical to the reference.
-//   * ORDERED path (any weights): one warp per site walks the site's
-//     bounding box in voxel order and four lanes add the terms
-//     (w, RN(w*ax), RN(w*ay), RN(w*az)) of the region's voxels in exactly
-//     the reference order (k_vote_prep / k_vote_scan below). The earlier
+//   * ORDERED path (any weights): the site's bounding box walked in voxel
+//     order finds its region's voxels; four lanes add their terms
+//     (w, RN(w*ax), RN(w*ay), RN(w*az)) in exactly the reference order
+//     (k_vote_prep, then the walk / sum kernels below). The earlier
 //     variant -- a stable radix sort of (site, (phi(v), v)) pairs, then
 //     k_vote_sum over the segments -- stays behind LRCVT_VOTE=sort.
 #pragma once
@@ -196,15 +196,15 @@ __global__ void __launch_bounds__(WARPS * 32) k_vote_sum(const unsigned long lon
 //   k_vote_prep  over the eligible list (voxel order): phi by chasing src,
 //                (site, phi) stored per voxel, per-site bounding box by warp
 //                match + reduce_min/max and six atomics per site group;
-//   k_vote_scan  one warp per site walks its box in chunks of 32 voxels
-//                (flat box order), picks the voxels of its region, forms their
-//                terms and lanes 0-3 add them in order -- the reference's
+//   k_vote_nseg .. k_vote_add  the boxes walked in parallel segments that
+//                compact each region's voxels in voxel order, then one warp
+//                per site adds their terms in that order -- the reference's
 //                exact accumulation order (_kernels.py:519-531).
 // A voxel belongs to region s iff sp[v].x == s: sp is reset to -1 whenever
 // the eligible set is rebuilt, and k_vote_prep writes every eligible voxel,
 // so no stale entry survives.
 constexpr int BOX_BIG = 0x3fffffff;
-constexpr int VS_DEPTH = 4;  // chunks of (site, phi) / weight loads in flight per warp in k_vote_scan
+constexpr int VS_DEPTH = 4;  // batches of loads in flight per warp in k_vote_walk (x2) / k_vote_add
 
 
 template <bool MG>
@@ -244,13 +244,12 @@ __global__ void __launch_bounds__(256) k_vote_prep(const int* __restrict__ list,
   }
 }
 
-// Largest boxes first: k_vote_scan runs one warp per site and the walk time
-// follows the box volume (a few 100k-voxel boxes among 3.8k-voxel medians at
-// C4), so in site order the last waves ran a handful of long warps on an
-// otherwise idle GPU (SM active 54 % of the elapsed cycles). Sites are
-// bucketed by floor(log2(box volume)) and the scan takes them bucket by
-// bucket, biggest first (order within a bucket is free: every site's chain
-// is independent).
+// Largest boxes first: k_vote_add runs one warp per site and its time
+// follows the region size (a few 50k-voxel regions among 3.8k-voxel medians
+// at C4); in site order the last waves ran a handful of long warps on an
+// otherwise idle GPU. Sites are bucketed by floor(log2(box volume)) and
+// taken bucket by bucket, biggest first (order within a bucket is free:
+// every site's chain is independent).
 constexpr int VO_BUCKETS = 64;
 __device__ __forceinline__ int vote_bucket(const int* __restrict__ box, int n_sites, int s) {
   const long long w = box[3 * n_sites + s] - box[s] + 1, h = box[4 * n_sites + s] - box[n_sites + s] + 1,
@@ -323,109 +322,226 @@ __device__ __forceinline__ double ordered_add_padded(double acc, const double* r
   return acc;
 }
 
-// One warp per site (order[]: largest boxes first); a (WARPS x 4 x VS_ROW) shared stage holds a chunk's
-// terms. The walk covers the box rows inside planes [zlo, zhi) (the whole
-// volume on one GPU). mode 0: every site, chains start at 0 (or init[s]);
+// The walk of site s in this call: its box rows inside planes [zlo, zhi);
+// false when the mode skips the site. mode 0: every site, chains start at 0;
 // multi-GPU slab steps: mode 1 = only sites whose box starts in this slab
 // (chains start at 0), mode 2 = only sites whose box starts in an earlier
 // slab (chains continue from init[s], the running sums handed over by the
-// previous slab). Sites a mode skips are left untouched in `sums`.
-// (A variant that read a 2-byte site tag per box voxel first and the 8-byte
-// entry only on a tag match moved more DRAM sectors, not fewer: 4.0 vs 3.7
-// GB per C4 launch, same time.)
-template <int WARPS>
-__global__ void __launch_bounds__(WARPS * 32) k_vote_scan(const int2* __restrict__ sp,
-                                                          const int* __restrict__ box,
-                                                          const int* __restrict__ order,
-                                                          const int* __restrict__ site_comp, int n_sites, Geo g,
-                                                          const double* __restrict__ w64,
-                                                          const float* __restrict__ w32, int w_mode, int zlo,
-                                                          int zhi, int mode, const double* __restrict__ init,
-                                                          double* __restrict__ sums) {
-  __shared__ __align__(16) double buf[WARPS][4][VS_ROW];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  if ((int)blockIdx.x * WARPS + wid >= n_sites) return;
-  const int s = order[blockIdx.x * WARPS + wid];
-  const int x0 = box[s], y0 = box[n_sites + s], bz0 = box[2 * n_sites + s];
-  const int bz1 = box[5 * n_sites + s];
-  if (mode == 1 && !(bz0 >= zlo && bz0 < zhi)) return;
-  if (mode == 2 && !(bz0 < zlo && bz1 >= zlo)) return;
-  const int z0 = bz0 > zlo ? bz0 : zlo;
+// previous slab). Sites a mode skips are left untouched in the sums.
+struct VoteRange {
+  int x0, y0, z0, W, H, D;
+  long long T;  // box voxels to walk (0: none)
+};
+__device__ __forceinline__ bool vote_range(const int* __restrict__ box, int n_sites, int s, int zlo, int zhi,
+                                           int mode, VoteRange& r) {
+  const int bz0 = box[2 * n_sites + s], bz1 = box[5 * n_sites + s];
+  if (mode == 1 && !(bz0 >= zlo && bz0 < zhi)) return false;
+  if (mode == 2 && !(bz0 < zlo && bz1 >= zlo)) return false;
+  r.x0 = box[s];
+  r.y0 = box[n_sites + s];
+  r.z0 = bz0 > zlo ? bz0 : zlo;
   const int z1 = bz1 < zhi - 1 ? bz1 : zhi - 1;
-  const int W = box[3 * n_sites + s] - x0 + 1, H = box[4 * n_sites + s] - y0 + 1, D = z1 - z0 + 1;
-  double acc = (init && mode != 1 && lane < 4) ? init[lane * n_sites + s] : 0.0;
-  if (W > 0 && H > 0 && D > 0) {
-    const long long T = (long long)W * H * D;
-    // flat box index k = lane + 32 * chunk -> (dx, dy, dz); 32 = qa * W + qb,
-    // so a chunk advance is dx += qb, dy += qa plus at most one x carry
+  r.W = box[3 * n_sites + s] - r.x0 + 1;
+  r.H = box[4 * n_sites + s] - r.y0 + 1;
+  r.D = z1 - r.z0 + 1;
+  r.T = (r.W > 0 && r.H > 0 && r.D > 0) ? (long long)r.W * r.H * r.D : 0;
+  return true;
+}
+
+// The ordered chains, walk and sum apart. The box walk has no order
+// dependence, only the sum does, so the walk runs in parallel and the
+// sequential part reads densely packed terms:
+//   k_vote_nseg   per site: its walk (the box rows in this call's planes)
+//                 cut into VS_SEG-voxel segments of flat box order;
+//   k_scan_excl   segment numbering per site (exclusive prefix sums);
+//   k_vote_walk   one warp per segment, grid-stride: COUNT = how many of
+//                 the segment's voxels belong to the site; after a prefix sum
+//                 over the counts, WRITE = those voxels' (phi, v) in voxel
+//                 order at the segment's offset. Each site's entries end up
+//                 contiguous and in increasing voxel order, every in-band
+//                 voxel exactly once (a counting sort by site, stable);
+//   k_vote_add    one warp per site, largest boxes first: lanes form 32
+//                 terms at a time (weights and entries loaded ahead), lanes
+//                 0-3 add them in order -- the reference's accumulation
+//                 (_kernels.py:519-531), so the sums are bit-identical.
+// (The previous one-warp-per-site walk that summed as it went was bound by
+// its largest boxes: 3.6 ms per C4 iteration, 1.6 ms on one of 8 slabs.)
+constexpr int VS_SEG = 4096;
+
+// nseg[s] = segments of site s's walk in this call (0: mode skips it / empty box)
+__global__ void k_vote_nseg(const int* __restrict__ box, int n_sites, int zlo, int zhi, int mode,
+                            int* __restrict__ nseg) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n_sites) return;
+  VoteRange rg;
+  nseg[s] = vote_range(box, n_sites, s, zlo, zhi, mode, rg) ? (int)((rg.T + VS_SEG - 1) / VS_SEG) : 0;
+}
+
+// out[i] = in[0] + ... + in[i-1] over n values, *total = the sum (one CTA;
+// every thread scans a contiguous run)
+constexpr int SCAN_THREADS = 1024;
+__global__ void __launch_bounds__(SCAN_THREADS) k_scan_excl(const int* __restrict__ in, int n, int* __restrict__ out,
+                                                            int* __restrict__ total) {
+  __shared__ int wsum[SCAN_THREADS / 32];
+  const int per = (n + SCAN_THREADS - 1) / SCAN_THREADS;
+  const int i0 = min(n, threadIdx.x * per), i1 = min(n, i0 + per);
+  int mine = 0;
+  for (int i = i0; i < i1; i++) mine += in[i];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int incl = mine;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  if (lane == 31) wsum[wid] = incl;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int w = 0; w < SCAN_THREADS / 32; w++) {
+      const int t = wsum[w];
+      wsum[w] = acc;
+      acc += t;
+    }
+    *total = acc;
+  }
+  __syncthreads();
+  int run = wsum[wid] + incl - mine;
+  for (int i = i0; i < i1; i++) {
+    const int v = in[i];
+    out[i] = run;
+    run += v;
+  }
+}
+
+// the site whose segment range [seg0[s], seg0[s] + nseg[s]) holds segment k
+__device__ __forceinline__ int vote_seg_site(const int* __restrict__ seg0, int n_sites, int k) {
+  int lo = 0, hi = n_sites - 1;  // largest s with seg0[s] <= k (empty sites share their successor's start)
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (__ldg(seg0 + mid) <= k) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
+// WRITE = false: cnt[k] = the segment's voxels of its site; WRITE = true:
+// their (phi, v) in voxel order at ent[off[k] ...]
+template <bool WRITE>
+__global__ void __launch_bounds__(128) k_vote_walk(const int2* __restrict__ sp, const int* __restrict__ box,
+                                                   int n_sites, Geo g, int zlo, int zhi, int mode,
+                                                   const int* __restrict__ seg0, const int* __restrict__ n_seg_total,
+                                                   int* __restrict__ cnt, const int* __restrict__ off,
+                                                   int2* __restrict__ ent) {
+  const int lane = threadIdx.x & 31;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  const int n_seg = *n_seg_total;
+  for (int k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; k < n_seg; k += warps) {  // warp-uniform
+    const int s = vote_seg_site(seg0, n_sites, k);
+    VoteRange rg;
+    vote_range(box, n_sites, s, zlo, zhi, mode, rg);
+    const long long kb = (long long)(k - __ldg(seg0 + s)) * VS_SEG;
+    const long long ke = min(rg.T, kb + VS_SEG);
+    int n_out = 0;
+    int2* out = WRITE ? ent + off[k] : nullptr;
+    const int W = rg.W, H = rg.H;
     const int qa = 32 / W, qb = 32 - qa * W;
-    int dx = lane % W, r = lane / W;
-    int dy = r % H, dz = r / H;
-    long long k = lane;  // flat index of this lane's next voxel to load
-    // two-stage pipeline: stage 1 (DA chunks ahead) = the (site, phi) entry
-    // of every lane's voxel; stage 2 (VS_DEPTH chunks ahead, once stage 1
-    // arrived) = the raw weight of the voxels of this site only
-    constexpr int DA = 2 * VS_DEPTH;
-    int vi[DA];
-    int2 s1[DA];
-    int2 pa[VS_DEPTH];
-    double wd[VS_DEPTH];
-    float wf[VS_DEPTH];
-    auto next_voxel = [&]() {
-      int v = -1;
-      if (k < T) v = (x0 + dx) + g.nx * ((y0 + dy) + g.ny * (z0 + dz));
-      k += 32;
+    long long kk = kb + lane;
+    int dx = (int)(kk % W);
+    const long long rr = kk / W;
+    int dy = (int)(rr % H), dz = (int)(rr / H);
+    int2 a[2 * VS_DEPTH];
+    int vv[2 * VS_DEPTH];
+    auto load = [&](int j) {
+      vv[j] = -1;
+      a[j] = make_int2(-1, -1);
+      if (kk < ke) {
+        vv[j] = (rg.x0 + dx) + g.nx * ((rg.y0 + dy) + g.ny * (rg.z0 + dz));
+        a[j] = __ldg(sp + vv[j]);
+      }
+      kk += 32;
       dx += qb;
       dy += qa;
       if (dx >= W) { dx -= W; dy++; }
       while (dy >= H) { dy -= H; dz++; }
-      return v;
-    };
-    auto load1 = [&](int j) {
-      vi[j] = next_voxel();
-      s1[j] = vi[j] >= 0 ? __ldg(sp + vi[j]) : make_int2(-1, -1);
-    };
-    auto load2 = [&](int j, int jp) {
-      pa[jp] = s1[j];
-      if (pa[jp].x == s) {  // raw weight: converted only when the term is formed
-        if (w_mode == 1) wd[jp] = __ldg(w64 + vi[j]);
-        else if (w_mode >= 2) wf[jp] = __ldg(w32 + vi[j]);
-      }
     };
 #pragma unroll
-    for (int j = 0; j < DA; j++) load1(j);
+    for (int j = 0; j < 2 * VS_DEPTH; j++) load(j);
+    for (long long base = kb; base < ke; base += 32 * 2 * VS_DEPTH) {
 #pragma unroll
-    for (int j = 0; j < VS_DEPTH; j++) load2(j, j);
-    double* row = &buf[wid][lane & 3][0];
-    for (long long base = 0; base < T; base += 32 * DA) {
-#pragma unroll
-      for (int j = 0; j < DA; j++) {
-        const int jp = j % VS_DEPTH;
-        const int2 e = pa[jp];
-        const bool mine = e.x == s;
-        double wt = 0.0;
-        if (mine)
-          wt = w_mode == 0 ? 1.0
-               : w_mode == 1 ? wd[jp]
-               : w_mode == 2 ? (double)wf[jp]
-                             : __dmul_rn((double)wf[jp], (double)wf[jp]);  // m**1.0 / m**2.0
-        load2((j + VS_DEPTH) % DA, jp);  // chunk + VS_DEPTH, whose stage 1 was issued VS_DEPTH chunks ago
-        load1(j);                        // chunk + DA into the slot this chunk's stage 1 left
+      for (int j = 0; j < 2 * VS_DEPTH; j++) {
+        const bool mine = a[j].x == s;
+        const int phi = a[j].y, v = vv[j];
+        load(j);
         const unsigned m = __ballot_sync(0xffffffffu, mine);
-        if (m) {
-          const int cnt = __popc(m);
-          // matching lanes take slots [0, cnt) in voxel order, the others
-          // write the +0.0 pads after them
-          const int below = __popc(m & ((1u << lane) - 1u));
-          const int slot = mine ? below : cnt + (lane - below);
-          double4 t = make_double4(0.0, 0.0, 0.0, 0.0);
-          if (mine) t = g.pack10 ? vote_term_packed(g, e.y, wt) : vote_term(g, e.y, wt);
-          buf[wid][0][slot] = t.x; buf[wid][1][slot] = t.y; buf[wid][2][slot] = t.z; buf[wid][3][slot] = t.w;
-          __syncwarp();
-          if (lane < 4) acc = ordered_add_padded(acc, row, cnt);
-          __syncwarp();
-        }
+        if (WRITE && mine) out[n_out + __popc(m & ((1u << lane) - 1u))] = make_int2(phi, v);
+        n_out += __popc(m);
       }
+    }
+    if (!WRITE && lane == 0) cnt[k] = n_out;
+  }
+}
+
+// one warp per site (order[]: largest boxes first): the ordered chains over
+// the site's entries ent[off[seg0[s]] .. off[seg0[s] + nseg[s]]) -- contiguous,
+// in voxel order. Entries are loaded VS_DEPTH batches ahead and the weights
+// of a batch two batches ahead (once its entries arrived).
+template <int WARPS, int DE = VS_DEPTH, int DW = 2>
+__global__ void __launch_bounds__(WARPS * 32) k_vote_add(const int* __restrict__ order, int n_sites, Geo g,
+                                                         const double* __restrict__ w64,
+                                                         const float* __restrict__ w32, int w_mode, int mode,
+                                                         const double* __restrict__ init,
+                                                         const int* __restrict__ seg0, const int* __restrict__ nseg,
+                                                         const int* __restrict__ off, const int* __restrict__ n_ent,
+                                                         const int* __restrict__ n_seg_total,
+                                                         const int2* __restrict__ ent, double* __restrict__ sums) {
+  __shared__ __align__(16) double buf[WARPS][4][VS_ROW];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if ((int)blockIdx.x * WARPS + wid >= n_sites) return;
+  const int s = order[blockIdx.x * WARPS + wid];
+  if (mode != 0 && nseg[s] == 0) return;  // a slab step this site does not take part in: untouched
+  const int k0 = seg0[s], k1 = k0 + nseg[s];
+  const int e0 = k0 < *n_seg_total ? off[k0] : *n_ent;
+  const int e1 = k1 < *n_seg_total ? off[k1] : *n_ent;
+  double acc = (init && mode != 1 && lane < 4) ? init[lane * n_sites + s] : 0.0;
+  double* row = &buf[wid][lane & 3][0];
+  // DE entry batches in flight; the weights of a batch are loaded DW batches ahead of its use
+  int2 q[DE];
+  double wd[DW];
+  float wf[DW];
+  auto ld_ent = [&](int j, int c) { q[j] = c + lane < e1 ? __ldg(ent + c + lane) : make_int2(0, -1); };
+  auto ld_w = [&](int jw, int j) {
+    if (q[j].y >= 0) {
+      if (w_mode == 1) wd[jw] = __ldg(w64 + q[j].y);
+      else if (w_mode >= 2) wf[jw] = __ldg(w32 + q[j].y);
+    }
+  };
+#pragma unroll
+  for (int j = 0; j < DE; j++) ld_ent(j, e0 + 32 * j);
+#pragma unroll
+  for (int j = 0; j < DW; j++) ld_w(j, j);
+  for (int c0 = e0; c0 < e1; c0 += 32 * DE) {
+#pragma unroll
+    for (int j = 0; j < DE; j++) {
+      const int c = c0 + 32 * j;
+      if (c >= e1) break;  // warp-uniform
+      const int jw = j % DW;
+      const int2 e = q[j];
+      const bool mine = e.y >= 0;
+      double wt = 0.0;
+      if (mine)
+        wt = w_mode == 0 ? 1.0
+             : w_mode == 1 ? wd[jw]
+             : w_mode == 2 ? (double)wf[jw]
+                           : __dmul_rn((double)wf[jw], (double)wf[jw]);  // m**1.0 / m**2.0
+      ld_w(jw, (j + DW) % DE);         // batch c + DW: its entries were loaded DE - DW batches ago
+      ld_ent(j, c + 32 * DE);          // batch c + DE into the slot this batch left
+      double4 t = make_double4(0.0, 0.0, 0.0, 0.0);  // lanes past the end: the +0.0 pads
+      if (mine) t = g.pack10 ? vote_term_packed(g, e.x, wt) : vote_term(g, e.x, wt);
+      buf[wid][0][lane] = t.x; buf[wid][1][lane] = t.y; buf[wid][2][lane] = t.z; buf[wid][3][lane] = t.w;
+      __syncwarp();
+      if (lane < 4) acc = ordered_add_padded(acc, row, min(32, e1 - c));
+      __syncwarp();
     }
   }
   if (lane < 4) sums[lane * n_sites + s] = acc;

@@ -54,14 +54,17 @@ def slab_bounds(nz: int, world: int) -> list[tuple[int, int]]:
     return out
 
 
-def balanced_slab_bounds(component: np.ndarray, dims, world: int) -> list[tuple[int, int]]:
-    """z-slabs holding about equal numbers of in-band voxels (the work of a
-    rank follows its in-band voxels, not its planes); every slab keeps at
-    least one plane. Any bounds give the same results bit for bit."""
+def plane_inband(component: np.ndarray, dims) -> np.ndarray:
+    """in-band voxels per z-plane"""
     nx, ny, nz = (int(d) for d in dims)
+    return np.count_nonzero(np.asarray(component).reshape(nz, ny * nx) >= 0, axis=1).astype(np.float64)
+
+
+def _cut(per: np.ndarray, world: int) -> list[tuple[int, int]]:
+    """z-slabs of about equal total `per` (a cost per plane); every slab keeps at least one plane"""
+    nz = per.size
     if world > nz:
         raise ValueError(f"cannot split {nz} planes into {world} non-empty slabs")
-    per = np.count_nonzero(np.asarray(component).reshape(nz, ny * nx) >= 0, axis=1).astype(np.float64)
     cum = np.concatenate([[0.0], np.cumsum(per)])
     total = cum[-1]
     cuts = [0]
@@ -71,6 +74,26 @@ def balanced_slab_bounds(component: np.ndarray, dims, world: int) -> list[tuple[
         cuts.append(z)
     cuts.append(nz)
     return [(cuts[r], cuts[r + 1]) for r in range(world)]
+
+
+def balanced_slab_bounds(component: np.ndarray, dims, world: int) -> list[tuple[int, int]]:
+    """z-slabs holding about equal numbers of in-band voxels (the work of a
+    rank follows its in-band voxels, not its planes). Any bounds give the
+    same results bit for bit."""
+    return _cut(plane_inband(component, dims), world)
+
+
+def cost_balanced_bounds(inband: np.ndarray, bounds, rank_cost) -> list[tuple[int, int]]:
+    """Re-cut the slabs from measured per-rank costs: each plane's cost is its
+    in-band voxel count times the measured cost per in-band voxel of the
+    slab that holds it now; the new slabs carry equal predicted cost."""
+    per = np.asarray(inband, dtype=np.float64).copy()
+    for (lo, hi), c in zip(bounds, rank_cost):
+        n = per[lo:hi].sum()
+        per[lo:hi] *= (float(c) / n) if n > 0 else 0.0
+    if per.sum() <= 0:
+        return list(bounds)
+    return _cut(per + 1e-12 * per.max(), len(bounds))
 
 
 class _DevBuf:
@@ -126,6 +149,9 @@ class Emulated:
             carry = step(r, carry)
         return carry
 
+    def gather_floats(self, per_rank: dict) -> list[float]:
+        return [float(per_rank[r]) for r in range(self.world)]
+
     def peer_pointers(self, own: dict):
         """own: {rank: (ss_ptr, dist_ptr)} -> lists over all ranks."""
         return [own[r][0] for r in range(self.world)], [own[r][1] for r in range(self.world)]
@@ -160,6 +186,14 @@ class TorchDist:
         out = [torch.empty_like(t) for _ in range(self.world)]
         self.dist.all_gather(out, t, group=self.group)
         return [int(v) for x in out for v in x.tolist()]
+
+    def gather_floats(self, per_rank: dict) -> list[float]:
+        import torch
+
+        t = torch.tensor([float(per_rank[self.rank])], dtype=torch.float64, device=self.device)
+        out = [torch.empty_like(t) for _ in range(self.world)]
+        self.dist.all_gather(out, t, group=self.group)
+        return [float(x.item()) for x in out]
 
     def sum_ints(self, per_rank: dict) -> list[int]:
         import torch
@@ -266,7 +300,8 @@ class GlobalClassifier:
         self.spacing = tuple(float(s) for s in spacing)
         self.n = int(np.prod(self.dims))
         # z-slabs with about equal in-band voxel counts unless given ([(zlo, zhi)] per rank)
-        self.bounds = list(bounds) if bounds is not None else balanced_slab_bounds(component, self.dims, coll.world)
+        self._inband = plane_inband(component, self.dims)
+        self.bounds = list(bounds) if bounds is not None else _cut(self._inband, coll.world)
         self.engines = {}
         comp_dev = None
         own = {}
@@ -285,13 +320,33 @@ class GlobalClassifier:
         self._ev = {r: [] for r in self.engines}
         self._lib_ms = {r: {} for r in self.engines}
         self.calls = {r: {} for r in self.engines}  # timed calls per category (timing mode)
-        pss, pdist = coll.peer_pointers(own)
-        zb = (ctypes.c_int64 * (coll.world + 1))(*([lo for lo, _ in self.bounds] + [self.dims[2]]))
-        arr_ss = (ctypes.c_void_p * coll.world)(*pss)
-        arr_d = (ctypes.c_void_p * coll.world)(*pdist)
-        for r, eng in self.engines.items():
-            _lib.check(self.L.lrcvt_mg_set_peers(eng.plan, coll.world, zb, arr_ss, arr_d), "lrcvt_mg_set_peers")
+        self._peers = coll.peer_pointers(own)
+        self._set_peers()
         self._S = 0
+
+    def _set_peers(self):
+        world = self.coll.world
+        pss, pdist = self._peers
+        zb = (ctypes.c_int64 * (world + 1))(*([lo for lo, _ in self.bounds] + [self.dims[2]]))
+        arr_ss = (ctypes.c_void_p * world)(*pss)
+        arr_d = (ctypes.c_void_p * world)(*pdist)
+        for r, eng in self.engines.items():
+            _lib.check(self.L.lrcvt_mg_set_peers(eng.plan, world, zb, arr_ss, arr_d), "lrcvt_mg_set_peers")
+
+    def rebalance(self, rank_cost: dict) -> list[tuple[int, int]]:
+        """Move the slab bounds so that every rank carries the same predicted
+        cost, from the costs measured on the current bounds ({local rank:
+        cost}; gathered over the collective). Results stay bit-identical:
+        the bounds only decide who computes what. Returns the new bounds."""
+        costs = self.coll.gather_floats(rank_cost)
+        new = cost_balanced_bounds(self._inband, self.bounds, costs)
+        if new != self.bounds:
+            self.bounds = new
+            for r, eng in self.engines.items():
+                lo, hi = new[r]
+                _lib.check(self.L.lrcvt_mg_set_slab(eng.plan, lo, hi), "lrcvt_mg_set_slab")
+            self._set_peers()
+        return new
 
     def reuse_sites(self, on: bool):
         """keep each rank's eligible list across classifies (a Lloyd loop: the

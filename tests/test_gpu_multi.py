@@ -197,8 +197,8 @@ def test_global_classify_two_processes_gloo_ipc():
 def test_global_lloyd_large_frontiers_matches_single_domain(world):
     """Frontiers of tens of thousands of voxels per slab (the thread-per-voxel
     eval kernels, not only the warp-per-voxel ones), balanced slabs, the
-    eligible list kept across two Lloyd iterations: arrays, counters and the
-    moved sites equal the single-domain engine's."""
+    eligible list kept across Lloyd iterations, slabs re-cut before the third:
+    arrays, counters and the moved sites equal the single-domain engine's."""
     import torch
 
     from paper_2208_06970_b200 import SeedingParams, seed_sites, voxel_weights
@@ -220,7 +220,10 @@ def test_global_lloyd_large_frontiers_matches_single_domain(world):
     gc.reuse_sites(True)
     p1, p2 = pos.clone(), pos.clone()
     try:
-        for _ in range(2):
+        for it in range(3):
+            if it == 2:  # re-cut the slabs mid-run (rebalance from made-up costs): still bit-identical
+                old = list(gc.bounds)
+                assert gc.rebalance({r: 3.0 if r == 0 else 1.0 for r in gc.engines}) != old
             st1 = eng.classify(p1, sc, want_state=True)
             st2 = gc.classify(p2, sc)
             assert st1["evaluations"] > 2048 * world * 10

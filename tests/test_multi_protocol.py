@@ -24,6 +24,22 @@ def test_slab_bounds():
         slab_bounds(3, 4)
 
 
+def test_cost_balanced_bounds():
+    """measured per-rank costs move the cuts toward the expensive slab; equal
+    intensities keep the in-band balance"""
+    from paper_2208_06970_b200.multigpu import cost_balanced_bounds, plane_inband
+
+    inb = np.ones(100)
+    b = [(0, 25), (25, 50), (50, 75), (75, 100)]
+    assert cost_balanced_bounds(inb, b, [1, 1, 1, 1]) == b
+    nb = cost_balanced_bounds(inb, b, [2, 1, 1, 1])
+    assert nb[0][1] < 25 and nb[0][0] == 0 and nb[-1][1] == 100
+    assert all(lo < hi for lo, hi in nb) and all(nb[r][1] == nb[r + 1][0] for r in range(3))
+    comp = np.full((6, 4, 4), -1, np.int32)
+    comp[:, :, :2] = 0
+    assert plane_inband(comp.reshape(-1), (4, 4, 6)).tolist() == [8.0] * 6
+
+
 class _CpuTorch:
     """torch with "cuda" tensors mapped to the CPU (the protocol test has no GPU)."""
 
@@ -57,6 +73,7 @@ def _worker(rank, world, port, outdir):
         coll = TorchDist(device="cpu")
         assert coll.local_ranks == [rank] and coll.world == world
         assert coll.all_counts([rank * 10 + 1]) == [r * 10 + 1 for r in range(world)]
+        assert coll.gather_floats({rank: 0.5 + rank}) == [0.5 + r for r in range(world)]  # rebalance costs
         for sizes in ([3, 5], [0, 4], [0, 0], [7, 0]):
             mine = sizes[rank] * PROP_BYTES
             local = torch.arange(mine, dtype=torch.int64).remainder(251).to(torch.uint8) + rank
