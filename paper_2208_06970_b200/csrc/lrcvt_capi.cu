@@ -256,9 +256,8 @@ struct lrcvt_plan {
   unsigned long long* vt_pv2 = nullptr;
   int* seg_b = nullptr;
   int* seg_e = nullptr;
-  int2* vt_sp = nullptr;  // (site, phi) per voxel for the bounding-box vote
+  int* vt_sp = nullptr;   // [2][n] site / phi planes per voxel for the bounding-box vote
   bool sp_stale = true;   // vt_sp must be reset to -1 before the next k_vote_prep
-  bool vote_deep = false;  // k_vote_add with 8 entry / 4 weight batches in flight (LRCVT_VOTE_DEEP=1)
   int* vt_box = nullptr;  // [6][S] per-site bounding boxes
   int* vt_order = nullptr;  // [S] sites by box volume, largest first (k_vote_add's schedule)
   int* vt_hist = nullptr;   // [2][VO_BUCKETS] bucket counts / cursors
@@ -738,7 +737,6 @@ int lrcvt_plan_create(lrcvt_plan** plan, int64_t nx, int64_t ny, int64_t nz, dou
   if (const char* e = getenv("LRCVT_EW_SMALL")) p->ew_small = atoi(e);
   if (const char* e = getenv("LRCVT_SWITCH")) p->class_switch = e[0] != '0';
   if (const char* e = getenv("LRCVT_VOTE")) p->vote_bbox = strcmp(e, "sort") != 0;
-  if (const char* e = getenv("LRCVT_VOTE_DEEP")) p->vote_deep = e[0] == '1';
   if (const char* e = getenv("LRCVT_COMPACT")) p->compact = e[0] == '1';
   if (const char* e = getenv("LRCVT_P1_MINB")) p->p1_big_minb = atoi(e);
   if (const char* e = getenv("LRCVT_P2_MINB")) p->p2_minb = atoi(e);
@@ -1091,7 +1089,7 @@ int lrcvt_classify(lrcvt_plan* p, int64_t n_sites, const double* d_site_pos,
 static int vote_buffers(lrcvt_plan* p, cudaStream_t st) {
   const size_t n = (size_t)p->g.n;
   if (!p->vt_sp) {
-    int rc = dalloc(&p->vt_sp, n);
+    int rc = dalloc(&p->vt_sp, 2 * n);
     rc |= dalloc(&p->vt_box, 6 * p->max_sites);
     rc |= dalloc(&p->vt_order, p->max_sites);
     rc |= dalloc(&p->vt_hist, 2 * VO_BUCKETS);
@@ -1103,7 +1101,7 @@ static int vote_buffers(lrcvt_plan* p, cudaStream_t st) {
     if (rc) return LRCVT_E_NOMEM;
   }
   if (p->sp_stale) {
-    CK(cudaMemsetAsync(p->vt_sp, 0xff, sizeof(int2) * n, st));
+    CK(cudaMemsetAsync(p->vt_sp, 0xff, sizeof(int) * n, st));  // the site plane
     p->sp_stale = false;
   }
   return 0;
@@ -1156,7 +1154,7 @@ static int vote_chains(lrcvt_plan* p, const int* d_box, int S, int w_mode, const
   } else {
     CK(cudaMemsetAsync(p->vt_tot + 1, 0, sizeof(int), st));
   }
-  (p->vote_deep ? k_vote_add<4, 8, 4> : k_vote_add<4>)<<<grid_for(S, 4), 128, 0, st>>>(
+  k_vote_add<4, 8, 4><<<grid_for(S, 4), 128, 0, st>>>(
       p->vt_order, S, g, (const double*)d_weights, (const float*)d_weights, w_mode, mode, d_init, p->vt_seg0,
       p->vt_nseg, p->vt_off, p->vt_tot + 1, p->vt_tot, p->vt_ent, d_out);
   CKL("k_vote_add"); LAUNCHED(1);

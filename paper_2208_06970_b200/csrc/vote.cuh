@@ -200,16 +200,18 @@ __global__ void __launch_bounds__(WARPS * 32) k_vote_sum(const unsigned long lon
 //                compact each region's voxels in voxel order, then one warp
 //                per site adds their terms in that order -- the reference's
 //                exact accumulation order (_kernels.py:519-531).
-// A voxel belongs to region s iff sp[v].x == s: sp is reset to -1 whenever
-// the eligible set is rebuilt, and k_vote_prep writes every eligible voxel,
-// so no stale entry survives.
+// The per-voxel entries are two int planes: site vs[v] and phi vs[n + v]
+// (the walks read the 4-byte site of every box voxel and the phi of their
+// own voxels only). A voxel belongs to region s iff vs[v] == s: the site
+// plane is reset to -1 whenever the eligible set is rebuilt, and
+// k_vote_prep writes every eligible voxel, so no stale entry survives.
 constexpr int BOX_BIG = 0x3fffffff;
 constexpr int VS_DEPTH = 4;  // batches of loads in flight per warp in k_vote_walk (x2) / k_vote_add
 
 
 template <bool MG>
 __global__ void __launch_bounds__(256) k_vote_prep(const int* __restrict__ list, int n, Geo g,
-                                                   const int2* __restrict__ ss, int2* __restrict__ sp,
+                                                   const int2* __restrict__ ss, int* __restrict__ vs,
                                                    int* __restrict__ box, int n_sites,
                                                    const PeerView* __restrict__ pv) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -227,7 +229,8 @@ __global__ void __launch_bounds__(256) k_vote_prep(const int* __restrict__ list,
       }
       // phi as packed coordinates when every axis fits 10 bits (saves the
       // scan a flat-index decode per term), else the flat index
-      sp[v] = make_int2(s, u >= 0 && g.pack10 ? phi_pack(g, u) : u);
+      vs[v] = s;
+      vs[g.n + v] = u >= 0 && g.pack10 ? phi_pack(g, u) : u;
     }
     const unsigned grp = __match_any_sync(0xffffffffu, s);
     const int x0 = __reduce_min_sync(grp, x), x1 = __reduce_max_sync(grp, x);
@@ -426,16 +429,20 @@ __device__ __forceinline__ int vote_seg_site(const int* __restrict__ seg0, int n
 }
 
 // WRITE = false: cnt[k] = the segment's voxels of its site; WRITE = true:
-// their (phi, v) in voxel order at ent[off[k] ...]
+// their (phi, v) in voxel order at ent[off[k] ...]. Sites are loaded
+// 2 * VS_DEPTH batches ahead, the phi of the site's own voxels VS_DEPTH
+// batches ahead (WRITE only).
 template <bool WRITE>
-__global__ void __launch_bounds__(128) k_vote_walk(const int2* __restrict__ sp, const int* __restrict__ box,
+__global__ void __launch_bounds__(128) k_vote_walk(const int* __restrict__ vs, const int* __restrict__ box,
                                                    int n_sites, Geo g, int zlo, int zhi, int mode,
                                                    const int* __restrict__ seg0, const int* __restrict__ n_seg_total,
                                                    int* __restrict__ cnt, const int* __restrict__ off,
                                                    int2* __restrict__ ent) {
+  constexpr int DA = 2 * VS_DEPTH;
   const int lane = threadIdx.x & 31;
   const int warps = (gridDim.x * blockDim.x) >> 5;
   const int n_seg = *n_seg_total;
+  const int* __restrict__ vphi = vs + g.n;
   for (int k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; k < n_seg; k += warps) {  // warp-uniform
     const int s = vote_seg_site(seg0, n_sites, k);
     VoteRange rg;
@@ -450,14 +457,14 @@ __global__ void __launch_bounds__(128) k_vote_walk(const int2* __restrict__ sp, 
     int dx = (int)(kk % W);
     const long long rr = kk / W;
     int dy = (int)(rr % H), dz = (int)(rr / H);
-    int2 a[2 * VS_DEPTH];
-    int vv[2 * VS_DEPTH];
+    int st[DA], vv[DA];
+    int ph[VS_DEPTH];
     auto load = [&](int j) {
       vv[j] = -1;
-      a[j] = make_int2(-1, -1);
+      st[j] = -1;
       if (kk < ke) {
         vv[j] = (rg.x0 + dx) + g.nx * ((rg.y0 + dy) + g.ny * (rg.z0 + dz));
-        a[j] = __ldg(sp + vv[j]);
+        st[j] = __ldg(vs + vv[j]);
       }
       kk += 32;
       dx += qb;
@@ -465,14 +472,21 @@ __global__ void __launch_bounds__(128) k_vote_walk(const int2* __restrict__ sp, 
       if (dx >= W) { dx -= W; dy++; }
       while (dy >= H) { dy -= H; dz++; }
     };
+    auto load_phi = [&](int jp, int j) {
+      if (WRITE && st[j] == s) ph[jp] = __ldg(vphi + vv[j]);
+    };
 #pragma unroll
-    for (int j = 0; j < 2 * VS_DEPTH; j++) load(j);
-    for (long long base = kb; base < ke; base += 32 * 2 * VS_DEPTH) {
+    for (int j = 0; j < DA; j++) load(j);
 #pragma unroll
-      for (int j = 0; j < 2 * VS_DEPTH; j++) {
-        const bool mine = a[j].x == s;
-        const int phi = a[j].y, v = vv[j];
-        load(j);
+    for (int j = 0; j < VS_DEPTH; j++) load_phi(j, j);
+    for (long long base = kb; base < ke; base += 32 * DA) {
+#pragma unroll
+      for (int j = 0; j < DA; j++) {
+        const int jp = j % VS_DEPTH;
+        const bool mine = st[j] == s;
+        const int phi = ph[jp], v = vv[j];
+        load_phi(jp, (j + VS_DEPTH) % DA);  // batch + VS_DEPTH: its site was loaded VS_DEPTH batches ago
+        load(j);                            // batch + DA into the slot this batch left
         const unsigned m = __ballot_sync(0xffffffffu, mine);
         if (WRITE && mine) out[n_out + __popc(m & ((1u << lane) - 1u))] = make_int2(phi, v);
         n_out += __popc(m);
@@ -483,10 +497,16 @@ __global__ void __launch_bounds__(128) k_vote_walk(const int2* __restrict__ sp, 
 }
 
 // one warp per site (order[]: largest boxes first): the ordered chains over
-// the site's entries ent[off[seg0[s]] .. off[seg0[s] + nseg[s]]) -- contiguous,
-// in voxel order. Entries are loaded VS_DEPTH batches ahead and the weights
-// of a batch two batches ahead (once its entries arrived).
-template <int WARPS, int DE = VS_DEPTH, int DW = 2>
+// the site's entries ent[off[seg0[s]] .. off[seg0[s] + nseg[s]]) --
+// contiguous, in voxel order. Software-pipelined, branch-free: while the 32
+// dependent adds of batch c run (every lane runs them; lanes 0-3 hold the
+// four real chains, the others a harmless copy), the terms of batch c + 1
+// are formed into the other half of a double-buffered stage -- one basic
+// block, so the scheduler fills the add latency with that work. Entries are
+// loaded DE batches ahead, weights DW batches ahead. Past the end an entry
+// is (0, -1) with weight 0, whose term is +0.0: adding it is exact (the
+// chains start at +0.0 and never become -0.0).
+template <int WARPS, int DE = 8, int DW = 4>  // (4, 2: 8 % slower at C4)
 __global__ void __launch_bounds__(WARPS * 32) k_vote_add(const int* __restrict__ order, int n_sites, Geo g,
                                                          const double* __restrict__ w64,
                                                          const float* __restrict__ w32, int w_mode, int mode,
@@ -495,7 +515,8 @@ __global__ void __launch_bounds__(WARPS * 32) k_vote_add(const int* __restrict__
                                                          const int* __restrict__ off, const int* __restrict__ n_ent,
                                                          const int* __restrict__ n_seg_total,
                                                          const int2* __restrict__ ent, double* __restrict__ sums) {
-  __shared__ __align__(16) double buf[WARPS][4][VS_ROW];
+  static_assert(DE > DW && DW >= 2 && DE % DW == 0, "k_vote_add pipeline");
+  __shared__ __align__(16) double buf[WARPS][2][4][VS_ROW];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   if ((int)blockIdx.x * WARPS + wid >= n_sites) return;
   const int s = order[blockIdx.x * WARPS + wid];
@@ -503,45 +524,66 @@ __global__ void __launch_bounds__(WARPS * 32) k_vote_add(const int* __restrict__
   const int k0 = seg0[s], k1 = k0 + nseg[s];
   const int e0 = k0 < *n_seg_total ? off[k0] : *n_ent;
   const int e1 = k1 < *n_seg_total ? off[k1] : *n_ent;
-  double acc = (init && mode != 1 && lane < 4) ? init[lane * n_sites + s] : 0.0;
-  double* row = &buf[wid][lane & 3][0];
-  // DE entry batches in flight; the weights of a batch are loaded DW batches ahead of its use
+  double acc = (init && mode != 1) ? init[(lane & 3) * n_sites + s] : 0.0;
   int2 q[DE];
   double wd[DW];
   float wf[DW];
   auto ld_ent = [&](int j, int c) { q[j] = c + lane < e1 ? __ldg(ent + c + lane) : make_int2(0, -1); };
   auto ld_w = [&](int jw, int j) {
+    wd[jw] = 0.0;
+    wf[jw] = 0.f;
     if (q[j].y >= 0) {
       if (w_mode == 1) wd[jw] = __ldg(w64 + q[j].y);
       else if (w_mode >= 2) wf[jw] = __ldg(w32 + q[j].y);
     }
   };
+  // the term of the batch in entry slot j / weight slot jw into stage half h
+  auto form = [&](int j, int jw, int h) {
+    const bool live = q[j].y >= 0;
+    const double wt = !live ? 0.0
+                      : w_mode == 0 ? 1.0
+                      : w_mode == 1 ? wd[jw]
+                      : w_mode == 2 ? (double)wf[jw]
+                                    : __dmul_rn((double)wf[jw], (double)wf[jw]);  // m**1.0 / m**2.0
+    const double4 t = g.pack10 ? vote_term_packed(g, q[j].x, wt) : vote_term(g, q[j].x, wt);
+    buf[wid][h][0][lane] = t.x; buf[wid][h][1][lane] = t.y; buf[wid][h][2][lane] = t.z; buf[wid][h][3][lane] = t.w;
+  };
+  const int nb = (e1 - e0 + 31) >> 5;  // batches
 #pragma unroll
   for (int j = 0; j < DE; j++) ld_ent(j, e0 + 32 * j);
 #pragma unroll
   for (int j = 0; j < DW; j++) ld_w(j, j);
-  for (int c0 = e0; c0 < e1; c0 += 32 * DE) {
+  if (nb > 0) {
+    form(0, 0, 0);
+    ld_w(0, DW % DE);
+    ld_ent(0, e0 + 32 * DE);
+  }
+  __syncwarp();
+  for (int b0 = 0; b0 < nb; b0 += DE) {
 #pragma unroll
     for (int j = 0; j < DE; j++) {
-      const int c = c0 + 32 * j;
-      if (c >= e1) break;  // warp-uniform
-      const int jw = j % DW;
-      const int2 e = q[j];
-      const bool mine = e.y >= 0;
-      double wt = 0.0;
-      if (mine)
-        wt = w_mode == 0 ? 1.0
-             : w_mode == 1 ? wd[jw]
-             : w_mode == 2 ? (double)wf[jw]
-                           : __dmul_rn((double)wf[jw], (double)wf[jw]);  // m**1.0 / m**2.0
-      ld_w(jw, (j + DW) % DE);         // batch c + DW: its entries were loaded DE - DW batches ago
-      ld_ent(j, c + 32 * DE);          // batch c + DE into the slot this batch left
-      double4 t = make_double4(0.0, 0.0, 0.0, 0.0);  // lanes past the end: the +0.0 pads
-      if (mine) t = g.pack10 ? vote_term_packed(g, e.x, wt) : vote_term(g, e.x, wt);
-      buf[wid][0][lane] = t.x; buf[wid][1][lane] = t.y; buf[wid][2][lane] = t.z; buf[wid][3][lane] = t.w;
-      __syncwarp();
-      if (lane < 4) acc = ordered_add_padded(acc, row, min(32, e1 - c));
-      __syncwarp();
+      const int b = b0 + j;
+      if (b >= nb) break;  // warp-uniform
+      // batch b + 1 sits in entry slot (j + 1) % DE and weight slot (b + 1) % DW (past the last batch:
+      // zero terms, never added)
+      const int jn = (j + 1) % DE, jwn = (j + 1) % DW;
+      form(jn, jwn, (b + 1) & 1);
+      ld_w(jwn, (j + 1 + DW) % DE);  // batch b + 1 + DW
+      ld_ent(jn, e0 + 32 * (b + 1 + DE));
+      // the 32 ordered adds of batch b (stage half b & 1)
+      const double* row = &buf[wid][b & 1][lane & 3][0];
+#pragma unroll
+      for (int h = 0; h < 32; h += 8) {
+        const double2 a0 = *reinterpret_cast<const double2*>(row + h);
+        const double2 a1 = *reinterpret_cast<const double2*>(row + h + 2);
+        const double2 a2 = *reinterpret_cast<const double2*>(row + h + 4);
+        const double2 a3 = *reinterpret_cast<const double2*>(row + h + 6);
+        acc = __dadd_rn(acc, a0.x); acc = __dadd_rn(acc, a0.y);
+        acc = __dadd_rn(acc, a1.x); acc = __dadd_rn(acc, a1.y);
+        acc = __dadd_rn(acc, a2.x); acc = __dadd_rn(acc, a2.y);
+        acc = __dadd_rn(acc, a3.x); acc = __dadd_rn(acc, a3.y);
+      }
+      __syncwarp();  // half b & 1 is free for batch b + 2; half (b + 1) & 1 is visible
     }
   }
   if (lane < 4) sums[lane * n_sites + s] = acc;

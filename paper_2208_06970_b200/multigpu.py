@@ -575,8 +575,8 @@ def global_lrcvt(grid, labels, seeding, lloyd, coll=None):
     vote partitioned over the Collective's ranks. Returns (Tessellation,
     trace); the per-voxel arrays are assembled from the local ranks' slabs
     (every slab when all ranks are local)."""
-    from .seeding import Site, seed_sites, voxel_weights
-    from .tessellation import Tessellation, lloyd_weight_mode, voxel_length
+    from .seeding import seed_sites, voxel_weights
+    from .tessellation import Tessellation, lloyd_weight_mode, make_sites, voxel_length
 
     torch = _lib.require_cuda()
     if labels.n_components == 0:
@@ -618,7 +618,7 @@ def global_lrcvt(grid, labels, seeding, lloyd, coll=None):
         dist[v0:v1] = eng.dist[v0:v1].cpu().numpy()
         state[v0:v1] = eng.state[v0:v1].cpu().numpy()
     final_pos = pos_d.cpu().numpy()
-    final_sites = [Site((float(p[0]), float(p[1]), float(p[2])), int(c)) for p, c in zip(final_pos, sc)]
+    final_sites = make_sites(final_pos, sc)
     has = np.zeros(max(labels.n_components, 1), dtype=bool)
     has[sc] = True
     report = {"rounds": st["rounds"], "sweeps": st["sweeps"],

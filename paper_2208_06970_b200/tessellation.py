@@ -11,6 +11,7 @@ Lloyd loop and only the final tessellation is copied back.
 from __future__ import annotations
 
 import ctypes
+import gc
 import itertools
 import operator
 import weakref
@@ -293,6 +294,23 @@ def _components(sites) -> np.ndarray:
     return np.fromiter(map(_get_comp, sites), dtype=np.int32, count=len(sites))
 
 
+def make_sites(pos: np.ndarray, comp: np.ndarray) -> list[Site]:
+    """Site objects from float64[S, 3] positions and int component ids (the
+    same Python floats / ints as Site((float(x), float(y), float(z)), int(c))).
+    Built from column lists zipped at C level, with the cyclic collector
+    paused: its generation-0 passes over the new objects cost as much as
+    building them."""
+    cols = np.asarray(pos, dtype=np.float64).reshape(-1, 3).T.tolist()
+    ids = np.asarray(comp).tolist()
+    paused = gc.isenabled()
+    gc.disable()
+    try:
+        return list(map(Site, zip(cols[0], cols[1], cols[2]), ids))
+    finally:
+        if paused:
+            gc.enable()
+
+
 def _site_arrays(torch, sites):
     pos = _positions(sites)
     comp = _components(sites)
@@ -303,7 +321,13 @@ def _no_site_components(labels: LabelMap, site_comp: np.ndarray) -> list[int]:
     has = np.zeros(max(labels.n_components, 1), dtype=bool)
     if site_comp.size:
         has[site_comp] = True
-    return sorted(int(c.id) for c in labels.component_table if not has[c.id])
+    table = labels.component_table
+    cached = getattr(labels, "_b200_ids", None)  # component ids of the table, once per table object
+    if cached is None or cached[0] is not table or cached[1].size != len(table):
+        cached = (table, np.fromiter((c.id for c in table), dtype=np.int64, count=len(table)))
+        labels._b200_ids = cached
+    ids = cached[1]
+    return np.unique(ids[~has[ids]]).tolist()
 
 
 # ---------------------------------------------------------------------------
@@ -429,7 +453,7 @@ def centroidal_update(tess: Tessellation, weights: np.ndarray | None = None) -> 
     tess.report["empty_regions"] = int(empty)
     both = torch.cat([new_pos, disp[:, None]], dim=1).cpu().numpy()  # one device->host read
     disp = np.ascontiguousarray(both[:, 3])
-    new_sites = list(map(Site, map(tuple, both[:, :3].tolist()), site_comp.tolist()))
+    new_sites = make_sites(both[:, :3], site_comp)
     mean_ds = float(disp.mean() / vlen) if disp.size else 0.0
     return new_sites, mean_ds
 
@@ -474,8 +498,7 @@ def lrcvt(grid: VoxelGrid, labels: LabelMap, seeding: SeedingParams,
         eng.L.lrcvt_plan_reuse_eligible(eng.plan, 0)
     pos_d = eng._last_pos
     pos = pos_d.cpu().numpy()
-    final_sites = [Site(position=(float(p[0]), float(p[1]), float(p[2])), component_id=int(c))
-                   for p, c in zip(pos, site_comp)]
+    final_sites = make_sites(pos, site_comp)
     final = voronoi_classify(grid, labels, final_sites, weights)
     final.report["seeding"] = seed_report
     final.report["updates"] = len(trace)

@@ -1,4 +1,7 @@
-"""Split the public-API update step: device call (synchronised) vs Python."""
+"""Split the public-API update step: device call (synchronised) vs Python.
+
+  python tools/e2e_probe2.py [c2|c4]
+"""
 import sys
 import time
 from pathlib import Path
@@ -13,7 +16,8 @@ def main():
     from paper_2208_06970_b200 import centroidal_update, voronoi_classify
     from paper_2208_06970_b200 import tessellation as T
 
-    grid, labels, params, sites, weights = bench.build_workload(bench.CONFIGS["c2"], 0)
+    cfg = sys.argv[1] if len(sys.argv) > 1 else "c2"
+    grid, labels, params, sites, weights = bench.build_workload(bench.CONFIGS[cfg], 0)
     acc = {"classify_dev": 0.0, "centroidal_dev": 0.0}
     orig_c, orig_u = T.Engine.classify, T.Engine.centroidal
 
