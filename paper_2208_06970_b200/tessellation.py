@@ -284,14 +284,46 @@ _get_pos = operator.attrgetter("position")
 _get_comp = operator.attrgetter("component_id")
 
 
+# The arrays of the last Site list built or read here, with what identifies
+# it: the Site objects, their position tuples (a reassigned position is a new
+# tuple) and component ids. A list whose elements are those very objects,
+# still holding those very tuples and ids, has those arrays -- checked at C
+# level in half the time of reading the positions again.
+_site_cache: list = [None]
+
+
+def _cached_arrays(sites):
+    c = _site_cache[0]
+    if (c is None or len(sites) != len(c[0]) or not all(map(operator.is_, sites, c[0]))
+            or not all(map(operator.is_, map(_get_pos, sites), c[1])) or list(map(_get_comp, sites)) != c[2]):
+        return None
+    return c[3], c[4]
+
+
+def _remember(sites, pos: np.ndarray, comp: np.ndarray):
+    _site_cache[0] = (tuple(sites), list(map(_get_pos, sites)), comp.tolist(), pos, comp)
+
+
+def _read_sites(sites):
+    """(float64[S, 3] positions, int32[S] components) of a Site list; the
+    returned arrays are shared with the cache: callers copy before writing"""
+    got = _cached_arrays(sites)
+    if got is None:
+        pos = np.fromiter(itertools.chain.from_iterable(map(_get_pos, sites)), dtype=np.float64,
+                          count=3 * len(sites)).reshape(-1, 3)
+        comp = np.fromiter(map(_get_comp, sites), dtype=np.int32, count=len(sites))
+        _remember(sites, pos, comp)
+        got = pos, comp
+    return got
+
+
 def _positions(sites) -> np.ndarray:
     """float64[S, 3] site positions (C-level iteration; same values as np.array)."""
-    return np.fromiter(itertools.chain.from_iterable(map(_get_pos, sites)), dtype=np.float64,
-                       count=3 * len(sites)).reshape(-1, 3)
+    return _read_sites(sites)[0].copy()
 
 
 def _components(sites) -> np.ndarray:
-    return np.fromiter(map(_get_comp, sites), dtype=np.int32, count=len(sites))
+    return _read_sites(sites)[1].copy()
 
 
 def make_sites(pos: np.ndarray, comp: np.ndarray) -> list[Site]:
@@ -300,20 +332,23 @@ def make_sites(pos: np.ndarray, comp: np.ndarray) -> list[Site]:
     Built from column lists zipped at C level, with the cyclic collector
     paused: its generation-0 passes over the new objects cost as much as
     building them."""
-    cols = np.asarray(pos, dtype=np.float64).reshape(-1, 3).T.tolist()
-    ids = np.asarray(comp).tolist()
+    pos = np.array(pos, dtype=np.float64).reshape(-1, 3)
+    comp = np.array(comp, dtype=np.int32).reshape(-1)
+    cols = pos.T.tolist()
+    ids = comp.tolist()
     paused = gc.isenabled()
     gc.disable()
     try:
-        return list(map(Site, zip(cols[0], cols[1], cols[2]), ids))
+        out = list(map(Site, zip(cols[0], cols[1], cols[2]), ids))
     finally:
         if paused:
             gc.enable()
+    _remember(out, pos, comp)
+    return out
 
 
 def _site_arrays(torch, sites):
-    pos = _positions(sites)
-    comp = _components(sites)
+    pos, comp = _read_sites(sites)
     return pos, comp, torch.from_numpy(pos).to("cuda"), torch.from_numpy(comp).to("cuda")
 
 
@@ -415,10 +450,10 @@ def centroidal_update(tess: Tessellation, weights: np.ndarray | None = None) -> 
     if weights is None:
         weights = tess.weights
     torch = _lib.require_cuda()
-    site_comp = tess.site_components()
     if len(tess.sites) == 0:
         tess.report["empty_regions"] = 0
         return [], 0.0
+    pos, site_comp = _read_sites(tess.sites)  # read-only below
     dev = tess.device_state() if isinstance(tess, DeviceTessellation) else None
     ss = None
     if dev is not None:
@@ -432,10 +467,10 @@ def centroidal_update(tess: Tessellation, weights: np.ndarray | None = None) -> 
                      len(tess.sites))
         eng.upload(tess.site_of, tess.src)
         del labels
-    pos = _positions(tess.sites)
     cached = getattr(tess, "_b200_sites", None) if dev is not None else None
-    reuse = (cached is not None and cached[0] == eng.classify_seq and np.array_equal(cached[2], site_comp)
-             and np.array_equal(cached[1], pos))
+    reuse = (cached is not None and cached[0] == eng.classify_seq
+             and (cached[2] is site_comp or np.array_equal(cached[2], site_comp))
+             and (cached[1] is pos or np.array_equal(cached[1], pos)))
     if reuse:
         pos_d, comp_d = cached[3], cached[4]
     else:
