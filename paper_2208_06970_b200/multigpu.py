@@ -162,11 +162,13 @@ class TorchDist:
     the GPU path; device="cpu" stages every collective through host memory
     (gloo) -- the CPU-coordinated tests of the protocol."""
 
-    def __init__(self, group=None, device: str = "cuda"):
+    def __init__(self, group=None, device: str | None = None):
         import torch.distributed as dist
 
         self.dist = dist
         self.group = group
+        if device is None:  # NCCL moves CUDA tensors; gloo (and any other backend) stages through host memory
+            device = "cuda" if dist.get_backend(group) == "nccl" else "cpu"
         self.device = device
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)

@@ -55,6 +55,21 @@ def test_reference_arm_same_config():
     assert ref["metric"] == ours["metric"] and ref["unit"] == ours["unit"]
 
 
+def test_bench_two_ranks_global_mode():
+    """--gpus 2 in global mode (the driver's multi-GPU default): two processes
+    share device 0 over gloo, each owns a z-slab, CUDA IPC peer reads, the
+    calibration re-cut of the slab bounds gathered over the collective"""
+    env = dict(os.environ, LRCVT_BENCH_DEVICE="0", LRCVT_BENCH_BACKEND="gloo")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                        "--master-addr", "127.0.0.1", "--master-port", "29563", "bench.py", "--gpus", "2",
+                        "--config", "c2", "--steps", "2", "--warmup", "3"],
+                       cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-3000:]
+    d = _line(r.stdout)
+    assert d["n_gpus"] == 2 and d["mode"] == "global" and d["scaling"] == "strong" and d["value"] > 0
+    assert len(d["slabs_z"]) == 2 and d["slabs_z"][0][0] == 0 and d["slabs_z"][1][1] == 128
+
+
 def test_bench_two_ranks_smoke():
     env = dict(os.environ, LRCVT_BENCH_DEVICE="0", LRCVT_BENCH_BACKEND="gloo")
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
