@@ -120,14 +120,17 @@ class Emulated:
         vals = list(per_rank.values())
         return [int(sum(v[i] for v in vals)) for i in range(len(vals[0]))]
 
-    def exchange_halo(self, lo: dict, hi: dict, torch) -> dict:
-        """rank r receives hi of r - 1 and lo of r + 1 (uint8 tensors)."""
+    def exchange_halo(self, lo: dict, hi: dict, torch, extra: dict | None = None):
+        """rank r receives hi of r - 1 and lo of r + 1 (uint8 tensors); with
+        `extra` ({rank: [ints]}) also returns their sums over the ranks."""
         out = {}
         for r in self.local_ranks:
             parts = ([hi[r - 1]] if r > 0 else []) + ([lo[r + 1]] if r + 1 < self.world else [])
             parts = [p for p in parts if p.numel()]
             out[r] = torch.cat(parts) if parts else torch.empty(0, dtype=torch.uint8, device="cuda")
-        return out
+        if extra is None:
+            return out
+        return out, self.sum_ints(extra)
 
     def allreduce(self, per_rank: dict, op: str, torch):
         ts = list(per_rank.values())
@@ -220,14 +223,39 @@ class TorchDist:
         """Concatenate every rank's proposal bytes in rank order."""
         return torch.cat(self._all_bytes(local[0], torch))
 
-    def exchange_halo(self, lo: dict, hi: dict, torch) -> dict:
-        r = self.rank
-        los = self._all_bytes(lo[r], torch)
-        his = self._all_bytes(hi[r], torch)
-        parts = ([his[r - 1]] if r > 0 else []) + ([los[r + 1]] if r + 1 < self.world else [])
-        parts = [p for p in parts if p.numel()]
-        got = torch.cat(parts) if parts else torch.empty(0, dtype=torch.uint8, device=self.device)
-        return {r: got.to(self.home)}
+    def exchange_halo(self, lo: dict, hi: dict, torch, extra: dict | None = None):
+        """rank r sends lo to r - 1 and hi to r + 1 and receives hi of r - 1 and
+        lo of r + 1: one all-gather of the list sizes (and of `extra`, whose
+        sums over the ranks come back too), then point-to-point transfers
+        between neighbours only (NVLink P2P under NCCL)."""
+        r, world = self.rank, self.world
+        mine_lo, mine_hi = lo[r], hi[r]
+        ex = list(extra[r]) if extra is not None else []
+        k = 2 + len(ex)
+        g = self.all_counts([int(mine_lo.numel()), int(mine_hi.numel())] + ex)
+        n = [g[q * k + j] for q in range(world) for j in range(2)]
+        sums = [sum(g[q * k + 2 + j] for q in range(world)) for j in range(len(ex))]
+        P2POp = self.dist.P2POp
+        ops, got = [], []
+        if r > 0 and n[2 * (r - 1) + 1]:  # hi of r - 1
+            buf = torch.empty(n[2 * (r - 1) + 1], dtype=torch.uint8, device=self.device)
+            ops.append(P2POp(self.dist.irecv, buf, r - 1, self.group))
+            got.append(buf)
+        if r + 1 < world and n[2 * (r + 1)]:  # lo of r + 1
+            buf = torch.empty(n[2 * (r + 1)], dtype=torch.uint8, device=self.device)
+            ops.append(P2POp(self.dist.irecv, buf, r + 1, self.group))
+            got.append(buf)
+        if r > 0 and mine_lo.numel():
+            ops.append(P2POp(self.dist.isend, self._to(mine_lo), r - 1, self.group))
+        if r + 1 < world and mine_hi.numel():
+            ops.append(P2POp(self.dist.isend, self._to(mine_hi), r + 1, self.group))
+        if ops:
+            for req in self.dist.batch_isend_irecv(ops):
+                req.wait()
+        out = torch.cat(got) if got else torch.empty(0, dtype=torch.uint8, device=self.device)
+        if extra is None:
+            return {r: out.to(self.home)}
+        return {r: out.to(self.home)}, sums
 
     def allreduce(self, per_rank: dict, op: str, torch):
         t = self._to(per_rank[self.rank].clone())
@@ -406,10 +434,9 @@ class GlobalClassifier:
             cats[r]["other"] = cats[r].get("other", 0.0) + ms.value
         return cats if breakdown else {r: sum(c.values()) for r, c in cats.items()}
 
-    def _round(self, phase: int, sweep: int, stats: dict) -> int:
-        """One relaxation round (or sweep) on all ranks; returns the global
-        number of improved proposals and sets the global frontier size."""
-        L, torch, st = self.L, self.torch, self._st()
+    def _eval_all(self, phase: int, sweep: int):
+        """eval on every local rank: ({rank: evaluated}, lo lists, hi lists)"""
+        L, st = self.L, self._st()
         counts, lo, hi = {}, {}, {}
         for r, eng in self.engines.items():
             ne, nlo, nhi = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
@@ -419,8 +446,12 @@ class GlobalClassifier:
             counts[r] = int(ne.value)
             lo[r] = self._bytes(L.lrcvt_mg_boundary(eng.plan, 0), int(nlo.value))
             hi[r] = self._bytes(L.lrcvt_mg_boundary(eng.plan, 1), int(nhi.value))
-        halo = self.coll.exchange_halo(lo, hi, torch)
-        nexts = {}
+        return counts, lo, hi
+
+    def _commit_all(self, halo: dict, sweep: int) -> dict:
+        """commit on every local rank: {rank: (own next frontier, own proposals committed)}"""
+        L, st = self.L, self._st()
+        done = {}
         for r, eng in self.engines.items():
             h = halo[r]
             nn, nc = ctypes.c_int64(), ctypes.c_int64()
@@ -428,8 +459,37 @@ class GlobalClassifier:
                                                             h.numel() // PROP_BYTES, sweep, ctypes.byref(nn),
                                                             ctypes.byref(nc), st),
                                           "lrcvt_mg_commit"), synced=True, cat="commit")
-            nexts[r] = [int(nn.value), counts[r], int(nc.value)]
-        tot = self.coll.sum_ints(nexts)
+            done[r] = (int(nn.value), int(nc.value))
+        return done
+
+    def _run_rounds(self, phase: int, stats: dict):
+        """Relaxation rounds until the global frontier is empty. One
+        collective per round besides the halo transfers: the all-gather of
+        the boundary-list sizes also carries every rank's frontier size and
+        its commits of the previous round, so the loop ends on a round whose
+        every frontier was empty (an eval of nothing) instead of a separate
+        all-reduce after each commit."""
+        if self._frontier <= 0:
+            return
+        prev = {r: 0 for r in self.engines}
+        while True:
+            counts, lo, hi = self._eval_all(phase, 0)
+            halo, tot = self.coll.exchange_halo(lo, hi, self.torch, {r: [counts[r], prev[r]] for r in self.engines})
+            stats["commits"] += tot[1]
+            if tot[0] == 0:
+                break
+            stats["rounds"] += 1
+            stats["evaluations"] += tot[0]
+            prev = {r: nc for r, (_, nc) in self._commit_all(halo, 0).items()}
+        self._frontier = 0
+
+    def _sweep(self, stats: dict) -> int:
+        """a verification sweep (phase 2) on all ranks; returns the global
+        number of improved proposals and sets the global frontier size"""
+        counts, lo, hi = self._eval_all(2, 1)
+        halo = self.coll.exchange_halo(lo, hi, self.torch)
+        done = self._commit_all(halo, 1)
+        tot = self.coll.sum_ints({r: [done[r][0], counts[r], done[r][1]] for r in self.engines})
         self._frontier = tot[0]
         stats["evaluations"] += tot[1]
         stats["commits"] += tot[2]
@@ -440,11 +500,6 @@ class GlobalClassifier:
         if n == 0 or not ptr:
             return torch.empty(0, dtype=torch.uint8, device="cuda")
         return as_tensor(torch, ptr, (n * PROP_BYTES,), "|u1").clone()
-
-    def _run_rounds(self, phase: int, stats: dict):
-        while self._frontier > 0:
-            stats["rounds"] += 1
-            self._round(phase, 0, stats)
 
     def classify(self, site_pos, site_comp) -> dict:
         """site_pos float64[S,3], site_comp int32[S] on the device; returns
@@ -478,7 +533,7 @@ class GlobalClassifier:
         while True:  # phase 2 + verification sweeps (tessellation.py:170-189)
             self._run_rounds(2, stats)
             stats["sweeps"] += 1
-            if self._round(2, 1, stats) == 0:
+            if self._sweep(stats) == 0:
                 break
         assigned = {}
         for r, eng in self.engines.items():
