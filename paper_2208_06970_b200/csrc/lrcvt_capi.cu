@@ -1143,9 +1143,11 @@ static int vote_chains(lrcvt_plan* p, const int* d_box, int S, int w_mode, const
     }
   }
   if (n_seg > 0) {
-    k_vote_walk<false><<<148 * 8, 128, 0, st>>>(p->vt_sp, d_box, S, g, zlo, zhi, mode, p->vt_seg0, p->vt_tot,
-                                                 p->vt_cnt, nullptr, nullptr);
-    CKL("k_vote_walk<count>"); LAUNCHED(1);
+    // segment counts from the eligible list (a COUNT walk of the boxes gives the same: vote.cuh)
+    CK(cudaMemsetAsync(p->vt_cnt, 0, sizeof(int) * (size_t)n_seg, st));
+    k_vote_count<<<grid_for(p->n_inband, 256, 148 * 16), 256, 0, st>>>(p->eligible, p->d_nel, p->vt_sp, d_box, S, g,
+                                                                        zlo, zhi, mode, p->vt_seg0, p->vt_cnt);
+    CKL("k_vote_count"); LAUNCHED(1);
     k_scan_excl<<<1, SCAN_THREADS, 0, st>>>(p->vt_cnt, n_seg, p->vt_off, p->vt_tot + 1);
     CKL("k_scan_excl"); LAUNCHED(1);
     k_vote_walk<true><<<148 * 8, 128, 0, st>>>(p->vt_sp, d_box, S, g, zlo, zhi, mode, p->vt_seg0, p->vt_tot,
