@@ -10,7 +10,10 @@
 
 namespace lrcvt {
 
-constexpr int P1_TAB = 4;  // distinct-site distance table
+#ifndef LRCVT_P1_TAB
+#define LRCVT_P1_TAB 3
+#endif
+constexpr int P1_TAB = LRCVT_P1_TAB;  // distinct-site distance table
 
 // Phase-1 evaluation (LOS candidates only):
 //   A  gather the 26 neighbours' LOS sites from the compact site1 array
@@ -216,13 +219,13 @@ __device__ __forceinline__ void p1_tile(const int* __restrict__ list, int n, con
       if (!((nbv >> k) & 1u)) continue;
       const int s = __ldg(site1 + v + off_dx(k) + off_dy(k) * g.nx + off_dz(k) * g.nxy);
       if (s < 0) continue;
-      double d;
-      if (s == orig_s) d = orig_d;  // the own site: the very dist3 of the current state
-      else if (s == ts[0]) d = td[0];
-      else if (s == ts[1]) d = td[1];
-      else if (s == ts[2]) d = td[2];
-      else if (s == ts[3]) d = td[3];
-      else {
+      double d = 0.0;
+      bool known = false;
+      if (s == orig_s) { d = orig_d; known = true; }  // the own site: the very dist3 of the current state
+#pragma unroll
+      for (int j = 0; j < P1_TAB; j++)
+        if (!known && s == ts[j]) { d = td[j]; known = true; }
+      if (!known) {
         const double4 sp = ld_d4(site_pos + s);
         d = dist3(px, py, pz, sp.x, sp.y, sp.z);
       }

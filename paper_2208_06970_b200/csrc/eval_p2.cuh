@@ -21,8 +21,14 @@
 
 namespace lrcvt {
 
-constexpr int P2_STAB = 4;  // distinct LOS sites
-constexpr int P2_NTAB = 6;  // distinct shortcut nodes
+#ifndef LRCVT_P2_STAB
+#define LRCVT_P2_STAB 4
+#endif
+#ifndef LRCVT_P2_NTAB
+#define LRCVT_P2_NTAB 4
+#endif
+constexpr int P2_STAB = LRCVT_P2_STAB;  // distinct LOS sites
+constexpr int P2_NTAB = LRCVT_P2_NTAB;  // distinct shortcut nodes
 
 // |c_w - c_v| for neighbour k: exact by offset class when the spacing is dyadic
 template <bool DYADIC>
@@ -180,13 +186,13 @@ __device__ __forceinline__ void p2_tile(const int* __restrict__ list, int n, con
         best_d = dpath; best_s = s; best_src = w;
       }
       if (u == -2) {
-        double d;
-        if (s == own_los) d = orig_d;  // the own LOS site: exactly the stored distance
-        else if (s == ts[0]) d = td[0];
-        else if (s == ts[1]) d = td[1];
-        else if (s == ts[2]) d = td[2];
-        else if (s == ts[3]) d = td[3];
-        else {
+        double d = 0.0;
+        bool known = false;
+        if (s == own_los) { d = orig_d; known = true; }  // the own LOS site: exactly the stored distance
+#pragma unroll
+        for (int j = 0; j < P2_STAB; j++)
+          if (!known && s == ts[j]) { d = td[j]; known = true; }
+        if (!known) {
           const double4 sp = ld_d4(site_pos + s);
           d = dist3(px, py, pz, sp.x, sp.y, sp.z);
         }
