@@ -25,7 +25,7 @@ namespace lrcvt {
 #define LRCVT_P2_STAB 4
 #endif
 #ifndef LRCVT_P2_NTAB
-#define LRCVT_P2_NTAB 2
+#define LRCVT_P2_NTAB 1
 #endif
 constexpr int P2_STAB = LRCVT_P2_STAB;  // distinct LOS sites
 constexpr int P2_NTAB = LRCVT_P2_NTAB;  // distinct shortcut nodes
