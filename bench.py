@@ -464,14 +464,15 @@ def run_global(args, cfg, world, rank, local):
         pos_d = step(pos_d)
     bounds0 = list(gc.bounds)
     if not args.no_rebalance:
-        # slab bounds from measured per-rank device time: one calibration iteration (not timed), re-cut,
-        # one more warm-up iteration on the new bounds
-        gc.set_timing(True)
-        gc.rank_ms()
-        pos_d = step(pos_d)
-        cost = gc.rank_ms()
-        gc.set_timing(False)
-        gc.rebalance(cost)
+        # slab bounds from measured per-rank device time: twice, a calibration iteration (not timed) and a
+        # re-cut; then one more warm-up iteration on the final bounds
+        for _ in range(2):
+            gc.set_timing(True)
+            gc.rank_ms()
+            pos_d = step(pos_d)
+            cost = gc.rank_ms()
+            gc.set_timing(False)
+            gc.rebalance(cost)
         pos_d = step(pos_d)
     if world > 1:
         torch.distributed.barrier()

@@ -34,7 +34,10 @@ __host__ __device__ inline int64_t coarse_words(int64_t bm_words) {
   return compact_tiles(bm_words) * CT_CWORDS;  // whole tiles: no bounds checks on the coarse reads
 }
 
-constexpr int CM_THREADS = 256;
+#ifndef LRCVT_CM_THREADS
+#define LRCVT_CM_THREADS 256
+#endif
+constexpr int CM_THREADS = LRCVT_CM_THREADS;
 constexpr int CM_SLOTS = 4 * CM_THREADS;  // sparse slots scanned per CTA step
 
 __device__ __forceinline__ void commit_one(const Prop& p, int2* __restrict__ ss, double* __restrict__ dist,
@@ -50,7 +53,7 @@ __device__ __forceinline__ void commit_one(const Prop& p, int2* __restrict__ ss,
   }
 }
 
-__global__ void __launch_bounds__(CM_THREADS, 8) k_commit(const Prop* __restrict__ imp, const uint8_t* __restrict__ pf,
+__global__ void __launch_bounds__(CM_THREADS, 2048 / CM_THREADS) k_commit(const Prop* __restrict__ imp, const uint8_t* __restrict__ pf,
                                                        int n_props, int* __restrict__ counters,
                                                        RoundCtl* __restrict__ ctl, Geo g,
                                                        const uint32_t* __restrict__ nbm, uint32_t* __restrict__ bm,

@@ -410,11 +410,11 @@ int launch_eval_kernel(lrcvt_plan* p, int var, int items, cudaStream_t st) {
       k_eval_p1<128, P1_MIN_BLOCKS_BIG><<<blocks, 128, 0, st>>>(c, g, cm, nb, sp, p->bm, p->imp, p->pf);
     else
       k_eval_p1<128><<<blocks, 128, 0, st>>>(c, g, cm, nb, sp, p->bm, p->imp, p->pf);
-  } else if (p->d_pv) {  // multi-GPU slab: far reads through the peer view
+  } else if (p->d_pv) {  // multi-GPU slab: far reads through the peer view (the one-domain register budget)
     if (var == 1)
-      k_eval_p2<64, true, true><<<blocks, 64, 0, st>>>(c, g, cm, nb, sp, p->bm, p->imp, p->pf, p->d_pv);
+      k_eval_p2<64, true, true, 12><<<blocks, 64, 0, st>>>(c, g, cm, nb, sp, p->bm, p->imp, p->pf, p->d_pv);
     else
-      k_eval_p2<64, false, true><<<blocks, 64, 0, st>>>(c, g, cm, nb, sp, p->bm, p->imp, p->pf, p->d_pv);
+      k_eval_p2<64, false, true, 12><<<blocks, 64, 0, st>>>(c, g, cm, nb, sp, p->bm, p->imp, p->pf, p->d_pv);
   } else if (bs == 32) {
     if (var == 1)
       k_eval_p2<32, true><<<blocks, 32, 0, st>>>(c, g, cm, nb, sp, p->bm, p->imp, p->pf);
