@@ -35,7 +35,7 @@ __host__ __device__ inline int64_t coarse_words(int64_t bm_words) {
 }
 
 #ifndef LRCVT_CM_THREADS
-#define LRCVT_CM_THREADS 256
+#define LRCVT_CM_THREADS 512
 #endif
 constexpr int CM_THREADS = LRCVT_CM_THREADS;
 constexpr int CM_SLOTS = 4 * CM_THREADS;  // sparse slots scanned per CTA step
