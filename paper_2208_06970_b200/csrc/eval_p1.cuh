@@ -38,7 +38,10 @@ constexpr int P1_SPEC = 1;  // queued rays per lane (the strict winner's)
 // to hide the dependent gathers) for larger ones. Measured on phase-1 time:
 // 512^3 -10% and 256^3 -5% with 8 for the large rounds (6, 7, 10 in between
 // or equal, 12 worse); 128^3 rounds stay below the threshold (5 is 2% faster there).
-constexpr int P1_MIN_BLOCKS = 5;
+#ifndef LRCVT_P1_MINB_SMALL
+#define LRCVT_P1_MINB_SMALL 5
+#endif
+constexpr int P1_MIN_BLOCKS = LRCVT_P1_MINB_SMALL;
 constexpr int P1_MIN_BLOCKS_BIG = 8;
 constexpr int P1_BIG_ROUND = 1 << 20;
 
