@@ -20,6 +20,11 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _lib
+
+try:  # the C builder of list[Site] (csrc/sites_ext.c, built by __graft_entry__.build)
+    from . import _sites
+except ImportError:  # pragma: no cover - the pure-Python builder below gives the same objects
+    _sites = None
 from .grid import NONE_ID, LabelMap, VoxelGrid
 from .seeding import SeedingParams, Site, seed_sites, voxel_weights
 
@@ -334,15 +339,18 @@ def make_sites(pos: np.ndarray, comp: np.ndarray) -> list[Site]:
     building them."""
     pos = np.array(pos, dtype=np.float64).reshape(-1, 3)
     comp = np.array(comp, dtype=np.int32).reshape(-1)
-    cols = pos.T.tolist()
-    ids = comp.tolist()
-    paused = gc.isenabled()
-    gc.disable()
-    try:
-        out = list(map(Site, zip(cols[0], cols[1], cols[2]), ids))
-    finally:
-        if paused:
-            gc.enable()
+    if _sites is not None:  # csrc/sites_ext.c: the same objects, built in C
+        out = _sites.make_sites(Site, pos.tobytes(), comp.tobytes())
+    else:
+        cols = pos.T.tolist()
+        ids = comp.tolist()
+        paused = gc.isenabled()
+        gc.disable()
+        try:
+            out = list(map(Site, zip(cols[0], cols[1], cols[2]), ids))
+        finally:
+            if paused:
+                gc.enable()
     _remember(out, pos, comp)
     return out
 
