@@ -1004,7 +1004,10 @@ int lrcvt_classify(lrcvt_plan* p, int64_t n_sites, const double* d_site_pos,
     p->eligible_valid = true;
     p->eligible_sites = S;
   }
-  const int el_grid = grid_for(p->n_inband, 256, 148 * 16);
+#ifndef LRCVT_EL_WAVES
+#define LRCVT_EL_WAVES 16
+#endif
+  const int el_grid = grid_for(p->n_inband, 256, 148 * LRCVT_EL_WAVES);  // the eligible-list passes
   if (!fast) {  // tessellation.py:120-122
     k_fill_state<<<grid_for(g.n, 256, 148 * 32), 256, 0, st>>>(ss, d_dist, g.n);
     CKL("k_fill_state"); LAUNCHED(1);
@@ -1145,7 +1148,7 @@ static int vote_chains(lrcvt_plan* p, const int* d_box, int S, int w_mode, const
   if (n_seg > 0) {
     // segment counts from the eligible list (a COUNT walk of the boxes gives the same: vote.cuh)
     CK(cudaMemsetAsync(p->vt_cnt, 0, sizeof(int) * (size_t)n_seg, st));
-    k_vote_count<<<grid_for(p->n_inband, 256, 148 * 16), 256, 0, st>>>(p->eligible, p->d_nel, p->vt_sp, d_box, S, g,
+    k_vote_count<<<grid_for(p->n_inband, 256, 148 * LRCVT_EL_WAVES), 256, 0, st>>>(p->eligible, p->d_nel, p->vt_sp, d_box, S, g,
                                                                         zlo, zhi, mode, p->vt_seg0, p->vt_cnt);
     CKL("k_vote_count"); LAUNCHED(1);
     k_scan_excl<<<1, SCAN_THREADS, 0, st>>>(p->vt_cnt, n_seg, p->vt_off, p->vt_tot + 1);
