@@ -14,6 +14,11 @@ namespace lrcvt {
 #define LRCVT_P1_TAB 3
 #endif
 constexpr int P1_TAB = LRCVT_P1_TAB;  // distinct-site distance table
+#ifndef LRCVT_P1_GATHER
+#define LRCVT_P1_GATHER 13
+#endif
+constexpr int P1_GATHER = LRCVT_P1_GATHER;  // neighbour loads in flight per batch (13 or 26)
+static_assert(26 % P1_GATHER == 0, "P1_GATHER divides 26");
 
 // Phase-1 evaluation (LOS candidates only):
 //   A  gather the 26 neighbours' LOS sites from the compact site1 array
@@ -93,17 +98,17 @@ __device__ __forceinline__ void p1_tile(const int* __restrict__ list, int n, con
     // two batches of 13 loads in flight (bounds the live registers of the
     // big-round variant, whose 64-register budget otherwise spills)
 #pragma unroll
-    for (int h = 0; h < 2; h++) {
-    int nw[13];
+    for (int h = 0; h < 26 / P1_GATHER; h++) {
+    int nw[P1_GATHER];
 #pragma unroll
-    for (int q = 0; q < 13; q++) {
-      const int k = 13 * h + q;
+    for (int q = 0; q < P1_GATHER; q++) {
+      const int k = P1_GATHER * h + q;
       const int w = v + off_dx(k) + off_dy(k) * g.nx + off_dz(k) * g.nxy;
       nw[q] = ((same >> k) & 1u) ? __ldg(site1 + w) : -1;
     }
 #pragma unroll
-    for (int q = 0; q < 13; q++) {
-      const int k = 13 * h + q;
+    for (int q = 0; q < P1_GATHER; q++) {
+      const int k = P1_GATHER * h + q;
       const int s = nw[q];
       // ---- B: distinct-site table; the voxel's own site is not entered: its
       // (skipping a batch's inserts when no lane of the warp sees a foreign
