@@ -91,7 +91,11 @@ int lrcvt_centroidal_update(lrcvt_plan *plan, int64_t n_sites, const double *d_s
 /* Sticky plan flag: the caller guarantees that centroidal_update is called
  * with the same site-component set as the preceding lrcvt_classify (true
  * inside a Lloyd loop, where components never change), so the eligible-voxel
- * list (tessellation.py:161-164) built by the classify is reused. */
+ * list (tessellation.py:161-164) built by the classify is reused.
+ * enable = 1 keeps the list the plan holds now; enable = 2 starts a new run:
+ * the list is dropped, the next classify builds it for its sites and later
+ * calls reuse that one (a loop whose sites may differ from the plan's last
+ * classify with the same site count). */
 int lrcvt_plan_reuse_eligible(lrcvt_plan *plan, int enable);
 
 /* split packed (site_of, src) into two int32[N] arrays */

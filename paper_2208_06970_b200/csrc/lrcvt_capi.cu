@@ -955,6 +955,7 @@ int lrcvt_plan_timing(const lrcvt_plan* p, int64_t* launches, int64_t* items, do
 int lrcvt_plan_reuse_eligible(lrcvt_plan* p, int enable) {
   if (!p) return set_error(LRCVT_E_ARG, "lrcvt_plan_reuse_eligible");
   p->reuse_eligible = enable != 0;
+  if (enable == 2) p->eligible_valid = false;  // a new run: the next classify builds the list
   return 0;
 }
 

@@ -382,7 +382,7 @@ class GlobalClassifier:
         """keep each rank's eligible list across classifies (a Lloyd loop: the
         site components do not change between iterations)"""
         for eng in self.engines.values():
-            _lib.check(self.L.lrcvt_plan_reuse_eligible(eng.plan, 1 if on else 0), "reuse_eligible")
+            _lib.check(self.L.lrcvt_plan_reuse_eligible(eng.plan, 2 if on else 0), "reuse_eligible")
 
     def _st(self):
         return _lib.stream_handle(self.torch)

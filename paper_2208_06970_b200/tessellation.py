@@ -534,7 +534,7 @@ def lrcvt(grid: VoxelGrid, labels: LabelMap, seeding: SeedingParams,
     _, site_comp, pos_d, comp_d = _site_arrays(torch, sites)
     mode, w_d = lloyd_weight_mode(torch, grid, seeding, weights)
     vlen = voxel_length(grid.dims, grid.spacing)
-    eng.L.lrcvt_plan_reuse_eligible(eng.plan, 1)  # site components fixed for the whole loop
+    eng.L.lrcvt_plan_reuse_eligible(eng.plan, 2)  # site components fixed for the whole loop (built by its first classify)
     try:
         trace = _lloyd_iterations(eng, pos_d, comp_d, mode, w_d, vlen, lloyd, trace)
     finally:

@@ -223,3 +223,33 @@ def test_clearance_dda_equals_reference_dda(kind, dims, iso, spacing):
     fast = out.cpu().numpy().astype(bool)
     assert np.array_equal(fast, t >= 1.0)
     assert 0.05 < fast.mean() < 0.95  # both outcomes well represented
+
+
+def test_reuse_run_rebuilds_eligible_list_for_new_sites(oracle_mod):
+    """A Lloyd-style run (lrcvt_plan_reuse_eligible(plan, 2)) on an engine whose
+    last classify had other site components but the same site count builds
+    its own eligible list instead of reusing the stale one."""
+    import torch
+
+    from paper_2208_06970_b200 import Site, VoxelGrid, voronoi_classify
+    from paper_2208_06970_b200.tessellation import engine_for
+
+    dims = (20, 16, 6)
+    grid = VoxelGrid(dims, (1, 1, 1), {})
+    comp = np.zeros(int(np.prod(dims)), np.int32)
+    comp.reshape(6, 16, 20)[:, :, 10:] = 1  # two components side by side
+    labels = _labels(comp, dims)
+    a = [Site((2.5, 3.5, 2.5), 0), Site((6.5, 9.5, 3.5), 0)]  # component 0 only
+    b = [Site((2.5, 3.5, 2.5), 0), Site((15.5, 9.5, 3.5), 1)]  # both components, same count
+    voronoi_classify(grid, labels, a)  # the shared engine now holds a's eligible list
+    eng = engine_for(labels, grid.spacing, len(b))
+    pos = torch.tensor([s.position for s in b], dtype=torch.float64).cuda()
+    sc = torch.tensor([s.component_id for s in b], dtype=torch.int32).cuda()
+    eng.L.lrcvt_plan_reuse_eligible(eng.plan, 2)
+    try:
+        eng.classify(pos, sc, want_state=True)
+    finally:
+        eng.L.lrcvt_plan_reuse_eligible(eng.plan, 0)
+    ref = oracle_mod.classify(dims, (1.0, 1.0, 1.0), comp, pos.cpu().numpy(), sc.cpu().numpy(), 2)
+    assert np.array_equal(eng.ss[:, 0].cpu().numpy(), ref["site_of"])
+    assert np.array_equal(eng.state.cpu().numpy(), ref["state"])

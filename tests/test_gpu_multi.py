@@ -215,7 +215,7 @@ def test_global_lloyd_large_frontiers_matches_single_domain(world):
     mode, w_d = lloyd_weight_mode(torch, grid, params, w)
     backoff = 0.5 * voxel_length(grid.dims, grid.spacing)
     eng = engine_for(labels, grid.spacing, S)
-    eng.L.lrcvt_plan_reuse_eligible(eng.plan, 1)
+    eng.L.lrcvt_plan_reuse_eligible(eng.plan, 2)
     gc = GlobalClassifier(grid.dims, grid.spacing, labels.component, labels.n_components, S, Emulated(world))
     gc.reuse_sites(True)
     p1, p2 = pos.clone(), pos.clone()

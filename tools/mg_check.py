@@ -40,7 +40,7 @@ def main():
     backoff = 0.5 * voxel_length(grid.dims, grid.spacing)
     L = _lib.lib()
     eng = engine_for(labels, grid.spacing, S)
-    L.lrcvt_plan_reuse_eligible(eng.plan, 1)
+    L.lrcvt_plan_reuse_eligible(eng.plan, 2)
     kw = {}
     if args.uniform:
         from paper_2208_06970_b200.multigpu import slab_bounds

@@ -57,7 +57,7 @@ def main():
     bbox = torch.empty((max(labels.n_components, 1), 6), dtype=torch.int32, device="cuda")
     lay = torch.empty(max(labels.n_components, 1), dtype=torch.int32, device="cuda")
     pairs = np.array([[0, 0], [0, 1], [1, 1]], np.int32)
-    L.lrcvt_plan_reuse_eligible(eng.plan, 1)
+    L.lrcvt_plan_reuse_eligible(eng.plan, 2)
     if a.host_rounds:
         _lib.check(L.lrcvt_plan_set_timing(eng.plan, 1), "set_timing")
 
